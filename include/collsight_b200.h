@@ -1,0 +1,62 @@
+/* collsight_b200.h — host-side extensions of the drop-in library.
+ *
+ * Entry points a maintainer of the reference would bind next to collsight.h
+ * to feed the B200 engine without going through a JSONL file:
+ *   - the packed-record replay of collsight_run_analyze (the same
+ *     run_detection + report rendering, records already in host memory);
+ *   - the scenario's layout / program / knobs lowered to the engine's plain
+ *     C tables (reference ScenarioConfig::build_topology / build_program,
+ *     proj/src/scenario.cpp:65-72);
+ *   - the JSONL trace codec (reference parse_trace_text / serialize_records,
+ *     proj/src/trace.cpp:155-346) producing/consuming packed records.
+ */
+#ifndef COLLSIGHT_B200_H_
+#define COLLSIGHT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "collsight.h"
+#include "csg_engine.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* collsight_run_analyze over packed records in host memory (pinned or
+ * pageable): H2D, device index, trigger + RCA, reports. */
+collsight_status collsight_b200_run_analyze_packed(
+    const collsight_scenario* scenario, const csg_packed_record* records,
+    size_t n, const char* report_out_path, collsight_result** out);
+
+/* Engine tables of a parsed scenario. The returned JSON text describes the
+ * layout and program as {"world_size","groups":[{"kind","members"}],
+ * "ops":[{"name","group","src","dst","deps"}]}; caller frees with
+ * collsight_b200_free. */
+collsight_status collsight_b200_scenario_layout_json(
+    const collsight_scenario* scenario, char** json_out);
+collsight_status collsight_b200_scenario_configs(
+    const collsight_scenario* scenario, csg_trigger_config* trigger,
+    csg_analysis_config* analysis, uint64_t* seed);
+
+/* build_layout + default_program (proj/src/topology.cpp:80-148,
+ * proj/src/program.cpp:25-119) as the JSON above. */
+collsight_status collsight_b200_layout_json(int tp, int pp, int dp,
+                                            int ranks_per_node,
+                                            int channels_per_pair,
+                                            int nics_per_node,
+                                            uint64_t msg_bytes,
+                                            char** json_out);
+
+/* JSONL <-> packed records. Parse errors follow the reference exactly
+ * (TraceParseError "line N: ..." -> status 3). */
+collsight_status collsight_b200_parse_trace(const char* text, size_t len,
+                                            csg_packed_record** out,
+                                            size_t* n);
+void collsight_b200_free(void* p);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* COLLSIGHT_B200_H_ */

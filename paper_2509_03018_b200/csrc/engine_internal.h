@@ -1,0 +1,135 @@
+// engine_internal.h — shared internals of the B200 trace-analysis engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "csg_engine.h"
+
+namespace csg {
+
+// Errors thrown inside the engine are mapped to csg_status at the C ABI.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define CSG_CUDA(call)                                                      \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      throw ::csg::Error(CSG_ERR_RUNTIME,                                   \
+                         std::string("CUDA: ") + cudaGetErrorString(e_) +   \
+                             " at " __FILE__ ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// Growable device buffer (bytes).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // Ensures capacity; contents are NOT preserved.
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    release();
+    size_t want = b < 256 ? 256 : b;
+    CSG_CUDA(cudaMalloc(&p, want));
+    bytes = want;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Error flags raised by device code (bitwise OR into one u32).
+enum : uint32_t {
+  DEV_ERR_RC_TABLE = 1u << 0,      // check_rc_table invariant (DataError)
+  DEV_ERR_POOL = 1u << 1,          // output pool overflow -> retry bigger
+  DEV_ERR_TOO_MANY_COMPS = 1u << 2,// > kFlowBuf completions of one (rank,op)
+  DEV_ERR_K_TOO_LARGE = 1u << 3,   // consecutive_iterations_k > kMaxK
+  DEV_ERR_DAG_SCRATCH = 1u << 4,   // reachability scratch too small
+  DEV_ERR_SCRATCH = 1u << 5,       // generic scratch overflow -> retry
+};
+
+constexpr int kMaxK = 64;         // consecutive_iterations_k supported
+constexpr int kFlowBuf = 256;     // completions per (rank, op) in a window
+constexpr uint32_t kNoPos = 0xFFFFFFFFu;
+
+// Rank-major, structure-of-arrays view of the store built by the index.
+struct StoreView {
+  uint64_t n = 0;          // records
+  int32_t R = 0;           // rank space [0, R)
+  int32_t nch = 0;         // channel space [0, nch)
+  const uint32_t* rank_off = nullptr;  // [R+1]
+  const uint32_t* perm = nullptr;      // rank-major pos -> store index
+  const double* ts = nullptr;
+  const double* runmax = nullptr;      // per-rank running max of ts
+  const int64_t* op = nullptr;
+  const int32_t* comm = nullptr;
+  const int32_t* chan = nullptr;
+  const uint8_t* ko = nullptr;         // kind | op_name << 1
+  const uint64_t* pa = nullptr;        // start_ms bits | ready | tx << 32
+  const uint64_t* pb = nullptr;        // msg_bytes | done
+};
+
+__host__ __device__ inline int ko_kind(uint8_t ko) { return ko & 1; }
+__host__ __device__ inline int ko_opname(uint8_t ko) { return ko >> 1; }
+
+// Device model tables (topology + program), see csg_model_create.
+struct ModelView {
+  int32_t world_size = 0;
+  int32_t n_groups = 0;
+  int32_t rank_space = 0;          // max(world, max member + 1)
+  const uint8_t* group_kind = nullptr;
+  const uint32_t* member_off = nullptr;  // [G+1]
+  const int32_t* members = nullptr;
+  const uint32_t* member_slot = nullptr; // first-occurrence membership slot
+  const int32_t* comp = nullptr;         // connected component per group
+  const int64_t* group_first_op = nullptr;  // per group; opn when none
+  const uint32_t* rg_off = nullptr;      // rank -> (group, slot) CSR [RS+1]
+  const int32_t* rg_group = nullptr;
+  const uint32_t* rg_slot = nullptr;
+  int32_t opn = 0;
+  const uint8_t* op_name = nullptr;      // [opn]
+  const uint32_t* par_off = nullptr;     // parents per program op [opn+1]
+  const int32_t* par_op = nullptr;
+  const int8_t* par_it = nullptr;        // iteration offset 0 or -1
+  int32_t n_levels = 0;
+  const uint32_t* lvl_off = nullptr;     // [n_levels+1]
+  const int32_t* lvl_ops = nullptr;      // ops ordered by level
+};
+
+// Ordered-key transform for doubles (non-NaN): unsigned compare == double
+// compare except -0 < +0.
+__host__ __device__ inline uint64_t dkey(double d) {
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dkey_inv(uint64_t k) {
+  uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+}
+
+// C++ truncating division, as static_cast<long>(op_seq / opn) in the
+// reference (proj/src/rca.cpp:339, :533, :813, :824).
+__host__ __device__ inline int64_t iter_of(int64_t op, int64_t opn) {
+  return op / opn;
+}
+
+}  // namespace csg

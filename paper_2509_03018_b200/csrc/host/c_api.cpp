@@ -1,0 +1,254 @@
+// c_api.cpp — collsight.h / collsight_b200.h over the B200 engine.
+//
+// Conventions of the reference C API (proj/src/c_api.cpp:27-158): opaque
+// handles, thread-local last-error text, ConfigError -> 2, TraceParseError
+// -> 3, any other failure -> 4, NULL arguments -> 5 before any work.
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "collsight.h"
+#include "collsight_b200.h"
+#include "host.h"
+
+struct collsight_scenario {
+  csh::Scenario cfg;
+};
+
+struct collsight_result {
+  std::string text;
+  std::string summary_json;
+  std::string reports_jsonl;
+  uint64_t triggers = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+collsight_status fail(collsight_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+template <typename Fn>
+collsight_status guarded(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const csh::ConfigError& e) {
+    return fail(COLLSIGHT_ERR_CONFIG, e.what());
+  } catch (const csh::TraceParseError& e) {
+    return fail(COLLSIGHT_ERR_TRACE_PARSE, e.what());
+  } catch (const std::exception& e) {
+    return fail(COLLSIGHT_ERR_RUNTIME, e.what());
+  }
+}
+
+// Engine status -> the same C++ error class the reference would raise.
+void check(csg_status s) {
+  if (s == CSG_OK) return;
+  const std::string msg = csg_last_error();
+  if (s == CSG_ERR_CONFIG) throw csh::ConfigError(msg);
+  throw std::runtime_error(msg);
+}
+
+// One engine context per process (device from COLLSIGHT_B200_DEVICE, else
+// 0); calls through the C API serialize on it.
+std::mutex g_mu;
+csg_ctx* g_ctx = nullptr;
+
+csg_ctx* engine() {
+  if (!g_ctx) {
+    const char* d = std::getenv("COLLSIGHT_B200_DEVICE");
+    check(csg_ctx_create(d ? std::atoi(d) : 0, &g_ctx));
+  }
+  return g_ctx;
+}
+
+struct Engine {
+  csg_store* store = nullptr;
+  csg_model* model = nullptr;
+  csg_results* res = nullptr;
+  ~Engine() {
+    csg_results_free(res);
+    csg_model_free(model);
+    csg_store_free(store);
+  }
+};
+
+collsight_result* analyze_records(const csh::Scenario& cfg,
+                                  const csg_packed_record* recs, size_t n,
+                                  const char* report_out_path) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const csh::Layout layout = cfg.layout();
+  const csh::Program program = cfg.program(layout);
+  const csh::Tables tables(layout, program);
+  csg_ctx* ctx = engine();
+  Engine e;
+  check(csg_store_create(ctx, &e.store));
+  check(csg_store_append(e.store, recs, n));
+  check(csg_model_create(ctx, &tables.topo, &tables.prog, &e.model));
+  check(csg_run_detection(e.store, e.model, &cfg.trigger, &cfg.analysis,
+                          cfg.seed, &e.res, nullptr, 0, nullptr));
+  std::vector<csg_report_view> views(csg_results_count(e.res));
+  for (size_t i = 0; i < views.size(); ++i) check(csg_results_get(e.res, i, &views[i]));
+  auto out = std::make_unique<collsight_result>();
+  out->reports_jsonl = csh::reports_to_jsonl(views, cfg);
+  out->text = csh::reports_to_text(views, cfg) + csh::analyze_summary_text();
+  out->summary_json = csh::analyze_summary_json(views.size());
+  out->triggers = views.size();
+  if (report_out_path) csh::write_file(report_out_path, out->reports_jsonl);
+  return out.release();
+}
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* collsight_version(void) { return "0.1.0"; }
+
+const char* collsight_last_error(void) { return g_last_error.c_str(); }
+
+collsight_status collsight_scenario_load(const char* path,
+                                         collsight_scenario** out) {
+  if (!path || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    *out = new collsight_scenario{csh::load_scenario_file(path)};
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_scenario_parse(const char* json_text,
+                                          collsight_scenario** out) {
+  if (!json_text || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    *out = new collsight_scenario{csh::parse_scenario(json_text)};
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_scenario_set_seed(collsight_scenario* s,
+                                             uint64_t seed) {
+  if (!s) return fail(COLLSIGHT_ERR_ARG, "null scenario");
+  s->cfg.seed = seed;
+  return COLLSIGHT_OK;
+}
+
+void collsight_scenario_free(collsight_scenario* s) { delete s; }
+
+collsight_status collsight_run_simulate(const collsight_scenario* s,
+                                        const char* trace_out_path,
+                                        collsight_result** out) {
+  (void)trace_out_path;
+  if (!s || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return fail(COLLSIGHT_ERR_RUNTIME,
+              "collsight-b200: the trace simulator is not part of this build; "
+              "use collsight_run_analyze on a recorded trace");
+}
+
+collsight_status collsight_run_e2e(const collsight_scenario* s,
+                                   const char* report_out_path,
+                                   collsight_result** out) {
+  (void)report_out_path;
+  if (!s || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return fail(COLLSIGHT_ERR_RUNTIME,
+              "collsight-b200: the trace simulator is not part of this build; "
+              "use collsight_run_analyze on a recorded trace");
+}
+
+collsight_status collsight_run_analyze(const collsight_scenario* s,
+                                       const char* trace_in_path,
+                                       const char* report_out_path,
+                                       collsight_result** out) {
+  if (!s || !trace_in_path || !out)
+    return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const std::vector<csg_packed_record> recs = csh::load_trace_file(trace_in_path);
+    *out = analyze_records(s->cfg, recs.data(), recs.size(), report_out_path);
+    return COLLSIGHT_OK;
+  });
+}
+
+const char* collsight_result_text(const collsight_result* r) {
+  return r ? r->text.c_str() : "";
+}
+const char* collsight_result_summary_json(const collsight_result* r) {
+  return r ? r->summary_json.c_str() : "";
+}
+const char* collsight_result_reports_jsonl(const collsight_result* r) {
+  return r ? r->reports_jsonl.c_str() : "";
+}
+uint64_t collsight_result_trigger_count(const collsight_result* r) {
+  return r ? r->triggers : 0;
+}
+void collsight_result_free(collsight_result* r) { delete r; }
+
+collsight_status collsight_b200_run_analyze_packed(
+    const collsight_scenario* s, const csg_packed_record* records, size_t n,
+    const char* report_out_path, collsight_result** out) {
+  if (!s || (!records && n) || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    *out = analyze_records(s->cfg, records, n, report_out_path);
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_scenario_layout_json(const collsight_scenario* s,
+                                                     char** json_out) {
+  if (!s || !json_out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const csh::Layout l = s->cfg.layout();
+    *json_out = dup(csh::layout_json(l, s->cfg.program(l)));
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_scenario_configs(const collsight_scenario* s,
+                                                 csg_trigger_config* trigger,
+                                                 csg_analysis_config* analysis,
+                                                 uint64_t* seed) {
+  if (!s) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  if (trigger) *trigger = s->cfg.trigger;
+  if (analysis) *analysis = s->cfg.analysis;
+  if (seed) *seed = s->cfg.seed;
+  return COLLSIGHT_OK;
+}
+
+collsight_status collsight_b200_layout_json(int tp, int pp, int dp, int rpn,
+                                            int cpp, int nics,
+                                            uint64_t msg_bytes,
+                                            char** json_out) {
+  if (!json_out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const csh::Layout l = csh::build_layout(tp, pp, dp, rpn, cpp, nics);
+    *json_out = dup(csh::layout_json(l, csh::default_program(l, msg_bytes)));
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_parse_trace(const char* text, size_t len,
+                                            csg_packed_record** out,
+                                            size_t* n) {
+  if ((!text && len) || !out || !n) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const auto v = csh::parse_trace_text(std::string_view(text, len));
+    *n = v.size();
+    *out = static_cast<csg_packed_record*>(
+        std::malloc(sizeof(csg_packed_record) * (v.size() + 1)));
+    if (!v.empty()) std::memcpy(*out, v.data(), v.size() * sizeof(csg_packed_record));
+    return COLLSIGHT_OK;
+  });
+}
+
+void collsight_b200_free(void* p) { std::free(p); }
+
+}  // extern "C"

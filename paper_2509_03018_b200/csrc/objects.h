@@ -1,0 +1,172 @@
+// objects.h — the engine's handle types (behind the opaque C ABI handles).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "engine_internal.h"
+#include "sort.cuh"
+
+struct csg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  double device_ms = 0;
+  csg::LaunchCounter lc;
+  // shared scratch
+  csg::DevBuf scratch_a, scratch_b, scratch_c, pinned_flag_dev;
+  uint32_t* host_flag = nullptr;  // pinned
+
+  // Times an engine phase on the context stream with CUDA events.
+  struct Timed {
+    csg_ctx* c;
+    explicit Timed(csg_ctx* ctx) : c(ctx) {
+      cudaEventRecord(c->ev_start, c->stream);
+    }
+    ~Timed() {
+      cudaEventRecord(c->ev_stop, c->stream);
+      if (cudaEventSynchronize(c->ev_stop) == cudaSuccess) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop);
+        c->device_ms += ms;
+      }
+    }
+  };
+};
+
+struct StoreStats {
+  unsigned long long ts_max_key;  // dkey of max timestamp
+  int min_rank, max_rank;
+  int min_chan, max_chan;
+  long long min_op, max_op;
+  unsigned long long n_nan;
+};
+
+struct csg_store {
+  csg_ctx* ctx = nullptr;
+  csg::DevBuf recs;  // packed AoS in store (emission) order
+  uint64_t n = 0;
+  bool indexed = false;
+  // stats (valid when indexed)
+  double last_ts = 0;  // max(0, max timestamp), runner.cpp:51-56
+  int32_t min_rank = 0, max_rank = -1;
+  int32_t min_chan = 0, max_chan = -1;
+  int64_t min_op = 0, max_op = -1;
+  // rank-major index
+  int32_t R = 0, nch = 0;
+  uint64_t max_seg = 0;  // longest rank segment
+  csg::DevBuf rank_off, perm, keys, ts, runmax, op, comm, chan, ko, pa, pb;
+  csg::SortScratch sort;
+  // op-ordered completion index for the straggler self-evidence pass
+  bool op_indexed = false;
+  uint64_t n_opidx = 0;
+  csg::DevBuf opidx_pos;     // rank-major positions of non-Recv completions,
+                             // ordered by (op_seq, store index)
+  csg::DevBuf opidx_keys;    // u64 op - min_op (sorted)
+  csg::DevBuf opidx_rank;    // rank of each entry
+  csg::DevBuf op_seg_off;    // dense [min_op, max_op+1] -> start in opidx
+  csg::DevBuf stats_dev;
+
+  csg::StoreView view() const {
+    csg::StoreView v;
+    v.n = n;
+    v.R = R;
+    v.nch = nch;
+    v.rank_off = rank_off.as<uint32_t>();
+    v.perm = perm.as<uint32_t>();
+    v.ts = ts.as<double>();
+    v.runmax = runmax.as<double>();
+    v.op = op.as<int64_t>();
+    v.comm = comm.as<int32_t>();
+    v.chan = chan.as<int32_t>();
+    v.ko = ko.as<uint8_t>();
+    v.pa = pa.as<uint64_t>();
+    v.pb = pb.as<uint64_t>();
+    return v;
+  }
+};
+
+struct csg_model {
+  csg_ctx* ctx = nullptr;
+  // host copies
+  int32_t world_size = 0, n_groups = 0, rank_space = 0, opn = 0;
+  std::vector<uint8_t> h_kind;
+  std::vector<uint32_t> h_member_off;
+  std::vector<int32_t> h_members;
+  std::vector<uint32_t> h_member_slot;
+  std::vector<int32_t> h_comp;
+  std::vector<uint32_t> h_rg_off;
+  std::vector<int32_t> h_rg_group;
+  std::vector<uint8_t> h_op_name;
+  int32_t n_levels = 0;
+  // device copies
+  csg::DevBuf group_kind, member_off, members, member_slot, comp,
+      group_first_op, rg_off, rg_group, rg_slot, op_name, par_off, par_op,
+      par_it, lvl_off, lvl_ops;
+  csg::ModelView view() const {
+    csg::ModelView v;
+    v.world_size = world_size;
+    v.n_groups = n_groups;
+    v.rank_space = rank_space;
+    v.group_kind = group_kind.as<uint8_t>();
+    v.member_off = member_off.as<uint32_t>();
+    v.members = members.as<int32_t>();
+    v.member_slot = member_slot.as<uint32_t>();
+    v.comp = comp.as<int32_t>();
+    v.group_first_op = group_first_op.as<int64_t>();
+    v.rg_off = rg_off.as<uint32_t>();
+    v.rg_group = rg_group.as<int32_t>();
+    v.rg_slot = rg_slot.as<uint32_t>();
+    v.opn = opn;
+    v.op_name = op_name.as<uint8_t>();
+    v.par_off = par_off.as<uint32_t>();
+    v.par_op = par_op.as<int32_t>();
+    v.par_it = par_it.as<int8_t>();
+    v.n_levels = n_levels;
+    v.lvl_off = lvl_off.as<uint32_t>();
+    v.lvl_ops = lvl_ops.as<int32_t>();
+    return v;
+  }
+};
+
+// Trigger baselines (proj/include/collsight/trigger.hpp:29-50), one slot per
+// rank id, resident on the device.
+struct TrigSlot {
+  double throughput;
+  double op_interval_ms;
+  int32_t interval_defined;
+  int32_t updates;
+  int32_t had_prev;
+  int32_t pad;
+};
+
+struct csg_trigger_state {
+  csg_ctx* ctx = nullptr;
+  int32_t cap = 0;
+  csg::DevBuf slots;  // TrigSlot[cap], zero = fresh
+  void ensure(int32_t ranks);
+};
+
+struct csg_results {
+  std::vector<csg_report_view> views;
+  std::vector<csg_suspect> suspects;
+  std::vector<csg_evidence> evidence;
+  std::vector<int32_t> affected;
+  // per report: offsets into the vectors above
+  struct Ofs {
+    size_t sus, nsus, exo, nexo, aff, naff, ev, nev;
+  };
+  std::vector<Ofs> ofs;
+  void finalize();
+};
+
+namespace csg {
+
+void store_build_index(csg_store* s);
+void store_build_op_index(csg_store* s, int32_t opn);
+
+// Per-thread error text for csg_last_error.
+void set_error(const std::string& msg);
+
+}  // namespace csg

@@ -1,0 +1,1873 @@
+// rca.cu — Algorithm 2 (dependency-driven root-cause analysis) on the device.
+//
+// Every tripped tick of a detection run is analyzed in one batch. The O(N)
+// work — each rank's store-order prefix at the trip time — is spread over
+// one warp per (trip, rank); the reference does the same scans serially per
+// group member (proj/src/rca.cpp:146-237, :327-349, :702-731). Group
+// reductions, the exoneration sweep and report assembly then run as one
+// thread block per trip over those compact per-rank summaries.
+//
+// Exact-semantics notes:
+//  * prefix = rank-local records before the first ts > t in STORE order,
+//    found by upper_bound on the per-rank running max (store.cu);
+//  * op-DAG reachability (DepIndex::depends_on, rca.cpp:94-139) is answered
+//    with candidate bitsets propagated over the periodic program DAG in
+//    (iteration, level) order, restricted to [min candidate op, max]: every
+//    parent edge points to a smaller global op, so nothing below the smallest
+//    candidate can lead to a candidate;
+//  * greedy exoneration, straggler candidate de-duplication and the
+//    self-evidence filter keep the reference's sequential order.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "rca.cuh"
+#include "rca_table.h"
+
+namespace csg {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kDecideThreads = 256;
+constexpr int kChTbl = 4096;  // max channel id + 1 (store.cu enforces)
+
+__device__ inline double as_double(uint64_t u) {
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+}
+
+// First index in [lo, hi) where the monotone predicate holds, else hi.
+// 32-ary warp search: three probes rounds cover 32k elements.
+template <typename P>
+__device__ uint32_t warp_partition_point(uint32_t lo, uint32_t hi, P pred) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const uint32_t len = hi - lo;
+    const uint32_t step = (len + 31) / 32;
+    uint32_t off = (lane + 1) * step;
+    if (off > len) off = len;
+    const unsigned mm = __ballot_sync(FULL, pred(lo + off - 1));
+    if (!mm) return hi;
+    const int f = __ffs(mm) - 1;
+    uint32_t offf = (f + 1) * step;
+    if (offf > len) offf = len;
+    const uint32_t qf = lo + offf - 1;
+    if (f) {
+      uint32_t offp = f * step;
+      if (offp > len) offp = len;
+      lo = lo + offp;
+    }
+    hi = qf;
+  }
+  const uint32_t q = lo + lane;
+  const unsigned mm = __ballot_sync(FULL, q < hi && pred(q));
+  return mm ? lo + __ffs(mm) - 1 : hi;
+}
+
+// Lower median sorted[(n-1)/2] of n virtual values (warp; O(n^2/32)).
+template <typename V>
+__device__ double warp_lower_median(int n, V val) {
+  const int lane = threadIdx.x & 31;
+  const int k = (n - 1) / 2;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool mine = false;
+    double vi = 0;
+    if (i < n) {
+      vi = val(i);
+      int less = 0, leq = 0;
+      for (int q = 0; q < n; ++q) {
+        const double vq = val(q);
+        less += vq < vi;
+        leq += vq <= vi;
+      }
+      mine = less <= k && k < leq;
+    }
+    const unsigned mm = __ballot_sync(FULL, mine);
+    if (mm) return __shfl_sync(FULL, vi, __ffs(mm) - 1);
+  }
+  return 0;  // unreachable for n >= 1
+}
+
+// ---------------------------------------------------------------------------
+// K1: per (trip, rank) prefix summary.
+// ---------------------------------------------------------------------------
+__global__ void k_rank_summary(StoreView s, int32_t J,
+                               const double* __restrict__ trip_t,
+                               double delta_a, RankSum* __restrict__ out,
+                               uint32_t* __restrict__ chan_pos, int32_t nch) {
+  extern __shared__ uint32_t sm_tbl[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const bool active = w < static_cast<int64_t>(s.R) * J;
+  const int32_t r = active ? static_cast<int32_t>(w / J) : 0;
+  const int32_t j = active ? static_cast<int32_t>(w % J) : 0;
+  uint32_t* tbl = sm_tbl + wib * nch;
+  if (!active) return;
+  for (int c = lane; c < nch; c += 32) tbl[c] = 0;
+  __syncwarp();
+  const double t = trip_t[j];
+  const double ws = t - delta_a;  // window_start, rca.cpp:405
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  const double* rm = s.runmax;
+  const uint32_t cend =
+      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
+  const uint32_t c = cend - b;
+  RankSum o;
+  o.cutoff = c;
+  o.flags = 0;
+  o.last_op = -1;
+  o.last_ts = 0;
+  o.last_chan = -1;
+  o.pad = 0;
+  o.onset = 0;
+  o.ready = o.tx = o.done = 0;
+  if (c > 0) {
+    o.flags |= RS_HAS_LAST;
+    o.last_op = s.op[cend - 1];
+    o.last_ts = s.ts[cend - 1];
+    o.last_chan = s.chan[cend - 1];
+    // stuck_on_incomplete (rca.cpp:216-237): the last prefix record with
+    // ts >= window_start is a state whose op has no prefix completion.
+    int64_t found = -1;
+    for (int64_t top = static_cast<int64_t>(cend) - 1;
+         top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
+      const int64_t p = top - lane;
+      const bool pr = p >= static_cast<int64_t>(b) && s.ts[p] >= ws;
+      const unsigned mm = __ballot_sync(FULL, pr);
+      if (mm) found = top - (__ffs(mm) - 1);
+    }
+    bool cand_stuck = false;
+    int64_t stuck_op = 0;
+    if (found >= 0 && ko_kind(s.ko[found]) == CSG_KIND_STATE) {
+      cand_stuck = true;
+      stuck_op = s.op[found];
+    }
+    const int64_t lop = o.last_op;
+    bool comp_hit = false, onset_found = false;
+    for (uint32_t base = b; base < cend; base += 32) {
+      const uint32_t p = base + lane;
+      const bool valid = p < cend;
+      const int64_t op = valid ? s.op[p] : 0;
+      const uint8_t ko = valid ? s.ko[p] : 0;
+      if (cand_stuck && !comp_hit)
+        comp_hit = __any_sync(FULL, valid && ko_kind(ko) == CSG_KIND_COMPLETION &&
+                                        op == stuck_op);
+      const unsigned mo = __ballot_sync(FULL, valid && op == lop);
+      if (!onset_found && mo) {
+        // stall_onset_of (rca.cpp:202-212): first prefix record of the op
+        o.onset = s.ts[base + __ffs(mo) - 1];
+        onset_found = true;
+      }
+      if (valid && op == lop && ko_kind(ko) == CSG_KIND_STATE)
+        atomicMax(&tbl[s.chan[p]], p + 1);  // latest per channel
+    }
+    __syncwarp();
+    if (cand_stuck && !comp_hit) o.flags |= RS_STUCK;
+    // progress_of(rank, last_op, t) (rca.cpp:167-196): sum over channels.
+    unsigned long long rd = 0, tx = 0, dn = 0;
+    int any = 0;
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint32_t q = tbl[ch];
+      if (q) {
+        any = 1;
+        const uint64_t a = s.pa[q - 1];
+        rd += a & 0xffffffffull;
+        tx += a >> 32;
+        dn += s.pb[q - 1];
+      }
+    }
+#pragma unroll
+    for (int x = 16; x; x >>= 1) {
+      rd += __shfl_xor_sync(FULL, rd, x);
+      tx += __shfl_xor_sync(FULL, tx, x);
+      dn += __shfl_xor_sync(FULL, dn, x);
+      any |= __shfl_xor_sync(FULL, any, x);
+    }
+    if (any) {
+      o.flags |= RS_PROG;
+      o.ready = rd;
+      o.tx = tx;
+      o.done = dn;
+    }
+  }
+  uint32_t* cp = chan_pos + (static_cast<uint64_t>(j) * s.R + r) * nch;
+  for (int ch = lane; ch < nch; ch += 32) cp[ch] = tbl[ch];
+  if (lane == 0) out[static_cast<uint64_t>(j) * s.R + r] = o;
+}
+
+// ---------------------------------------------------------------------------
+// K2: group_iterations (rca.cpp:327-349) for straggler trips: per
+// (trip, member slot, iteration) min start / max end of the member's prefix
+// completions with comm_id == group.
+// ---------------------------------------------------------------------------
+__global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
+                              const int32_t* __restrict__ strag_trip,
+                              const RankSum* __restrict__ rs, int64_t it_min,
+                              int32_t n_it, uint32_t M,
+                              unsigned long long* __restrict__ tbl_s,
+                              unsigned long long* __restrict__ tbl_e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(s.R) * Js) return;
+  const int32_t r = static_cast<int32_t>(w / Js);
+  const int32_t js = static_cast<int32_t>(w % Js);
+  if (r >= m.rank_space) return;
+  const uint32_t g0 = m.rg_off[r], g1 = m.rg_off[r + 1];
+  if (g0 == g1) return;
+  const int32_t j = strag_trip[js];
+  const uint32_t b = s.rank_off[r];
+  const uint32_t cend = b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff;
+  for (uint32_t p = b + lane; p < cend; p += 32) {
+    if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
+    const int32_t cm = s.comm[p];
+    uint32_t slot = kNoPos;
+    for (uint32_t q = g0; q < g1; ++q)
+      if (m.rg_group[q] == cm) {
+        slot = m.rg_slot[q];
+        break;
+      }
+    if (slot == kNoPos) continue;
+    const int64_t it = iter_of(s.op[p], m.opn) - it_min;
+    const uint64_t idx = (static_cast<uint64_t>(js) * M + slot) * n_it + it;
+    atomicMin(&tbl_s[idx], static_cast<unsigned long long>(dkey(as_double(s.pa[p]))));
+    atomicMax(&tbl_e[idx], static_cast<unsigned long long>(dkey(s.ts[p])));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: complete_iterations (rca.cpp:352-372) + group_has_late_member
+// (rca.cpp:374-396), one warp per (straggler trip, group).
+// ---------------------------------------------------------------------------
+__global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
+                              int32_t n_it, uint32_t M, int32_t k,
+                              double thr,
+                              const unsigned long long* __restrict__ tbl_s,
+                              const unsigned long long* __restrict__ tbl_e,
+                              GroupIter* __restrict__ gi,
+                              int64_t* __restrict__ gi_last) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(m.n_groups) * Js) return;
+  const int32_t js = static_cast<int32_t>(w / m.n_groups);
+  const int32_t g = static_cast<int32_t>(w % m.n_groups);
+  const uint32_t mo = m.member_off[g];
+  const int32_t mm = static_cast<int32_t>(m.member_off[g + 1] - mo);
+  GroupIter out{0, 0};
+  int64_t* last = gi_last + (static_cast<uint64_t>(js) * m.n_groups + g) * k;
+  if (mm >= 2 && m.opn > 0) {
+    const uint64_t rowbase = static_cast<uint64_t>(js) * M;
+    int32_t count = 0, got = 0;
+    int64_t latest = 0;
+    for (int64_t top = n_it - 1; top >= 0; top -= 32) {
+      const int64_t it = top - lane;
+      bool present = it >= 0;
+      for (int32_t i = 0; present && i < mm; ++i) {
+        const uint32_t slot = m.member_slot[mo + i];
+        present = tbl_s[(rowbase + slot) * n_it + it] != ~0ull;
+      }
+      unsigned bm = __ballot_sync(FULL, present);
+      if (count == 0 && bm) latest = top - (__ffs(bm) - 1);
+      count += __popc(bm);
+      while (bm && got < k) {
+        const int f = __ffs(bm) - 1;
+        if (lane == 0) last[k - 1 - got] = top - f + it_min;
+        ++got;
+        bm &= bm - 1;
+      }
+    }
+    out.n_common = count;
+    if (count > 0) {
+      // lower medians of starts / ends at the latest common iteration
+      auto sv = [&](int i) {
+        return dkey_inv(tbl_s[(rowbase + m.member_slot[mo + i]) * n_it + latest]);
+      };
+      auto ev = [&](int i) {
+        return dkey_inv(tbl_e[(rowbase + m.member_slot[mo + i]) * n_it + latest]);
+      };
+      const double ms = warp_lower_median(mm, sv);
+      const double me = warp_lower_median(mm, ev);
+      bool late = false;
+      for (int32_t i = lane; i < mm; i += 32)
+        late |= (sv(i) - ms >= thr) || (ev(i) - me >= thr);
+      out.late = __any_sync(FULL, late) ? 1 : 0;
+    }
+  }
+  if (lane == 0) gi[static_cast<uint64_t>(js) * m.n_groups + g] = out;
+}
+
+// ---------------------------------------------------------------------------
+// K4: affected_groups (rca.cpp:400-461), one block per trip. Reachability
+// from the trigger rank's groups is the static group graph's connected
+// component (computed once per model on the host).
+// ---------------------------------------------------------------------------
+__global__ void k_affected(StoreView s, ModelView m, int32_t J,
+                           const int32_t* __restrict__ trip_kind,
+                           const int32_t* __restrict__ trip_rank,
+                           const int32_t* __restrict__ js_of,
+                           const RankSum* __restrict__ rs,
+                           const GroupIter* __restrict__ gi,
+                           int32_t* __restrict__ aff,
+                           uint8_t* __restrict__ aff_flag,
+                           int32_t* __restrict__ n_aff) {
+  __shared__ int32_t comps[64];
+  __shared__ int32_t ncomp;
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t base;
+  const int32_t j = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  if (tid == 0) {
+    ncomp = 0;
+    base = 0;
+    const int32_t sr = trip_rank[j];
+    if (sr >= 0 && sr < m.rank_space) {
+      for (uint32_t q = m.rg_off[sr]; q < m.rg_off[sr + 1]; ++q) {
+        const int32_t cid = m.comp[m.rg_group[q]];
+        bool seen = false;
+        for (int32_t i = 0; i < ncomp; ++i) seen |= comps[i] == cid;
+        if (!seen && ncomp < 64) comps[ncomp++] = cid;
+      }
+    }
+  }
+  __syncthreads();
+  const bool strag = trip_kind[j] == CSG_TRIGGER_STRAGGLER;
+  const int32_t js = js_of[j];
+  for (int32_t g0 = 0; g0 < m.n_groups; g0 += blockDim.x) {
+    const int32_t g = g0 + tid;
+    int hit = 0;
+    if (g < m.n_groups) {
+      bool reach = false;
+      const int32_t cg = m.comp[g];
+      for (int32_t i = 0; i < ncomp; ++i) reach |= comps[i] == cg;
+      if (reach) {
+        bool flag = false;
+        for (uint32_t q = m.member_off[g]; q < m.member_off[g + 1] && !flag; ++q) {
+          const int32_t r = m.members[q];
+          if (r >= 0 && r < s.R &&
+              (rs[static_cast<uint64_t>(j) * s.R + r].flags & RS_STUCK))
+            flag = true;
+        }
+        if (!flag && strag && js >= 0 &&
+            gi[static_cast<uint64_t>(js) * m.n_groups + g].late)
+          flag = true;
+        hit = flag ? 1 : 0;
+      }
+      aff_flag[static_cast<uint64_t>(j) * m.n_groups + g] = static_cast<uint8_t>(hit);
+    }
+    int x = hit;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    if (hit)
+      aff[static_cast<uint64_t>(j) * m.n_groups + base + (warp ? wsum[warp - 1] : 0) +
+          x - 1] = g;
+    __syncthreads();
+    if (tid == 0) base += wsum[nwarps - 1];
+    __syncthreads();
+  }
+  if (tid == 0) n_aff[j] = base;
+}
+
+// ---------------------------------------------------------------------------
+// K5: straggler flow rules (rca.cpp:702-786) per (straggler trip, member of
+// an affected group with enough history): the first op (ascending) with a
+// skewed window flow, and the first op with an incomplete window flow.
+// ---------------------------------------------------------------------------
+__global__ void k_flow(StoreView s, ModelView m, int32_t Js,
+                       const int32_t* __restrict__ strag_trip,
+                       const double* __restrict__ trip_t, double delta_a,
+                       double skew, int32_t k, uint32_t M,
+                       const uint32_t* __restrict__ slot_group,
+                       const RankSum* __restrict__ rs,
+                       const GroupIter* __restrict__ gi,
+                       const uint8_t* __restrict__ aff_flag,
+                       FlowSum* __restrict__ fs, uint32_t* __restrict__ err) {
+  constexpr int kWarps = 4;
+  __shared__ uint32_t buf[kWarps][kFlowBuf];
+  __shared__ uint32_t sbits[kWarps][kChTbl / 32];
+  __shared__ uint32_t cbits[kWarps][kChTbl / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(M) * Js) return;
+  const int32_t js = static_cast<int32_t>(w / M);
+  const uint32_t slot = static_cast<uint32_t>(w % M);
+  const int32_t g = static_cast<int32_t>(slot_group[slot]);
+  const int32_t j = strag_trip[js];
+  FlowSum out;
+  memset(&out, 0, sizeof(out));
+  const uint64_t gidx = static_cast<uint64_t>(js) * m.n_groups + g;
+  const bool run = aff_flag[static_cast<uint64_t>(j) * m.n_groups + g] &&
+                   m.member_off[g + 1] - m.member_off[g] >= 2 &&
+                   gi[gidx].n_common >= k && m.member_slot[slot] == slot;
+  const int32_t r = m.members[slot];
+  if (!run || r < 0 || r >= s.R) {
+    if (lane == 0) fs[static_cast<uint64_t>(js) * M + slot] = out;
+    return;
+  }
+  const double t = trip_t[j];
+  const double ws = t - delta_a;
+  const uint32_t b = s.rank_off[r];
+  const uint32_t e = b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff;
+  const double* rm = s.runmax;
+  // records before p0 all have ts < ws (running max below ws)
+  const uint32_t p0 =
+      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] >= ws; });
+  auto win_comp = [&](uint32_t p) {
+    const uint8_t ko = s.ko[p];
+    return ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV &&
+           s.comm[p] == g && s.ts[p] >= ws;
+  };
+  auto win_state = [&](uint32_t p) {
+    const uint8_t ko = s.ko[p];
+    if (ko_kind(ko) != CSG_KIND_STATE || s.comm[p] != g || s.ts[p] < ws)
+      return false;
+    const uint64_t pi = static_cast<uint64_t>(s.op[p]) % static_cast<uint64_t>(m.opn);
+    return m.op_name[pi] != CSG_OP_RECV;
+  };
+  // (a) FlowSkewed: ops ascending
+  {
+    bool have_prev = false;
+    int64_t prev = 0;
+    for (;;) {
+      long long cur = LLONG_MAX;
+      for (uint32_t p = p0 + lane; p < e; p += 32)
+        if (win_comp(p)) {
+          const int64_t op = s.op[p];
+          if ((!have_prev || op > prev) && op < cur) cur = op;
+        }
+#pragma unroll
+      for (int x = 16; x; x >>= 1) cur = min(cur, __shfl_xor_sync(FULL, cur, x));
+      if (cur == LLONG_MAX) break;
+      int n = 0;
+      for (uint32_t base = p0; base < e; base += 32) {
+        const uint32_t p = base + lane;
+        const bool pr = p < e && win_comp(p) && s.op[p] == cur;
+        const unsigned mm = __ballot_sync(FULL, pr);
+        if (pr) {
+          const int idx = n + __popc(mm & ((1u << lane) - 1u));
+          if (idx < kFlowBuf) buf[wib][idx] = p;
+        }
+        n += __popc(mm);
+      }
+      __syncwarp();
+      if (n > kFlowBuf) {
+        if (lane == 0) atomicOr(err, DEV_ERR_TOO_MANY_COMPS);
+        break;
+      }
+      if (n >= 2) {
+        auto dur = [&](int i) {
+          const uint32_t p = buf[wib][i];
+          return s.ts[p] - as_double(s.pa[p]);
+        };
+        const double med = warp_lower_median(n, dur);
+        int hit = -1;
+        if (med > 0) {
+          const double lim = __dmul_rn(skew, med);
+          for (int base = 0; base < n && hit < 0; base += 32) {
+            const int i = base + lane;
+            const unsigned mm = __ballot_sync(FULL, i < n && dur(i) > lim);
+            if (mm) hit = base + __ffs(mm) - 1;
+          }
+        }
+        if (hit >= 0) {
+          const uint32_t p = buf[wib][hit];
+          out.flags |= 1;
+          out.skew_op = cur;
+          out.skew_chan = s.chan[p];
+          out.skew_start = as_double(s.pa[p]);
+          out.skew_end = s.ts[p];
+          break;
+        }
+      }
+      __syncwarp();
+      have_prev = true;
+      prev = cur;
+    }
+  }
+  // (b) FlowIncomplete: window state ops ascending
+  {
+    const int words = (s.nch + 31) / 32;
+    bool have_prev = false;
+    int64_t prev = 0;
+    for (;;) {
+      long long cur = LLONG_MAX;
+      for (uint32_t p = p0 + lane; p < e; p += 32)
+        if (win_state(p)) {
+          const int64_t op = s.op[p];
+          if ((!have_prev || op > prev) && op < cur) cur = op;
+        }
+#pragma unroll
+      for (int x = 16; x; x >>= 1) cur = min(cur, __shfl_xor_sync(FULL, cur, x));
+      if (cur == LLONG_MAX) break;
+      for (int q = lane; q < words; q += 32) {
+        sbits[wib][q] = 0;
+        cbits[wib][q] = 0;
+      }
+      __syncwarp();
+      for (uint32_t p = p0 + lane; p < e; p += 32)
+        if (win_state(p) && s.op[p] == cur) {
+          const int32_t ch = s.chan[p];
+          atomicOr(&sbits[wib][ch >> 5], 1u << (ch & 31));
+        }
+      // completed_channels: every prefix completion of the group (not just
+      // the window), Recv completions excluded (rca.cpp:718,724).
+      for (uint32_t p = b + lane; p < e; p += 32) {
+        const uint8_t ko = s.ko[p];
+        if (ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV &&
+            s.comm[p] == g && s.op[p] == cur) {
+          const int32_t ch = s.chan[p];
+          atomicOr(&cbits[wib][ch >> 5], 1u << (ch & 31));
+        }
+      }
+      __syncwarp();
+      bool any = false;
+      int first = -1;
+      for (int q = 0; q < words; ++q) {
+        const uint32_t sb = sbits[wib][q], cb = cbits[wib][q];
+        any |= (sb & cb) != 0;
+        if (first < 0 && (sb & ~cb)) first = q * 32 + __ffs(sb & ~cb) - 1;
+      }
+      if (any && first >= 0) {
+        out.flags |= 2;
+        out.inc_op = cur;
+        out.inc_chan = first;
+        break;
+      }
+      __syncwarp();
+      have_prev = true;
+      prev = cur;
+    }
+  }
+  if (lane == 0) fs[static_cast<uint64_t>(js) * M + slot] = out;
+}
+
+// ---------------------------------------------------------------------------
+// K6: per-trip decision (one block per trip).
+// ---------------------------------------------------------------------------
+struct DecideArgs {
+  StoreView s;
+  ModelView m;
+  int32_t J;
+  const double* trip_t;
+  const int32_t* trip_kind;
+  const int32_t* trip_rank;
+  const int32_t* js_of;
+  const RankSum* rs;
+  const uint32_t* chan_pos;
+  int32_t nch;
+  const int32_t* aff;
+  const int32_t* n_aff;
+  const GroupIter* gi;
+  const int64_t* gi_last;
+  int32_t k;
+  const FlowSum* fs;
+  const unsigned long long* tbl_s;
+  const unsigned long long* tbl_e;
+  int64_t it_min;
+  int32_t n_it;
+  uint32_t M;
+  double delta_a, thr, skew;
+  uint64_t N;
+  const uint64_t* opk;
+  const uint32_t* opp;
+  const int32_t* oprank;
+  uint64_t n_opidx;
+  int64_t min_op;
+  uint32_t scratch_per_trip;  // u32 words
+  Pools pools;
+  TripOut* out;
+  uint32_t* err;
+};
+
+enum { P_CAND = 0, P_CEV = 1, P_SUS = 2, P_EV = 3, P_BITS = 4 };
+
+struct BlockShared {
+  int abort;
+  int32_t ncand;
+  uint32_t cev_used;
+  int32_t nret;
+  int32_t nexo;
+  int32_t nsus;
+  uint32_t nev;
+  unsigned long long cand_base, cev_base, sus_base, exo_base, ev_base,
+      bits_base;
+  unsigned long long cap_cand, cap_cev;
+  int64_t i64a, i64b;
+  int32_t i32a, i32b, i32c;
+  uint64_t u64a, u64b, u64c;
+  double med_s[kMaxK], med_e[kMaxK];
+  int64_t win[kMaxK];
+  int32_t red_i[32];
+  long long red_l[32];
+  unsigned long long red_u[3][32];
+  uint32_t chtbl[kChTbl];
+  uint32_t hist[256];
+};
+
+__device__ unsigned long long pool_alloc(unsigned long long* used, int which,
+                                         unsigned long long n,
+                                         unsigned long long cap, uint32_t* err,
+                                         uint32_t flag, bool* ok) {
+  const unsigned long long b = atomicAdd(&used[which], n);
+  *ok = b + n <= cap;
+  if (!*ok) atomicOr(err, flag);
+  return b;
+}
+
+__device__ int block_sum_i(int v, BlockShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  __syncthreads();
+  if (lane == 0) sh.red_i[warp] = v;
+  __syncthreads();
+  int t = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh.red_i[i];
+  __syncthreads();
+  return t;
+}
+
+__device__ long long block_min_l(long long v, BlockShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+  __syncthreads();
+  if (lane == 0) sh.red_l[warp] = v;
+  __syncthreads();
+  long long t = LLONG_MAX;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = min(t, sh.red_l[i]);
+  __syncthreads();
+  return t;
+}
+
+// Lexicographic minimum of (done, tx, ready) over the block.
+__device__ void block_min_prog(uint64_t& d, uint64_t& t, uint64_t& r,
+                               BlockShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t d2 = __shfl_xor_sync(FULL, d, o);
+    const uint64_t t2 = __shfl_xor_sync(FULL, t, o);
+    const uint64_t r2 = __shfl_xor_sync(FULL, r, o);
+    if (prog_less(d2, t2, r2, d, t, r)) {
+      d = d2;
+      t = t2;
+      r = r2;
+    }
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sh.red_u[0][warp] = d;
+    sh.red_u[1][warp] = t;
+    sh.red_u[2][warp] = r;
+  }
+  __syncthreads();
+  d = sh.red_u[0][0];
+  t = sh.red_u[1][0];
+  r = sh.red_u[2][0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+    if (prog_less(sh.red_u[0][i], sh.red_u[1][i], sh.red_u[2][i], d, t, r)) {
+      d = sh.red_u[0][i];
+      t = sh.red_u[1][i];
+      r = sh.red_u[2][i];
+    }
+  __syncthreads();
+}
+
+// Stable order-preserving compaction of pred over [0, n) into dst (block).
+template <typename P>
+__device__ int block_compact(int n, P pred, uint32_t* dst, BlockShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  int base = 0;
+  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const int hit = (i < n && pred(i)) ? 1 : 0;
+    const unsigned mm = __ballot_sync(FULL, hit);
+    __syncthreads();
+    if (lane == 0) sh.red_i[warp] = __popc(mm);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int q = 0; q < nw; ++q) {
+      if (q < warp) before += sh.red_i[q];
+      total += sh.red_i[q];
+    }
+    if (hit) dst[base + before + __popc(mm & ((1u << lane) - 1u))] = i;
+    base += total;
+  }
+  __syncthreads();
+  return base;
+}
+
+// Stable placement sort of n items by a strict-weak "less(a, b)" on item
+// indices: out[pos(i)] = in[i] where pos = #less + #equal-before.
+template <typename L>
+__device__ void block_stable_sort(int n, const uint32_t* in, uint32_t* out,
+                                  L less) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int pos = 0;
+    const uint32_t a = in[i];
+    for (int q = 0; q < n; ++q) {
+      const uint32_t b = in[q];
+      if (less(b, a) || (q < i && !less(a, b))) ++pos;
+    }
+    out[pos] = a;
+  }
+  __syncthreads();
+}
+
+// k-th smallest of a virtual list (radix select on ordered double keys).
+// get(i, &key) returns false for excluded items.
+template <typename G>
+__device__ double block_select(uint64_t n, uint64_t kth, G get,
+                               BlockShared& sh) {
+  uint64_t prefix = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.hist[i] = 0;
+    __syncthreads();
+    const uint64_t mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      uint64_t key;
+      if (!get(i, &key)) continue;
+      if ((key & mask) != (prefix & mask)) continue;
+      atomicAdd(&sh.hist[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t acc = 0;
+      int bsel = 255;
+      for (int bk = 0; bk < 256; ++bk) {
+        if (acc + sh.hist[bk] > kth) {
+          bsel = bk;
+          break;
+        }
+        acc += sh.hist[bk];
+      }
+      sh.u64a = prefix | (static_cast<uint64_t>(bsel) << shift);
+      sh.u64b = kth - acc;
+    }
+    __syncthreads();
+    prefix = sh.u64a;
+    kth = sh.u64b;
+    __syncthreads();
+  }
+  return dkey_inv(prefix);
+}
+
+// progress_of(rank, op, t) by a block scan of the rank's prefix
+// (rca.cpp:167-196); fills sh.chtbl with latest position + 1 per channel.
+__device__ void block_progress_scan(const DecideArgs& a, int32_t r,
+                                    uint32_t cutoff, int64_t op,
+                                    BlockShared& sh) {
+  for (int c = threadIdx.x; c < a.nch; c += blockDim.x) sh.chtbl[c] = 0;
+  __syncthreads();
+  const uint32_t b = a.s.rank_off[r];
+  for (uint32_t p = b + threadIdx.x; p < b + cutoff; p += blockDim.x)
+    if (a.s.op[p] == op && ko_kind(a.s.ko[p]) == CSG_KIND_STATE)
+      atomicMax(&sh.chtbl[a.s.chan[p]], p + 1);
+  __syncthreads();
+}
+
+__device__ void write_trip(const DecideArgs& a, int32_t j, int verdict,
+                           int32_t naff, uint64_t scanned, BlockShared& sh) {
+  if (threadIdx.x == 0) {
+    TripOut o;
+    o.verdict = verdict;
+    o.n_aff = naff;
+    o.scanned = scanned;
+    o.sus_off = static_cast<uint32_t>(sh.sus_base);
+    o.n_sus = sh.nsus;
+    o.exo_off = static_cast<uint32_t>(sh.exo_base);
+    o.n_exo = sh.nexo;
+    o.ev_off = static_cast<uint32_t>(sh.ev_base);
+    o.n_ev = sh.nev;
+    a.out[j] = o;
+  }
+}
+
+__device__ csg_suspect to_suspect(const Cand& c) {
+  csg_suspect s;
+  s.rank = c.rank;
+  s.category = c.cat;
+  s.side = c.side;
+  s.reserved = 0;
+  s.group = c.group;
+  s.reserved2 = 0;
+  s.stuck_op = c.op;
+  s.onset_ms = c.onset;
+  return s;
+}
+
+// Appends one evidence ref to the current candidate (thread 0 only).
+__device__ void add_cev(const DecideArgs& a, BlockShared& sh, Cand& c,
+                        int32_t rank, int32_t ch, double tms, int64_t op) {
+  if (sh.cev_used >= sh.cap_cev) {
+    atomicOr(a.err, DEV_ERR_POOL);
+    sh.abort = 1;
+    return;
+  }
+  csg_evidence e;
+  e.rank = rank;
+  e.channel = ch;
+  e.time_ms = tms;
+  e.op_seq = op;
+  a.pools.cev[sh.cev_base + sh.cev_used] = e;
+  ++sh.cev_used;
+  ++c.ev_n;
+}
+
+__device__ void push_cand(const DecideArgs& a, BlockShared& sh, const Cand& c) {
+  if (sh.ncand >= static_cast<int32_t>(sh.cap_cand)) {
+    atomicOr(a.err, DEV_ERR_POOL);
+    sh.abort = 1;
+    return;
+  }
+  a.pools.cand[sh.cand_base + sh.ncand] = c;
+  ++sh.ncand;
+}
+
+// Evidence refs of a per-channel table (ascending channel), thread 0.
+__device__ void add_table_evidence(const DecideArgs& a, BlockShared& sh,
+                                   Cand& c, int32_t rank,
+                                   const uint32_t* tbl) {
+  for (int ch = 0; ch < a.nch; ++ch) {
+    const uint32_t q = tbl[ch];
+    if (q) add_cev(a, sh, c, rank, ch, a.s.ts[q - 1], a.s.op[q - 1]);
+  }
+}
+
+// Final assembly shared by both analyzers: given candidates (in append
+// order) and a keep mask / exoneration decisions already made by the
+// caller in sorted order (ord/keep), emit exonerated + de-duplicated
+// suspects (first per rank wins, evidence in candidate order) and sort the
+// suspects by rank (stable).
+__device__ void emit_reports(const DecideArgs& a, BlockShared& sh,
+                             const uint32_t* ord, const uint8_t* keep, int C,
+                             uint32_t* scratch) {
+  const Cand* cands = a.pools.cand + sh.cand_base;
+  // first-retained-per-rank flags
+  uint8_t* first = reinterpret_cast<uint8_t*>(scratch);
+  for (int x = threadIdx.x; x < C; x += blockDim.x) {
+    uint8_t f = 0;
+    if (keep[x]) {
+      f = 1;
+      const int32_t r = cands[ord[x]].rank;
+      for (int y = 0; y < x; ++y)
+        if (keep[y] && cands[ord[y]].rank == r) {
+          f = 0;
+          break;
+        }
+    }
+    first[x] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nsus = 0, nexo = 0;
+    uint32_t nev = 0;
+    for (int x = 0; x < C; ++x) {
+      const Cand& c = cands[ord[x]];
+      if (!keep[x]) {
+        a.pools.sus[sh.exo_base + nexo++] = to_suspect(c);
+      } else if (first[x]) {
+        a.pools.sus[sh.sus_base + nsus++] = to_suspect(c);
+        for (uint32_t q = 0; q < c.ev_n; ++q)
+          a.pools.ev[sh.ev_base + nev++] = a.pools.cev[sh.cev_base + c.ev_off + q];
+      }
+    }
+    sh.nsus = nsus;
+    sh.nexo = nexo;
+    sh.nev = nev;
+  }
+  __syncthreads();
+  // stable sort suspects by rank
+  csg_suspect* sus = a.pools.sus + sh.sus_base;
+  const int ns = sh.nsus;
+  uint32_t* idx = scratch;
+  uint32_t* srt = scratch + ns;
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) idx[i] = i;
+  __syncthreads();
+  block_stable_sort(ns, idx, srt, [&](uint32_t x, uint32_t y) {
+    return sus[x].rank < sus[y].rank;
+  });
+  csg_suspect* tmp = a.pools.sus + sh.exo_base + sh.nexo;  // spare room
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) tmp[i] = sus[srt[i]];
+  __syncthreads();
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) sus[i] = tmp[i];
+  __syncthreads();
+}
+
+// ---- failure ---------------------------------------------------------------
+
+__device__ void decide_failure(const DecideArgs& a, int32_t j, BlockShared& sh,
+                               uint32_t* scratch) {
+  const int32_t naff = a.n_aff[j];
+  const int32_t* aff = a.aff + static_cast<uint64_t>(j) * a.m.n_groups;
+  const RankSum* rs = a.rs + static_cast<uint64_t>(j) * a.s.R;
+  const int32_t R = a.s.R;
+  // capacities: Σ members of the affected groups
+  int tot = 0;
+  for (int32_t i = threadIdx.x; i < naff; i += blockDim.x) {
+    const int32_t g = aff[i];
+    tot += static_cast<int>(a.m.member_off[g + 1] - a.m.member_off[g]);
+  }
+  tot = block_sum_i(tot, sh);
+  if (threadIdx.x == 0) {
+    bool ok1, ok2, ok3, ok4;
+    sh.cap_cand = tot;
+    sh.cap_cev = static_cast<unsigned long long>(tot) * (2 * a.nch + 1);
+    sh.cand_base = pool_alloc(a.pools.used, P_CAND, sh.cap_cand,
+                              a.pools.cand_cap, a.err, DEV_ERR_POOL, &ok1);
+    sh.cev_base = pool_alloc(a.pools.used, P_CEV, sh.cap_cev, a.pools.cev_cap,
+                             a.err, DEV_ERR_POOL, &ok2);
+    sh.sus_base = pool_alloc(a.pools.used, P_SUS, 3ull * tot, a.pools.sus_cap,
+                             a.err, DEV_ERR_POOL, &ok3);
+    sh.exo_base = sh.sus_base + tot;
+    sh.ev_base = pool_alloc(a.pools.used, P_EV, sh.cap_cev, a.pools.ev_cap,
+                            a.err, DEV_ERR_POOL, &ok4);
+    sh.abort = !(ok1 && ok2 && ok3 && ok4);
+    sh.ncand = 0;
+    sh.cev_used = 0;
+  }
+  __syncthreads();
+  if (sh.abort) return;
+  uint32_t* lst = scratch;                 // member indices
+  uint32_t* lst2 = scratch + a.scratch_per_trip / 4;
+  for (int32_t ai = 0; ai < naff; ++ai) {
+    const int32_t g = aff[ai];
+    const uint32_t mo = a.m.member_off[g];
+    const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
+    // last_logs_of_group + check_min_op (rca.cpp:562-571, :249-261)
+    int nlog = 0;
+    long long mn = LLONG_MAX;
+    for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const int32_t r = a.m.members[mo + i];
+      if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST)) {
+        ++nlog;
+        mn = min(mn, static_cast<long long>(rs[r].last_op));
+      }
+    }
+    nlog = block_sum_i(nlog, sh);
+    if (nlog == 0) continue;
+    mn = block_min_l(mn, sh);
+    int neq = 0;
+    for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const int32_t r = a.m.members[mo + i];
+      if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) && rs[r].last_op == mn)
+        ++neq;
+    }
+    neq = block_sum_i(neq, sh);
+    int ns;
+    if (neq < nlog) {
+      ns = block_compact(m, [&](int i) {
+        const int32_t r = a.m.members[mo + i];
+        return r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
+               rs[r].last_op == mn;
+      }, lst, sh);
+    } else {
+      // check_min_data over members with progress (rca.cpp:573-580)
+      int nk = 0;
+      uint64_t d = ~0ull, tx = ~0ull, rd = ~0ull;
+      for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const int32_t r = a.m.members[mo + i];
+        if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
+            (rs[r].flags & RS_PROG)) {
+          ++nk;
+          if (prog_less(rs[r].done, rs[r].tx, rs[r].ready, d, tx, rd)) {
+            d = rs[r].done;
+            tx = rs[r].tx;
+            rd = rs[r].ready;
+          }
+        }
+      }
+      nk = block_sum_i(nk, sh);
+      if (nk == 0) continue;
+      block_min_prog(d, tx, rd, sh);
+      ns = block_compact(m, [&](int i) {
+        const int32_t r = a.m.members[mo + i];
+        return r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
+               (rs[r].flags & RS_PROG) && rs[r].done == d && rs[r].tx == tx &&
+               rs[r].ready == rd;
+      }, lst, sh);
+    }
+    // suspects sorted by rank
+    block_stable_sort(ns, lst, lst2, [&](uint32_t x, uint32_t y) {
+      return a.m.members[mo + x] < a.m.members[mo + y];
+    });
+    for (int q = 0; q < ns; ++q) {
+      const uint32_t mi = lst2[q];
+      const int32_t r = a.m.members[mo + mi];
+      const RankSum own = rs[r];
+      const int64_t op = own.last_op;
+      // ring successor (rca.cpp:598-605): members[(pos+1) % n], pos = first
+      // occurrence (members are unique, so pos == mi)
+      int32_t succ = -1;
+      if (m >= 2) succ = a.m.members[mo + (mi + 1) % m];
+      bool peer_known = false;
+      uint64_t prd = 0, ptx = 0, pdn = 0;
+      const uint32_t* peer_tbl = nullptr;
+      if (succ >= 0 && succ < R) {
+        const RankSum sr = rs[succ];
+        if ((sr.flags & RS_HAS_LAST) && sr.last_op == op) {
+          peer_known = (sr.flags & RS_PROG) != 0;
+          prd = sr.ready;
+          ptx = sr.tx;
+          pdn = sr.done;
+          peer_tbl = a.chan_pos + (static_cast<uint64_t>(j) * R + succ) * a.nch;
+        } else {
+          block_progress_scan(a, succ, sr.cutoff, op, sh);
+          for (int c = 0; c < a.nch; ++c) {
+            const uint32_t pq = sh.chtbl[c];
+            if (pq) {
+              peer_known = true;
+              const uint64_t pa = a.s.pa[pq - 1];
+              prd += pa & 0xffffffffull;
+              ptx += pa >> 32;
+              pdn += a.s.pb[pq - 1];
+            }
+          }
+          peer_tbl = sh.chtbl;
+        }
+      }
+      if (threadIdx.x == 0) {
+        Cand c;
+        memset(&c, 0, sizeof(c));
+        c.rank = r;
+        c.group = g;
+        c.op = op;
+        c.onset = own.onset;
+        c.known = (own.flags & RS_PROG) ? 1 : 0;
+        c.ready = own.ready;
+        c.tx = own.tx;
+        c.done = own.done;
+        c.it_lo = 0;
+        c.it_hi = -1;
+        c.ev_off = sh.cev_used;
+        c.ev_n = 0;
+        if (c.known)
+          add_table_evidence(a, sh, c, r,
+                             a.chan_pos + (static_cast<uint64_t>(j) * R + r) * a.nch);
+        if (peer_known) add_table_evidence(a, sh, c, succ, peer_tbl);
+        if (c.known) {
+          int cat, side;
+          if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat,
+                        &side)) {
+            atomicOr(a.err, DEV_ERR_RC_TABLE);
+            sh.abort = 1;
+          }
+          c.cat = static_cast<uint8_t>(cat);
+          c.side = static_cast<uint8_t>(side);
+        } else {
+          c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
+          c.side = CSG_SIDE_UNDETERMINED;
+        }
+        if (c.ev_n == 0) add_cev(a, sh, c, r, own.last_chan, own.last_ts, op);
+        push_cand(a, sh, c);
+      }
+      __syncthreads();
+      if (sh.abort) return;
+    }
+  }
+  // ---- exonerate (rca.cpp:479-526) ----
+  const int C = sh.ncand;
+  const Cand* cands = a.pools.cand + sh.cand_base;
+  uint32_t* idx = scratch;
+  uint32_t* ord = scratch + C;
+  int64_t* U = reinterpret_cast<int64_t*>(scratch + 2 * C + (C & 1));
+  uint32_t* ret = reinterpret_cast<uint32_t*>(U + C);
+  uint8_t* keep = reinterpret_cast<uint8_t*>(ret + C);
+  uint32_t* tail = reinterpret_cast<uint32_t*>(keep + ((C + 3) & ~3));
+  for (int i = threadIdx.x; i < C; i += blockDim.x) idx[i] = i;
+  __syncthreads();
+  block_stable_sort(C, idx, ord, [&](uint32_t x, uint32_t y) {
+    if (cands[x].op != cands[y].op) return cands[x].op < cands[y].op;
+    return cands[x].rank < cands[y].rank;
+  });
+  // distinct valid (>= 0) candidate ops, ascending
+  if (threadIdx.x == 0) {
+    int K = 0;
+    for (int x = 0; x < C; ++x) {
+      const int64_t op = cands[ord[x]].op;
+      if (op >= 0 && (K == 0 || U[K - 1] != op)) U[K++] = op;
+    }
+    sh.i32a = K;
+  }
+  __syncthreads();
+  const int K = sh.i32a;
+  const int words = (K + 63) / 64;
+  int64_t lo = 0, hi = -1;
+  unsigned long long* bits = nullptr;
+  const int32_t opn = a.m.opn;
+  if (K >= 2) {
+    lo = U[0];
+    hi = U[K - 1];
+    const unsigned long long V = static_cast<unsigned long long>(hi - lo + 1);
+    if (threadIdx.x == 0) {
+      bool ok;
+      sh.bits_base = pool_alloc(a.pools.used, P_BITS, V * words, a.pools.bits_cap,
+                                a.err, DEV_ERR_DAG_SCRATCH, &ok);
+      if (!ok) sh.abort = 1;
+    }
+    __syncthreads();
+    if (sh.abort) return;
+    bits = a.pools.bits + sh.bits_base;
+    for (unsigned long long i = threadIdx.x; i < V * words; i += blockDim.x)
+      bits[i] = 0;
+    __syncthreads();
+    for (int64_t it = lo / opn; it <= hi / opn; ++it) {
+      for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
+        const uint32_t l0 = a.m.lvl_off[lv];
+        const uint32_t nl = a.m.lvl_off[lv + 1] - l0;
+        for (uint32_t q = threadIdx.x; q < nl * words; q += blockDim.x) {
+          const int32_t sop = a.m.lvl_ops[l0 + q / words];
+          const int w = q % words;
+          const int64_t v = it * opn + sop;
+          if (v < lo || v > hi) continue;
+          unsigned long long acc = 0;
+          for (uint32_t pe = a.m.par_off[sop]; pe < a.m.par_off[sop + 1]; ++pe) {
+            const int64_t pit = it + a.m.par_it[pe];
+            if (pit < 0) continue;
+            const int64_t pv = pit * opn + a.m.par_op[pe];
+            if (pv < lo) continue;
+            acc |= bits[(pv - lo) * words + w];
+            // pv itself a candidate op?
+            int l = 0, h = K;
+            while (l < h) {
+              const int md = (l + h) >> 1;
+              if (U[md] < pv) l = md + 1; else h = md;
+            }
+            if (l < K && U[l] == pv && (l >> 6) == w) acc |= 1ull << (l & 63);
+          }
+          bits[(v - lo) * words + w] = acc;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // greedy pass
+  if (threadIdx.x == 0) sh.nret = 0;
+  __syncthreads();
+  for (int x = 0; x < C; ++x) {
+    const Cand& c = cands[ord[x]];
+    bool drop = false;
+    for (int q = threadIdx.x; q < sh.nret; q += blockDim.x) {
+      const Cand& u = cands[ret[q]];
+      if (u.rank == c.rank) continue;
+      bool path;
+      if (u.op == c.op) {
+        path = u.known && c.known &&
+               prog_less(u.done, u.tx, u.ready, c.done, c.tx, c.ready);
+      } else if (c.op < 0 || u.op < 0 || K < 2) {
+        path = false;
+      } else {
+        int l = 0, h = K;
+        while (l < h) {
+          const int md = (l + h) >> 1;
+          if (U[md] < u.op) l = md + 1; else h = md;
+        }
+        path = (bits[(c.op - lo) * words + (l >> 6)] >> (l & 63)) & 1ull;
+      }
+      drop |= path;
+    }
+    drop = __syncthreads_or(drop);
+    if (threadIdx.x == 0) {
+      keep[x] = drop ? 0 : 1;
+      if (!drop) ret[sh.nret++] = ord[x];
+    }
+    __syncthreads();
+  }
+  emit_reports(a, sh, ord, keep, C, tail);
+  write_trip(a, j, sh.nsus ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED,
+             naff, 2 * a.N, sh);
+}
+
+// ---- straggler -------------------------------------------------------------
+
+// self_faulted (rca.cpp:821-848) for one lateness candidate.
+__device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
+                             BlockShared& sh, uint32_t* lst) {
+  const double t = a.trip_t[j];
+  const int32_t r = c.rank;
+  const int32_t opn = a.m.opn;
+  if (r < 0 || r >= a.s.R) return false;
+  const uint32_t b = a.s.rank_off[r], e = a.s.rank_off[r + 1];
+  // the rank's qualifying completions (FILTER ts <= t, not Recv, iteration
+  // within [iter_lo, iter_hi])
+  const int n = block_compact(static_cast<int>(e - b), [&](int i) {
+    const uint32_t p = b + i;
+    const uint8_t ko = a.s.ko[p];
+    if (ko_kind(ko) != CSG_KIND_COMPLETION || ko_opname(ko) == CSG_OP_RECV)
+      return false;
+    if (a.s.ts[p] > t) return false;
+    const int64_t it = iter_of(a.s.op[p], opn);
+    return it >= c.it_lo && it <= c.it_hi;
+  }, lst, sh);
+  for (int x = 0; x < n; ++x) {
+    const int64_t o = a.s.op[b + lst[x]];
+    bool dup = false;
+    for (int y = threadIdx.x; y < x; y += blockDim.x)
+      dup |= a.s.op[b + lst[y]] == o;
+    if (__syncthreads_or(dup)) continue;
+    // max of my durations for op o
+    double mine = -INFINITY;
+    for (int y = x + threadIdx.x; y < n; y += blockDim.x) {
+      const uint32_t p = b + lst[y];
+      if (a.s.op[p] == o) mine = fmax(mine, a.s.ts[p] - as_double(a.s.pa[p]));
+    }
+    // block max via ordered keys
+    {
+      unsigned long long kk = mine == -INFINITY ? 0ull : dkey(mine);
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+      for (int q = 16; q; q >>= 1) kk = max(kk, __shfl_xor_sync(FULL, kk, q));
+      __syncthreads();
+      if (lane == 0) sh.red_u[0][warp] = kk;
+      __syncthreads();
+      kk = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) kk = max(kk, sh.red_u[0][q]);
+      __syncthreads();
+      mine = dkey_inv(kk);
+    }
+    // op segment [sb, se) in the op index
+    if (threadIdx.x == 0) {
+      const uint64_t key = static_cast<uint64_t>(o - a.min_op);
+      uint64_t l = 0, h = a.n_opidx;
+      while (l < h) {
+        const uint64_t md = (l + h) >> 1;
+        if (a.opk[md] < key) l = md + 1; else h = md;
+      }
+      sh.u64a = l;
+      h = a.n_opidx;
+      while (l < h) {
+        const uint64_t md = (l + h) >> 1;
+        if (a.opk[md] <= key) l = md + 1; else h = md;
+      }
+      sh.u64b = l;
+    }
+    __syncthreads();
+    const uint64_t sb = sh.u64a, se = sh.u64b;
+    __syncthreads();
+    int nsib = 0;
+    for (uint64_t y = sb + threadIdx.x; y < se; y += blockDim.x) {
+      const uint32_t p = a.opp[y];
+      nsib += (a.oprank[y] != r && a.s.ts[p] <= t);
+    }
+    nsib = block_sum_i(nsib, sh);
+    double med;
+    if (nsib > 0) {
+      med = block_select(se - sb, static_cast<uint64_t>((nsib - 1) / 2),
+                         [&](uint64_t i, uint64_t* key) {
+                           const uint64_t y = sb + i;
+                           const uint32_t p = a.opp[y];
+                           if (a.oprank[y] == r || a.s.ts[p] > t) return false;
+                           *key = dkey(a.s.ts[p] - as_double(a.s.pa[p]));
+                           return true;
+                         },
+                         sh);
+    } else {
+      // cohort of (program op name, iteration) (rca.cpp:833-840)
+      const int64_t it = iter_of(o, opn);
+      const uint8_t nm = a.m.op_name[static_cast<uint64_t>(o % opn)];
+      // ops with iteration == it: [it*opn, it*opn + opn - 1] for it > 0;
+      // op/opn truncates toward zero, so iteration 0 also holds (-opn, 0).
+      const int64_t olo = it > 0 ? it * opn : it * opn - (opn - 1);
+      const int64_t ohi = it >= 0 ? it * opn + (opn - 1) : it * opn;
+      if (threadIdx.x == 0) {
+        const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
+        const bool empty = ohi < a.min_op;
+        const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
+        uint64_t l = 0, h = a.n_opidx;
+        while (l < h) {
+          const uint64_t md = (l + h) >> 1;
+          if (a.opk[md] < k0) l = md + 1; else h = md;
+        }
+        sh.u64a = l;
+        h = a.n_opidx;
+        while (l < h) {
+          const uint64_t md = (l + h) >> 1;
+          if (a.opk[md] <= k1) l = md + 1; else h = md;
+        }
+        sh.u64b = empty ? sh.u64a : l;
+      }
+      __syncthreads();
+      const uint64_t cb = sh.u64a, ce = sh.u64b;
+      __syncthreads();
+      int nco = 0;
+      for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x) {
+        const uint32_t p = a.opp[y];
+        nco += (ko_opname(a.s.ko[p]) == nm && a.s.ts[p] <= t);
+      }
+      nco = block_sum_i(nco, sh);
+      if (nco < 2) continue;
+      med = block_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
+                         [&](uint64_t i, uint64_t* key) {
+                           const uint32_t p = a.opp[cb + i];
+                           if (ko_opname(a.s.ko[p]) != nm || a.s.ts[p] > t)
+                             return false;
+                           *key = dkey(a.s.ts[p] - as_double(a.s.pa[p]));
+                           return true;
+                         },
+                         sh);
+    }
+    if (med <= 0) continue;
+    if (mine > __dmul_rn(a.skew, med)) return true;
+  }
+  return false;
+}
+
+// Lower median sorted[(n-1)/2] of n virtual values (block; O(n^2/threads)).
+template <typename V>
+__device__ double block_lower_median(int n, V val, BlockShared& sh) {
+  const int k = (n - 1) / 2;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double vi = val(i);
+    int less = 0, leq = 0;
+    for (int q = 0; q < n; ++q) {
+      const double vq = val(q);
+      less += vq < vi;
+      leq += vq <= vi;
+    }
+    if (less <= k && k < leq) {
+      uint64_t u;
+      memcpy(&u, &vi, 8);
+      sh.u64c = u;
+    }
+  }
+  __syncthreads();
+  const double r = as_double(sh.u64c);
+  __syncthreads();
+  return r;
+}
+
+__device__ void decide_straggler(const DecideArgs& a, int32_t j,
+                                 BlockShared& sh, uint32_t* scratch) {
+  const int32_t naff = a.n_aff[j];
+  const int32_t* aff = a.aff + static_cast<uint64_t>(j) * a.m.n_groups;
+  const int32_t R = a.s.R;
+  const double t = a.trip_t[j];
+  const int32_t js = a.js_of[j];
+  const int32_t k = a.k;
+  const int32_t opn = a.m.opn;
+  int tot = 0;
+  for (int32_t i = threadIdx.x; i < naff; i += blockDim.x) {
+    const int32_t g = aff[i];
+    tot += static_cast<int>(a.m.member_off[g + 1] - a.m.member_off[g]);
+  }
+  tot = block_sum_i(tot, sh);
+  if (threadIdx.x == 0) {
+    bool ok1, ok2, ok3, ok4;
+    sh.cap_cand = 2ull * tot;
+    sh.cap_cev = static_cast<unsigned long long>(tot) * (k + 1);
+    sh.cand_base = pool_alloc(a.pools.used, P_CAND, sh.cap_cand,
+                              a.pools.cand_cap, a.err, DEV_ERR_POOL, &ok1);
+    sh.cev_base = pool_alloc(a.pools.used, P_CEV, sh.cap_cev, a.pools.cev_cap,
+                             a.err, DEV_ERR_POOL, &ok2);
+    sh.sus_base = pool_alloc(a.pools.used, P_SUS, 3 * sh.cap_cand,
+                             a.pools.sus_cap, a.err, DEV_ERR_POOL, &ok3);
+    sh.exo_base = sh.sus_base + sh.cap_cand;
+    sh.ev_base = pool_alloc(a.pools.used, P_EV, sh.cap_cev, a.pools.ev_cap,
+                            a.err, DEV_ERR_POOL, &ok4);
+    sh.abort = !(ok1 && ok2 && ok3 && ok4);
+    sh.ncand = 0;
+    sh.cev_used = 0;
+  }
+  __syncthreads();
+  if (sh.abort) return;
+  // scratch: already_candidate bitmap | A | B
+  uint32_t* mark = scratch;
+  const uint32_t mwords = static_cast<uint32_t>((R + 31) / 32 + 1);
+  const uint32_t P = (a.scratch_per_trip - mwords) / 2;
+  uint32_t* A = scratch + mwords;
+  uint32_t* B = A + P;
+  for (uint32_t i = threadIdx.x; i < mwords; i += blockDim.x) mark[i] = 0;
+  __syncthreads();
+  auto is_marked = [&](int32_t r) {
+    return r >= 0 && r < R && ((mark[r >> 5] >> (r & 31)) & 1u);
+  };
+  auto set_mark = [&](int32_t r) {
+    if (r >= 0 && r < R) mark[r >> 5] |= 1u << (r & 31);
+  };
+  bool any_history = false;
+  const uint64_t rowbase = static_cast<uint64_t>(js) * a.M;
+  for (int32_t ai = 0; ai < naff; ++ai) {
+    const int32_t g = aff[ai];
+    const uint32_t mo = a.m.member_off[g];
+    const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
+    if (m < 2) continue;
+    const uint64_t gidx = static_cast<uint64_t>(js) * a.m.n_groups + g;
+    if (a.gi[gidx].n_common < k) continue;
+    any_history = true;
+    const int64_t gfo = a.m.group_first_op[g];
+    for (int q = threadIdx.x; q < k; q += blockDim.x)
+      sh.win[q] = a.gi_last[gidx * k + q];
+    __syncthreads();
+    auto cell = [&](int i, int q) {
+      return (rowbase + a.m.member_slot[mo + i]) * a.n_it +
+             static_cast<uint64_t>(sh.win[q] - a.it_min);
+    };
+    // lower medians of starts / ends per window iteration (rca.cpp:670-681)
+    for (int q = 0; q < k; ++q) {
+      const double ms = block_lower_median(
+          m, [&](int i) { return dkey_inv(a.tbl_s[cell(i, q)]); }, sh);
+      const double me = block_lower_median(
+          m, [&](int i) { return dkey_inv(a.tbl_e[cell(i, q)]); }, sh);
+      if (threadIdx.x == 0) {
+        sh.med_s[q] = ms;
+        sh.med_e[q] = me;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      bool sl = true, el = true;
+      for (int q = 0; q < k; ++q) {
+        if (dkey_inv(a.tbl_s[cell(i, q)]) - sh.med_s[q] < a.thr) sl = false;
+        if (dkey_inv(a.tbl_e[cell(i, q)]) - sh.med_e[q] < a.thr) el = false;
+      }
+      A[i] = (sl ? 1u : 0u) | (el ? 2u : 0u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < m && !sh.abort; ++i) {
+        if (!A[i]) continue;
+        const int32_t r = a.m.members[mo + i];
+        Cand c;
+        memset(&c, 0, sizeof(c));
+        c.rank = r;
+        c.cat = (A[i] & 1u) ? CSG_RC_STRAGGLER_LATE_START
+                            : CSG_RC_STRAGGLER_LATE_END;
+        c.side = CSG_SIDE_LOCAL;
+        c.group = g;
+        c.op = sh.win[k - 1] * opn + gfo;
+        c.onset = dkey_inv(a.tbl_s[cell(i, 0)]);
+        c.it_lo = sh.win[0];
+        c.it_hi = sh.win[k - 1];
+        c.ev_off = sh.cev_used;
+        for (int q = 0; q < k; ++q)
+          add_cev(a, sh, c, r, -1, dkey_inv(a.tbl_s[cell(i, q)]),
+                  sh.win[q] * opn + gfo);
+        set_mark(r);
+        push_cand(a, sh, c);
+      }
+    }
+    __syncthreads();
+    if (sh.abort) return;
+    // flow-level supplement: (rank, op) map order == ascending rank
+    for (int i = threadIdx.x; i < m; i += blockDim.x) A[i] = i;
+    __syncthreads();
+    block_stable_sort(m, A, B, [&](uint32_t x, uint32_t y) {
+      return a.m.members[mo + x] < a.m.members[mo + y];
+    });
+    if (threadIdx.x == 0) {
+      for (int pass = 0; pass < 2 && !sh.abort; ++pass) {
+        for (int x = 0; x < m && !sh.abort; ++x) {
+          const uint32_t i = B[x];
+          const int32_t r = a.m.members[mo + i];
+          if (r < 0 || r >= R || is_marked(r)) continue;
+          const FlowSum f = a.fs[static_cast<uint64_t>(js) * a.M +
+                                 a.m.member_slot[mo + i]];
+          Cand c;
+          memset(&c, 0, sizeof(c));
+          c.rank = r;
+          c.side = CSG_SIDE_LOCAL;
+          c.group = g;
+          c.it_lo = 0;
+          c.it_hi = -1;
+          c.ev_off = sh.cev_used;
+          if (pass == 0 && (f.flags & 1)) {
+            c.cat = CSG_RC_FLOW_SKEWED;
+            c.op = f.skew_op;
+            c.onset = f.skew_start;
+            add_cev(a, sh, c, r, f.skew_chan, f.skew_end, f.skew_op);
+          } else if (pass == 1 && (f.flags & 2)) {
+            c.cat = CSG_RC_FLOW_INCOMPLETE;
+            c.op = f.inc_op;
+            c.onset = t;
+            add_cev(a, sh, c, r, f.inc_chan, t, f.inc_op);
+          } else {
+            continue;
+          }
+          set_mark(r);
+          push_cand(a, sh, c);
+        }
+      }
+    }
+    __syncthreads();
+    if (sh.abort) return;
+  }
+  const int C = sh.ncand;
+  if (C == 0) {
+    write_trip(a, j,
+               any_history ? CSG_VERDICT_NO_STRAGGLER
+                           : CSG_VERDICT_INSUFFICIENT_HISTORY,
+               naff, 2 * a.N, sh);
+    return;
+  }
+  // self-evidence filter (rca.cpp:795-869)
+  Cand* cands = a.pools.cand + sh.cand_base;
+  int any_self = 0;
+  for (int x = 0; x < C; ++x) {
+    const Cand c = cands[x];
+    const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, j, c, sh, A);
+    if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
+    any_self |= sf ? 1 : 0;
+    __syncthreads();
+  }
+  uint32_t* idx = A;
+  uint32_t* ord = B;
+  uint8_t* keep = reinterpret_cast<uint8_t*>(B + C);
+  uint32_t* tail = reinterpret_cast<uint32_t*>(keep + ((C + 3) & ~3));
+  for (int i = threadIdx.x; i < C; i += blockDim.x) idx[i] = i;
+  __syncthreads();
+  block_stable_sort(C, idx, ord, [&](uint32_t x, uint32_t y) {
+    if (cands[x].op != cands[y].op) return cands[x].op < cands[y].op;
+    return cands[x].rank < cands[y].rank;
+  });
+  for (int x = threadIdx.x; x < C; x += blockDim.x)
+    keep[x] = (!any_self || cands[ord[x]].pad) ? 1 : 0;
+  __syncthreads();
+  emit_reports(a, sh, ord, keep, C, tail);
+  write_trip(a, j, sh.nsus ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_NO_STRAGGLER,
+             naff, 3 * a.N, sh);
+}
+
+__global__ void __launch_bounds__(kDecideThreads)
+    k_decide(DecideArgs a) {
+  extern __shared__ unsigned char dyn[];
+  BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
+  const int32_t j = blockIdx.x;
+  if (threadIdx.x == 0) {
+    sh.abort = 0;
+    sh.nsus = sh.nexo = 0;
+    sh.nev = 0;
+    sh.sus_base = sh.exo_base = sh.ev_base = 0;
+  }
+  __syncthreads();
+  uint32_t* scratch = a.pools.u32 + static_cast<uint64_t>(j) * a.scratch_per_trip;
+  const int32_t naff = a.n_aff[j];
+  if (naff == 0 || a.m.opn == 0) {
+    write_trip(a, j, CSG_VERDICT_FALSE_TRIGGER, naff, a.N, sh);
+    return;
+  }
+  if (a.trip_kind[j] == CSG_TRIGGER_FAILURE)
+    decide_failure(a, j, sh, scratch);
+  else
+    decide_straggler(a, j, sh, scratch);
+}
+
+}  // namespace
+}  // namespace csg
+
+namespace csg {
+
+namespace {
+
+template <typename T>
+T* upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  b.ensure(v.size() * sizeof(T) + sizeof(T));
+  if (!v.empty())
+    CSG_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T),
+                             cudaMemcpyHostToDevice, st));
+  return b.as<T>();
+}
+
+void validate_analysis(const csg_analysis_config& c) {
+  // AnalysisConfig::validate (proj/src/rca.cpp:63-71)
+  if (!(c.straggler_threshold_ms > 0))
+    throw Error(CSG_ERR_CONFIG, "analysis: straggler_threshold_ms must be > 0");
+  if (c.consecutive_iterations_k < 1)
+    throw Error(CSG_ERR_CONFIG,
+                "analysis: consecutive_iterations_k must be >= 1");
+  if (!(c.delta_ms > 0))
+    throw Error(CSG_ERR_CONFIG, "analysis: delta_ms must be > 0");
+  if (!(c.flow_skew_factor > 1))
+    throw Error(CSG_ERR_CONFIG, "analysis: flow_skew_factor must be > 1");
+}
+
+}  // namespace
+
+void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
+               const csg_trigger_event* trips, int32_t J, bool affected_only,
+               RcaResult& out) {
+  out = RcaResult();
+  out.G = m->n_groups;
+  if (J <= 0) return;
+  if (!affected_only) validate_analysis(cfg);
+  if (cfg.consecutive_iterations_k > kMaxK)
+    throw Error(CSG_ERR_RUNTIME,
+                "engine: consecutive_iterations_k > 64 is not supported");
+  store_build_index(s);
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  const StoreView sv = s->view();
+  const ModelView mv = m->view();
+  const int32_t R = s->R;
+  const int32_t nch = std::max(s->nch, 1);
+  const int32_t G = m->n_groups;
+  const int32_t opn = m->opn;
+  const int32_t k = cfg.consecutive_iterations_k;
+  const uint32_t M = G ? m->h_member_off[G] : 0;
+
+  std::vector<double> h_t(J);
+  std::vector<int32_t> h_kind(J), h_rank(J), h_js(J, -1), h_strag;
+  for (int32_t j = 0; j < J; ++j) {
+    h_t[j] = trips[j].time_ms;
+    h_kind[j] = trips[j].kind;
+    h_rank[j] = trips[j].suspect_rank;
+    if (trips[j].kind == CSG_TRIGGER_STRAGGLER) {
+      h_js[j] = static_cast<int32_t>(h_strag.size());
+      h_strag.push_back(j);
+    }
+  }
+  const int32_t Js = static_cast<int32_t>(h_strag.size());
+  DevBuf d_t, d_kind, d_rank, d_js, d_strag;
+  const double* dt = upload(d_t, h_t, st);
+  const int32_t* dkind = upload(d_kind, h_kind, st);
+  const int32_t* drank = upload(d_rank, h_rank, st);
+  const int32_t* djs = upload(d_js, h_js, st);
+  const int32_t* dstrag = upload(d_strag, h_strag, st);
+
+  // K1: per (trip, rank) prefix summaries
+  DevBuf rs, chan_pos;
+  rs.ensure(static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum));
+  chan_pos.ensure(static_cast<size_t>(J) * std::max(R, 1) * nch * 4);
+  if (R > 0) {
+    int wpb = 32768 / (nch * 4);
+    wpb = std::max(1, std::min(8, wpb));
+    const uint64_t warps = static_cast<uint64_t>(R) * J;
+    k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
+                     wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
+                                          rs.as<RankSum>(),
+                                          chan_pos.as<uint32_t>(), nch);
+    ++c->lc.launches;
+  }
+  // K2/K3: straggler iteration tables
+  DevBuf tbl_s, tbl_e, gi, gi_last;
+  int64_t it_min = 0;
+  int32_t n_it = 1;
+  gi.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max(G, 1) * sizeof(GroupIter));
+  gi_last.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max(G, 1) * k * 8);
+  if (Js > 0) {
+    CSG_CUDA(cudaMemsetAsync(gi.p, 0, gi.bytes, st));
+    if (opn > 0 && M > 0) {
+      it_min = iter_of(s->min_op, opn);
+      const int64_t it_max = iter_of(s->max_op, opn);
+      const int64_t span = s->n ? it_max - it_min + 1 : 1;
+      const double bytes = 16.0 * Js * M * static_cast<double>(span);
+      if (span > (1ll << 30) || bytes > 24e9)
+        throw Error(CSG_ERR_RUNTIME,
+                    "engine: straggler iteration tables exceed the device budget");
+      n_it = static_cast<int32_t>(span);
+      const size_t cells = static_cast<size_t>(Js) * M * n_it;
+      tbl_s.ensure(cells * 8);
+      tbl_e.ensure(cells * 8);
+      CSG_CUDA(cudaMemsetAsync(tbl_s.p, 0xff, cells * 8, st));
+      CSG_CUDA(cudaMemsetAsync(tbl_e.p, 0, cells * 8, st));
+      if (R > 0) {
+        const uint64_t warps = static_cast<uint64_t>(R) * Js;
+        k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                        st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
+                              M, tbl_s.as<unsigned long long>(),
+                              tbl_e.as<unsigned long long>());
+        ++c->lc.launches;
+      }
+      const uint64_t gw = static_cast<uint64_t>(G) * Js;
+      k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
+          mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
+          tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
+          gi.as<GroupIter>(), gi_last.as<int64_t>());
+      ++c->lc.launches;
+    }
+  }
+  // K4: affected groups
+  DevBuf aff, aff_flag, n_aff;
+  aff.ensure(static_cast<size_t>(J) * std::max(G, 1) * 4);
+  aff_flag.ensure(static_cast<size_t>(J) * std::max(G, 1));
+  n_aff.ensure(static_cast<size_t>(J) * 4);
+  k_affected<<<J, 256, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
+                                gi.as<GroupIter>(), aff.as<int32_t>(),
+                                aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
+  ++c->lc.launches;
+  std::vector<int32_t> h_naff(J);
+  out.aff.assign(static_cast<size_t>(J) * G, 0);
+  CSG_CUDA(cudaMemcpyAsync(h_naff.data(), n_aff.p, J * 4, cudaMemcpyDeviceToHost, st));
+  if (G)
+    CSG_CUDA(cudaMemcpyAsync(out.aff.data(), aff.p, static_cast<size_t>(J) * G * 4,
+                             cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  CSG_CUDA(cudaGetLastError());
+  out.trips.assign(J, TripOut{});
+  for (int32_t j = 0; j < J; ++j) out.trips[j].n_aff = h_naff[j];
+  if (affected_only) return;
+
+  // K5: flow rules
+  DevBuf fs, slot_group, err;
+  err.ensure(4);
+  CSG_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+  fs.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max<uint32_t>(M, 1) * sizeof(FlowSum));
+  if (Js > 0 && opn > 0 && M > 0) {
+    store_build_op_index(s, opn);
+    std::vector<uint32_t> h_sg(M);
+    for (int32_t g = 0; g < G; ++g)
+      for (uint32_t q = m->h_member_off[g]; q < m->h_member_off[g + 1]; ++q)
+        h_sg[q] = static_cast<uint32_t>(g);
+    upload(slot_group, h_sg, st);
+    const uint64_t warps = static_cast<uint64_t>(M) * Js;
+    k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
+        sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+        slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+        aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
+    ++c->lc.launches;
+  }
+
+  // K6: decide. Pool sizes from the affected lists.
+  uint64_t tot_all = 0, tot_max = 0;
+  int32_t m_max = 1;
+  for (int32_t g = 0; g < G; ++g)
+    m_max = std::max<int32_t>(m_max, m->h_member_off[g + 1] - m->h_member_off[g]);
+  for (int32_t j = 0; j < J; ++j) {
+    uint64_t tot = 0;
+    for (int32_t i = 0; i < h_naff[j]; ++i) {
+      const int32_t g = out.aff[static_cast<size_t>(j) * G + i];
+      tot += m->h_member_off[g + 1] - m->h_member_off[g];
+    }
+    tot_all += tot;
+    tot_max = std::max(tot_max, tot);
+  }
+  const uint64_t per_ev = std::max<uint64_t>(2 * nch + 1, k + 1);
+  uint64_t cand_cap = 2 * tot_all + 16;
+  uint64_t cev_cap = tot_all * per_ev + 16;
+  uint64_t sus_cap = 6 * tot_all + 16;
+  uint64_t ev_cap = cev_cap;
+  uint64_t bits_cap = 1ull << 22;
+  const uint64_t C2 = 2 * tot_max + 8;
+  const uint64_t mwords = (static_cast<uint64_t>(R) + 31) / 32 + 1;
+  uint64_t spt = std::max<uint64_t>(12 * C2, 4 * static_cast<uint64_t>(m_max));
+  spt = std::max<uint64_t>(spt, mwords + 2 * std::max<uint64_t>(
+                                                std::max<uint64_t>(m_max, s->max_seg),
+                                                8 * C2));
+  spt += 64;
+  if (spt > 0xFFFFFFF0ull)
+    throw Error(CSG_ERR_RUNTIME, "engine: per-trip scratch exceeds 2^32 words");
+
+  DevBuf p_cand, p_cev, p_sus, p_ev, p_bits, p_u32, p_used, d_out;
+  d_out.ensure(static_cast<size_t>(J) * sizeof(TripOut));
+  p_used.ensure(8 * 8);
+  p_u32.ensure(static_cast<size_t>(J) * spt * 4);
+  DecideArgs a;
+  a.s = sv;
+  a.m = mv;
+  a.J = J;
+  a.trip_t = dt;
+  a.trip_kind = dkind;
+  a.trip_rank = drank;
+  a.js_of = djs;
+  a.rs = rs.as<RankSum>();
+  a.chan_pos = chan_pos.as<uint32_t>();
+  a.nch = nch;
+  a.aff = aff.as<int32_t>();
+  a.n_aff = n_aff.as<int32_t>();
+  a.gi = gi.as<GroupIter>();
+  a.gi_last = gi_last.as<int64_t>();
+  a.k = k;
+  a.fs = fs.as<FlowSum>();
+  a.tbl_s = tbl_s.as<unsigned long long>();
+  a.tbl_e = tbl_e.as<unsigned long long>();
+  a.it_min = it_min;
+  a.n_it = n_it;
+  a.M = M;
+  a.delta_a = cfg.delta_ms;
+  a.thr = cfg.straggler_threshold_ms;
+  a.skew = cfg.flow_skew_factor;
+  a.N = s->n;
+  a.opk = s->opidx_keys.as<uint64_t>();
+  a.opp = s->opidx_pos.as<uint32_t>();
+  a.oprank = s->opidx_rank.as<int32_t>();
+  a.n_opidx = s->op_indexed ? s->n_opidx : 0;
+  a.min_op = s->min_op;
+  a.scratch_per_trip = static_cast<uint32_t>(spt);
+  a.out = d_out.as<TripOut>();
+  a.err = err.as<uint32_t>();
+  const size_t shm = sizeof(BlockShared);
+  CSG_CUDA(cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(shm)));
+  uint32_t h_err = 0;
+  unsigned long long used[8];
+  for (int attempt = 0;; ++attempt) {
+    p_cand.ensure(cand_cap * sizeof(Cand));
+    p_cev.ensure(cev_cap * sizeof(csg_evidence));
+    p_sus.ensure(sus_cap * sizeof(csg_suspect));
+    p_ev.ensure(ev_cap * sizeof(csg_evidence));
+    p_bits.ensure(bits_cap * 8);
+    a.pools.cand = p_cand.as<Cand>();
+    a.pools.cand_cap = cand_cap;
+    a.pools.cev = p_cev.as<csg_evidence>();
+    a.pools.cev_cap = cev_cap;
+    a.pools.sus = p_sus.as<csg_suspect>();
+    a.pools.sus_cap = sus_cap;
+    a.pools.ev = p_ev.as<csg_evidence>();
+    a.pools.ev_cap = ev_cap;
+    a.pools.bits = p_bits.as<unsigned long long>();
+    a.pools.bits_cap = bits_cap;
+    a.pools.u32 = p_u32.as<uint32_t>();
+    a.pools.u32_cap = static_cast<unsigned long long>(J) * spt;
+    a.pools.used = p_used.as<unsigned long long>();
+    CSG_CUDA(cudaMemsetAsync(p_used.p, 0, 8 * 8, st));
+    // keep K5 errors, clear decide-retry flags
+    k_decide<<<J, kDecideThreads, shm, st>>>(a);
+    ++c->lc.launches;
+    CSG_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(used, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaStreamSynchronize(st));
+    CSG_CUDA(cudaGetLastError());
+    if (h_err & DEV_ERR_RC_TABLE)
+      throw Error(CSG_ERR_RUNTIME,
+                  "check_rc_table: counters violate the pipeline invariant");
+    if (h_err & DEV_ERR_TOO_MANY_COMPS)
+      throw Error(CSG_ERR_RUNTIME,
+                  "engine: more than 256 completions of one (rank, op) in the "
+                  "analysis window");
+    if (!(h_err & (DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH))) break;
+    if (attempt >= 6)
+      throw Error(CSG_ERR_RUNTIME, "engine: RCA output pools exhausted");
+    if (h_err & DEV_ERR_DAG_SCRATCH) bits_cap = std::max<uint64_t>(bits_cap * 4, used[P_BITS] * 2);
+    if (h_err & DEV_ERR_POOL) {
+      cand_cap *= 4;
+      cev_cap *= 4;
+      sus_cap *= 4;
+      ev_cap *= 4;
+    }
+    h_err &= ~(DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH);
+    CSG_CUDA(cudaMemcpyAsync(err.p, &h_err, 4, cudaMemcpyHostToDevice, st));
+  }
+  std::vector<TripOut> to(J);
+  CSG_CUDA(cudaMemcpyAsync(to.data(), d_out.p, J * sizeof(TripOut),
+                           cudaMemcpyDeviceToHost, st));
+  out.sus.resize(used[P_SUS]);
+  out.ev.resize(used[P_EV]);
+  if (used[P_SUS])
+    CSG_CUDA(cudaMemcpyAsync(out.sus.data(), p_sus.p, used[P_SUS] * sizeof(csg_suspect),
+                             cudaMemcpyDeviceToHost, st));
+  if (used[P_EV])
+    CSG_CUDA(cudaMemcpyAsync(out.ev.data(), p_ev.p, used[P_EV] * sizeof(csg_evidence),
+                             cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  out.trips = to;
+}
+
+}  // namespace csg

@@ -1,0 +1,500 @@
+// store.cu — device TraceStore: ingest statistics, the rank-major index and
+// the store queries.
+//
+// Reference semantics (proj/src/trace.cpp:99-144, proj/src/rca.cpp:77-90):
+// the store index is emission order; RankIndex lists each rank's records in
+// store order. Here the index is one stable radix sort by rank (store order
+// preserved inside a rank), a gather of the packed records into rank-major
+// structure-of-arrays columns, and a per-rank running maximum of the
+// timestamp. The running max is monotone even though per-rank timestamps are
+// not, so every reference "prefix scan that breaks at the
+// first ts > t" becomes one upper_bound over it.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "objects.h"
+
+namespace csg {
+namespace {
+
+__device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long v) {
+  atomicMax(a, v);
+}
+
+__global__ void k_stats(const csg_packed_record* __restrict__ r, uint64_t n,
+                        StoreStats* __restrict__ st) {
+  unsigned long long tsk = 0;
+  int mnr = INT_MAX, mxr = INT_MIN, mnc = INT_MAX, mxc = INT_MIN;
+  long long mno = LLONG_MAX, mxo = LLONG_MIN;
+  unsigned long long nan = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double t = r[i].ts;
+    if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
+    mnr = min(mnr, r[i].rank);
+    mxr = max(mxr, r[i].rank);
+    mnc = min(mnc, r[i].channel);
+    mxc = max(mxc, r[i].channel);
+    mno = min(mno, (long long)r[i].op_seq);
+    mxo = max(mxo, (long long)r[i].op_seq);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    tsk = max(tsk, __shfl_xor_sync(0xffffffffu, tsk, o));
+    mnr = min(mnr, __shfl_xor_sync(0xffffffffu, mnr, o));
+    mxr = max(mxr, __shfl_xor_sync(0xffffffffu, mxr, o));
+    mnc = min(mnc, __shfl_xor_sync(0xffffffffu, mnc, o));
+    mxc = max(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
+    mno = min(mno, __shfl_xor_sync(0xffffffffu, mno, o));
+    mxo = max(mxo, __shfl_xor_sync(0xffffffffu, mxo, o));
+    nan += __shfl_xor_sync(0xffffffffu, nan, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_u64(&st->ts_max_key, tsk);
+    atomicMin(&st->min_rank, mnr);
+    atomicMax(&st->max_rank, mxr);
+    atomicMin(&st->min_chan, mnc);
+    atomicMax(&st->max_chan, mxc);
+    atomicMin(&st->min_op, mno);
+    atomicMax(&st->max_op, mxo);
+    if (nan) atomicAdd(&st->n_nan, nan);
+  }
+}
+
+__global__ void k_rank_keys(const csg_packed_record* __restrict__ r, uint64_t n,
+                            uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    keys[i] = static_cast<uint32_t>(r[i].rank);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// rank_off[r] = first sorted position with key >= r, r in [0, R].
+__global__ void k_rank_off(const uint32_t* __restrict__ keys, uint64_t n,
+                           int32_t R, uint32_t* __restrict__ off) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > R) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < static_cast<uint32_t>(r)) lo = mid + 1; else hi = mid;
+  }
+  off[r] = static_cast<uint32_t>(lo);
+}
+
+// Gather packed AoS records into rank-major SoA columns.
+__global__ void k_gather(const csg_packed_record* __restrict__ r,
+                         const uint32_t* __restrict__ perm, uint64_t n,
+                         double* __restrict__ ts, int64_t* __restrict__ op,
+                         int32_t* __restrict__ comm, int32_t* __restrict__ chan,
+                         uint8_t* __restrict__ ko, uint64_t* __restrict__ pa,
+                         uint64_t* __restrict__ pb) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    // 48-byte records are 16-byte aligned: three 16-byte vector loads.
+    const ulonglong2* rec =
+        reinterpret_cast<const ulonglong2*>(r + perm[p]);
+    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1), h1 = __ldg(rec + 2);
+    double t;
+    memcpy(&t, &h0.x, 8);
+    ts[p] = t;
+    op[p] = static_cast<int64_t>(h0.y);
+    const uint64_t w2 = hm.x, w3 = hm.y;
+    comm[p] = static_cast<int32_t>(w2 >> 32);
+    chan[p] = static_cast<int32_t>(w3 & 0xffffffffu);
+    const uint8_t kind = static_cast<uint8_t>((w3 >> 32) & 0xff);
+    const uint8_t name = static_cast<uint8_t>((w3 >> 40) & 0xff);
+    ko[p] = static_cast<uint8_t>((kind & 1) | (name << 1));
+    pa[p] = h1.x;  // start_ms bits | ready | tx << 32
+    pb[p] = h1.y;  // msg_bytes | done (| reserved << 32)
+    if (kind & 1) pb[p] = h1.y & 0xffffffffull;
+  }
+}
+
+// Per-rank inclusive running max of ts (one warp per rank, chunked scan).
+__global__ void k_runmax(const double* __restrict__ ts,
+                         const uint32_t* __restrict__ off, int32_t R,
+                         double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= R) return;
+  const uint32_t b = off[w], e = off[w + 1];
+  double carry = -INFINITY;
+  for (uint32_t base = b; base < e; base += 32) {
+    const uint32_t p = base + lane;
+    double x = p < e ? ts[p] : -INFINITY;
+    if (x != x) x = -INFINITY;  // NaN never breaks a prefix
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = fmax(x, y);
+    }
+    x = fmax(x, carry);
+    if (p < e) out[p] = x;
+    carry = __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+__global__ void k_opidx_rank(StoreView s, const uint32_t* __restrict__ pos,
+                             uint64_t n, int32_t* __restrict__ rank) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = pos[i];
+    int32_t lo = 0, hi = s.R;  // last r with rank_off[r] <= p
+    while (hi - lo > 1) {
+      const int32_t md = (lo + hi) >> 1;
+      if (s.rank_off[md] <= p) lo = md; else hi = md;
+    }
+    rank[i] = lo;
+  }
+}
+
+// ---- query ---------------------------------------------------------------
+
+// Pass 1: per listed rank, count records with t0 <= ts <= t1.
+__global__ void k_query_count(StoreView s, const int32_t* __restrict__ ranks,
+                              int32_t nr, double t0, double t1,
+                              uint32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= nr) return;
+  const int32_t r = ranks[w];
+  uint32_t c = 0;
+  if (r >= 0 && r < s.R) {
+    for (uint32_t p = s.rank_off[r] + lane; p < s.rank_off[r + 1]; p += 32) {
+      const double t = s.ts[p];
+      c += !(t < t0 || t > t1);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) counts[w] = c;
+}
+
+// Pass 2: order-preserving compaction (rank order, then store order).
+__global__ void k_query_write(StoreView s, const int32_t* __restrict__ ranks,
+                              int32_t nr, double t0, double t1,
+                              const uint32_t* __restrict__ offs,
+                              uint64_t* __restrict__ okey,
+                              uint32_t* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= nr) return;
+  const int32_t r = ranks[w];
+  if (r < 0 || r >= s.R) return;
+  uint32_t o = offs[w];
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  for (uint32_t base = b; base < e; base += 32) {
+    const uint32_t p = base + lane;
+    bool hit = false;
+    double t = 0;
+    if (p < e) {
+      t = s.ts[p];
+      hit = !(t < t0 || t > t1);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+      okey[at] = dkey(t == 0.0 ? 0.0 : t);  // -0 sorts with +0 (== in ref)
+      oval[at] = s.perm[p];
+    }
+    o += __popc(m);
+  }
+}
+
+// ---- last_log_per_rank -----------------------------------------------------
+
+__global__ void k_last_log(StoreView s, const int32_t* __restrict__ members,
+                           int32_t nm, double t, uint64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= nm) return;
+  const int32_t r = members[w];
+  // best = (ts, store idx) maximal among ts <= t; store idx breaks ties
+  // toward the later append (proj/src/trace.cpp:135).
+  bool found = false;
+  double bt = 0;
+  uint32_t bi = 0;
+  if (r >= 0 && r < s.R) {
+    for (uint32_t p = s.rank_off[r] + lane; p < s.rank_off[r + 1]; p += 32) {
+      const double x = s.ts[p];
+      if (x > t) continue;
+      const uint32_t i = s.perm[p];
+      if (!found || x > bt || (x == bt && i > bi)) {
+        found = true;
+        bt = x;
+        bi = i;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int f2 = __shfl_xor_sync(0xffffffffu, (int)found, o);
+    const double t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+    const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (f2 && (!found || t2 > bt || (t2 == bt && i2 > bi))) {
+      found = true;
+      bt = t2;
+      bi = i2;
+    }
+  }
+  if (lane == 0) out[w] = found ? bi : ~0ull;
+}
+
+// ---- op-ordered completion index -----------------------------------------
+
+__global__ void k_opidx_flags(StoreView s, uint32_t* __restrict__ flags) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t ko = s.ko[p];
+    flags[p] = (ko_kind(ko) == CSG_KIND_COMPLETION &&
+                ko_opname(ko) != CSG_OP_RECV)
+                   ? 1u
+                   : 0u;
+  }
+}
+
+__global__ void k_opidx_scatter(StoreView s, const uint32_t* __restrict__ offs,
+                                int64_t min_op, uint64_t* __restrict__ keys,
+                                uint32_t* __restrict__ vals) {
+  // entry value = rank-major position; the rank is recovered afterwards
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t ko = s.ko[p];
+    if (ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV) {
+      const uint32_t at = offs[p];
+      keys[at] = static_cast<uint64_t>(s.op[p] - min_op);
+      vals[at] = static_cast<uint32_t>(p);
+    }
+  }
+}
+
+unsigned grid_for(uint64_t n, int threads = 256) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g > 148ull * 64) g = 148ull * 64;
+  if (g == 0) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+void store_build_index(csg_store* s) {
+  if (s->indexed) return;
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  const uint64_t n = s->n;
+  const csg_packed_record* recs = s->recs.as<csg_packed_record>();
+  StoreStats h{};
+  h.ts_max_key = 0;
+  h.min_rank = INT32_MAX;
+  h.max_rank = INT32_MIN;
+  h.min_chan = INT32_MAX;
+  h.max_chan = INT32_MIN;
+  h.min_op = INT64_MAX;
+  h.max_op = INT64_MIN;
+  s->stats_dev.ensure(sizeof(StoreStats));
+  CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
+                           cudaMemcpyHostToDevice, st));
+  if (n) {
+    k_stats<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>());
+    ++c->lc.launches;
+  }
+  CSG_CUDA(cudaMemcpyAsync(&h, s->stats_dev.p, sizeof(h),
+                           cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  if (n && h.min_rank < 0)
+    throw Error(CSG_ERR_RUNTIME,
+                "engine: negative rank in trace record (ranks must be >= 0)");
+  if (n && h.min_chan < 0)
+    throw Error(CSG_ERR_RUNTIME,
+                "engine: negative channel in trace record (channels must be >= 0)");
+  if (n && h.max_chan >= 4096)
+    throw Error(CSG_ERR_RUNTIME, "engine: channel id >= 4096 unsupported");
+  if (h.n_nan)
+    throw Error(CSG_ERR_RUNTIME, "engine: NaN timestamp in trace record");
+  if (n > 0xFFFFFFF0ull)
+    throw Error(CSG_ERR_RUNTIME, "engine: store exceeds 2^32 records");
+  const double mx = n ? dkey_inv(h.ts_max_key) : 0.0;
+  s->last_ts = (n && mx > 0.0) ? mx : 0.0;
+  s->min_rank = n ? h.min_rank : 0;
+  s->max_rank = n ? h.max_rank : -1;
+  s->min_chan = n ? h.min_chan : 0;
+  s->max_chan = n ? h.max_chan : -1;
+  s->min_op = n ? h.min_op : 0;
+  s->max_op = n ? h.max_op : -1;
+  s->R = s->max_rank + 1;
+  s->nch = s->max_chan + 1;
+  const int32_t R = s->R;
+
+  s->rank_off.ensure((static_cast<size_t>(R) + 1) * 4);
+  s->perm.ensure(n * 4 + 4);
+  s->keys.ensure(n * 4 + 4);
+  s->ts.ensure(n * 8 + 8);
+  s->runmax.ensure(n * 8 + 8);
+  s->op.ensure(n * 8 + 8);
+  s->comm.ensure(n * 4 + 4);
+  s->chan.ensure(n * 4 + 4);
+  s->ko.ensure(n + 8);
+  s->pa.ensure(n * 8 + 8);
+  s->pb.ensure(n * 8 + 8);
+  if (n) {
+    k_rank_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->keys.as<uint32_t>(),
+                                             s->perm.as<uint32_t>());
+    ++c->lc.launches;
+    radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
+                   bits_for(static_cast<uint64_t>(R > 0 ? R - 1 : 0)), s->sort,
+                   st, c->lc);
+    k_gather<<<grid_for(n), 256, 0, st>>>(
+        recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
+        s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
+        s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
+    ++c->lc.launches;
+  }
+  k_rank_off<<<(R + 1 + 255) / 256, 256, 0, st>>>(s->keys.as<uint32_t>(), n, R,
+                                                 s->rank_off.as<uint32_t>());
+  ++c->lc.launches;
+  if (n && R) {
+    k_runmax<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
+        s->ts.as<double>(), s->rank_off.as<uint32_t>(), R,
+        s->runmax.as<double>());
+    ++c->lc.launches;
+  }
+  {
+    std::vector<uint32_t> ro(static_cast<size_t>(R) + 1);
+    CSG_CUDA(cudaMemcpyAsync(ro.data(), s->rank_off.p, ro.size() * 4,
+                             cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaStreamSynchronize(st));
+    uint64_t mx = 0;
+    for (int32_t r = 0; r < R; ++r) mx = std::max<uint64_t>(mx, ro[r + 1] - ro[r]);
+    s->max_seg = mx;
+  }
+  CSG_CUDA(cudaGetLastError());
+  s->indexed = true;
+  s->op_indexed = false;
+}
+
+void store_build_op_index(csg_store* s, int32_t opn) {
+  (void)opn;
+  if (s->op_indexed) return;
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  const uint64_t n = s->n;
+  StoreView v = s->view();
+  DevBuf flags;
+  flags.ensure(n * 4 + 4);
+  uint32_t count = 0;
+  if (n) {
+    k_opidx_flags<<<grid_for(n), 256, 0, st>>>(v, flags.as<uint32_t>());
+    ++c->lc.launches;
+    // total = last exclusive offset + last flag
+    uint32_t last_flag = 0;
+    CSG_CUDA(cudaMemcpyAsync(&last_flag, flags.as<uint32_t>() + n - 1, 4,
+                             cudaMemcpyDeviceToHost, st));
+    exclusive_scan_u32(flags.as<uint32_t>(), n, c->scratch_a, st, c->lc);
+    uint32_t last_off = 0;
+    CSG_CUDA(cudaMemcpyAsync(&last_off, flags.as<uint32_t>() + n - 1, 4,
+                             cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaStreamSynchronize(st));
+    count = last_off + last_flag;
+  }
+  s->n_opidx = count;
+  s->opidx_keys.ensure(static_cast<size_t>(count) * 8 + 8);
+  s->opidx_pos.ensure(static_cast<size_t>(count) * 4 + 4);
+  if (count) {
+    k_opidx_scatter<<<grid_for(n), 256, 0, st>>>(
+        v, flags.as<uint32_t>(), s->min_op, s->opidx_keys.as<uint64_t>(),
+        s->opidx_pos.as<uint32_t>());
+    ++c->lc.launches;
+    const uint64_t range = static_cast<uint64_t>(s->max_op - s->min_op);
+    radix_sort_u64(s->opidx_keys.as<uint64_t>(), s->opidx_pos.as<uint32_t>(),
+                   count, bits_for(range), s->sort, st, c->lc);
+  }
+  s->opidx_rank.ensure(static_cast<size_t>(count) * 4 + 4);
+  if (count) {
+    k_opidx_rank<<<grid_for(count), 256, 0, st>>>(
+        s->view(), s->opidx_pos.as<uint32_t>(), count,
+        s->opidx_rank.as<int32_t>());
+    ++c->lc.launches;
+  }
+  CSG_CUDA(cudaGetLastError());
+  s->op_indexed = true;
+}
+
+// ---- query / last_log host entry points --------------------------------------
+
+void store_query(csg_store* s, const int32_t* ranks, size_t nr, double t0,
+                 double t1, std::vector<uint64_t>& out) {
+  if (t0 > t1) throw Error(CSG_ERR_RUNTIME, "query: t0 > t1");
+  store_build_index(s);
+  out.clear();
+  // Set semantics (std::find over the rank span): unique ranks, ascending,
+  // so the compaction yields (rank, store index) order before the ts sort.
+  std::vector<int32_t> rs(ranks, ranks + nr);
+  std::sort(rs.begin(), rs.end());
+  rs.erase(std::unique(rs.begin(), rs.end()), rs.end());
+  rs.erase(std::remove_if(rs.begin(), rs.end(),
+                          [&](int32_t r) { return r < 0 || r >= s->R; }),
+           rs.end());
+  if (rs.empty() || s->n == 0) return;
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  const int32_t k = static_cast<int32_t>(rs.size());
+  DevBuf d_ranks, d_counts;
+  d_ranks.ensure(k * 4);
+  d_counts.ensure((k + 1) * 4);
+  CSG_CUDA(cudaMemcpyAsync(d_ranks.p, rs.data(), k * 4, cudaMemcpyHostToDevice, st));
+  StoreView v = s->view();
+  const unsigned g = static_cast<unsigned>((static_cast<uint64_t>(k) * 32 + 255) / 256);
+  k_query_count<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
+                                   d_counts.as<uint32_t>());
+  ++c->lc.launches;
+  CSG_CUDA(cudaMemsetAsync(d_counts.as<uint32_t>() + k, 0, 4, st));
+  exclusive_scan_u32(d_counts.as<uint32_t>(), k + 1, c->scratch_a, st, c->lc);
+  uint32_t total = 0;
+  CSG_CUDA(cudaMemcpyAsync(&total, d_counts.as<uint32_t>() + k, 4,
+                           cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  if (!total) return;
+  DevBuf keys, vals;
+  keys.ensure(total * 8);
+  vals.ensure(total * 4);
+  k_query_write<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
+                                   d_counts.as<uint32_t>(), keys.as<uint64_t>(),
+                                   vals.as<uint32_t>());
+  ++c->lc.launches;
+  SortScratch ss;
+  radix_sort_u64(keys.as<uint64_t>(), vals.as<uint32_t>(), total, 64, ss, st,
+                 c->lc);
+  std::vector<uint32_t> h(total);
+  CSG_CUDA(cudaMemcpyAsync(h.data(), vals.p, total * 4, cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  out.assign(h.begin(), h.end());
+}
+
+void store_last_log(csg_store* s, const int32_t* members, size_t nm, double t,
+                    std::vector<std::pair<int32_t, uint64_t>>& out) {
+  if (nm == 0) throw Error(CSG_ERR_RUNTIME, "last_log_per_rank: empty group");
+  store_build_index(s);
+  out.clear();
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  DevBuf d_m, d_o;
+  d_m.ensure(nm * 4);
+  d_o.ensure(nm * 8);
+  CSG_CUDA(cudaMemcpyAsync(d_m.p, members, nm * 4, cudaMemcpyHostToDevice, st));
+  const unsigned g = static_cast<unsigned>((nm * 32 + 255) / 256);
+  k_last_log<<<g, 256, 0, st>>>(s->view(), d_m.as<int32_t>(),
+                                static_cast<int32_t>(nm), t, d_o.as<uint64_t>());
+  ++c->lc.launches;
+  std::vector<uint64_t> h(nm);
+  CSG_CUDA(cudaMemcpyAsync(h.data(), d_o.p, nm * 8, cudaMemcpyDeviceToHost, st));
+  CSG_CUDA(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < nm; ++i)
+    if (h[i] != ~0ull) out.emplace_back(members[i], h[i]);
+}
+
+}  // namespace csg

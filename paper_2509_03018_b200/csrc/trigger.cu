@@ -1,0 +1,338 @@
+// trigger.cu — Algorithm 1 (the trigger) on the device.
+//
+// Reference: evaluate (proj/src/trigger.cpp:57-136) runs one full-store
+// TraceStore::query per sampled rank per tick (trace.cpp:101-119) and folds
+// the window into an EMA baseline. Here every (tick, sampled rank) window is
+// reduced in parallel from the rank-major columns (one warp each; the window
+// is a FILTER over the rank's records, so order does not matter for the
+// statistics used: count, has-state, completion count, byte sum, min/max
+// end), and the EMA recurrence runs as one thread per sampled rank over all
+// ticks. Baselines of distinct ranks never interact; ticks couple them only
+// through "lowest tripped rank wins", resolved per tick afterwards.
+//
+// Floating point: the EMA and threshold products use explicit _rn intrinsics
+// (and the file is built with -fmad=false) so no FMA contraction happens,
+// matching the reference's SSE2 build.
+#include "objects.h"
+#include "trigger.cuh"
+
+namespace csg {
+namespace {
+
+__global__ void k_window_stats(StoreView s, const double* __restrict__ ticks,
+                               int32_t T, const int32_t* __restrict__ sampled,
+                               int32_t S, double delta,
+                               WinStat* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(T) * S) return;
+  const int32_t k = static_cast<int32_t>(w / S), si = static_cast<int32_t>(w % S);
+  const double t = ticks[k];
+  const double t0 = t - delta;  // store.query({r}, t - cfg.delta_ms, t)
+  const int32_t r = sampled[si];
+  uint32_t nrec = 0, ncomp = 0, hstate = 0;
+  unsigned long long bytes = 0;
+  double mn = INFINITY, mx = -INFINITY;
+  if (r >= 0 && r < s.R) {
+    const uint32_t e = s.rank_off[r + 1];
+    for (uint32_t p = s.rank_off[r] + lane; p < e; p += 32) {
+      const double x = s.ts[p];
+      if (x < t0 || x > t) continue;
+      ++nrec;
+      if (ko_kind(s.ko[p]) == CSG_KIND_COMPLETION) {
+        ++ncomp;
+        bytes += s.pb[p];
+        mn = fmin(mn, x);
+        mx = fmax(mx, x);
+      } else {
+        hstate = 1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nrec += __shfl_xor_sync(0xffffffffu, nrec, o);
+    ncomp += __shfl_xor_sync(0xffffffffu, ncomp, o);
+    hstate |= __shfl_xor_sync(0xffffffffu, hstate, o);
+    bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    WinStat ws;
+    ws.n_rec = nrec;
+    ws.n_comp = ncomp;
+    ws.has_state = hstate;
+    ws.pad = 0;
+    ws.bytes = bytes;
+    ws.min_end = mn;
+    ws.max_end = mx;
+    out[w] = ws;
+  }
+}
+
+// One baseline step (trigger.cpp:76-133). Returns 0 none, 1 failure,
+// 2 straggler.
+__device__ int ema_step(TrigSlot& b, const WinStat& w, const TrigParams& p) {
+  const bool had_prev = b.had_prev != 0;
+  b.had_prev = w.n_rec > 0 ? 1 : 0;
+  if (w.n_comp == 0) {
+    const bool failure = w.has_state || (w.n_rec == 0 && had_prev);
+    return failure ? 1 : 0;
+  }
+  // Σ (double)msg_bytes: integer-valued, exact below 2^53 in any order.
+  const double window_bytes = static_cast<double>(w.bytes);
+  const double throughput = __ddiv_rn(window_bytes, p.delta);
+  double mean_interval = 0;
+  bool interval_defined = false;
+  if (w.n_comp >= 2) {
+    mean_interval = __ddiv_rn(__dsub_rn(w.max_end, w.min_end),
+                              static_cast<double>(w.n_comp - 1));
+    interval_defined = true;
+  }
+  const bool warmed = b.updates >= p.warmup;
+  bool straggler = false;
+  if (warmed && b.throughput > 0 &&
+      throughput <= __dmul_rn(p.drop, b.throughput))
+    straggler = true;
+  if (warmed && !straggler && interval_defined && b.interval_defined &&
+      b.op_interval_ms > 0 &&
+      mean_interval >= __dmul_rn(p.inflate, b.op_interval_ms))
+    straggler = true;
+  if (straggler) return 2;
+  const double keep = __dsub_rn(1.0, p.alpha);
+  b.throughput = b.updates == 0
+                     ? throughput
+                     : __dadd_rn(__dmul_rn(keep, b.throughput),
+                                 __dmul_rn(p.alpha, throughput));
+  if (interval_defined) {
+    b.op_interval_ms = !b.interval_defined
+                           ? mean_interval
+                           : __dadd_rn(__dmul_rn(keep, b.op_interval_ms),
+                                       __dmul_rn(p.alpha, mean_interval));
+    b.interval_defined = 1;
+  }
+  b.updates += 1;
+  return 0;
+}
+
+// run_detection: thread per sampled rank, sequential over ticks.
+__global__ void k_ema_ticks(const WinStat* __restrict__ ws, int32_t T, int32_t S,
+                            TrigParams p, uint8_t* __restrict__ trip) {
+  const int32_t si = blockIdx.x * blockDim.x + threadIdx.x;
+  if (si >= S) return;
+  TrigSlot b{0, 0, 0, 0, 0, 0};
+  for (int32_t k = 0; k < T; ++k)
+    trip[static_cast<int64_t>(k) * S + si] =
+        static_cast<uint8_t>(ema_step(b, ws[static_cast<int64_t>(k) * S + si], p));
+}
+
+// Lowest tripped sampled rank wins (sampled is ascending); compact the
+// tripped ticks in tick order. One block.
+__global__ void k_pick_trips(const uint8_t* __restrict__ trip,
+                             const double* __restrict__ ticks, int32_t T,
+                             const int32_t* __restrict__ sampled, int32_t S,
+                             csg_trigger_event* __restrict__ events,
+                             int32_t* __restrict__ n_events) {
+  __shared__ int32_t base;
+  __shared__ int32_t wsum[32];
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t k0 = 0; k0 < T; k0 += blockDim.x) {
+    const int32_t k = k0 + threadIdx.x;
+    int kind = -1, rank = -1;
+    if (k < T) {
+      for (int32_t s = 0; s < S; ++s) {
+        const uint8_t c = trip[static_cast<int64_t>(k) * S + s];
+        if (c) {
+          kind = c == 1 ? CSG_TRIGGER_FAILURE : CSG_TRIGGER_STRAGGLER;
+          rank = sampled[s];
+          break;
+        }
+      }
+    }
+    const int hit = kind >= 0;
+    // block exclusive scan of hit
+    int x = hit;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const int excl = (warp ? wsum[warp - 1] : 0) + x - hit;
+    if (hit) {
+      csg_trigger_event e;
+      e.kind = kind;
+      e.suspect_rank = rank;
+      e.time_ms = ticks[k];
+      events[base + excl] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_events = base;
+}
+
+// csg_evaluate: one tick, the caller's sampled list in order (duplicates
+// allowed, exactly like the reference loop), baselines persisted in the
+// state's per-rank slots.
+__global__ void k_ema_single(const WinStat* __restrict__ ws,
+                             const int32_t* __restrict__ sampled, int32_t S,
+                             TrigParams p, double t, TrigSlot* __restrict__ slots,
+                             csg_trigger_event* __restrict__ ev,
+                             int32_t* __restrict__ tripped) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t hit = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    const int32_t r = sampled[s];
+    const int c = ema_step(slots[r], ws[s], p);
+    if (c && !hit) {
+      hit = 1;
+      ev->kind = c == 1 ? CSG_TRIGGER_FAILURE : CSG_TRIGGER_STRAGGLER;
+      ev->suspect_rank = r;
+      ev->time_ms = t;
+    }
+  }
+  *tripped = hit;
+}
+
+// Tick times by FP accumulation exactly as runner.cpp:69-71:
+// for (t = I; t <= last_ts; t += I) if (t >= delta) evaluate.
+__global__ void k_ticks(double I, double last_ts, double delta, int64_t cap,
+                        double* __restrict__ ticks, int32_t* __restrict__ n) {
+  if (threadIdx.x || blockIdx.x) return;
+  int64_t c = 0;
+  for (double t = I; t <= last_ts; t = __dadd_rn(t, I)) {
+    if (t < delta) continue;
+    if (c < cap) ticks[c] = t;
+    ++c;
+  }
+  *n = static_cast<int32_t>(c < cap ? c : cap);
+}
+
+}  // namespace
+
+void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
+                          const int32_t* d_sampled, int32_t S, double delta,
+                          WinStat* d_out) {
+  if (T <= 0 || S <= 0) return;
+  csg_ctx* c = s->ctx;
+  const uint64_t warps = static_cast<uint64_t>(T) * S;
+  k_window_stats<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                   c->stream>>>(s->view(), d_ticks, T, d_sampled, S, delta,
+                                d_out);
+  ++c->lc.launches;
+  CSG_CUDA(cudaGetLastError());
+}
+
+int32_t trigger_ticks(csg_store* s, double I, double delta, DevBuf& ticks) {
+  csg_ctx* c = s->ctx;
+  // The loop runs while t <= last_ts; bound the tick count generously.
+  const double est = s->last_ts / I;
+  if (!(est < 5e7))
+    throw Error(CSG_ERR_RUNTIME, "run_detection: too many detection ticks");
+  const int64_t cap = static_cast<int64_t>(est) + 4;
+  ticks.ensure(static_cast<size_t>(cap) * 8 + 8);
+  DevBuf dn;
+  dn.ensure(4);
+  k_ticks<<<1, 1, 0, c->stream>>>(I, s->last_ts, delta, cap, ticks.as<double>(),
+                                  dn.as<int32_t>());
+  ++c->lc.launches;
+  int32_t n = 0;
+  CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CSG_CUDA(cudaStreamSynchronize(c->stream));
+  return n;
+}
+
+int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
+                    const int32_t* d_sampled, int32_t S, const TrigParams& p,
+                    DevBuf& events) {
+  csg_ctx* c = s->ctx;
+  events.ensure(static_cast<size_t>(T + 1) * sizeof(csg_trigger_event));
+  if (T <= 0 || S <= 0) return 0;
+  DevBuf ws, trip, dn;
+  ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
+  trip.ensure(static_cast<size_t>(T) * S);
+  dn.ensure(4);
+  trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
+  k_ema_ticks<<<(S + 127) / 128, 128, 0, c->stream>>>(ws.as<WinStat>(), T, S, p,
+                                                      trip.as<uint8_t>());
+  ++c->lc.launches;
+  k_pick_trips<<<1, 1024, 0, c->stream>>>(trip.as<uint8_t>(), d_ticks, T,
+                                          d_sampled, S,
+                                          events.as<csg_trigger_event>(),
+                                          dn.as<int32_t>());
+  ++c->lc.launches;
+  int32_t n = 0;
+  CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CSG_CUDA(cudaStreamSynchronize(c->stream));
+  return n;
+}
+
+void trigger_evaluate_single(csg_store* s, const int32_t* sampled, int32_t S,
+                             double t, csg_trigger_state* state,
+                             const TrigParams& p, int* tripped,
+                             csg_trigger_event* event) {
+  csg_ctx* c = s->ctx;
+  *tripped = 0;
+  if (S <= 0) return;
+  int32_t mx = 0;
+  for (int32_t i = 0; i < S; ++i) {
+    if (sampled[i] < 0)
+      throw Error(CSG_ERR_ARG, "evaluate: negative sampled rank");
+    mx = std::max(mx, sampled[i]);
+  }
+  state->ensure(mx + 1);
+  DevBuf d_s, d_t, ws, ev, tr;
+  d_s.ensure(S * 4);
+  d_t.ensure(8);
+  ws.ensure(S * sizeof(WinStat));
+  ev.ensure(sizeof(csg_trigger_event));
+  tr.ensure(4);
+  CSG_CUDA(cudaMemcpyAsync(d_s.p, sampled, S * 4, cudaMemcpyHostToDevice, c->stream));
+  CSG_CUDA(cudaMemcpyAsync(d_t.p, &t, 8, cudaMemcpyHostToDevice, c->stream));
+  trigger_window_stats(s, d_t.as<double>(), 1, d_s.as<int32_t>(), S, p.delta,
+                       ws.as<WinStat>());
+  k_ema_single<<<1, 32, 0, c->stream>>>(ws.as<WinStat>(), d_s.as<int32_t>(), S, p,
+                                        t, state->slots.as<TrigSlot>(),
+                                        ev.as<csg_trigger_event>(),
+                                        tr.as<int32_t>());
+  ++c->lc.launches;
+  CSG_CUDA(cudaMemcpyAsync(tripped, tr.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CSG_CUDA(cudaMemcpyAsync(event, ev.p, sizeof(*event), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CSG_CUDA(cudaStreamSynchronize(c->stream));
+  CSG_CUDA(cudaGetLastError());
+}
+
+}  // namespace csg
+
+void csg_trigger_state::ensure(int32_t ranks) {
+  if (ranks <= cap) return;
+  int32_t nc = cap ? cap : 64;
+  while (nc < ranks) nc *= 2;
+  csg::DevBuf nb;
+  nb.ensure(static_cast<size_t>(nc) * sizeof(TrigSlot));
+  CSG_CUDA(cudaMemsetAsync(nb.p, 0, static_cast<size_t>(nc) * sizeof(TrigSlot),
+                           ctx->stream));
+  if (cap)
+    CSG_CUDA(cudaMemcpyAsync(nb.p, slots.p, static_cast<size_t>(cap) * sizeof(TrigSlot),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+  std::swap(slots.p, nb.p);
+  std::swap(slots.bytes, nb.bytes);
+  cap = nc;
+}

@@ -1,0 +1,74 @@
+"""GPU parity on the reference's fault catalog (clean + scenarios 1-7).
+
+Golden inputs/outputs come from the reference itself
+(tests/golden/make_golden.py): the reference simulator's trace and the
+reference run_detection's reports. The B200 engine must reproduce the
+structured reports (suspects, exonerated, affected groups, evidence,
+records_scanned) exactly and the reports_to_jsonl bytes through the drop-in
+C API."""
+import json
+import os
+
+import pytest
+
+from tests.conftest import GOLDEN
+from tests.golden import codec
+
+CATALOG = ["clean"] + [f"scenario{i}" for i in range(1, 8)]
+MANIFEST = json.load(open(os.path.join(GOLDEN, "manifest.json")))
+
+
+def golden(name):
+    recs = codec.load_file(os.path.join(GOLDEN, f"catalog_{name}.rec.xz"))
+    reports = open(os.path.join(GOLDEN, f"catalog_{name}.reports.jsonl")).read()
+    full = [json.loads(l) for l in open(os.path.join(GOLDEN, f"catalog_{name}.full.jsonl"))]
+    return recs, reports, full
+
+
+def first_diff(got, want):
+    for i, (a, b) in enumerate(zip(got, want)):
+        if a != b:
+            return i, a, b
+    return len(want), got[len(want):], want[len(got):]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CATALOG)
+def test_catalog_structured_reports(eng, name):
+    recs, _, full = golden(name)
+    assert len(recs) == MANIFEST[name]["records"]
+    scen = eng.Scenario.load(os.path.join(GOLDEN, "configs", name + ".json"))
+    topo, prog = scen.layout()
+    tcfg, acfg, seed = scen.configs()
+    store = eng.TraceStore(records=recs)
+    model = eng.Model(topo, prog)
+    got, sampled = eng.run_detection(store, model, tcfg, acfg, seed)
+    assert sampled == MANIFEST[name]["sampled"]
+    assert len(got) == len(full), first_diff(got, full)
+    assert got == full, first_diff(got, full)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CATALOG)
+def test_catalog_reports_jsonl_bytes_c_api(eng, name):
+    recs, reports, full = golden(name)
+    scen = eng.Scenario.load(os.path.join(GOLDEN, "configs", name + ".json"))
+    res = eng.run_analyze_packed(scen, recs)
+    assert res.trigger_count == len(full)
+    assert res.reports_jsonl == reports
+    assert res.summary_json == ('{"completed":false,"end_ms":0,"events":0,"records":0,'
+                                '"triggers":%d,"rank_completion_ms":[]}' % len(full))
+
+
+@pytest.mark.gpu
+def test_catalog_c_api_file_path(eng, oracle, tmp_path):
+    """collsight_run_analyze on a JSONL file written by the reference."""
+    cfg_path = os.path.join(GOLDEN, "configs", "scenario1.json")
+    recs, text = oracle.simulate(open(cfg_path).read(), with_jsonl=True)
+    trace = tmp_path / "trace.jsonl"
+    trace.write_text(text)
+    out = tmp_path / "reports.jsonl"
+    res = eng.run_analyze(eng.Scenario.load(cfg_path), str(trace), str(out))
+    _, reports, _ = golden("scenario1")
+    assert res.reports_jsonl == reports
+    assert out.read_text() == reports
