@@ -1089,7 +1089,7 @@ __device__ void decide_failure(const DecideArgs& a, int32_t j, BlockShared& sh,
   const Cand* cands = a.pools.cand + sh.cand_base;
   uint32_t* idx = scratch;
   uint32_t* ord = scratch + C;
-  int64_t* U = reinterpret_cast<int64_t*>(scratch + 2 * C + (C & 1));
+  int64_t* U = reinterpret_cast<int64_t*>(scratch + 2 * C);  // 8-aligned
   uint32_t* ret = reinterpret_cast<uint32_t*>(U + C);
   uint8_t* keep = reinterpret_cast<uint8_t*>(ret + C);
   uint32_t* tail = reinterpret_cast<uint32_t*>(keep + ((C + 3) & ~3));
@@ -1548,7 +1548,7 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
 
 __global__ void __launch_bounds__(kDecideThreads)
     k_decide(DecideArgs a) {
-  extern __shared__ unsigned char dyn[];
+  extern __shared__ __align__(16) unsigned char dyn[];
   BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
   const int32_t j = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -1761,7 +1761,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   spt = std::max<uint64_t>(spt, mwords + 2 * std::max<uint64_t>(
                                                 std::max<uint64_t>(m_max, s->max_seg),
                                                 8 * C2));
-  spt += 64;
+  spt = (spt + 64 + 3) & ~3ull;  // 16-byte aligned per-trip slices
   if (spt > 0xFFFFFFF0ull)
     throw Error(CSG_ERR_RUNTIME, "engine: per-trip scratch exceeds 2^32 words");
 
