@@ -55,6 +55,19 @@ collsight_status collsight_b200_parse_trace(const char* text, size_t len,
                                             size_t* n);
 void collsight_b200_free(void* p);
 
+/* The engine context the collsight_* calls run on (created on first use on
+ * device $COLLSIGHT_B200_DEVICE, default 0), for csg_ctx_stats /
+ * csg_ctx_profile / csg_ctx_kernel_stats. */
+collsight_status collsight_b200_engine_context(csg_ctx** out);
+
+/* Synthetic trace of the scenario's layout/program/faults in emission order
+ * (benchmark input generator, csrc/host/synth.cpp; not the reference
+ * simulator). target_records = 0 means no cap; otherwise the earliest
+ * target_records records are kept. Caller frees with collsight_b200_free. */
+collsight_status collsight_b200_synthesize(const collsight_scenario* scenario,
+                                           uint64_t target_records,
+                                           csg_packed_record** out, size_t* n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -217,6 +217,16 @@ void csg_ctx_free(csg_ctx* ctx);
  * kernel launches issued. */
 csg_status csg_ctx_stats(csg_ctx* ctx, double* device_ms, uint64_t* launches);
 void csg_ctx_reset_stats(csg_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (off by default).
+ * csg_ctx_kernel_stats writes {"kernel": [total_ms, launches], ...} as JSON
+ * (NUL-terminated, truncated to cap) and the byte counters of the
+ * host<->device copies the engine issued since the last reset. */
+csg_status csg_ctx_profile(csg_ctx* ctx, int enable);
+csg_status csg_ctx_kernel_stats(csg_ctx* ctx, char* json, size_t cap,
+                                uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* Marks the store's device index stale so the next analysis rebuilds it
+ * (the benchmark re-times ingest + index every step). */
+csg_status csg_store_invalidate(csg_store* store);
 
 /* TraceStore (proj/include/collsight/trace.hpp:101-124).
  * append copies `n` packed records from HOST memory (pinned or pageable)

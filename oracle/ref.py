@@ -242,3 +242,30 @@ def check_rc_table(c, peer=None):
     _check(lib().ref_check_rc_table(C.byref(a), C.byref(b) if b else None,
                                     C.byref(cat), C.byref(side)))
     return cat.value, side.value
+
+
+class RefStore:
+    """A reference TraceStore built once in this process (CPU leg of bench)."""
+
+    def __init__(self, recs: np.ndarray):
+        recs, p, n = _recs(recs)
+        lib().ref_store_new.restype = C.c_void_p
+        self.h = C.c_void_p(lib().ref_store_new(p, n))
+        self.n = len(recs)
+
+    def window(self, cfg_json: str, t: float):
+        """-> (evaluate seconds, analyze seconds, tripped, full report or None)"""
+        e = C.c_double()
+        a = C.c_double()
+        tr = C.c_int()
+        full = C.c_void_p()
+        _check(lib().ref_window(self.h, cfg_json.encode(), C.c_double(t), C.byref(e),
+                                C.byref(a), C.byref(tr), C.byref(full)))
+        rep = json.loads(_take(full)) if tr.value else None
+        return e.value, a.value, bool(tr.value), rep
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            lib().ref_store_free.argtypes = [C.c_void_p]
+            lib().ref_store_free(self.h)
+            self.h = None

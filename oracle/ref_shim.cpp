@@ -526,4 +526,47 @@ int ref_check_rc_table(const csg_progress* c, const csg_progress* peer,
   });
 }
 
+// ---- benchmark CPU leg: one store, many windows ----------------------------
+
+void* ref_store_new(const csg_packed_record* recs, size_t n) {
+  auto* st = new TraceStore();
+  for (std::size_t i = 0; i < n; ++i) st->append(unpack(recs[i], i));
+  return st;
+}
+
+void ref_store_free(void* s) { delete static_cast<TraceStore*>(s); }
+
+// One detection window of the reference: evaluate at tick
+// t with the scenario's sampled ranks (fresh trigger state), then analyze
+// its trigger if it tripped. Times each phase separately.
+int ref_window(void* store, const char* cfg_json, double t, double* eval_s,
+               double* analyze_s, int* tripped, char** full) {
+  return guard([&] {
+    const ScenarioConfig cfg = parse_scenario(cfg_json);
+    const Topology topo = cfg.build_topology();
+    const OpProgram program = cfg.build_program(topo);
+    const TraceStore& st = *static_cast<const TraceStore*>(store);
+    const auto sampled = sample_ranks(topo, cfg.trigger, cfg.sim.seed);
+    TriggerState state;
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto trig = evaluate(st, sampled, t, state, cfg.trigger);
+    const auto t1 = std::chrono::steady_clock::now();
+    *eval_s = std::chrono::duration<double>(t1 - t0).count();
+    *tripped = trig.has_value() ? 1 : 0;
+    *analyze_s = 0;
+    if (trig) {
+      AnalysisContext ctx;
+      ctx.topo = &topo;
+      ctx.program = &program;
+      ctx.cfg = cfg.analysis;
+      const auto t2 = std::chrono::steady_clock::now();
+      const RootCauseReport r = analyze(st, ctx, *trig);
+      const auto t3 = std::chrono::steady_clock::now();
+      *analyze_s = std::chrono::duration<double>(t3 - t2).count();
+      if (full) *full = dup(full_report(r));
+    }
+    return 0;
+  });
+}
+
 }  // extern "C"

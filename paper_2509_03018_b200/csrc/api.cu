@@ -3,6 +3,7 @@
 // crosses this boundary; every entry point maps failures to csg_status and
 // the thread-local message of csg_last_error().
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -238,6 +239,49 @@ void csg_ctx_reset_stats(csg_ctx* c) {
   if (!c) return;
   c->device_ms = 0;
   c->lc.launches = 0;
+  c->h2d_bytes = c->d2h_bytes = 0;
+  c->lc.prof.totals.clear();
+}
+
+csg_status csg_ctx_profile(csg_ctx* c, int enable) {
+  if (!c) return fail(CSG_ERR_ARG, "null argument");
+  c->lc.prof.enabled = enable != 0;
+  return CSG_OK;
+}
+
+csg_status csg_ctx_kernel_stats(csg_ctx* c, char* json, size_t cap,
+                                uint64_t* h2d, uint64_t* d2h) {
+  if (!c) return fail(CSG_ERR_ARG, "null argument");
+  return guarded([&] {
+    CSG_CUDA(cudaStreamSynchronize(c->stream));
+    c->lc.prof.collect();
+    std::string o = "{";
+    bool first = true;
+    for (const auto& [name, t] : c->lc.prof.totals) {
+      if (!first) o += ",";
+      first = false;
+      char buf[160];
+      snprintf(buf, sizeof(buf), "\"%s\":[%.6f,%llu]", name.c_str(), t.first,
+               static_cast<unsigned long long>(t.second));
+      o += buf;
+    }
+    o += "}";
+    if (json && cap) {
+      const size_t k = std::min(cap - 1, o.size());
+      std::memcpy(json, o.data(), k);
+      json[k] = 0;
+    }
+    if (h2d) *h2d = c->h2d_bytes;
+    if (d2h) *d2h = c->d2h_bytes;
+    return CSG_OK;
+  });
+}
+
+csg_status csg_store_invalidate(csg_store* s) {
+  if (!s) return fail(CSG_ERR_ARG, "null argument");
+  s->indexed = false;
+  s->op_indexed = false;
+  return CSG_OK;
 }
 
 csg_status csg_store_create(csg_ctx* ctx, csg_store** out) {
@@ -288,6 +332,7 @@ static csg_status append_impl(csg_store* s, const csg_packed_record* src,
     }
     CSG_CUDA(cudaMemcpyAsync(s->recs.as<csg_packed_record>() + s->n, src,
                              n * sizeof(csg_packed_record), kind, s->ctx->stream));
+    if (kind == cudaMemcpyHostToDevice) s->ctx->h2d_bytes += n * sizeof(csg_packed_record);
     s->n += n;
     s->indexed = false;
     s->op_indexed = false;
@@ -639,6 +684,7 @@ csg_status csg_run_detection(csg_store* store, const csg_model* model,
         CSG_CUDA(cudaMemcpyAsync(trips.data(), events.p,
                                  n * sizeof(csg_trigger_event),
                                  cudaMemcpyDeviceToHost, c->stream));
+      c->d2h_bytes += n * sizeof(csg_trigger_event);
       CSG_CUDA(cudaStreamSynchronize(c->stream));
     }
     RcaResult r;

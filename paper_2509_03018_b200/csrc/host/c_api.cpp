@@ -251,4 +251,27 @@ collsight_status collsight_b200_parse_trace(const char* text, size_t len,
 
 void collsight_b200_free(void* p) { std::free(p); }
 
+collsight_status collsight_b200_engine_context(csg_ctx** out) {
+  if (!out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_mu);
+    *out = engine();
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_synthesize(const collsight_scenario* s,
+                                           uint64_t target,
+                                           csg_packed_record** out, size_t* n) {
+  if (!s || !out || !n) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const auto v = csh::synthesize(s->cfg, target);
+    *n = v.size();
+    *out = static_cast<csg_packed_record*>(
+        std::malloc(sizeof(csg_packed_record) * (v.size() + 1)));
+    if (!v.empty()) std::memcpy(*out, v.data(), v.size() * sizeof(csg_packed_record));
+    return COLLSIGHT_OK;
+  });
+}
+
 }  // extern "C"

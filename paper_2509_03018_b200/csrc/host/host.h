@@ -85,6 +85,9 @@ struct Scenario {
 Scenario parse_scenario(const std::string& json_text);
 Scenario load_scenario_file(const std::string& path);
 
+// Synthetic benchmark traces (synth.cpp). target = 0: no record cap.
+std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target);
+
 // Trace codec.
 std::vector<csg_packed_record> parse_trace_text(std::string_view text);
 std::vector<csg_packed_record> load_trace_file(const std::string& path);

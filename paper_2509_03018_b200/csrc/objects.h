@@ -13,6 +13,7 @@ struct csg_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   double device_ms = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
   csg::LaunchCounter lc;
   // shared scratch
   csg::DevBuf scratch_a, scratch_b, scratch_c, pinned_flag_dev;
@@ -31,6 +32,7 @@ struct csg_ctx {
         cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop);
         c->device_ms += ms;
       }
+      c->lc.prof.collect();
     }
   };
 };

@@ -1650,11 +1650,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     int wpb = 32768 / (nch * 4);
     wpb = std::max(1, std::min(8, wpb));
     const uint64_t warps = static_cast<uint64_t>(R) * J;
-    k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
-                     wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
-                                          rs.as<RankSum>(),
-                                          chan_pos.as<uint32_t>(), nch);
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_rank_summary", st);
+      k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
+                       wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
+                                            rs.as<RankSum>(),
+                                            chan_pos.as<uint32_t>(), nch);
+    }
   }
   // K2/K3: straggler iteration tables
   DevBuf tbl_s, tbl_e, gi, gi_last;
@@ -1680,18 +1682,22 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       CSG_CUDA(cudaMemsetAsync(tbl_e.p, 0, cells * 8, st));
       if (R > 0) {
         const uint64_t warps = static_cast<uint64_t>(R) * Js;
-        k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
-                        st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
-                              M, tbl_s.as<unsigned long long>(),
-                              tbl_e.as<unsigned long long>());
-        ++c->lc.launches;
+        {
+          ProfScope ps_(c->lc, "k_iter_tables", st);
+          k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                          st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
+                                M, tbl_s.as<unsigned long long>(),
+                                tbl_e.as<unsigned long long>());
+        }
       }
       const uint64_t gw = static_cast<uint64_t>(G) * Js;
-      k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
-          mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
-          tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
-          gi.as<GroupIter>(), gi_last.as<int64_t>());
-      ++c->lc.launches;
+      {
+        ProfScope ps_(c->lc, "k_group_iters", st);
+        k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
+            mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
+            tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
+            gi.as<GroupIter>(), gi_last.as<int64_t>());
+      }
     }
   }
   // K4: affected groups
@@ -1699,10 +1705,12 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   aff.ensure(static_cast<size_t>(J) * std::max(G, 1) * 4);
   aff_flag.ensure(static_cast<size_t>(J) * std::max(G, 1));
   n_aff.ensure(static_cast<size_t>(J) * 4);
-  k_affected<<<J, 256, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
-                                gi.as<GroupIter>(), aff.as<int32_t>(),
-                                aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_affected", st);
+    k_affected<<<J, 256, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
+                                  gi.as<GroupIter>(), aff.as<int32_t>(),
+                                  aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
+  }
   std::vector<int32_t> h_naff(J);
   out.aff.assign(static_cast<size_t>(J) * G, 0);
   CSG_CUDA(cudaMemcpyAsync(h_naff.data(), n_aff.p, J * 4, cudaMemcpyDeviceToHost, st));
@@ -1728,11 +1736,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
         h_sg[q] = static_cast<uint32_t>(g);
     upload(slot_group, h_sg, st);
     const uint64_t warps = static_cast<uint64_t>(M) * Js;
-    k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
-        sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
-        slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
-        aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_flow", st);
+      k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
+          sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+          slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+          aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
+    }
   }
 
   // K6: decide. Pool sizes from the affected lists.
@@ -1829,8 +1839,10 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     a.pools.used = p_used.as<unsigned long long>();
     CSG_CUDA(cudaMemsetAsync(p_used.p, 0, 8 * 8, st));
     // keep K5 errors, clear decide-retry flags
-    k_decide<<<J, kDecideThreads, shm, st>>>(a);
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_decide", st);
+      k_decide<<<J, kDecideThreads, shm, st>>>(a);
+    }
     CSG_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
     CSG_CUDA(cudaMemcpyAsync(used, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
     CSG_CUDA(cudaStreamSynchronize(st));
@@ -1867,6 +1879,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     CSG_CUDA(cudaMemcpyAsync(out.ev.data(), p_ev.p, used[P_EV] * sizeof(csg_evidence),
                              cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));
+  c->d2h_bytes += J * sizeof(TripOut) + used[P_SUS] * sizeof(csg_suspect) +
+                  used[P_EV] * sizeof(csg_evidence) +
+                  static_cast<uint64_t>(J) * (4 + static_cast<uint64_t>(G) * 4);
   out.trips = to;
 }
 

@@ -183,13 +183,17 @@ void scan_rec(uint32_t* data, uint64_t n, uint32_t* tmp, cudaStream_t st,
               LaunchCounter& lc) {
   if (n == 0) return;
   const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-  k_scan_block<<<static_cast<unsigned>(nb), kThreads, 0, st>>>(
-      data, n, nb > 1 ? tmp : nullptr);
-  ++lc.launches;
+  {
+    ProfScope ps_(lc, "k_scan_block", st);
+    k_scan_block<<<static_cast<unsigned>(nb), kThreads, 0, st>>>(
+        data, n, nb > 1 ? tmp : nullptr);
+  }
   if (nb > 1) {
     scan_rec(tmp, nb, tmp + nb, st, lc);
-    k_scan_add<<<static_cast<unsigned>(nb), kThreads, 0, st>>>(data, n, tmp);
-    ++lc.launches;
+    {
+      ProfScope ps_(lc, "k_scan_add", st);
+      k_scan_add<<<static_cast<unsigned>(nb), kThreads, 0, st>>>(data, n, tmp);
+    }
   }
 }
 
@@ -209,13 +213,17 @@ void radix_sort_impl(K* keys, uint32_t* vals, uint64_t n, int nbits,
   uint32_t* vb = s.vals2.as<uint32_t>();
   int passes = 0;
   for (int shift = 0; shift < nbits; shift += 8, ++passes) {
-    k_upsweep<K><<<ntiles, kThreads, 0, st>>>(ka, n, shift,
-                                              s.counts.as<uint32_t>(), ntiles);
-    ++lc.launches;
+    {
+      ProfScope ps_(lc, "k_upsweep", st);
+      k_upsweep<K><<<ntiles, kThreads, 0, st>>>(ka, n, shift,
+                                                s.counts.as<uint32_t>(), ntiles);
+    }
     scan_rec(s.counts.as<uint32_t>(), nc, s.scan_tmp.as<uint32_t>(), st, lc);
-    k_downsweep<K><<<ntiles, kThreads, 0, st>>>(
-        ka, va, kb, vb, n, shift, s.counts.as<uint32_t>(), ntiles);
-    ++lc.launches;
+    {
+      ProfScope ps_(lc, "k_downsweep", st);
+      k_downsweep<K><<<ntiles, kThreads, 0, st>>>(
+          ka, va, kb, vb, n, shift, s.counts.as<uint32_t>(), ntiles);
+    }
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }

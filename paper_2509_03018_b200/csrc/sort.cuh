@@ -7,12 +7,77 @@
 // serves the straggler self-evidence pass (proj/src/rca.cpp:803-815).
 #pragma once
 
+#include <map>
+#include <string>
+#include <vector>
+
 #include "engine_internal.h"
 
 namespace csg {
 
+// Per-kernel CUDA-event timing on the launching stream (enabled on demand;
+// the benchmark reads it to compute each kernel's achieved bandwidth).
+struct Profiler {
+  bool enabled = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::map<std::string, std::pair<double, uint64_t>> totals;
+  cudaEvent_t take() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  // Call after the stream has been synchronized.
+  void collect() {
+    for (const Rec& r : pending) {
+      float ms = 0;
+      if (r.b && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+        auto& t = totals[r.name];
+        t.first += ms;
+        t.second += 1;
+      }
+    }
+    pending.clear();
+    used = 0;
+  }
+  ~Profiler() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct LaunchCounter {
   uint64_t launches = 0;
+  Profiler prof;
+};
+
+struct ProfScope {
+  LaunchCounter& lc;
+  cudaStream_t st;
+  bool on;
+  ProfScope(LaunchCounter& l, const char* name, cudaStream_t s)
+      : lc(l), st(s), on(l.prof.enabled) {
+    ++lc.launches;
+    if (on) {
+      cudaEvent_t a = lc.prof.take();
+      cudaEventRecord(a, st);
+      lc.prof.pending.push_back({name, a, nullptr});
+    }
+  }
+  ~ProfScope() {
+    if (on) {
+      cudaEvent_t b = lc.prof.take();
+      cudaEventRecord(b, st);
+      lc.prof.pending.back().b = b;
+    }
+  }
 };
 
 struct SortScratch {

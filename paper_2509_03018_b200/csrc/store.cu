@@ -300,8 +300,10 @@ void store_build_index(csg_store* s) {
   CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
                            cudaMemcpyHostToDevice, st));
   if (n) {
-    k_stats<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_stats", st);
+      k_stats<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>());
+    }
   }
   CSG_CUDA(cudaMemcpyAsync(&h, s->stats_dev.p, sizeof(h),
                            cudaMemcpyDeviceToHost, st));
@@ -342,26 +344,34 @@ void store_build_index(csg_store* s) {
   s->pa.ensure(n * 8 + 8);
   s->pb.ensure(n * 8 + 8);
   if (n) {
-    k_rank_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->keys.as<uint32_t>(),
-                                             s->perm.as<uint32_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_rank_keys", st);
+      k_rank_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->keys.as<uint32_t>(),
+                                               s->perm.as<uint32_t>());
+    }
     radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
                    bits_for(static_cast<uint64_t>(R > 0 ? R - 1 : 0)), s->sort,
                    st, c->lc);
-    k_gather<<<grid_for(n), 256, 0, st>>>(
-        recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
-        s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
-        s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_gather", st);
+      k_gather<<<grid_for(n), 256, 0, st>>>(
+          recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
+          s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
+          s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
+    }
   }
-  k_rank_off<<<(R + 1 + 255) / 256, 256, 0, st>>>(s->keys.as<uint32_t>(), n, R,
-                                                 s->rank_off.as<uint32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_rank_off", st);
+    k_rank_off<<<(R + 1 + 255) / 256, 256, 0, st>>>(s->keys.as<uint32_t>(), n, R,
+                                                   s->rank_off.as<uint32_t>());
+  }
   if (n && R) {
-    k_runmax<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
-        s->ts.as<double>(), s->rank_off.as<uint32_t>(), R,
-        s->runmax.as<double>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_runmax", st);
+      k_runmax<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
+          s->ts.as<double>(), s->rank_off.as<uint32_t>(), R,
+          s->runmax.as<double>());
+    }
   }
   {
     std::vector<uint32_t> ro(static_cast<size_t>(R) + 1);
@@ -388,8 +398,10 @@ void store_build_op_index(csg_store* s, int32_t opn) {
   flags.ensure(n * 4 + 4);
   uint32_t count = 0;
   if (n) {
-    k_opidx_flags<<<grid_for(n), 256, 0, st>>>(v, flags.as<uint32_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_opidx_flags", st);
+      k_opidx_flags<<<grid_for(n), 256, 0, st>>>(v, flags.as<uint32_t>());
+    }
     // total = last exclusive offset + last flag
     uint32_t last_flag = 0;
     CSG_CUDA(cudaMemcpyAsync(&last_flag, flags.as<uint32_t>() + n - 1, 4,
@@ -405,20 +417,24 @@ void store_build_op_index(csg_store* s, int32_t opn) {
   s->opidx_keys.ensure(static_cast<size_t>(count) * 8 + 8);
   s->opidx_pos.ensure(static_cast<size_t>(count) * 4 + 4);
   if (count) {
-    k_opidx_scatter<<<grid_for(n), 256, 0, st>>>(
-        v, flags.as<uint32_t>(), s->min_op, s->opidx_keys.as<uint64_t>(),
-        s->opidx_pos.as<uint32_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_opidx_scatter", st);
+      k_opidx_scatter<<<grid_for(n), 256, 0, st>>>(
+          v, flags.as<uint32_t>(), s->min_op, s->opidx_keys.as<uint64_t>(),
+          s->opidx_pos.as<uint32_t>());
+    }
     const uint64_t range = static_cast<uint64_t>(s->max_op - s->min_op);
     radix_sort_u64(s->opidx_keys.as<uint64_t>(), s->opidx_pos.as<uint32_t>(),
                    count, bits_for(range), s->sort, st, c->lc);
   }
   s->opidx_rank.ensure(static_cast<size_t>(count) * 4 + 4);
   if (count) {
-    k_opidx_rank<<<grid_for(count), 256, 0, st>>>(
-        s->view(), s->opidx_pos.as<uint32_t>(), count,
-        s->opidx_rank.as<int32_t>());
-    ++c->lc.launches;
+    {
+      ProfScope ps_(c->lc, "k_opidx_rank", st);
+      k_opidx_rank<<<grid_for(count), 256, 0, st>>>(
+          s->view(), s->opidx_pos.as<uint32_t>(), count,
+          s->opidx_rank.as<int32_t>());
+    }
   }
   CSG_CUDA(cudaGetLastError());
   s->op_indexed = true;
@@ -449,9 +465,11 @@ void store_query(csg_store* s, const int32_t* ranks, size_t nr, double t0,
   CSG_CUDA(cudaMemcpyAsync(d_ranks.p, rs.data(), k * 4, cudaMemcpyHostToDevice, st));
   StoreView v = s->view();
   const unsigned g = static_cast<unsigned>((static_cast<uint64_t>(k) * 32 + 255) / 256);
-  k_query_count<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
-                                   d_counts.as<uint32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_query_count", st);
+    k_query_count<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
+                                     d_counts.as<uint32_t>());
+  }
   CSG_CUDA(cudaMemsetAsync(d_counts.as<uint32_t>() + k, 0, 4, st));
   exclusive_scan_u32(d_counts.as<uint32_t>(), k + 1, c->scratch_a, st, c->lc);
   uint32_t total = 0;
@@ -462,10 +480,12 @@ void store_query(csg_store* s, const int32_t* ranks, size_t nr, double t0,
   DevBuf keys, vals;
   keys.ensure(total * 8);
   vals.ensure(total * 4);
-  k_query_write<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
-                                   d_counts.as<uint32_t>(), keys.as<uint64_t>(),
-                                   vals.as<uint32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_query_write", st);
+    k_query_write<<<g, 256, 0, st>>>(v, d_ranks.as<int32_t>(), k, t0, t1,
+                                     d_counts.as<uint32_t>(), keys.as<uint64_t>(),
+                                     vals.as<uint32_t>());
+  }
   SortScratch ss;
   radix_sort_u64(keys.as<uint64_t>(), vals.as<uint32_t>(), total, 64, ss, st,
                  c->lc);
@@ -487,9 +507,11 @@ void store_last_log(csg_store* s, const int32_t* members, size_t nm, double t,
   d_o.ensure(nm * 8);
   CSG_CUDA(cudaMemcpyAsync(d_m.p, members, nm * 4, cudaMemcpyHostToDevice, st));
   const unsigned g = static_cast<unsigned>((nm * 32 + 255) / 256);
-  k_last_log<<<g, 256, 0, st>>>(s->view(), d_m.as<int32_t>(),
-                                static_cast<int32_t>(nm), t, d_o.as<uint64_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_last_log", st);
+    k_last_log<<<g, 256, 0, st>>>(s->view(), d_m.as<int32_t>(),
+                                  static_cast<int32_t>(nm), t, d_o.as<uint64_t>());
+  }
   std::vector<uint64_t> h(nm);
   CSG_CUDA(cudaMemcpyAsync(h.data(), d_o.p, nm * 8, cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));

@@ -232,10 +232,12 @@ void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
   if (T <= 0 || S <= 0) return;
   csg_ctx* c = s->ctx;
   const uint64_t warps = static_cast<uint64_t>(T) * S;
-  k_window_stats<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
-                   c->stream>>>(s->view(), d_ticks, T, d_sampled, S, delta,
-                                d_out);
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_window_stats", c->stream);
+    k_window_stats<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                     c->stream>>>(s->view(), d_ticks, T, d_sampled, S, delta,
+                                  d_out);
+  }
   CSG_CUDA(cudaGetLastError());
 }
 
@@ -249,9 +251,11 @@ int32_t trigger_ticks(csg_store* s, double I, double delta, DevBuf& ticks) {
   ticks.ensure(static_cast<size_t>(cap) * 8 + 8);
   DevBuf dn;
   dn.ensure(4);
-  k_ticks<<<1, 1, 0, c->stream>>>(I, s->last_ts, delta, cap, ticks.as<double>(),
-                                  dn.as<int32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_ticks", c->stream);
+    k_ticks<<<1, 1, 0, c->stream>>>(I, s->last_ts, delta, cap, ticks.as<double>(),
+                                    dn.as<int32_t>());
+  }
   int32_t n = 0;
   CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaStreamSynchronize(c->stream));
@@ -269,14 +273,18 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
   trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
-  k_ema_ticks<<<(S + 127) / 128, 128, 0, c->stream>>>(ws.as<WinStat>(), T, S, p,
-                                                      trip.as<uint8_t>());
-  ++c->lc.launches;
-  k_pick_trips<<<1, 1024, 0, c->stream>>>(trip.as<uint8_t>(), d_ticks, T,
-                                          d_sampled, S,
-                                          events.as<csg_trigger_event>(),
-                                          dn.as<int32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_ema_ticks", c->stream);
+    k_ema_ticks<<<(S + 127) / 128, 128, 0, c->stream>>>(ws.as<WinStat>(), T, S, p,
+                                                        trip.as<uint8_t>());
+  }
+  {
+    ProfScope ps_(c->lc, "k_pick_trips", c->stream);
+    k_pick_trips<<<1, 1024, 0, c->stream>>>(trip.as<uint8_t>(), d_ticks, T,
+                                            d_sampled, S,
+                                            events.as<csg_trigger_event>(),
+                                            dn.as<int32_t>());
+  }
   int32_t n = 0;
   CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaStreamSynchronize(c->stream));
@@ -307,11 +315,13 @@ void trigger_evaluate_single(csg_store* s, const int32_t* sampled, int32_t S,
   CSG_CUDA(cudaMemcpyAsync(d_t.p, &t, 8, cudaMemcpyHostToDevice, c->stream));
   trigger_window_stats(s, d_t.as<double>(), 1, d_s.as<int32_t>(), S, p.delta,
                        ws.as<WinStat>());
-  k_ema_single<<<1, 32, 0, c->stream>>>(ws.as<WinStat>(), d_s.as<int32_t>(), S, p,
-                                        t, state->slots.as<TrigSlot>(),
-                                        ev.as<csg_trigger_event>(),
-                                        tr.as<int32_t>());
-  ++c->lc.launches;
+  {
+    ProfScope ps_(c->lc, "k_ema_single", c->stream);
+    k_ema_single<<<1, 32, 0, c->stream>>>(ws.as<WinStat>(), d_s.as<int32_t>(), S, p,
+                                          t, state->slots.as<TrigSlot>(),
+                                          ev.as<csg_trigger_event>(),
+                                          tr.as<int32_t>());
+  }
   CSG_CUDA(cudaMemcpyAsync(tripped, tr.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaMemcpyAsync(event, ev.p, sizeof(*event), cudaMemcpyDeviceToHost,
                            c->stream));

@@ -105,6 +105,29 @@ class Context:
     def reset_stats(self):
         lib().csg_ctx_reset_stats(self.h)
 
+    def profile(self, enable: bool = True):
+        _check(lib().csg_ctx_profile(self.h, C.c_int(1 if enable else 0)))
+
+    def kernel_stats(self):
+        """-> ({kernel: (total_ms, launches)}, h2d_bytes, d2h_bytes)"""
+        buf = C.create_string_buffer(1 << 16)
+        h2d = C.c_uint64()
+        d2h = C.c_uint64()
+        _check(lib().csg_ctx_kernel_stats(self.h, buf, C.c_size_t(len(buf)),
+                                          C.byref(h2d), C.byref(d2h)))
+        return ({k: tuple(v) for k, v in json.loads(buf.value.decode()).items()},
+                h2d.value, d2h.value)
+
+    @classmethod
+    def of_c_api(cls) -> "Context":
+        """The context the collsight_* C API runs on (not owned)."""
+        c = cls.__new__(cls)
+        c.h = C.c_void_p()
+        _ccheck(lib().collsight_b200_engine_context(C.byref(c.h)))
+        c.device = -1
+        c.close = lambda: None
+        return c
+
     def close(self):
         if self.h:
             lib().csg_ctx_free(self.h)
@@ -158,6 +181,9 @@ class TraceStore:
 
     def build_index(self):
         _check(lib().csg_store_build_index(self.h))
+
+    def invalidate(self):
+        _check(lib().csg_store_invalidate(self.h))
 
     def query(self, ranks: Sequence[int], t0: float, t1: float) -> List[int]:
         r = np.ascontiguousarray(ranks, dtype=np.int32)
@@ -484,5 +510,20 @@ def parse_trace(text: str) -> np.ndarray:
     try:
         return np.frombuffer(C.string_at(out.value, n.value * 48),
                              dtype=_abi.RECORD_DTYPE).copy()
+    finally:
+        lib().collsight_b200_free(out)
+
+
+def synthesize(scenario: Scenario, target_records: int = 0) -> np.ndarray:
+    """Synthetic trace for the scenario (benchmark generator, synth.cpp)."""
+    out = C.c_void_p()
+    n = C.c_size_t()
+    _ccheck(lib().collsight_b200_synthesize(scenario.h, C.c_uint64(target_records),
+                                            C.byref(out), C.byref(n)))
+    try:
+        arr = np.empty(n.value, dtype=_abi.RECORD_DTYPE)
+        if n.value:
+            C.memmove(arr.ctypes.data, out.value, n.value * 48)
+        return arr
     finally:
         lib().collsight_b200_free(out)
