@@ -281,6 +281,7 @@ csg_status csg_store_invalidate(csg_store* s) {
   if (!s) return fail(CSG_ERR_ARG, "null argument");
   s->indexed = false;
   s->op_indexed = false;
+  s->flow_indexed = false;
   return CSG_OK;
 }
 
@@ -336,6 +337,7 @@ static csg_status append_impl(csg_store* s, const csg_packed_record* src,
     s->n += n;
     s->indexed = false;
     s->op_indexed = false;
+    s->flow_indexed = false;
     return CSG_OK;
   });
 }
@@ -355,6 +357,7 @@ csg_status csg_store_clear(csg_store* s) {
   s->n = 0;
   s->indexed = false;
   s->op_indexed = false;
+  s->flow_indexed = false;
   return CSG_OK;
 }
 
@@ -667,7 +670,9 @@ csg_status csg_run_detection(csg_store* store, const csg_model* model,
       for (size_t i = 0; i < sampled.size() && i < sampled_cap; ++i)
         sampled_out[i] = sampled[i];
     store_build_index(store);
-    DevBuf ticks, events, d_s;
+    DevBuf& ticks = c->buf("det.ticks");
+    DevBuf& events = c->buf("det.events");
+    DevBuf& d_s = c->buf("det.sampled");
     const int32_t T = trigger_ticks(store, tcfg->detect_interval_ms,
                                     tcfg->delta_ms, ticks);
     std::vector<csg_trigger_event> trips;

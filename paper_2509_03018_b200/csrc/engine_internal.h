@@ -83,6 +83,16 @@ struct StoreView {
   const uint8_t* ko = nullptr;         // kind | op_name << 1
   const uint64_t* pa = nullptr;        // start_ms bits | ready | tx << 32
   const uint64_t* pb = nullptr;        // msg_bytes | done
+  const uint32_t* rank_of = nullptr;   // rank per rank-major position
+};
+
+// Flow index view (see store_build_flow_index).
+struct FlowView {
+  uint64_t n = 0;
+  int op_shift = 0, rank_shift = 0;
+  int64_t min_op = 0;
+  const unsigned long long* keys = nullptr;
+  const uint32_t* pos = nullptr;
 };
 
 __host__ __device__ inline int ko_kind(uint8_t ko) { return ko & 1; }

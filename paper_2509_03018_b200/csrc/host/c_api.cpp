@@ -68,30 +68,42 @@ csg_ctx* engine() {
   return g_ctx;
 }
 
-struct Engine {
-  csg_store* store = nullptr;
-  csg_model* model = nullptr;
+// Device store + layout tables kept across calls, so repeated replays reuse
+// their HBM allocations (the model is rebuilt only when the layout changes).
+csg_store* g_store = nullptr;
+csg_model* g_model = nullptr;
+std::string g_model_key;
+
+struct Results {
   csg_results* res = nullptr;
-  ~Engine() {
-    csg_results_free(res);
-    csg_model_free(model);
-    csg_store_free(store);
-  }
+  ~Results() { csg_results_free(res); }
 };
 
 collsight_result* analyze_records(const csh::Scenario& cfg,
                                   const csg_packed_record* recs, size_t n,
                                   const char* report_out_path) {
   std::lock_guard<std::mutex> lk(g_mu);
-  const csh::Layout layout = cfg.layout();
-  const csh::Program program = cfg.program(layout);
-  const csh::Tables tables(layout, program);
   csg_ctx* ctx = engine();
-  Engine e;
-  check(csg_store_create(ctx, &e.store));
-  check(csg_store_append(e.store, recs, n));
-  check(csg_model_create(ctx, &tables.topo, &tables.prog, &e.model));
-  check(csg_run_detection(e.store, e.model, &cfg.trigger, &cfg.analysis,
+  const std::string key = std::to_string(cfg.tp) + "," + std::to_string(cfg.pp) +
+                          "," + std::to_string(cfg.dp) + "," +
+                          std::to_string(cfg.ranks_per_node) + "," +
+                          std::to_string(cfg.channels_per_pair) + "," +
+                          std::to_string(cfg.nics_per_node) + "," +
+                          std::to_string(cfg.msg_bytes);
+  if (!g_model || key != g_model_key) {
+    const csh::Layout layout = cfg.layout();
+    const csh::Program program = cfg.program(layout);
+    const csh::Tables tables(layout, program);
+    if (g_model) csg_model_free(g_model);
+    g_model = nullptr;
+    check(csg_model_create(ctx, &tables.topo, &tables.prog, &g_model));
+    g_model_key = key;
+  }
+  if (!g_store) check(csg_store_create(ctx, &g_store));
+  check(csg_store_clear(g_store));
+  check(csg_store_append(g_store, recs, n));
+  Results e;
+  check(csg_run_detection(g_store, g_model, &cfg.trigger, &cfg.analysis,
                           cfg.seed, &e.res, nullptr, 0, nullptr));
   std::vector<csg_report_view> views(csg_results_count(e.res));
   for (size_t i = 0; i < views.size(); ++i) check(csg_results_get(e.res, i, &views[i]));

@@ -167,6 +167,13 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target) {
         start = std::max(start, ready[r]);
         blk |= blocked[r] != 0;
       }
+      // Rendezvous: a send starts only once its receiver is free for the
+      // matching receive (which depends on this send), so no stage runs
+      // ahead of the pipeline, and a receiver that waits forever blocks it.
+      if (op.name == CSG_OP_SEND && op.dst >= 0 && op.dst < W) {
+        start = std::max(start, ready[op.dst]);
+        blk |= blocked[op.dst] != 0;
+      }
       if (blk || start > t_end) {
         op_stalled[s] = 1;
         for (int32_t r : ex[s]) blocked[r] = 1;
@@ -174,10 +181,7 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target) {
         continue;
       }
       any_started = true;
-      // does this instance hang? A send whose receiver waits forever hangs
-      // too (its flows cannot drain).
-      const bool recv_gone = op.name == CSG_OP_SEND && op.dst >= 0 && op.dst < W &&
-                             blocked[op.dst] != 0;
+      // does this instance hang?
       bool touches_dead = false;
       if (hang_node >= 0)
         for (int32_t r : ex[s])
@@ -192,7 +196,7 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target) {
         rend[i] = start + d;
         inst_end = std::max(inst_end, rend[i]);
       }
-      const bool stalls = (touches_dead && inst_end > hang_at) || recv_gone;
+      const bool stalls = touches_dead && inst_end > hang_at;
       const uint64_t total = chunks[s];
       for (size_t i = 0; i < ex[s].size(); ++i) {
         const int32_t r = ex[s][i];

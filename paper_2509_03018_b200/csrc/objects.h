@@ -3,6 +3,7 @@
 
 #include <map>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "engine_internal.h"
@@ -18,6 +19,10 @@ struct csg_ctx {
   // shared scratch
   csg::DevBuf scratch_a, scratch_b, scratch_c, pinned_flag_dev;
   uint32_t* host_flag = nullptr;  // pinned
+  // Named grow-only device buffers reused across calls (no cudaMalloc /
+  // cudaFree on the analysis path once warm).
+  std::map<std::string, csg::DevBuf> arena;
+  csg::DevBuf& buf(const char* name) { return arena[name]; }
 
   // Times an engine phase on the context stream with CUDA events.
   struct Timed {
@@ -68,6 +73,12 @@ struct csg_store {
   csg::DevBuf opidx_keys;    // u64 op - min_op (sorted)
   csg::DevBuf opidx_rank;    // rank of each entry
   csg::DevBuf op_seg_off;    // dense [min_op, max_op+1] -> start in opidx
+  // flow index: rank-major positions ordered by (rank, op_seq, channel,
+  // store order); keys packed rank | op - min_op | channel
+  bool flow_indexed = false;
+  int flow_key_bits = 0, flow_op_shift = 0, flow_rank_shift = 0;
+  csg::DevBuf fl_keys;  // u64 keys (sorted)
+  csg::DevBuf fl_pos;   // u32 rank-major positions
   csg::DevBuf stats_dev;
 
   csg::StoreView view() const {
@@ -85,7 +96,18 @@ struct csg_store {
     v.ko = ko.as<uint8_t>();
     v.pa = pa.as<uint64_t>();
     v.pb = pb.as<uint64_t>();
+    v.rank_of = keys.as<uint32_t>();
     return v;
+  }
+  csg::FlowView flow_view() const {
+    csg::FlowView f;
+    f.n = flow_indexed ? n : 0;
+    f.op_shift = flow_op_shift;
+    f.rank_shift = flow_rank_shift;
+    f.min_op = min_op;
+    f.keys = fl_keys.as<unsigned long long>();
+    f.pos = fl_pos.as<uint32_t>();
+    return f;
   }
 };
 
@@ -167,6 +189,8 @@ namespace csg {
 
 void store_build_index(csg_store* s);
 void store_build_op_index(csg_store* s, int32_t opn);
+// Returns false (and builds nothing) when the packed key exceeds 64 bits.
+bool store_build_flow_index(csg_store* s);
 
 // Per-thread error text for csg_last_error.
 void set_error(const std::string& msg);

@@ -19,6 +19,7 @@
 //    self-evidence filter keep the reference's sequential order.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "rca.cuh"
@@ -167,6 +168,122 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
     __syncwarp();
     if (cand_stuck && !comp_hit) o.flags |= RS_STUCK;
     // progress_of(rank, last_op, t) (rca.cpp:167-196): sum over channels.
+    unsigned long long rd = 0, tx = 0, dn = 0;
+    int any = 0;
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint32_t q = tbl[ch];
+      if (q) {
+        any = 1;
+        const uint64_t a = s.pa[q - 1];
+        rd += a & 0xffffffffull;
+        tx += a >> 32;
+        dn += s.pb[q - 1];
+      }
+    }
+#pragma unroll
+    for (int x = 16; x; x >>= 1) {
+      rd += __shfl_xor_sync(FULL, rd, x);
+      tx += __shfl_xor_sync(FULL, tx, x);
+      dn += __shfl_xor_sync(FULL, dn, x);
+      any |= __shfl_xor_sync(FULL, any, x);
+    }
+    if (any) {
+      o.flags |= RS_PROG;
+      o.ready = rd;
+      o.tx = tx;
+      o.done = dn;
+    }
+  }
+  uint32_t* cp = chan_pos + (static_cast<uint64_t>(j) * s.R + r) * nch;
+  for (int ch = lane; ch < nch; ch += 32) cp[ch] = tbl[ch];
+  if (lane == 0) out[static_cast<uint64_t>(j) * s.R + r] = o;
+}
+
+// K1 (flow-index form): the same summary with every "scan the prefix for
+// records of op X" replaced by a lookup in the (rank, op, channel)-ordered
+// flow index: the (rank, op) entries are one contiguous range, so stall
+// onset, "completion of the stuck op inside the prefix" and the per-channel
+// latest state are O(log n + entries of that op), not O(prefix).
+__global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
+                                  const double* __restrict__ trip_t,
+                                  double delta_a, RankSum* __restrict__ out,
+                                  uint32_t* __restrict__ chan_pos, int32_t nch) {
+  extern __shared__ uint32_t sm_tbl[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(s.R) * J) return;
+  const int32_t r = static_cast<int32_t>(w / J);
+  const int32_t j = static_cast<int32_t>(w % J);
+  uint32_t* tbl = sm_tbl + wib * nch;
+  for (int c = lane; c < nch; c += 32) tbl[c] = 0;
+  __syncwarp();
+  const double t = trip_t[j];
+  const double ws = t - delta_a;
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  const double* rm = s.runmax;
+  const uint32_t cend =
+      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
+  const uint32_t c = cend - b;
+  RankSum o;
+  o.cutoff = c;
+  o.flags = 0;
+  o.last_op = -1;
+  o.last_ts = 0;
+  o.last_chan = -1;
+  o.pad = 0;
+  o.onset = 0;
+  o.ready = o.tx = o.done = 0;
+  if (c > 0) {
+    o.flags |= RS_HAS_LAST;
+    o.last_op = s.op[cend - 1];
+    o.last_ts = s.ts[cend - 1];
+    o.last_chan = s.chan[cend - 1];
+    int64_t found = -1;
+    for (int64_t top = static_cast<int64_t>(cend) - 1;
+         top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
+      const int64_t p = top - lane;
+      const bool pr = p >= static_cast<int64_t>(b) && s.ts[p] >= ws;
+      const unsigned mm = __ballot_sync(FULL, pr);
+      if (mm) found = top - (__ffs(mm) - 1);
+    }
+    bool cand_stuck = false;
+    int64_t stuck_op = 0;
+    if (found >= 0 && ko_kind(s.ko[found]) == CSG_KIND_STATE) {
+      cand_stuck = true;
+      stuck_op = s.op[found];
+    }
+    const unsigned long long rk = static_cast<unsigned long long>(r) << f.rank_shift;
+    auto range_of = [&](int64_t op, uint32_t& fo, uint32_t& fe) {
+      const unsigned long long k0 =
+          rk | (static_cast<unsigned long long>(op - f.min_op) << f.op_shift);
+      const unsigned long long k1 = k0 + (1ull << f.op_shift);
+      fo = warp_partition_point(b, e, [&](uint32_t i) { return f.keys[i] >= k0; });
+      fe = warp_partition_point(fo, e, [&](uint32_t i) { return f.keys[i] >= k1; });
+    };
+    uint32_t fo, fe;
+    range_of(o.last_op, fo, fe);
+    uint32_t first = 0xFFFFFFFFu;
+    for (uint32_t i = fo + lane; i < fe; i += 32) {
+      const uint32_t p = f.pos[i];
+      if (p >= cend) continue;
+      first = min(first, p);
+      if (ko_kind(s.ko[p]) == CSG_KIND_STATE) atomicMax(&tbl[s.chan[p]], p + 1);
+    }
+#pragma unroll
+    for (int x = 16; x; x >>= 1) first = min(first, __shfl_xor_sync(FULL, first, x));
+    o.onset = s.ts[first];  // stall_onset_of: first prefix record of the op
+    if (cand_stuck) {
+      uint32_t so = fo, se = fe;
+      if (stuck_op != o.last_op) range_of(stuck_op, so, se);
+      bool hit = false;
+      for (uint32_t i = so + lane; i < se && !hit; i += 32) {
+        const uint32_t p = f.pos[i];
+        hit = p < cend && ko_kind(s.ko[p]) == CSG_KIND_COMPLETION;
+      }
+      if (!__any_sync(FULL, hit)) o.flags |= RS_STUCK;
+    }
+    __syncwarp();
     unsigned long long rd = 0, tx = 0, dn = 0;
     int any = 0;
     for (int ch = lane; ch < nch; ch += 32) {
@@ -913,289 +1030,7 @@ __device__ void emit_reports(const DecideArgs& a, BlockShared& sh,
   __syncthreads();
 }
 
-// ---- failure ---------------------------------------------------------------
-
-__device__ void decide_failure(const DecideArgs& a, int32_t j, BlockShared& sh,
-                               uint32_t* scratch) {
-  const int32_t naff = a.n_aff[j];
-  const int32_t* aff = a.aff + static_cast<uint64_t>(j) * a.m.n_groups;
-  const RankSum* rs = a.rs + static_cast<uint64_t>(j) * a.s.R;
-  const int32_t R = a.s.R;
-  // capacities: Σ members of the affected groups
-  int tot = 0;
-  for (int32_t i = threadIdx.x; i < naff; i += blockDim.x) {
-    const int32_t g = aff[i];
-    tot += static_cast<int>(a.m.member_off[g + 1] - a.m.member_off[g]);
-  }
-  tot = block_sum_i(tot, sh);
-  if (threadIdx.x == 0) {
-    bool ok1, ok2, ok3, ok4;
-    sh.cap_cand = tot;
-    sh.cap_cev = static_cast<unsigned long long>(tot) * (2 * a.nch + 1);
-    sh.cand_base = pool_alloc(a.pools.used, P_CAND, sh.cap_cand,
-                              a.pools.cand_cap, a.err, DEV_ERR_POOL, &ok1);
-    sh.cev_base = pool_alloc(a.pools.used, P_CEV, sh.cap_cev, a.pools.cev_cap,
-                             a.err, DEV_ERR_POOL, &ok2);
-    sh.sus_base = pool_alloc(a.pools.used, P_SUS, 3ull * tot, a.pools.sus_cap,
-                             a.err, DEV_ERR_POOL, &ok3);
-    sh.exo_base = sh.sus_base + tot;
-    sh.ev_base = pool_alloc(a.pools.used, P_EV, sh.cap_cev, a.pools.ev_cap,
-                            a.err, DEV_ERR_POOL, &ok4);
-    sh.abort = !(ok1 && ok2 && ok3 && ok4);
-    sh.ncand = 0;
-    sh.cev_used = 0;
-  }
-  __syncthreads();
-  if (sh.abort) return;
-  uint32_t* lst = scratch;                 // member indices
-  uint32_t* lst2 = scratch + a.scratch_per_trip / 4;
-  for (int32_t ai = 0; ai < naff; ++ai) {
-    const int32_t g = aff[ai];
-    const uint32_t mo = a.m.member_off[g];
-    const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
-    // last_logs_of_group + check_min_op (rca.cpp:562-571, :249-261)
-    int nlog = 0;
-    long long mn = LLONG_MAX;
-    for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const int32_t r = a.m.members[mo + i];
-      if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST)) {
-        ++nlog;
-        mn = min(mn, static_cast<long long>(rs[r].last_op));
-      }
-    }
-    nlog = block_sum_i(nlog, sh);
-    if (nlog == 0) continue;
-    mn = block_min_l(mn, sh);
-    int neq = 0;
-    for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const int32_t r = a.m.members[mo + i];
-      if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) && rs[r].last_op == mn)
-        ++neq;
-    }
-    neq = block_sum_i(neq, sh);
-    int ns;
-    if (neq < nlog) {
-      ns = block_compact(m, [&](int i) {
-        const int32_t r = a.m.members[mo + i];
-        return r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
-               rs[r].last_op == mn;
-      }, lst, sh);
-    } else {
-      // check_min_data over members with progress (rca.cpp:573-580)
-      int nk = 0;
-      uint64_t d = ~0ull, tx = ~0ull, rd = ~0ull;
-      for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        const int32_t r = a.m.members[mo + i];
-        if (r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
-            (rs[r].flags & RS_PROG)) {
-          ++nk;
-          if (prog_less(rs[r].done, rs[r].tx, rs[r].ready, d, tx, rd)) {
-            d = rs[r].done;
-            tx = rs[r].tx;
-            rd = rs[r].ready;
-          }
-        }
-      }
-      nk = block_sum_i(nk, sh);
-      if (nk == 0) continue;
-      block_min_prog(d, tx, rd, sh);
-      ns = block_compact(m, [&](int i) {
-        const int32_t r = a.m.members[mo + i];
-        return r >= 0 && r < R && (rs[r].flags & RS_HAS_LAST) &&
-               (rs[r].flags & RS_PROG) && rs[r].done == d && rs[r].tx == tx &&
-               rs[r].ready == rd;
-      }, lst, sh);
-    }
-    // suspects sorted by rank
-    block_stable_sort(ns, lst, lst2, [&](uint32_t x, uint32_t y) {
-      return a.m.members[mo + x] < a.m.members[mo + y];
-    });
-    for (int q = 0; q < ns; ++q) {
-      const uint32_t mi = lst2[q];
-      const int32_t r = a.m.members[mo + mi];
-      const RankSum own = rs[r];
-      const int64_t op = own.last_op;
-      // ring successor (rca.cpp:598-605): members[(pos+1) % n], pos = first
-      // occurrence (members are unique, so pos == mi)
-      int32_t succ = -1;
-      if (m >= 2) succ = a.m.members[mo + (mi + 1) % m];
-      bool peer_known = false;
-      uint64_t prd = 0, ptx = 0, pdn = 0;
-      const uint32_t* peer_tbl = nullptr;
-      if (succ >= 0 && succ < R) {
-        const RankSum sr = rs[succ];
-        if ((sr.flags & RS_HAS_LAST) && sr.last_op == op) {
-          peer_known = (sr.flags & RS_PROG) != 0;
-          prd = sr.ready;
-          ptx = sr.tx;
-          pdn = sr.done;
-          peer_tbl = a.chan_pos + (static_cast<uint64_t>(j) * R + succ) * a.nch;
-        } else {
-          block_progress_scan(a, succ, sr.cutoff, op, sh);
-          for (int c = 0; c < a.nch; ++c) {
-            const uint32_t pq = sh.chtbl[c];
-            if (pq) {
-              peer_known = true;
-              const uint64_t pa = a.s.pa[pq - 1];
-              prd += pa & 0xffffffffull;
-              ptx += pa >> 32;
-              pdn += a.s.pb[pq - 1];
-            }
-          }
-          peer_tbl = sh.chtbl;
-        }
-      }
-      if (threadIdx.x == 0) {
-        Cand c;
-        memset(&c, 0, sizeof(c));
-        c.rank = r;
-        c.group = g;
-        c.op = op;
-        c.onset = own.onset;
-        c.known = (own.flags & RS_PROG) ? 1 : 0;
-        c.ready = own.ready;
-        c.tx = own.tx;
-        c.done = own.done;
-        c.it_lo = 0;
-        c.it_hi = -1;
-        c.ev_off = sh.cev_used;
-        c.ev_n = 0;
-        if (c.known)
-          add_table_evidence(a, sh, c, r,
-                             a.chan_pos + (static_cast<uint64_t>(j) * R + r) * a.nch);
-        if (peer_known) add_table_evidence(a, sh, c, succ, peer_tbl);
-        if (c.known) {
-          int cat, side;
-          if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat,
-                        &side)) {
-            atomicOr(a.err, DEV_ERR_RC_TABLE);
-            sh.abort = 1;
-          }
-          c.cat = static_cast<uint8_t>(cat);
-          c.side = static_cast<uint8_t>(side);
-        } else {
-          c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
-          c.side = CSG_SIDE_UNDETERMINED;
-        }
-        if (c.ev_n == 0) add_cev(a, sh, c, r, own.last_chan, own.last_ts, op);
-        push_cand(a, sh, c);
-      }
-      __syncthreads();
-      if (sh.abort) return;
-    }
-  }
-  // ---- exonerate (rca.cpp:479-526) ----
-  const int C = sh.ncand;
-  const Cand* cands = a.pools.cand + sh.cand_base;
-  uint32_t* idx = scratch;
-  uint32_t* ord = scratch + C;
-  int64_t* U = reinterpret_cast<int64_t*>(scratch + 2 * C);  // 8-aligned
-  uint32_t* ret = reinterpret_cast<uint32_t*>(U + C);
-  uint8_t* keep = reinterpret_cast<uint8_t*>(ret + C);
-  uint32_t* tail = reinterpret_cast<uint32_t*>(keep + ((C + 3) & ~3));
-  for (int i = threadIdx.x; i < C; i += blockDim.x) idx[i] = i;
-  __syncthreads();
-  block_stable_sort(C, idx, ord, [&](uint32_t x, uint32_t y) {
-    if (cands[x].op != cands[y].op) return cands[x].op < cands[y].op;
-    return cands[x].rank < cands[y].rank;
-  });
-  // distinct valid (>= 0) candidate ops, ascending
-  if (threadIdx.x == 0) {
-    int K = 0;
-    for (int x = 0; x < C; ++x) {
-      const int64_t op = cands[ord[x]].op;
-      if (op >= 0 && (K == 0 || U[K - 1] != op)) U[K++] = op;
-    }
-    sh.i32a = K;
-  }
-  __syncthreads();
-  const int K = sh.i32a;
-  const int words = (K + 63) / 64;
-  int64_t lo = 0, hi = -1;
-  unsigned long long* bits = nullptr;
-  const int32_t opn = a.m.opn;
-  if (K >= 2) {
-    lo = U[0];
-    hi = U[K - 1];
-    const unsigned long long V = static_cast<unsigned long long>(hi - lo + 1);
-    if (threadIdx.x == 0) {
-      bool ok;
-      sh.bits_base = pool_alloc(a.pools.used, P_BITS, V * words, a.pools.bits_cap,
-                                a.err, DEV_ERR_DAG_SCRATCH, &ok);
-      if (!ok) sh.abort = 1;
-    }
-    __syncthreads();
-    if (sh.abort) return;
-    bits = a.pools.bits + sh.bits_base;
-    for (unsigned long long i = threadIdx.x; i < V * words; i += blockDim.x)
-      bits[i] = 0;
-    __syncthreads();
-    for (int64_t it = lo / opn; it <= hi / opn; ++it) {
-      for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
-        const uint32_t l0 = a.m.lvl_off[lv];
-        const uint32_t nl = a.m.lvl_off[lv + 1] - l0;
-        for (uint32_t q = threadIdx.x; q < nl * words; q += blockDim.x) {
-          const int32_t sop = a.m.lvl_ops[l0 + q / words];
-          const int w = q % words;
-          const int64_t v = it * opn + sop;
-          if (v < lo || v > hi) continue;
-          unsigned long long acc = 0;
-          for (uint32_t pe = a.m.par_off[sop]; pe < a.m.par_off[sop + 1]; ++pe) {
-            const int64_t pit = it + a.m.par_it[pe];
-            if (pit < 0) continue;
-            const int64_t pv = pit * opn + a.m.par_op[pe];
-            if (pv < lo) continue;
-            acc |= bits[(pv - lo) * words + w];
-            // pv itself a candidate op?
-            int l = 0, h = K;
-            while (l < h) {
-              const int md = (l + h) >> 1;
-              if (U[md] < pv) l = md + 1; else h = md;
-            }
-            if (l < K && U[l] == pv && (l >> 6) == w) acc |= 1ull << (l & 63);
-          }
-          bits[(v - lo) * words + w] = acc;
-        }
-        __syncthreads();
-      }
-    }
-  }
-  // greedy pass
-  if (threadIdx.x == 0) sh.nret = 0;
-  __syncthreads();
-  for (int x = 0; x < C; ++x) {
-    const Cand& c = cands[ord[x]];
-    bool drop = false;
-    for (int q = threadIdx.x; q < sh.nret; q += blockDim.x) {
-      const Cand& u = cands[ret[q]];
-      if (u.rank == c.rank) continue;
-      bool path;
-      if (u.op == c.op) {
-        path = u.known && c.known &&
-               prog_less(u.done, u.tx, u.ready, c.done, c.tx, c.ready);
-      } else if (c.op < 0 || u.op < 0 || K < 2) {
-        path = false;
-      } else {
-        int l = 0, h = K;
-        while (l < h) {
-          const int md = (l + h) >> 1;
-          if (U[md] < u.op) l = md + 1; else h = md;
-        }
-        path = (bits[(c.op - lo) * words + (l >> 6)] >> (l & 63)) & 1ull;
-      }
-      drop |= path;
-    }
-    drop = __syncthreads_or(drop);
-    if (threadIdx.x == 0) {
-      keep[x] = drop ? 0 : 1;
-      if (!drop) ret[sh.nret++] = ord[x];
-    }
-    __syncthreads();
-  }
-  emit_reports(a, sh, ord, keep, C, tail);
-  write_trip(a, j, sh.nsus ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED,
-             naff, 2 * a.N, sh);
-}
+// ---- failure: see k_fail_count / k_fail_cands / k_exonerate ---------------
 
 // ---- straggler -------------------------------------------------------------
 
@@ -1546,6 +1381,682 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
              naff, 3 * a.N, sh);
 }
 
+// ---------------------------------------------------------------------------
+// Failure analysis (analyze_failure, proj/src/rca.cpp:540-631), three stages:
+//  K_fail_count  warp per (trip, affected group): last_logs_of_group +
+//                check_min_op, else check_min_data -> suspect count
+//  (scan)        candidate offsets in (trip, group asc) order
+//  K_fail_cands  warp per (trip, affected group): one Candidate per suspect,
+//                rank-sorted inside the group, with progress + evidence
+//                (own channels, then the ring successor's on the same op)
+//  K_exonerate   block per trip: stable (op, rank) order, op-DAG
+//                reachability bitsets, chunked greedy exoneration, report.
+// ---------------------------------------------------------------------------
+struct FailItem {
+  int32_t j;      // trip
+  int32_t g;      // affected group
+};
+
+struct GroupPick {
+  int32_t mode;   // 0 no suspects, 1 strict min op, 2 min progress
+  int32_t count;
+  int64_t min_op;
+  uint64_t d, t, r;  // min (done, tx, ready) for mode 2
+};
+
+__host__ __device__ constexpr int kEvSlots(int nch) { return 2 * nch + 1; }
+
+__global__ void k_fail_count(StoreView s, ModelView m,
+                             const FailItem* __restrict__ items, int32_t n_items,
+                             const RankSum* __restrict__ rs,
+                             GroupPick* __restrict__ pick,
+                             uint32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_items) return;
+  const FailItem it = items[w];
+  const RankSum* rsj = rs + static_cast<uint64_t>(it.j) * s.R;
+  const uint32_t mo = m.member_off[it.g];
+  const int32_t mm = static_cast<int32_t>(m.member_off[it.g + 1] - mo);
+  int nlog = 0;
+  long long mn = LLONG_MAX;
+  for (int32_t i = lane; i < mm; i += 32) {
+    const int32_t r = m.members[mo + i];
+    if (r >= 0 && r < s.R && (rsj[r].flags & RS_HAS_LAST)) {
+      ++nlog;
+      mn = min(mn, static_cast<long long>(rsj[r].last_op));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nlog += __shfl_xor_sync(FULL, nlog, o);
+    mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+  }
+  GroupPick pk;
+  pk.mode = 0;
+  pk.count = 0;
+  pk.min_op = mn;
+  pk.d = pk.t = pk.r = ~0ull;
+  if (nlog > 0) {
+    int neq = 0;
+    for (int32_t i = lane; i < mm; i += 32) {
+      const int32_t r = m.members[mo + i];
+      neq += (r >= 0 && r < s.R && (rsj[r].flags & RS_HAS_LAST) &&
+              rsj[r].last_op == mn);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) neq += __shfl_xor_sync(FULL, neq, o);
+    if (neq < nlog) {
+      pk.mode = 1;
+      pk.count = neq;
+    } else {
+      uint64_t d = ~0ull, t = ~0ull, rd = ~0ull;
+      int nk = 0;
+      for (int32_t i = lane; i < mm; i += 32) {
+        const int32_t r = m.members[mo + i];
+        if (r >= 0 && r < s.R && (rsj[r].flags & RS_HAS_LAST) &&
+            (rsj[r].flags & RS_PROG)) {
+          ++nk;
+          if (prog_less(rsj[r].done, rsj[r].tx, rsj[r].ready, d, t, rd)) {
+            d = rsj[r].done;
+            t = rsj[r].tx;
+            rd = rsj[r].ready;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        nk += __shfl_xor_sync(FULL, nk, o);
+        const uint64_t d2 = __shfl_xor_sync(FULL, d, o);
+        const uint64_t t2 = __shfl_xor_sync(FULL, t, o);
+        const uint64_t r2 = __shfl_xor_sync(FULL, rd, o);
+        if (prog_less(d2, t2, r2, d, t, rd)) {
+          d = d2;
+          t = t2;
+          rd = r2;
+        }
+      }
+      if (nk > 0) {
+        int ns = 0;
+        for (int32_t i = lane; i < mm; i += 32) {
+          const int32_t r = m.members[mo + i];
+          ns += (r >= 0 && r < s.R && (rsj[r].flags & RS_HAS_LAST) &&
+                 (rsj[r].flags & RS_PROG) && rsj[r].done == d && rsj[r].tx == t &&
+                 rsj[r].ready == rd);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(FULL, ns, o);
+        pk.mode = 2;
+        pk.count = ns;
+        pk.d = d;
+        pk.t = t;
+        pk.r = rd;
+      }
+    }
+  }
+  if (lane == 0) {
+    pick[w] = pk;
+    cnt[w] = static_cast<uint32_t>(pk.count);
+  }
+}
+
+__device__ inline bool is_suspect(const GroupPick& pk, const RankSum* rsj,
+                                  int32_t r, int32_t R) {
+  if (r < 0 || r >= R || !(rsj[r].flags & RS_HAS_LAST)) return false;
+  if (pk.mode == 1) return rsj[r].last_op == pk.min_op;
+  if (pk.mode == 2)
+    return (rsj[r].flags & RS_PROG) && rsj[r].done == pk.d &&
+           rsj[r].tx == pk.t && rsj[r].ready == pk.r;
+  return false;
+}
+
+__global__ void k_fail_cands(StoreView s, ModelView m,
+                             const FailItem* __restrict__ items, int32_t n_items,
+                             const RankSum* __restrict__ rs,
+                             const uint32_t* __restrict__ chan_pos, int32_t nch,
+                             const GroupPick* __restrict__ pick,
+                             const uint32_t* __restrict__ off,
+                             Cand* __restrict__ cand,
+                             csg_evidence* __restrict__ cev,
+                             uint32_t* __restrict__ err) {
+  constexpr int kWarps = 4;
+  __shared__ uint32_t tbl[kWarps][kChTbl / 8];  // slow-path successor table
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_items) return;
+  const FailItem it = items[w];
+  const GroupPick pk = pick[w];
+  if (pk.mode == 0) return;
+  const RankSum* rsj = rs + static_cast<uint64_t>(it.j) * s.R;
+  const uint32_t mo = m.member_off[it.g];
+  const int32_t mm = static_cast<int32_t>(m.member_off[it.g + 1] - mo);
+  const uint32_t base = off[w];
+  const int EV = kEvSlots(nch);
+  // Pass 1 (lane-parallel): one candidate per suspect at its rank-sorted slot.
+  for (int32_t i = lane; i < mm; i += 32) {
+    const int32_t r = m.members[mo + i];
+    if (!is_suspect(pk, rsj, r, s.R)) continue;
+    uint32_t pos = 0;
+    for (int32_t k = 0; k < mm; ++k) {
+      const int32_t rk = m.members[mo + k];
+      pos += (rk < r && is_suspect(pk, rsj, rk, s.R));
+    }
+    const RankSum own = rsj[r];
+    Cand c;
+    memset(&c, 0, sizeof(c));
+    c.rank = r;
+    c.group = it.g;
+    c.op = own.last_op;
+    c.onset = own.onset;
+    c.known = (own.flags & RS_PROG) ? 1 : 0;
+    c.ready = own.ready;
+    c.tx = own.tx;
+    c.done = own.done;
+    c.it_lo = 0;
+    c.it_hi = -1;
+    const uint32_t ci = base + pos;
+    c.ev_off = ci * EV;
+    c.ev_n = 0;
+    csg_evidence* ev = cev + static_cast<uint64_t>(ci) * EV;
+    const uint32_t* ct = chan_pos + (static_cast<uint64_t>(it.j) * s.R + r) * nch;
+    if (c.known)
+      for (int ch = 0; ch < nch; ++ch)
+        if (ct[ch]) {
+          const uint32_t q = ct[ch] - 1;
+          ev[c.ev_n++] = csg_evidence{r, ch, s.ts[q], s.op[q]};
+        }
+    // ring successor members[(pos+1) % n] on the suspect's op
+    // (rca.cpp:598-605); fast path when that is the successor's own last op.
+    bool slow = false;
+    bool peer_known = false;
+    uint64_t prd = 0, ptx = 0, pdn = 0;
+    if (mm >= 2) {
+      const int32_t succ = m.members[mo + (i + 1) % mm];
+      if (succ >= 0 && succ < s.R) {
+        const RankSum sr = rsj[succ];
+        if ((sr.flags & RS_HAS_LAST) && sr.last_op == c.op) {
+          peer_known = (sr.flags & RS_PROG) != 0;
+          prd = sr.ready;
+          ptx = sr.tx;
+          pdn = sr.done;
+          const uint32_t* st =
+              chan_pos + (static_cast<uint64_t>(it.j) * s.R + succ) * nch;
+          if (peer_known)
+            for (int ch = 0; ch < nch; ++ch)
+              if (st[ch]) {
+                const uint32_t q = st[ch] - 1;
+                ev[c.ev_n++] = csg_evidence{succ, ch, s.ts[q], s.op[q]};
+              }
+        } else if (sr.cutoff > 0) {
+          slow = true;  // resolved cooperatively below
+        }
+      }
+    }
+    if (!slow) {
+      if (c.known) {
+        int cat, side;
+        if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat, &side))
+          atomicOr(err, DEV_ERR_RC_TABLE);
+        c.cat = static_cast<uint8_t>(cat);
+        c.side = static_cast<uint8_t>(side);
+      } else {
+        c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
+        c.side = CSG_SIDE_UNDETERMINED;
+      }
+      if (c.ev_n == 0)
+        ev[c.ev_n++] = csg_evidence{r, own.last_chan, own.last_ts, c.op};
+    }
+    c.pad = slow ? 1 : 0;
+    cand[ci] = c;
+  }
+  __syncwarp();
+  // Pass 2 (warp-cooperative): successors whose last op differs from the
+  // suspect's need a prefix scan for progress_of(succ, op, t).
+  const int words = (nch + 7) / 8 * 8 <= kChTbl / 8 ? nch : kChTbl / 8;
+  for (int32_t i0 = 0; i0 < mm; i0 += 32) {
+    const int32_t i = i0 + lane;
+    bool need = false;
+    uint32_t ci = 0;
+    if (i < mm) {
+      const int32_t r = m.members[mo + i];
+      if (is_suspect(pk, rsj, r, s.R)) {
+        uint32_t pos = 0;
+        for (int32_t k = 0; k < mm; ++k) {
+          const int32_t rk = m.members[mo + k];
+          pos += (rk < r && is_suspect(pk, rsj, rk, s.R));
+        }
+        ci = base + pos;
+        need = cand[ci].pad != 0;
+      }
+    }
+    unsigned todo = __ballot_sync(FULL, need);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t cc = __shfl_sync(FULL, ci, src);
+      const int32_t mi = i0 + src;
+      Cand c = cand[cc];
+      const int32_t succ = m.members[mo + (mi + 1) % mm];
+      const uint32_t b = s.rank_off[succ];
+      const uint32_t e = b + rsj[succ].cutoff;
+      for (int ch = lane; ch < nch; ch += 32) tbl[wib][ch] = 0;
+      __syncwarp();
+      for (uint32_t p = b + lane; p < e; p += 32)
+        if (s.op[p] == c.op && ko_kind(s.ko[p]) == CSG_KIND_STATE)
+          atomicMax(&tbl[wib][s.chan[p]], p + 1);
+      __syncwarp();
+      if (lane == 0) {
+        bool peer_known = false;
+        uint64_t prd = 0, ptx = 0, pdn = 0;
+        csg_evidence* ev = cev + static_cast<uint64_t>(cc) * EV;
+        for (int ch = 0; ch < nch; ++ch) {
+          const uint32_t q = tbl[wib][ch];
+          if (!q) continue;
+          peer_known = true;
+          const uint64_t pa = s.pa[q - 1];
+          prd += pa & 0xffffffffull;
+          ptx += pa >> 32;
+          pdn += s.pb[q - 1];
+          ev[c.ev_n++] = csg_evidence{succ, ch, s.ts[q - 1], s.op[q - 1]};
+        }
+        if (c.known) {
+          int cat, side;
+          if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat,
+                        &side))
+            atomicOr(err, DEV_ERR_RC_TABLE);
+          c.cat = static_cast<uint8_t>(cat);
+          c.side = static_cast<uint8_t>(side);
+        } else {
+          c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
+          c.side = CSG_SIDE_UNDETERMINED;
+        }
+        if (c.ev_n == 0) {
+          const RankSum own = rsj[c.rank];
+          ev[c.ev_n++] = csg_evidence{c.rank, own.last_chan, own.last_ts, c.op};
+        }
+        c.pad = 0;
+        cand[cc] = c;
+      }
+      __syncwarp();
+    }
+  }
+  (void)words;
+}
+
+struct ExoTrip {
+  int32_t j;
+  int32_t naff;
+  uint32_t cand_base;   // first candidate of the trip
+  uint32_t n_cand;      // filled on device from the scan (see k_exonerate)
+  uint32_t first_item, n_items;
+  uint64_t scratch_off;  // bytes into the scratch pool (16-aligned)
+  uint32_t sus_off, ev_off;  // output regions (upper bounds from the host)
+};
+
+struct ExoArgs {
+  int debug;
+  StoreView s;
+  ModelView m;
+  const Cand* cand;
+  const csg_evidence* cev;
+  int32_t EV;
+  const uint32_t* off;   // exclusive scan of item counts (n_items + 1)
+  ExoTrip* trips;
+  int32_t n_trips;
+  unsigned char* scratch;
+  unsigned long long* bits;
+  unsigned long long bits_cap;
+  unsigned long long* bits_used;
+  csg_suspect* sus;
+  csg_evidence* ev;
+  TripOut* out;
+  uint64_t N;
+  uint32_t* err;
+};
+
+__device__ inline bool cand_before(const Cand* c, uint32_t x, uint32_t y) {
+  // stable (stuck_op, rank) order; ties keep append order
+  if (c[x].op != c[y].op) return c[x].op < c[y].op;
+  if (c[x].rank != c[y].rank) return c[x].rank < c[y].rank;
+  return x < y;
+}
+
+// In-place block bitonic sort of idx[0, P) (P power of two) by `less`;
+// entries >= n are padding (sort last).
+template <typename L>
+__device__ void block_bitonic(uint32_t* idx, uint32_t n, uint32_t P, L less) {
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) idx[i] = i < n ? i : 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const uint32_t a = idx[i], b = idx[l];
+          const bool up = (i & k) == 0;
+          bool a_lt_b;
+          if (a == 0xFFFFFFFFu) a_lt_b = false;
+          else if (b == 0xFFFFFFFFu) a_lt_b = true;
+          else a_lt_b = less(a, b);
+          const bool swap = up ? !a_lt_b : a_lt_b;
+          if (swap && !(a == b)) {
+            idx[i] = b;
+            idx[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ inline uint32_t pow2_ceil(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+constexpr int kExoThreads = 512;
+constexpr size_t kExoSmemMax = 192 * 1024;
+
+__global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
+  extern __shared__ __align__(16) unsigned long long exo_dyn[];
+  __shared__ uint32_t rel[256][8];
+  __shared__ uint8_t pre[256];
+  __shared__ uint32_t keepmask[8];
+  __shared__ int32_t sh_i[8];
+  __shared__ unsigned long long sh_u[2];
+  __shared__ uint32_t wsum[16];
+  __shared__ uint32_t scan3[16][3];
+  ExoTrip& tp = a.trips[blockIdx.x];
+  const int tid = threadIdx.x;
+  const uint32_t cbase = a.off[tp.first_item];
+  const uint32_t C = a.off[tp.first_item + tp.n_items] - cbase;
+  const Cand* cands = a.cand + cbase;
+  TripOut o;
+  memset(&o, 0, sizeof(o));
+  o.n_aff = tp.naff;
+  o.sus_off = tp.sus_off;
+  o.ev_off = tp.ev_off;
+  o.scanned = 2 * a.N;
+  if (C == 0) {
+    if (tid == 0) {
+      o.verdict = CSG_VERDICT_UNDETERMINED;
+      o.exo_off = tp.sus_off;
+      a.out[tp.j] = o;
+    }
+    return;
+  }
+  // scratch layout (all 16-aligned)
+  const uint32_t P = pow2_ceil(C);
+  unsigned char* sp = a.scratch + tp.scratch_off;
+  uint32_t* ord = reinterpret_cast<uint32_t*>(sp);
+  int64_t* U = reinterpret_cast<int64_t*>(sp + ((P * 4 + 15) & ~15u));
+  uint32_t* ret = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(U) +
+                                              ((C * 8 + 15) & ~15u));
+  uint8_t* keep = reinterpret_cast<uint8_t*>(ret) + ((C * 4 + 15) & ~15u);
+  const uint32_t Rs = static_cast<uint32_t>(a.s.R > 0 ? a.s.R : 1);
+  uint32_t* minpos = reinterpret_cast<uint32_t*>(keep + ((C + 15) & ~15u));
+  uint32_t* rbits = minpos + ((Rs + 3) & ~3u);
+  uint32_t* woff = rbits + (((Rs + 31) / 32 + 3) & ~3u);
+  csg_suspect* stmp =
+      reinterpret_cast<csg_suspect*>(woff + (((Rs + 31) / 32 + 3) & ~3u));
+  // 1. stable (op, rank) order
+  block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) { return cand_before(cands, x, y); });
+  // 2. distinct valid (>= 0) candidate ops, ascending (ordered compaction)
+  {
+    int Kc = 0;
+    const int nw = blockDim.x >> 5;
+    for (uint32_t base = 0; base < C; base += blockDim.x) {
+      const uint32_t x = base + tid;
+      int64_t op = -1, prev = -1;
+      bool fl = false;
+      if (x < C) {
+        op = cands[ord[x]].op;
+        prev = x ? cands[ord[x - 1]].op : -1;
+        fl = op >= 0 && (x == 0 || prev != op);
+      }
+      const unsigned bm = __ballot_sync(FULL, fl);
+      if ((tid & 31) == 0) wsum[tid >> 5] = __popc(bm);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int q = 0; q < nw; ++q) {
+        if (q < (tid >> 5)) before += wsum[q];
+        total += wsum[q];
+      }
+      if (fl) U[Kc + before + __popc(bm & ((1u << (tid & 31)) - 1u))] = op;
+      Kc += total;
+      __syncthreads();
+    }
+    if (tid == 0) sh_i[0] = Kc;
+  }
+  __syncthreads();
+  const int K = sh_i[0];
+  const int words = (K + 63) / 64;
+  const int32_t opn = a.m.opn;
+  int64_t lo = 0, hi = -1;
+  unsigned long long* bits = nullptr;
+  int32_t* cidx = nullptr;  // dense op -> candidate bit over [lo, hi], -1 if none
+  if (K >= 2) {
+    lo = U[0];
+    hi = U[K - 1];
+    const unsigned long long V = static_cast<unsigned long long>(hi - lo + 1);
+    const unsigned long long want = V * words + (V + 1) / 2;
+    if (tid == 0) {
+      const unsigned long long b0 = atomicAdd(a.bits_used, want);
+      sh_u[0] = b0;
+      sh_i[1] = b0 + want <= a.bits_cap;
+      if (!sh_i[1]) atomicOr(a.err, DEV_ERR_DAG_SCRATCH);
+    }
+    __syncthreads();
+    if (!sh_i[1]) return;
+    if (a.debug && tid == 0)
+      printf("exo trip %d C=%u K=%d V=%llu words=%d iters=%lld levels=%d\n", tp.j, C, K,
+             V, words, (long long)(hi / opn - lo / opn + 1), a.m.n_levels);
+    if ((V * words + (V + 1) / 2) * 8 <= kExoSmemMax) {
+      bits = exo_dyn;  // ancestor bitsets resident in shared memory
+    } else {
+      bits = a.bits + sh_u[0];
+    }
+    cidx = reinterpret_cast<int32_t*>(bits + V * words);
+    for (unsigned long long i = tid; i < V * words; i += blockDim.x) bits[i] = 0;
+    for (unsigned long long i = tid; i < V; i += blockDim.x) cidx[i] = -1;
+    __syncthreads();
+    for (int i = tid; i < K; i += blockDim.x) cidx[U[i] - lo] = i;
+    __syncthreads();
+    // ancestor bitsets over [lo, hi] in (iteration, level) order
+    for (int64_t it = lo / opn; it <= hi / opn; ++it) {
+      for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
+        const uint32_t l0 = a.m.lvl_off[lv];
+        const uint32_t nl = a.m.lvl_off[lv + 1] - l0;
+        for (uint32_t q = tid; q < nl * words; q += blockDim.x) {
+          const int32_t sop = a.m.lvl_ops[l0 + q / words];
+          const int wd = q % words;
+          const int64_t v = it * opn + sop;
+          if (v < lo || v > hi) continue;
+          unsigned long long acc = 0;
+          const uint32_t pe0 = __ldg(a.m.par_off + sop), pe1 = __ldg(a.m.par_off + sop + 1);
+#pragma unroll 8
+          for (uint32_t pe = pe0; pe < pe1; ++pe) {
+            const int64_t pit = it + __ldg(a.m.par_it + pe);
+            const int64_t pv = pit * opn + __ldg(a.m.par_op + pe);
+            if (pit < 0 || pv < lo) continue;
+            acc |= bits[(pv - lo) * words + wd];
+            const int l = cidx[pv - lo];
+            if (l >= 0 && (l >> 6) == wd) acc |= 1ull << (l & 63);
+          }
+          bits[(v - lo) * words + wd] = acc;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  auto drops = [&](const Cand& c, const Cand& u) {
+    if (u.rank == c.rank) return false;
+    if (u.op == c.op)
+      return u.known && c.known && prog_less(u.done, u.tx, u.ready, c.done, c.tx, c.ready);
+    if (c.op < 0 || u.op < 0 || K < 2) return false;
+    const int l = cidx[u.op - lo];
+    return ((bits[(c.op - lo) * words + (l >> 6)] >> (l & 63)) & 1ull) != 0;
+  };
+  // 3. greedy exoneration (rca.cpp:487-514) in chunks of 256: drops by
+  //    retained candidates of earlier chunks in parallel, then the in-chunk
+  //    order resolved with bit masks by one thread.
+  int nret = 0;
+  for (uint32_t base = 0; base < C; base += 256) {
+    const uint32_t n_in = min(256u, C - base);
+    const int nwg = 8;  // warps taking part in the 256-wide chunk
+    if (tid < static_cast<int>(n_in)) {
+      const Cand c = cands[ord[base + tid]];
+      bool p = false;
+      for (int q = 0; q < nret && !p; ++q) p = drops(c, cands[ret[q]]);
+      pre[tid] = p;
+      uint32_t row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (!p)
+        for (int jj = 0; jj < tid; ++jj)
+          if (drops(c, cands[ord[base + jj]])) row[jj >> 5] |= 1u << (jj & 31);
+      for (int q = 0; q < 8; ++q) rel[tid][q] = row[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t i = 0; i < n_in; ++i) {
+        bool dropped = pre[i];
+        for (int q = 0; q < 8 && !dropped; ++q) dropped = (rel[i][q] & mask[q]) != 0;
+        if (!dropped) mask[i >> 5] |= 1u << (i & 31);
+      }
+      for (int q = 0; q < 8; ++q) keepmask[q] = mask[q];
+    }
+    __syncthreads();
+    const bool k = tid < static_cast<int>(n_in) &&
+                   ((keepmask[tid >> 5] >> (tid & 31)) & 1u);
+    if (tid < static_cast<int>(n_in)) keep[base + tid] = k ? 1 : 0;
+    // ordered append of this chunk's retained candidates
+    const unsigned bm = __ballot_sync(FULL, k);
+    if ((tid & 31) == 0 && (tid >> 5) < nwg) wsum[tid >> 5] = __popc(bm);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int q = 0; q < nwg; ++q) {
+      if (q < (tid >> 5)) before += wsum[q];
+      total += wsum[q];
+    }
+    if (k) ret[nret + before + __popc(bm & ((1u << (tid & 31)) - 1u))] = ord[base + tid];
+    nret += total;
+    __syncthreads();
+  }
+  // 4. report: exonerated in sorted order; suspects = first retained entry
+  //    per rank (its evidence in that order); suspects sorted by rank.
+  const int32_t R = a.s.R > 0 ? a.s.R : 1;
+  const uint32_t rw = static_cast<uint32_t>(R + 31) / 32;
+  for (int32_t r = tid; r < R; r += blockDim.x) minpos[r] = 0xFFFFFFFFu;
+  for (uint32_t w = tid; w < rw; w += blockDim.x) rbits[w] = 0;
+  __syncthreads();
+  for (uint32_t x = tid; x < C; x += blockDim.x)
+    if (keep[x]) {
+      const int32_t r = cands[ord[x]].rank;
+      if (r >= 0 && r < R) atomicMin(&minpos[r], x);
+    }
+  __syncthreads();
+  csg_suspect* sus = a.sus + tp.sus_off;  // [C] suspects, then [C] exonerated
+  csg_suspect* exo = sus + C;
+  csg_evidence* evo = a.ev + tp.ev_off;
+  uint32_t run_e = 0, run_s = 0, run_v = 0;
+  const int nwb = blockDim.x >> 5;
+  for (uint32_t base = 0; base < C; base += blockDim.x) {
+    const uint32_t x = base + tid;
+    const bool valid = x < C;
+    Cand c;
+    if (valid) c = cands[ord[x]];
+    const bool isexo = valid && !keep[x];
+    const bool isfirst = valid && keep[x] && c.rank >= 0 && c.rank < R &&
+                         minpos[c.rank] == x;
+    const uint32_t evn = isfirst ? c.ev_n : 0;
+    // block exclusive scan of (isexo, isfirst, evn)
+    uint32_t e = isexo, f = isfirst, v = evn;
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t e2 = __shfl_up_sync(FULL, e, o), f2 = __shfl_up_sync(FULL, f, o),
+                     v2 = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) {
+        e += e2;
+        f += f2;
+        v += v2;
+      }
+    }
+    if (lane == 31) {
+      scan3[warp][0] = e;
+      scan3[warp][1] = f;
+      scan3[warp][2] = v;
+    }
+    __syncthreads();
+    uint32_t be = 0, bf = 0, bv = 0, te = 0, tf = 0, tv = 0;
+    for (int q = 0; q < nwb; ++q) {
+      if (q < warp) {
+        be += scan3[q][0];
+        bf += scan3[q][1];
+        bv += scan3[q][2];
+      }
+      te += scan3[q][0];
+      tf += scan3[q][1];
+      tv += scan3[q][2];
+    }
+    if (isexo) exo[run_e + be + e - 1] = to_suspect(c);
+    if (isfirst) {
+      sus[run_s + bf + f - 1] = to_suspect(c);
+      atomicOr(&rbits[c.rank >> 5], 1u << (c.rank & 31));
+      const uint32_t v0 = run_v + bv + v - evn;
+      for (uint32_t q = 0; q < evn; ++q) evo[v0 + q] = a.cev[c.ev_off + q];
+    }
+    run_e += te;
+    run_s += tf;
+    run_v += tv;
+    __syncthreads();
+  }
+  // suspect ranks are unique: rank-sorted position = number of suspect ranks
+  // below it (prefix popcount over the rank bitmap)
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (uint32_t w = 0; w < rw; ++w) {
+      const uint32_t c = __popc(rbits[w]);
+      woff[w] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < run_s; i += blockDim.x) {
+    const int32_t r = sus[i].rank;
+    const uint32_t pos = woff[r >> 5] + __popc(rbits[r >> 5] & ((1u << (r & 31)) - 1u));
+    stmp[pos] = sus[i];
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < run_s; i += blockDim.x) sus[i] = stmp[i];
+  if (tid == 0) {
+    o.verdict = run_s ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED;
+    o.n_sus = run_s;
+    o.exo_off = tp.sus_off + C;
+    o.n_exo = run_e;
+    o.n_ev = run_v;
+    a.out[tp.j] = o;
+  }
+}
+
+struct PackSeg {
+  uint32_t src, dst, n, kind;  // kind 0 suspects, 1 evidence
+};
+
+__global__ void k_pack(const PackSeg* __restrict__ segs,
+                       const csg_suspect* __restrict__ sus,
+                       const csg_evidence* __restrict__ ev,
+                       csg_suspect* __restrict__ osus,
+                       csg_evidence* __restrict__ oev) {
+  const PackSeg sg = segs[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < sg.n; i += blockDim.x) {
+    if (sg.kind == 0) osus[sg.dst + i] = sus[sg.src + i];
+    else oev[sg.dst + i] = ev[sg.src + i];
+  }
+}
+
 __global__ void __launch_bounds__(kDecideThreads)
     k_decide(DecideArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -1558,16 +2069,14 @@ __global__ void __launch_bounds__(kDecideThreads)
     sh.sus_base = sh.exo_base = sh.ev_base = 0;
   }
   __syncthreads();
-  uint32_t* scratch = a.pools.u32 + static_cast<uint64_t>(j) * a.scratch_per_trip;
+  uint32_t* scratch = a.pools.u32 + (a.js_of[j] >= 0 ? static_cast<uint64_t>(j) * a.scratch_per_trip : 0);
   const int32_t naff = a.n_aff[j];
   if (naff == 0 || a.m.opn == 0) {
     write_trip(a, j, CSG_VERDICT_FALSE_TRIGGER, naff, a.N, sh);
     return;
   }
-  if (a.trip_kind[j] == CSG_TRIGGER_FAILURE)
-    decide_failure(a, j, sh, scratch);
-  else
-    decide_straggler(a, j, sh, scratch);
+  if (a.trip_kind[j] == CSG_TRIGGER_FAILURE) return;  // k_exonerate
+  decide_straggler(a, j, sh, scratch);
 }
 
 }  // namespace
@@ -1635,22 +2144,29 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
   }
   const int32_t Js = static_cast<int32_t>(h_strag.size());
-  DevBuf d_t, d_kind, d_rank, d_js, d_strag;
-  const double* dt = upload(d_t, h_t, st);
-  const int32_t* dkind = upload(d_kind, h_kind, st);
-  const int32_t* drank = upload(d_rank, h_rank, st);
-  const int32_t* djs = upload(d_js, h_js, st);
-  const int32_t* dstrag = upload(d_strag, h_strag, st);
+  const double* dt = upload(c->buf("rca.t"), h_t, st);
+  const int32_t* dkind = upload(c->buf("rca.kind"), h_kind, st);
+  const int32_t* drank = upload(c->buf("rca.rank"), h_rank, st);
+  const int32_t* djs = upload(c->buf("rca.js"), h_js, st);
+  const int32_t* dstrag = upload(c->buf("rca.strag"), h_strag, st);
 
   // K1: per (trip, rank) prefix summaries
-  DevBuf rs, chan_pos;
+  DevBuf& rs = c->buf("rca.rs");
+  DevBuf& chan_pos = c->buf("rca.chan_pos");
   rs.ensure(static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum));
   chan_pos.ensure(static_cast<size_t>(J) * std::max(R, 1) * nch * 4);
   if (R > 0) {
     int wpb = 32768 / (nch * 4);
     wpb = std::max(1, std::min(8, wpb));
     const uint64_t warps = static_cast<uint64_t>(R) * J;
-    {
+    static const bool no_fi = std::getenv("CSG_DISABLE_FLOW_INDEX") != nullptr;
+    if (!no_fi && store_build_flow_index(s)) {
+      ProfScope ps_(c->lc, "k_rank_summary_fi", st);
+      k_rank_summary_fi<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
+                          wpb * nch * 4, st>>>(sv, s->flow_view(), J, dt, cfg.delta_ms,
+                                               rs.as<RankSum>(),
+                                               chan_pos.as<uint32_t>(), nch);
+    } else {
       ProfScope ps_(c->lc, "k_rank_summary", st);
       k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
                        wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
@@ -1659,11 +2175,16 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
   }
   // K2/K3: straggler iteration tables
-  DevBuf tbl_s, tbl_e, gi, gi_last;
+  DevBuf& tbl_s = c->buf("rca.tbl_s");
+  DevBuf& tbl_e = c->buf("rca.tbl_e");
+  DevBuf& gi = c->buf("rca.gi");
+  DevBuf& gi_last = c->buf("rca.gi_last");
   int64_t it_min = 0;
   int32_t n_it = 1;
   gi.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max(G, 1) * sizeof(GroupIter));
   gi_last.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max(G, 1) * k * 8);
+  tbl_s.ensure(8);
+  tbl_e.ensure(8);
   if (Js > 0) {
     CSG_CUDA(cudaMemsetAsync(gi.p, 0, gi.bytes, st));
     if (opn > 0 && M > 0) {
@@ -1682,26 +2203,24 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       CSG_CUDA(cudaMemsetAsync(tbl_e.p, 0, cells * 8, st));
       if (R > 0) {
         const uint64_t warps = static_cast<uint64_t>(R) * Js;
-        {
-          ProfScope ps_(c->lc, "k_iter_tables", st);
-          k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
-                          st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
-                                M, tbl_s.as<unsigned long long>(),
-                                tbl_e.as<unsigned long long>());
-        }
+        ProfScope ps_(c->lc, "k_iter_tables", st);
+        k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                        st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
+                              M, tbl_s.as<unsigned long long>(),
+                              tbl_e.as<unsigned long long>());
       }
       const uint64_t gw = static_cast<uint64_t>(G) * Js;
-      {
-        ProfScope ps_(c->lc, "k_group_iters", st);
-        k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
-            mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
-            tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
-            gi.as<GroupIter>(), gi_last.as<int64_t>());
-      }
+      ProfScope ps_(c->lc, "k_group_iters", st);
+      k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
+          mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
+          tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
+          gi.as<GroupIter>(), gi_last.as<int64_t>());
     }
   }
   // K4: affected groups
-  DevBuf aff, aff_flag, n_aff;
+  DevBuf& aff = c->buf("rca.aff");
+  DevBuf& aff_flag = c->buf("rca.aff_flag");
+  DevBuf& n_aff = c->buf("rca.n_aff");
   aff.ensure(static_cast<size_t>(J) * std::max(G, 1) * 4);
   aff_flag.ensure(static_cast<size_t>(J) * std::max(G, 1));
   n_aff.ensure(static_cast<size_t>(J) * 4);
@@ -1719,14 +2238,17 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                              cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));
   CSG_CUDA(cudaGetLastError());
+  c->d2h_bytes += static_cast<uint64_t>(J) * 4 + static_cast<uint64_t>(J) * G * 4;
   out.trips.assign(J, TripOut{});
   for (int32_t j = 0; j < J; ++j) out.trips[j].n_aff = h_naff[j];
   if (affected_only) return;
 
-  // K5: flow rules
-  DevBuf fs, slot_group, err;
+  DevBuf& err = c->buf("rca.err");
   err.ensure(4);
   CSG_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+  // K5: straggler flow rules
+  DevBuf& fs = c->buf("rca.fs");
+  DevBuf& slot_group = c->buf("rca.slot_group");
   fs.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max<uint32_t>(M, 1) * sizeof(FlowSum));
   if (Js > 0 && opn > 0 && M > 0) {
     store_build_op_index(s, opn);
@@ -1736,16 +2258,19 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
         h_sg[q] = static_cast<uint32_t>(g);
     upload(slot_group, h_sg, st);
     const uint64_t warps = static_cast<uint64_t>(M) * Js;
-    {
-      ProfScope ps_(c->lc, "k_flow", st);
-      k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
-          sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
-          slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
-          aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
-    }
+    ProfScope ps_(c->lc, "k_flow", st);
+    k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
+        sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+        slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+        aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
   }
 
-  // K6: decide. Pool sizes from the affected lists.
+  // ---- failure trips: per-group candidates + per-trip exoneration ----
+  const int EV = kEvSlots(nch);
+  std::vector<FailItem> items;
+  std::vector<ExoTrip> exo;
+  std::vector<uint64_t> item_m;  // members per item (upper bound of its cands)
+  uint64_t cand_ub = 0, sus_fail = 0, ev_fail = 0, scratch_bytes = 0;
   uint64_t tot_all = 0, tot_max = 0;
   int32_t m_max = 1;
   for (int32_t g = 0; g < G; ++g)
@@ -1758,27 +2283,101 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
     tot_all += tot;
     tot_max = std::max(tot_max, tot);
+    if (h_kind[j] != CSG_TRIGGER_FAILURE || h_naff[j] == 0 || opn == 0) continue;
+    ExoTrip e;
+    std::memset(&e, 0, sizeof(e));
+    e.j = j;
+    e.naff = h_naff[j];
+    e.first_item = static_cast<uint32_t>(items.size());
+    e.n_items = static_cast<uint32_t>(h_naff[j]);
+    for (int32_t i = 0; i < h_naff[j]; ++i)
+      items.push_back(FailItem{j, out.aff[static_cast<size_t>(j) * G + i]});
+    const uint64_t C = tot;
+    uint64_t P = 1;
+    while (P < C) P <<= 1;
+    const uint64_t Rs = std::max<int32_t>(R, 1);
+    const uint64_t need = ((P * 4 + 15) & ~15ull) + ((C * 8 + 15) & ~15ull) +
+                          ((C * 4 + 15) & ~15ull) + ((C + 15) & ~15ull) +
+                          4 * ((Rs + 3) & ~3ull) + 8 * (((Rs + 31) / 32 + 3) & ~3ull) +
+                          32 * C + 64;
+    e.scratch_off = scratch_bytes;
+    scratch_bytes += (need + 255) & ~255ull;
+    e.sus_off = static_cast<uint32_t>(sus_fail);
+    sus_fail += 2 * C;
+    e.ev_off = static_cast<uint32_t>(ev_fail);
+    ev_fail += C * EV;
+    cand_ub += C;
+    exo.push_back(e);
   }
-  const uint64_t per_ev = std::max<uint64_t>(2 * nch + 1, k + 1);
-  uint64_t cand_cap = 2 * tot_all + 16;
-  uint64_t cev_cap = tot_all * per_ev + 16;
-  uint64_t sus_cap = 6 * tot_all + 16;
-  uint64_t ev_cap = cev_cap;
-  uint64_t bits_cap = 1ull << 22;
+  if (sus_fail > 0xF0000000ull || ev_fail > 0xF0000000ull || cand_ub * EV > 0xF0000000ull)
+    throw Error(CSG_ERR_RUNTIME, "engine: failure analysis outputs exceed 2^32 entries");
+  const int32_t n_items = static_cast<int32_t>(items.size());
+  DevBuf& d_items = c->buf("rca.items");
+  DevBuf& d_pick = c->buf("rca.pick");
+  DevBuf& d_off = c->buf("rca.off");
+  DevBuf& d_cand = c->buf("rca.cand");
+  DevBuf& d_cev = c->buf("rca.cev");
+  DevBuf& d_exo = c->buf("rca.exo");
+  DevBuf& d_exs = c->buf("rca.exo_scratch");
+  if (n_items > 0) {
+    upload(d_items, items, st);
+    d_pick.ensure(static_cast<size_t>(n_items) * sizeof(GroupPick));
+    d_off.ensure(static_cast<size_t>(n_items + 1) * 4);
+    CSG_CUDA(cudaMemsetAsync(d_off.as<uint32_t>() + n_items, 0, 4, st));
+    d_cand.ensure(cand_ub * sizeof(Cand) + sizeof(Cand));
+    d_cev.ensure(cand_ub * EV * sizeof(csg_evidence) + sizeof(csg_evidence));
+    upload(d_exo, exo, st);
+    d_exs.ensure(scratch_bytes + 256);
+    {
+      ProfScope ps_(c->lc, "k_fail_count", st);
+      k_fail_count<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 255) / 256),
+                     256, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
+                                   rs.as<RankSum>(), d_pick.as<GroupPick>(),
+                                   d_off.as<uint32_t>());
+    }
+    exclusive_scan_u32(d_off.as<uint32_t>(), static_cast<uint64_t>(n_items) + 1,
+                       c->buf("rca.scan_tmp"), st, c->lc);
+    {
+      ProfScope ps_(c->lc, "k_fail_cands", st);
+      k_fail_cands<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 127) / 128),
+                     128, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
+                                   rs.as<RankSum>(), chan_pos.as<uint32_t>(), nch,
+                                   d_pick.as<GroupPick>(), d_off.as<uint32_t>(),
+                                   d_cand.as<Cand>(), d_cev.as<csg_evidence>(),
+                                   err.as<uint32_t>());
+    }
+  }
+
+  // ---- output pools: failure regions first, straggler bump allocations after
   const uint64_t C2 = 2 * tot_max + 8;
+  const uint64_t per_ev = std::max<uint64_t>(2 * nch + 1, k + 1);
+  uint64_t cand_cap = Js ? 2 * tot_all + 16 : 16;
+  uint64_t cev_cap = Js ? tot_all * per_ev + 16 : 16;
+  uint64_t sus_cap = sus_fail + (Js ? 6 * tot_all : 0) + 16;
+  uint64_t ev_cap = ev_fail + (Js ? tot_all * per_ev : 0) + 16;
+  uint64_t bits_cap = 1ull << 22;
   const uint64_t mwords = (static_cast<uint64_t>(R) + 31) / 32 + 1;
-  uint64_t spt = std::max<uint64_t>(12 * C2, 4 * static_cast<uint64_t>(m_max));
-  spt = std::max<uint64_t>(spt, mwords + 2 * std::max<uint64_t>(
-                                                std::max<uint64_t>(m_max, s->max_seg),
-                                                8 * C2));
+  uint64_t spt = 16;
+  if (Js) {
+    spt = std::max<uint64_t>(12 * C2, 4 * static_cast<uint64_t>(m_max));
+    spt = std::max<uint64_t>(spt, mwords + 2 * std::max<uint64_t>(
+                                                  std::max<uint64_t>(m_max, s->max_seg),
+                                                  8 * C2));
+  }
   spt = (spt + 64 + 3) & ~3ull;  // 16-byte aligned per-trip slices
   if (spt > 0xFFFFFFF0ull)
     throw Error(CSG_ERR_RUNTIME, "engine: per-trip scratch exceeds 2^32 words");
-
-  DevBuf p_cand, p_cev, p_sus, p_ev, p_bits, p_u32, p_used, d_out;
+  DevBuf& p_cand = c->buf("rca.p_cand");
+  DevBuf& p_cev = c->buf("rca.p_cev");
+  DevBuf& p_sus = c->buf("rca.p_sus");
+  DevBuf& p_ev = c->buf("rca.p_ev");
+  DevBuf& p_bits = c->buf("rca.p_bits");
+  DevBuf& p_u32 = c->buf("rca.p_u32");
+  DevBuf& p_used = c->buf("rca.p_used");
+  DevBuf& d_out = c->buf("rca.out");
   d_out.ensure(static_cast<size_t>(J) * sizeof(TripOut));
   p_used.ensure(8 * 8);
-  p_u32.ensure(static_cast<size_t>(J) * spt * 4);
+  p_u32.ensure(static_cast<size_t>(Js ? J : 1) * spt * 4);
   DecideArgs a;
   a.s = sv;
   a.m = mv;
@@ -1837,8 +2436,34 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     a.pools.u32 = p_u32.as<uint32_t>();
     a.pools.u32_cap = static_cast<unsigned long long>(J) * spt;
     a.pools.used = p_used.as<unsigned long long>();
-    CSG_CUDA(cudaMemsetAsync(p_used.p, 0, 8 * 8, st));
-    // keep K5 errors, clear decide-retry flags
+    unsigned long long init_used[8] = {0, 0, sus_fail, ev_fail, 0, 0, 0, 0};
+    CSG_CUDA(cudaMemcpyAsync(p_used.p, init_used, 8 * 8, cudaMemcpyHostToDevice, st));
+    if (!exo.empty()) {
+      ExoArgs ea;
+      ea.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
+      ea.s = sv;
+      ea.m = mv;
+      ea.cand = d_cand.as<Cand>();
+      ea.cev = d_cev.as<csg_evidence>();
+      ea.EV = EV;
+      ea.off = d_off.as<uint32_t>();
+      ea.trips = d_exo.as<ExoTrip>();
+      ea.n_trips = static_cast<int32_t>(exo.size());
+      ea.scratch = d_exs.as<unsigned char>();
+      ea.bits = p_bits.as<unsigned long long>();
+      ea.bits_cap = bits_cap;
+      ea.bits_used = p_used.as<unsigned long long>() + P_BITS;
+      ea.sus = p_sus.as<csg_suspect>();
+      ea.ev = p_ev.as<csg_evidence>();
+      ea.out = d_out.as<TripOut>();
+      ea.N = s->n;
+      ea.err = err.as<uint32_t>();
+      CSG_CUDA(cudaFuncSetAttribute(k_exonerate,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kExoSmemMax)));
+      ProfScope ps_(c->lc, "k_exonerate", st);
+      k_exonerate<<<static_cast<unsigned>(exo.size()), kExoThreads, kExoSmemMax, st>>>(ea);
+    }
     {
       ProfScope ps_(c->lc, "k_decide", st);
       k_decide<<<J, kDecideThreads, shm, st>>>(a);
@@ -1857,31 +2482,59 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (!(h_err & (DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH))) break;
     if (attempt >= 6)
       throw Error(CSG_ERR_RUNTIME, "engine: RCA output pools exhausted");
-    if (h_err & DEV_ERR_DAG_SCRATCH) bits_cap = std::max<uint64_t>(bits_cap * 4, used[P_BITS] * 2);
+    if (h_err & DEV_ERR_DAG_SCRATCH)
+      bits_cap = std::max<uint64_t>(bits_cap * 4, used[P_BITS] * 2);
     if (h_err & DEV_ERR_POOL) {
       cand_cap *= 4;
       cev_cap *= 4;
-      sus_cap *= 4;
-      ev_cap *= 4;
+      sus_cap = sus_fail + (sus_cap - sus_fail) * 4;
+      ev_cap = ev_fail + (ev_cap - ev_fail) * 4;
     }
     h_err &= ~(DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH);
     CSG_CUDA(cudaMemcpyAsync(err.p, &h_err, 4, cudaMemcpyHostToDevice, st));
   }
+  // ---- pack the reports densely and bring them back in three copies
   std::vector<TripOut> to(J);
   CSG_CUDA(cudaMemcpyAsync(to.data(), d_out.p, J * sizeof(TripOut),
                            cudaMemcpyDeviceToHost, st));
-  out.sus.resize(used[P_SUS]);
-  out.ev.resize(used[P_EV]);
-  if (used[P_SUS])
-    CSG_CUDA(cudaMemcpyAsync(out.sus.data(), p_sus.p, used[P_SUS] * sizeof(csg_suspect),
+  CSG_CUDA(cudaStreamSynchronize(st));
+  std::vector<PackSeg> segs;
+  uint64_t ns_tot = 0, ne_tot = 0;
+  for (int32_t j = 0; j < J; ++j) {
+    TripOut& t = to[j];
+    segs.push_back(PackSeg{t.sus_off, static_cast<uint32_t>(ns_tot), t.n_sus, 0});
+    t.sus_off = static_cast<uint32_t>(ns_tot);
+    ns_tot += t.n_sus;
+    segs.push_back(PackSeg{t.exo_off, static_cast<uint32_t>(ns_tot), t.n_exo, 0});
+    t.exo_off = static_cast<uint32_t>(ns_tot);
+    ns_tot += t.n_exo;
+    segs.push_back(PackSeg{t.ev_off, static_cast<uint32_t>(ne_tot), t.n_ev, 1});
+    t.ev_off = static_cast<uint32_t>(ne_tot);
+    ne_tot += t.n_ev;
+  }
+  DevBuf& d_segs = c->buf("rca.segs");
+  DevBuf& d_psus = c->buf("rca.packed_sus");
+  DevBuf& d_pev = c->buf("rca.packed_ev");
+  upload(d_segs, segs, st);
+  d_psus.ensure(ns_tot * sizeof(csg_suspect) + 32);
+  d_pev.ensure(ne_tot * sizeof(csg_evidence) + 32);
+  {
+    ProfScope ps_(c->lc, "k_pack", st);
+    k_pack<<<static_cast<unsigned>(segs.size()), 128, 0, st>>>(
+        d_segs.as<PackSeg>(), p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
+        d_psus.as<csg_suspect>(), d_pev.as<csg_evidence>());
+  }
+  out.sus.resize(ns_tot);
+  out.ev.resize(ne_tot);
+  if (ns_tot)
+    CSG_CUDA(cudaMemcpyAsync(out.sus.data(), d_psus.p, ns_tot * sizeof(csg_suspect),
                              cudaMemcpyDeviceToHost, st));
-  if (used[P_EV])
-    CSG_CUDA(cudaMemcpyAsync(out.ev.data(), p_ev.p, used[P_EV] * sizeof(csg_evidence),
+  if (ne_tot)
+    CSG_CUDA(cudaMemcpyAsync(out.ev.data(), d_pev.p, ne_tot * sizeof(csg_evidence),
                              cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));
-  c->d2h_bytes += J * sizeof(TripOut) + used[P_SUS] * sizeof(csg_suspect) +
-                  used[P_EV] * sizeof(csg_evidence) +
-                  static_cast<uint64_t>(J) * (4 + static_cast<uint64_t>(G) * 4);
+  c->d2h_bytes += J * sizeof(TripOut) + ns_tot * sizeof(csg_suspect) +
+                  ne_tot * sizeof(csg_evidence) + 8 * 8 + 4;
   out.trips = to;
 }
 

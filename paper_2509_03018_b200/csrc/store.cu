@@ -23,22 +23,34 @@ __device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long 
   atomicMax(a, v);
 }
 
-__global__ void k_stats(const csg_packed_record* __restrict__ r, uint64_t n,
-                        StoreStats* __restrict__ st) {
+// One pass over the packed records: store statistics (max timestamp, rank /
+// channel / op ranges, NaN count) and the (rank, store index) sort pairs.
+__global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n,
+                             StoreStats* __restrict__ st,
+                             uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
   unsigned long long tsk = 0;
   int mnr = INT_MAX, mxr = INT_MIN, mnc = INT_MAX, mxc = INT_MIN;
   long long mno = LLONG_MAX, mxo = LLONG_MIN;
   unsigned long long nan = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const double t = r[i].ts;
+    const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + i);
+    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1);
+    double t;
+    memcpy(&t, &h0.x, 8);
+    const long long op = static_cast<long long>(h0.y);
+    const int rank = static_cast<int>(hm.x & 0xffffffffu);
+    const int chan = static_cast<int>(hm.y & 0xffffffffu);
     if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
-    mnr = min(mnr, r[i].rank);
-    mxr = max(mxr, r[i].rank);
-    mnc = min(mnc, r[i].channel);
-    mxc = max(mxc, r[i].channel);
-    mno = min(mno, (long long)r[i].op_seq);
-    mxo = max(mxo, (long long)r[i].op_seq);
+    mnr = min(mnr, rank);
+    mxr = max(mxr, rank);
+    mnc = min(mnc, chan);
+    mxc = max(mxc, chan);
+    mno = min(mno, op);
+    mxo = max(mxo, op);
+    keys[i] = static_cast<uint32_t>(rank);
+    vals[i] = static_cast<uint32_t>(i);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -60,16 +72,6 @@ __global__ void k_stats(const csg_packed_record* __restrict__ r, uint64_t n,
     atomicMin(&st->min_op, mno);
     atomicMax(&st->max_op, mxo);
     if (nan) atomicAdd(&st->n_nan, nan);
-  }
-}
-
-__global__ void k_rank_keys(const csg_packed_record* __restrict__ r, uint64_t n,
-                            uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    keys[i] = static_cast<uint32_t>(r[i].rank);
-    vals[i] = static_cast<uint32_t>(i);
   }
 }
 
@@ -150,6 +152,18 @@ __global__ void k_opidx_rank(StoreView s, const uint32_t* __restrict__ pos,
       if (s.rank_off[md] <= p) lo = md; else hi = md;
     }
     rank[i] = lo;
+  }
+}
+
+__global__ void k_flow_keys(StoreView s, int64_t min_op, int op_shift,
+                            int rank_shift, unsigned long long* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    keys[p] = (static_cast<unsigned long long>(s.rank_of[p]) << rank_shift) |
+              (static_cast<unsigned long long>(s.op[p] - min_op) << op_shift) |
+              static_cast<unsigned long long>(s.chan[p]);
+    vals[p] = static_cast<uint32_t>(p);
   }
 }
 
@@ -299,11 +313,13 @@ void store_build_index(csg_store* s) {
   s->stats_dev.ensure(sizeof(StoreStats));
   CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
                            cudaMemcpyHostToDevice, st));
+  s->perm.ensure(n * 4 + 4);
+  s->keys.ensure(n * 4 + 4);
   if (n) {
-    {
-      ProfScope ps_(c->lc, "k_stats", st);
-      k_stats<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>());
-    }
+    ProfScope ps_(c->lc, "k_stats_keys", st);
+    k_stats_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
+                                              s->keys.as<uint32_t>(),
+                                              s->perm.as<uint32_t>());
   }
   CSG_CUDA(cudaMemcpyAsync(&h, s->stats_dev.p, sizeof(h),
                            cudaMemcpyDeviceToHost, st));
@@ -333,8 +349,6 @@ void store_build_index(csg_store* s) {
   const int32_t R = s->R;
 
   s->rank_off.ensure((static_cast<size_t>(R) + 1) * 4);
-  s->perm.ensure(n * 4 + 4);
-  s->keys.ensure(n * 4 + 4);
   s->ts.ensure(n * 8 + 8);
   s->runmax.ensure(n * 8 + 8);
   s->op.ensure(n * 8 + 8);
@@ -344,11 +358,6 @@ void store_build_index(csg_store* s) {
   s->pa.ensure(n * 8 + 8);
   s->pb.ensure(n * 8 + 8);
   if (n) {
-    {
-      ProfScope ps_(c->lc, "k_rank_keys", st);
-      k_rank_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->keys.as<uint32_t>(),
-                                               s->perm.as<uint32_t>());
-    }
     radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
                    bits_for(static_cast<uint64_t>(R > 0 ? R - 1 : 0)), s->sort,
                    st, c->lc);
@@ -385,6 +394,7 @@ void store_build_index(csg_store* s) {
   CSG_CUDA(cudaGetLastError());
   s->indexed = true;
   s->op_indexed = false;
+  s->flow_indexed = false;
 }
 
 void store_build_op_index(csg_store* s, int32_t opn) {
@@ -394,7 +404,7 @@ void store_build_op_index(csg_store* s, int32_t opn) {
   cudaStream_t st = c->stream;
   const uint64_t n = s->n;
   StoreView v = s->view();
-  DevBuf flags;
+  DevBuf& flags = c->buf("opidx.flags");
   flags.ensure(n * 4 + 4);
   uint32_t count = 0;
   if (n) {
@@ -438,6 +448,36 @@ void store_build_op_index(csg_store* s, int32_t opn) {
   }
   CSG_CUDA(cudaGetLastError());
   s->op_indexed = true;
+}
+
+bool store_build_flow_index(csg_store* s) {
+  store_build_index(s);
+  if (s->flow_indexed) return true;
+  const int cb = bits_for(static_cast<uint64_t>(std::max(s->nch, 1) - 1));
+  const int ob = bits_for(static_cast<uint64_t>(s->max_op - s->min_op));
+  const int rb = bits_for(static_cast<uint64_t>(std::max(s->R, 1) - 1));
+  if (cb + ob + rb > 64) return false;
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  const uint64_t n = s->n;
+  s->flow_op_shift = cb;
+  s->flow_rank_shift = cb + ob;
+  s->flow_key_bits = cb + ob + rb;
+  s->fl_keys.ensure(n * 8 + 8);
+  s->fl_pos.ensure(n * 4 + 4);
+  if (n) {
+    {
+      ProfScope ps_(c->lc, "k_flow_keys", st);
+      k_flow_keys<<<grid_for(n), 256, 0, st>>>(
+          s->view(), s->min_op, s->flow_op_shift, s->flow_rank_shift,
+          s->fl_keys.as<unsigned long long>(), s->fl_pos.as<uint32_t>());
+    }
+    radix_sort_u64(reinterpret_cast<uint64_t*>(s->fl_keys.p), s->fl_pos.as<uint32_t>(),
+                   n, s->flow_key_bits, s->sort, st, c->lc);
+  }
+  CSG_CUDA(cudaGetLastError());
+  s->flow_indexed = true;
+  return true;
 }
 
 // ---- query / last_log host entry points --------------------------------------

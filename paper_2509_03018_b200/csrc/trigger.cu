@@ -249,7 +249,7 @@ int32_t trigger_ticks(csg_store* s, double I, double delta, DevBuf& ticks) {
     throw Error(CSG_ERR_RUNTIME, "run_detection: too many detection ticks");
   const int64_t cap = static_cast<int64_t>(est) + 4;
   ticks.ensure(static_cast<size_t>(cap) * 8 + 8);
-  DevBuf dn;
+  DevBuf& dn = c->buf("trig.ticks_n");
   dn.ensure(4);
   {
     ProfScope ps_(c->lc, "k_ticks", c->stream);
@@ -268,7 +268,9 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   csg_ctx* c = s->ctx;
   events.ensure(static_cast<size_t>(T + 1) * sizeof(csg_trigger_event));
   if (T <= 0 || S <= 0) return 0;
-  DevBuf ws, trip, dn;
+  DevBuf& ws = c->buf("trig.ws");
+  DevBuf& trip = c->buf("trig.trip");
+  DevBuf& dn = c->buf("trig.n");
   ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);

@@ -14,12 +14,21 @@ import pytest
 from tests.conftest import GOLDEN
 from tests.golden import codec
 
-CATALOG = ["clean"] + [f"scenario{i}" for i in range(1, 8)]
+CATALOG = ["clean"] + [f"scenario{i}" for i in range(1, 8)] + \
+    ["synth_hang_128", "synth_strag_128"]
 MANIFEST = json.load(open(os.path.join(GOLDEN, "manifest.json")))
 
 
 def golden(name):
-    recs = codec.load_file(os.path.join(GOLDEN, f"catalog_{name}.rec.xz"))
+    path = os.path.join(GOLDEN, f"catalog_{name}.rec.xz")
+    if os.path.exists(path):
+        recs = codec.load_file(path)
+    else:  # synthetic trace: regenerate deterministically and pin its bytes
+        from paper_2509_03018_b200 import engine
+        recs = engine.synthesize(engine.Scenario.load(
+            os.path.join(GOLDEN, "configs", name + ".json")), 0)
+        from tests.golden.make_golden import fnv1a64
+        assert fnv1a64(recs.tobytes()) == MANIFEST[name]["records_fnv1a64"]
     reports = open(os.path.join(GOLDEN, f"catalog_{name}.reports.jsonl")).read()
     full = [json.loads(l) for l in open(os.path.join(GOLDEN, f"catalog_{name}.full.jsonl"))]
     return recs, reports, full
@@ -72,3 +81,24 @@ def test_catalog_c_api_file_path(eng, oracle, tmp_path):
     _, reports, _ = golden("scenario1")
     assert res.reports_jsonl == reports
     assert out.read_text() == reports
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["scenario1", "scenario5", "synth_hang_128"])
+def test_prefix_scan_fallback_matches(name, tmp_path):
+    """The flow-index lookups and the plain prefix-scan summary kernel must
+    agree (the scan path is the fallback for >64-bit flow keys)."""
+    import subprocess
+    import sys
+    code = (
+        "import json,os,sys; sys.path.insert(0, %r);"
+        "from tests.test_gpu_catalog import golden; from paper_2509_03018_b200 import engine as E;"
+        "from tests.conftest import GOLDEN;"
+        "recs,_,full = golden(%r);"
+        "s = E.Scenario.load(os.path.join(GOLDEN,'configs',%r+'.json'));"
+        "t,p = s.layout(); tc,ac,seed = s.configs();"
+        "got,_ = E.run_detection(E.TraceStore(records=recs), E.Model(t,p), tc, ac, seed);"
+        "assert got == full; print('ok')" % (os.path.dirname(GOLDEN).rsplit('/tests', 1)[0], name, name))
+    env = dict(os.environ, CSG_DISABLE_FLOW_INDEX="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
