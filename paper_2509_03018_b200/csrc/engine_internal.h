@@ -90,9 +90,14 @@ struct StoreView {
 struct FlowView {
   uint64_t n = 0;
   int op_shift = 0, rank_shift = 0;
+  int narrow = 0;  // keys stored as u32 (key bits <= 32)
   int64_t min_op = 0;
-  const unsigned long long* keys = nullptr;
+  const void* keys = nullptr;
   const uint32_t* pos = nullptr;
+  __device__ unsigned long long key(uint64_t i) const {
+    return narrow ? static_cast<const uint32_t*>(keys)[i]
+                  : static_cast<const unsigned long long*>(keys)[i];
+  }
 };
 
 __host__ __device__ inline int ko_kind(uint8_t ko) { return ko & 1; }

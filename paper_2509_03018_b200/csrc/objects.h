@@ -105,7 +105,8 @@ struct csg_store {
     f.op_shift = flow_op_shift;
     f.rank_shift = flow_rank_shift;
     f.min_op = min_op;
-    f.keys = fl_keys.as<unsigned long long>();
+    f.narrow = flow_key_bits <= 32 ? 1 : 0;
+    f.keys = fl_keys.p;
     f.pos = fl_pos.as<uint32_t>();
     return f;
   }

@@ -133,7 +133,11 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
     // stuck_on_incomplete (rca.cpp:216-237): the last prefix record with
     // ts >= window_start is a state whose op has no prefix completion.
     int64_t found = -1;
-    for (int64_t top = static_cast<int64_t>(cend) - 1;
+    // The prefix's running max bounds every timestamp in it: a rank that
+    // has been silent since before the window has nothing to scan.
+    const int64_t scan_from =
+        rm[cend - 1] >= ws ? static_cast<int64_t>(cend) - 1 : static_cast<int64_t>(b) - 1;
+    for (int64_t top = scan_from;
          top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
       const int64_t p = top - lane;
       const bool pr = p >= static_cast<int64_t>(b) && s.ts[p] >= ws;
@@ -240,7 +244,11 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
     o.last_ts = s.ts[cend - 1];
     o.last_chan = s.chan[cend - 1];
     int64_t found = -1;
-    for (int64_t top = static_cast<int64_t>(cend) - 1;
+    // The prefix's running max bounds every timestamp in it: a rank that
+    // has been silent since before the window has nothing to scan.
+    const int64_t scan_from =
+        rm[cend - 1] >= ws ? static_cast<int64_t>(cend) - 1 : static_cast<int64_t>(b) - 1;
+    for (int64_t top = scan_from;
          top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
       const int64_t p = top - lane;
       const bool pr = p >= static_cast<int64_t>(b) && s.ts[p] >= ws;
@@ -258,8 +266,8 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
       const unsigned long long k0 =
           rk | (static_cast<unsigned long long>(op - f.min_op) << f.op_shift);
       const unsigned long long k1 = k0 + (1ull << f.op_shift);
-      fo = warp_partition_point(b, e, [&](uint32_t i) { return f.keys[i] >= k0; });
-      fe = warp_partition_point(fo, e, [&](uint32_t i) { return f.keys[i] >= k1; });
+      fo = warp_partition_point(b, e, [&](uint32_t i) { return f.key(i) >= k0; });
+      fe = warp_partition_point(fo, e, [&](uint32_t i) { return f.key(i) >= k1; });
     };
     uint32_t fo, fe;
     range_of(o.last_op, fo, fe);
@@ -1520,7 +1528,9 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
                              csg_evidence* __restrict__ cev,
                              uint32_t* __restrict__ err) {
   constexpr int kWarps = 4;
+  constexpr int kStage = 256;  // members staged in shared memory
   __shared__ uint32_t tbl[kWarps][kChTbl / 8];  // slow-path successor table
+  __shared__ int32_t srank[kWarps][kStage];     // suspect ranks, else INT_MAX
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= n_items) return;
@@ -1532,15 +1542,32 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
   const int32_t mm = static_cast<int32_t>(m.member_off[it.g + 1] - mo);
   const uint32_t base = off[w];
   const int EV = kEvSlots(nch);
+  const bool staged = mm <= kStage;
+  if (staged) {
+    for (int32_t i = lane; i < mm; i += 32) {
+      const int32_t r = m.members[mo + i];
+      srank[wib][i] = is_suspect(pk, rsj, r, s.R) ? r : INT_MAX;
+    }
+    __syncwarp();
+  }
+  // rank-sorted slot of a suspect among the group's suspects
+  auto slot_of = [&](int32_t r) {
+    uint32_t pos = 0;
+    if (staged) {
+      for (int32_t k = 0; k < mm; ++k) pos += srank[wib][k] < r;
+    } else {
+      for (int32_t k = 0; k < mm; ++k) {
+        const int32_t rk = m.members[mo + k];
+        pos += (rk < r && is_suspect(pk, rsj, rk, s.R));
+      }
+    }
+    return pos;
+  };
   // Pass 1 (lane-parallel): one candidate per suspect at its rank-sorted slot.
   for (int32_t i = lane; i < mm; i += 32) {
     const int32_t r = m.members[mo + i];
-    if (!is_suspect(pk, rsj, r, s.R)) continue;
-    uint32_t pos = 0;
-    for (int32_t k = 0; k < mm; ++k) {
-      const int32_t rk = m.members[mo + k];
-      pos += (rk < r && is_suspect(pk, rsj, rk, s.R));
-    }
+    if (staged ? srank[wib][i] == INT_MAX : !is_suspect(pk, rsj, r, s.R)) continue;
+    const uint32_t pos = slot_of(r);
     const RankSum own = rsj[r];
     Cand c;
     memset(&c, 0, sizeof(c));
@@ -1619,13 +1646,8 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
     uint32_t ci = 0;
     if (i < mm) {
       const int32_t r = m.members[mo + i];
-      if (is_suspect(pk, rsj, r, s.R)) {
-        uint32_t pos = 0;
-        for (int32_t k = 0; k < mm; ++k) {
-          const int32_t rk = m.members[mo + k];
-          pos += (rk < r && is_suspect(pk, rsj, rk, s.R));
-        }
-        ci = base + pos;
+      if (staged ? srank[wib][i] != INT_MAX : is_suspect(pk, rsj, r, s.R)) {
+        ci = base + slot_of(r);
         need = cand[ci].pad != 0;
       }
     }

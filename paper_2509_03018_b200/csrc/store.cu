@@ -33,24 +33,40 @@ __global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n
   int mnr = INT_MAX, mxr = INT_MIN, mnc = INT_MAX, mxc = INT_MIN;
   long long mno = LLONG_MAX, mxo = LLONG_MIN;
   unsigned long long nan = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + i);
-    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1);
-    double t;
-    memcpy(&t, &h0.x, 8);
-    const long long op = static_cast<long long>(h0.y);
-    const int rank = static_cast<int>(hm.x & 0xffffffffu);
-    const int chan = static_cast<int>(hm.y & 0xffffffffu);
-    if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
-    mnr = min(mnr, rank);
-    mxr = max(mxr, rank);
-    mnc = min(mnc, chan);
-    mxc = max(mxc, chan);
-    mno = min(mno, op);
-    mxo = max(mxo, op);
-    keys[i] = static_cast<uint32_t>(rank);
-    vals[i] = static_cast<uint32_t>(i);
+  // 4 records in flight per thread (independent 16-byte loads) to keep
+  // enough bytes outstanding for HBM.
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < n;
+       i0 += 4 * stride) {
+    ulonglong2 h0[4], hm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = i0 + k * stride;
+      if (i < n) {
+        const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + i);
+        h0[k] = __ldg(rec);
+        hm[k] = __ldg(rec + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = i0 + k * stride;
+      if (i >= n) break;
+      double t;
+      memcpy(&t, &h0[k].x, 8);
+      const long long op = static_cast<long long>(h0[k].y);
+      const int rank = static_cast<int>(hm[k].x & 0xffffffffu);
+      const int chan = static_cast<int>(hm[k].y & 0xffffffffu);
+      if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
+      mnr = min(mnr, rank);
+      mxr = max(mxr, rank);
+      mnc = min(mnc, chan);
+      mxc = max(mxc, chan);
+      mno = min(mno, op);
+      mxo = max(mxo, op);
+      keys[i] = static_cast<uint32_t>(rank);
+      vals[i] = static_cast<uint32_t>(i);
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -63,7 +79,34 @@ __global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n
     mxo = max(mxo, __shfl_xor_sync(0xffffffffu, mxo, o));
     nan += __shfl_xor_sync(0xffffffffu, nan, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  // block reduction, then one set of global atomics per block (hundreds of
+  // blocks, not tens of thousands of warps, contend on the 8 counters)
+  __shared__ unsigned long long s_tsk[32], s_nan[32];
+  __shared__ int s_mnr[32], s_mxr[32], s_mnc[32], s_mxc[32];
+  __shared__ long long s_mno[32], s_mxo[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_tsk[warp] = tsk;
+    s_nan[warp] = nan;
+    s_mnr[warp] = mnr;
+    s_mxr[warp] = mxr;
+    s_mnc[warp] = mnc;
+    s_mxc[warp] = mxc;
+    s_mno[warp] = mno;
+    s_mxo[warp] = mxo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      tsk = max(tsk, s_tsk[w]);
+      nan += s_nan[w];
+      mnr = min(mnr, s_mnr[w]);
+      mxr = max(mxr, s_mxr[w]);
+      mnc = min(mnc, s_mnc[w]);
+      mxc = max(mxc, s_mxc[w]);
+      mno = min(mno, s_mno[w]);
+      mxo = max(mxo, s_mxo[w]);
+    }
     atomic_max_u64(&st->ts_max_key, tsk);
     atomicMin(&st->min_rank, mnr);
     atomicMax(&st->max_rank, mxr);
@@ -117,27 +160,38 @@ __global__ void k_gather(const csg_packed_record* __restrict__ r,
   }
 }
 
-// Per-rank inclusive running max of ts (one warp per rank, chunked scan).
+// Per-rank inclusive running max of ts: one warp per rank, 8 chunks of 32
+// records loaded per step (independent loads in flight), scanned in
+// registers with the carry chained through the chunks.
 __global__ void k_runmax(const double* __restrict__ ts,
                          const uint32_t* __restrict__ off, int32_t R,
                          double* __restrict__ out) {
+  constexpr int kChunks = 8;
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= R) return;
   const uint32_t b = off[w], e = off[w + 1];
   double carry = -INFINITY;
-  for (uint32_t base = b; base < e; base += 32) {
-    const uint32_t p = base + lane;
-    double x = p < e ? ts[p] : -INFINITY;
-    if (x != x) x = -INFINITY;  // NaN never breaks a prefix
+  for (uint32_t base = b; base < e; base += 32 * kChunks) {
+    double x[kChunks];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x = fmax(x, y);
+    for (int k = 0; k < kChunks; ++k) {
+      const uint32_t p = base + k * 32 + lane;
+      x[k] = p < e ? __ldg(ts + p) : -INFINITY;
+      if (x[k] != x[k]) x[k] = -INFINITY;  // NaN never breaks a prefix
     }
-    x = fmax(x, carry);
-    if (p < e) out[p] = x;
-    carry = __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x[k], o);
+        if (lane >= o) x[k] = fmax(x[k], y);
+      }
+      x[k] = fmax(x[k], carry);
+      carry = __shfl_sync(0xffffffffu, x[k], 31);
+      const uint32_t p = base + k * 32 + lane;
+      if (p < e) out[p] = x[k];
+    }
   }
 }
 
@@ -155,14 +209,16 @@ __global__ void k_opidx_rank(StoreView s, const uint32_t* __restrict__ pos,
   }
 }
 
+template <typename K>
 __global__ void k_flow_keys(StoreView s, int64_t min_op, int op_shift,
-                            int rank_shift, unsigned long long* __restrict__ keys,
+                            int rank_shift, K* __restrict__ keys,
                             uint32_t* __restrict__ vals) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
        p += (uint64_t)gridDim.x * blockDim.x) {
-    keys[p] = (static_cast<unsigned long long>(s.rank_of[p]) << rank_shift) |
-              (static_cast<unsigned long long>(s.op[p] - min_op) << op_shift) |
-              static_cast<unsigned long long>(s.chan[p]);
+    keys[p] = static_cast<K>(
+        (static_cast<unsigned long long>(s.rank_of[p]) << rank_shift) |
+        (static_cast<unsigned long long>(s.op[p] - min_op) << op_shift) |
+        static_cast<unsigned long long>(s.chan[p]));
     vals[p] = static_cast<uint32_t>(p);
   }
 }
@@ -317,7 +373,8 @@ void store_build_index(csg_store* s) {
   s->keys.ensure(n * 4 + 4);
   if (n) {
     ProfScope ps_(c->lc, "k_stats_keys", st);
-    k_stats_keys<<<grid_for(n), 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
+    const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, 148ull * 8));
+    k_stats_keys<<<g, 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
                                               s->keys.as<uint32_t>(),
                                               s->perm.as<uint32_t>());
   }
@@ -465,10 +522,19 @@ bool store_build_flow_index(csg_store* s) {
   s->flow_key_bits = cb + ob + rb;
   s->fl_keys.ensure(n * 8 + 8);
   s->fl_pos.ensure(n * 4 + 4);
-  if (n) {
+  if (n && s->flow_key_bits <= 32) {
     {
       ProfScope ps_(c->lc, "k_flow_keys", st);
-      k_flow_keys<<<grid_for(n), 256, 0, st>>>(
+      k_flow_keys<uint32_t><<<grid_for(n), 256, 0, st>>>(
+          s->view(), s->min_op, s->flow_op_shift, s->flow_rank_shift,
+          s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>());
+    }
+    radix_sort_u32(s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>(), n,
+                   s->flow_key_bits, s->sort, st, c->lc);
+  } else if (n) {
+    {
+      ProfScope ps_(c->lc, "k_flow_keys", st);
+      k_flow_keys<unsigned long long><<<grid_for(n), 256, 0, st>>>(
           s->view(), s->min_op, s->flow_op_shift, s->flow_rank_shift,
           s->fl_keys.as<unsigned long long>(), s->fl_pos.as<uint32_t>());
     }

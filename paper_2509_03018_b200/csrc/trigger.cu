@@ -71,6 +71,71 @@ __global__ void k_window_stats(StoreView s, const double* __restrict__ ticks,
   }
 }
 
+// The same window statistics with one pass over each sampled rank's
+// records: a block per sampled rank bins every record into the (few) tick
+// windows that contain it, accumulating in shared memory. Window k holds x
+// iff !(x < t_k - delta) && !(x > t_k) (trace.cpp:107 with t0 = t_k - delta).
+__global__ void k_window_bins(StoreView s, const double* __restrict__ ticks,
+                              int32_t T, const int32_t* __restrict__ sampled,
+                              int32_t S, double delta,
+                              WinStat* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char wb_dyn[];
+  double* st = reinterpret_cast<double*>(wb_dyn);                       // [T]
+  unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
+  unsigned long long* mn = bytes + T;
+  unsigned long long* mx = mn + T;
+  uint32_t* nrec = reinterpret_cast<uint32_t*>(mx + T);
+  uint32_t* ncomp = nrec + T;
+  uint32_t* hstate = ncomp + T;
+  const int32_t si = blockIdx.x;
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    st[k] = ticks[k];
+    bytes[k] = 0;
+    mn[k] = ~0ull;
+    mx[k] = 0;
+    nrec[k] = ncomp[k] = hstate[k] = 0;
+  }
+  __syncthreads();
+  const int32_t r = sampled[si];
+  if (r >= 0 && r < s.R) {
+    const uint32_t e = s.rank_off[r + 1];
+    for (uint32_t p = s.rank_off[r] + threadIdx.x; p < e; p += blockDim.x) {
+      const double x = s.ts[p];
+      int32_t lo = 0, hi = T;  // first tick with t_k >= x
+      while (lo < hi) {
+        const int32_t md = (lo + hi) >> 1;
+        if (st[md] < x) lo = md + 1; else hi = md;
+      }
+      const bool comp = ko_kind(s.ko[p]) == CSG_KIND_COMPLETION;
+      for (int32_t k = lo; k < T && !(x < st[k] - delta); ++k) {
+        if (x > st[k]) continue;
+        atomicAdd(&nrec[k], 1u);
+        if (comp) {
+          atomicAdd(&ncomp[k], 1u);
+          atomicAdd(&bytes[k], static_cast<unsigned long long>(s.pb[p]));
+          const unsigned long long kk = dkey(x);
+          atomicMin(&mn[k], kk);
+          atomicMax(&mx[k], kk);
+        } else {
+          hstate[k] = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    WinStat w;
+    w.n_rec = nrec[k];
+    w.n_comp = ncomp[k];
+    w.has_state = hstate[k];
+    w.pad = 0;
+    w.bytes = bytes[k];
+    w.min_end = ncomp[k] ? dkey_inv(mn[k]) : INFINITY;
+    w.max_end = ncomp[k] ? dkey_inv(mx[k]) : -INFINITY;
+    out[static_cast<int64_t>(k) * S + si] = w;
+  }
+}
+
 // One baseline step (trigger.cpp:76-133). Returns 0 none, 1 failure,
 // 2 straggler.
 __device__ int ema_step(TrigSlot& b, const WinStat& w, const TrigParams& p) {
@@ -231,6 +296,17 @@ void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
                           WinStat* d_out) {
   if (T <= 0 || S <= 0) return;
   csg_ctx* c = s->ctx;
+  const size_t smem = static_cast<size_t>(T) * 44;
+  if (smem <= 200 * 1024) {
+    CSG_CUDA(cudaFuncSetAttribute(k_window_bins,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(200 * 1024)));
+    ProfScope ps_(c->lc, "k_window_bins", c->stream);
+    k_window_bins<<<S, 512, smem, c->stream>>>(s->view(), d_ticks, T, d_sampled, S,
+                                               delta, d_out);
+    CSG_CUDA(cudaGetLastError());
+    return;
+  }
   const uint64_t warps = static_cast<uint64_t>(T) * S;
   {
     ProfScope ps_(c->lc, "k_window_stats", c->stream);
