@@ -67,6 +67,12 @@ collsight_status collsight_b200_engine_context(csg_ctx** out);
 collsight_status collsight_b200_synthesize(const collsight_scenario* scenario,
                                            uint64_t target_records,
                                            csg_packed_record** out, size_t* n);
+/* Same trace restricted to ranks in [rank_lo, rank_hi): one shard's records
+ * in emission order (rank-range sharding, csg_ctx_comm_init). */
+collsight_status collsight_b200_synthesize_ranks(const collsight_scenario* scenario,
+                                                 uint64_t target_records,
+                                                 int32_t rank_lo, int32_t rank_hi,
+                                                 csg_packed_record** out, size_t* n);
 
 #ifdef __cplusplus
 } /* extern "C" */

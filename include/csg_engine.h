@@ -228,6 +228,18 @@ csg_status csg_ctx_kernel_stats(csg_ctx* ctx, char* json, size_t cap,
  * (the benchmark re-times ingest + index every step). */
 csg_status csg_store_invalidate(csg_store* store);
 
+/* Sharded mode: one context per GPU, each store holding
+ * the records of a rank range (store order preserved inside a rank). After
+ * csg_ctx_comm_init every analysis call on the context combines the shards
+ * with NCCL collectives on the context stream and returns the same results
+ * on every rank. csg_comm_unique_id is called on one rank and its 128 bytes
+ * broadcast to the others (the Python driver uses torch.distributed). */
+csg_status csg_comm_unique_id(unsigned char* out, size_t cap);
+csg_status csg_ctx_comm_init(csg_ctx* ctx, const unsigned char* id, size_t len,
+                             int nranks, int rank);
+csg_status csg_ctx_comm_info(csg_ctx* ctx, int* nranks, int* rank,
+                             uint64_t* collectives);
+
 /* TraceStore (proj/include/collsight/trace.hpp:101-124).
  * append copies `n` packed records from HOST memory (pinned or pageable)
  * into HBM, in emission order; append_device takes records already in HBM on

@@ -41,6 +41,14 @@ def json_include() -> str:
     raise RuntimeError("nlohmann/json.hpp not found (needed by the host layer)")
 
 
+def nccl_include() -> str:
+    for c in glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages",
+                                    "nvidia", "nccl", "include")) + ["/usr/include"]:
+        if os.path.exists(os.path.join(c, "nccl.h")):
+            return c
+    raise RuntimeError("nccl.h not found")
+
+
 def _headers():
     return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
             + glob.glob(os.path.join(CSRC, "host", "*.h"))
@@ -74,6 +82,7 @@ def build(verbose: bool = False) -> str:
         if _stale(src, obj, hdr):
             jobs.append([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-fmad=false",
                          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC,
+                         "-I", nccl_include(),
                          "-c", src, "-o", obj])
     for src in sorted(glob.glob(os.path.join(CSRC, "host", "*.cpp"))):
         obj = os.path.join(OBJ, "host_" + os.path.basename(src) + ".o")

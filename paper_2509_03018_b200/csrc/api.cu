@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "objects.h"
 #include "rca.cuh"
 #include "rca_table.h"
@@ -219,6 +220,7 @@ void csg_ctx_free(csg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  csg_comm_release(c);
   c->scratch_a.release();
   c->scratch_b.release();
   c->scratch_c.release();

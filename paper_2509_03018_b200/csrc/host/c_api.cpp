@@ -275,9 +275,16 @@ collsight_status collsight_b200_engine_context(csg_ctx** out) {
 collsight_status collsight_b200_synthesize(const collsight_scenario* s,
                                            uint64_t target,
                                            csg_packed_record** out, size_t* n) {
+  return collsight_b200_synthesize_ranks(s, target, 0, 0x7fffffff, out, n);
+}
+
+collsight_status collsight_b200_synthesize_ranks(const collsight_scenario* s,
+                                                 uint64_t target, int32_t rank_lo,
+                                                 int32_t rank_hi,
+                                                 csg_packed_record** out, size_t* n) {
   if (!s || !out || !n) return fail(COLLSIGHT_ERR_ARG, "null argument");
   return guarded([&] {
-    const auto v = csh::synthesize(s->cfg, target);
+    const auto v = csh::synthesize(s->cfg, target, rank_lo, rank_hi);
     *n = v.size();
     *out = static_cast<csg_packed_record*>(
         std::malloc(sizeof(csg_packed_record) * (v.size() + 1)));

@@ -86,7 +86,11 @@ Scenario parse_scenario(const std::string& json_text);
 Scenario load_scenario_file(const std::string& path);
 
 // Synthetic benchmark traces (synth.cpp). target = 0: no record cap.
-std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target);
+// Only records of ranks in [rank_lo, rank_hi) are emitted (a shard's view;
+// the schedule is still simulated for every rank).
+std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target,
+                                          int32_t rank_lo = 0,
+                                          int32_t rank_hi = 0x7fffffff);
 
 // Trace codec.
 std::vector<csg_packed_record> parse_trace_text(std::string_view text);

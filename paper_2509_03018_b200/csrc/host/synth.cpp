@@ -51,7 +51,8 @@ struct Rec {
 
 }  // namespace
 
-std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target) {
+std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
+                                          int32_t rank_lo, int32_t rank_hi) {
   const Layout l = sc.layout();
   const Program p = sc.program(l);
   const int opn = static_cast<int>(p.ops.size());
@@ -128,6 +129,7 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target) {
   out.reserve(target ? target + target / 8 : 1 << 20);
   uint64_t seq = 0;
   auto emit = [&](double key, const csg_packed_record& r) {
+    if (r.rank < rank_lo || r.rank >= rank_hi) return;  // another shard's rank
     if (std::isfinite(stop_logs_at) && key > stop_logs_at &&
         r.rank / l.ranks_per_node == hang_node)
       return;

@@ -15,6 +15,10 @@ struct csg_ctx {
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   double device_ms = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  // sharded mode (csg_ctx_comm_init): NCCL communicator over nranks GPUs
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  uint64_t collectives = 0;
   csg::LaunchCounter lc;
   // shared scratch
   csg::DevBuf scratch_a, scratch_b, scratch_c, pinned_flag_dev;
@@ -48,12 +52,14 @@ struct StoreStats {
   int min_chan, max_chan;
   long long min_op, max_op;
   unsigned long long n_nan;
+  unsigned long long n_total;  // records over all shards
 };
 
 struct csg_store {
   csg_ctx* ctx = nullptr;
   csg::DevBuf recs;  // packed AoS in store (emission) order
   uint64_t n = 0;
+  uint64_t n_global = 0;  // records over all shards (== n unsharded)
   bool indexed = false;
   // stats (valid when indexed)
   double last_ts = 0;  // max(0, max timestamp), runner.cpp:51-56
@@ -72,6 +78,9 @@ struct csg_store {
                              // ordered by (op_seq, store index)
   csg::DevBuf opidx_keys;    // u64 op - min_op (sorted)
   csg::DevBuf opidx_rank;    // rank of each entry
+  csg::DevBuf opidx_ts;      // end_ms (timestamp) of each entry
+  csg::DevBuf opidx_dur;     // end_ms - start_ms
+  csg::DevBuf opidx_nm;      // record op_name
   csg::DevBuf op_seg_off;    // dense [min_op, max_op+1] -> start in opidx
   // flow index: rank-major positions ordered by (rank, op_seq, channel,
   // store order); keys packed rank | op - min_op | channel

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "comm.cuh"
 #include "rca.cuh"
 #include "rca_table.h"
 
@@ -97,7 +98,8 @@ __device__ double warp_lower_median(int n, V val) {
 __global__ void k_rank_summary(StoreView s, int32_t J,
                                const double* __restrict__ trip_t,
                                double delta_a, RankSum* __restrict__ out,
-                               uint32_t* __restrict__ chan_pos, int32_t nch) {
+                               unsigned long long* __restrict__ chan_key,
+                               int32_t nch) {
   extern __shared__ uint32_t sm_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -116,12 +118,14 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
   const uint32_t cend =
       warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
   const uint32_t c = cend - b;
+  // A rank without prefix records leaves an all-zero summary, so summaries
+  // of ranks owned by other shards combine by summation (see comm.cu).
   RankSum o;
   o.cutoff = c;
   o.flags = 0;
-  o.last_op = -1;
+  o.last_op = 0;
   o.last_ts = 0;
-  o.last_chan = -1;
+  o.last_chan = 0;
   o.pad = 0;
   o.onset = 0;
   o.ready = o.tx = o.done = 0;
@@ -198,8 +202,11 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
       o.done = dn;
     }
   }
-  uint32_t* cp = chan_pos + (static_cast<uint64_t>(j) * s.R + r) * nch;
-  for (int ch = lane; ch < nch; ch += 32) cp[ch] = tbl[ch];
+  // per-channel evidence: the latest state's timestamp as an ordered key
+  // (0 = no state on that channel); the op is the rank's last op.
+  unsigned long long* ck = chan_key + (static_cast<uint64_t>(j) * s.R + r) * nch;
+  for (int ch = lane; ch < nch; ch += 32)
+    ck[ch] = tbl[ch] ? static_cast<unsigned long long>(dkey(s.ts[tbl[ch] - 1])) : 0ull;
   if (lane == 0) out[static_cast<uint64_t>(j) * s.R + r] = o;
 }
 
@@ -211,7 +218,8 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
 __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
                                   const double* __restrict__ trip_t,
                                   double delta_a, RankSum* __restrict__ out,
-                                  uint32_t* __restrict__ chan_pos, int32_t nch) {
+                                  unsigned long long* __restrict__ chan_key,
+                                  int32_t nch) {
   extern __shared__ uint32_t sm_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -229,12 +237,14 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
   const uint32_t cend =
       warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
   const uint32_t c = cend - b;
+  // A rank without prefix records leaves an all-zero summary, so summaries
+  // of ranks owned by other shards combine by summation (see comm.cu).
   RankSum o;
   o.cutoff = c;
   o.flags = 0;
-  o.last_op = -1;
+  o.last_op = 0;
   o.last_ts = 0;
-  o.last_chan = -1;
+  o.last_chan = 0;
   o.pad = 0;
   o.onset = 0;
   o.ready = o.tx = o.done = 0;
@@ -318,9 +328,110 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
       o.done = dn;
     }
   }
-  uint32_t* cp = chan_pos + (static_cast<uint64_t>(j) * s.R + r) * nch;
-  for (int ch = lane; ch < nch; ch += 32) cp[ch] = tbl[ch];
+  // per-channel evidence: the latest state's timestamp as an ordered key
+  // (0 = no state on that channel); the op is the rank's last op.
+  unsigned long long* ck = chan_key + (static_cast<uint64_t>(j) * s.R + r) * nch;
+  for (int ch = lane; ch < nch; ch += 32)
+    ck[ch] = tbl[ch] ? static_cast<unsigned long long>(dkey(s.ts[tbl[ch] - 1])) : 0ull;
   if (lane == 0) out[static_cast<uint64_t>(j) * s.R + r] = o;
+}
+
+// ---------------------------------------------------------------------------
+// K1b: ring-successor progress (rca.cpp:596-605). For every membership slot
+// (trip, group, member s) whose ring predecessor p has a prefix: progress_of
+// (s, last_op(p), t) with per-channel evidence. A suspect at ring position i
+// reads the slot of position i+1. Computed by the shard owning s.
+// ---------------------------------------------------------------------------
+struct SuccProg {
+  uint32_t known;
+  uint32_t pad;
+  unsigned long long ready, tx, done;
+};
+
+__global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
+                            uint32_t M, const uint32_t* __restrict__ slot_group,
+                            const RankSum* __restrict__ rs,
+                            SuccProg* __restrict__ out,
+                            unsigned long long* __restrict__ sp_key,
+                            int32_t nch) {
+  extern __shared__ uint32_t sp_tbl[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(M) * J) return;
+  const int32_t j = static_cast<int32_t>(w / M);
+  const uint32_t q = static_cast<uint32_t>(w % M);
+  uint32_t* tbl = sp_tbl + wib * nch;
+  for (int c = lane; c < nch; c += 32) tbl[c] = 0;
+  __syncwarp();
+  const int32_t g = static_cast<int32_t>(slot_group[q]);
+  const uint32_t mo = m.member_off[g];
+  const int32_t mm = static_cast<int32_t>(m.member_off[g + 1] - mo);
+  const int32_t i = static_cast<int32_t>(q - mo);
+  const int32_t sr = m.members[q];
+  SuccProg o{0, 0, 0, 0, 0};
+  const RankSum* rsj = rs + static_cast<uint64_t>(j) * s.R;
+  bool go = mm >= 2 && sr >= 0 && sr < s.R && s.rank_off[sr + 1] > s.rank_off[sr];
+  int32_t pred = -1;
+  if (go) {
+    pred = m.members[mo + (i + mm - 1) % mm];
+    go = pred >= 0 && pred < s.R && (rsj[pred].flags & RS_HAS_LAST);
+  }
+  if (go) {
+    const int64_t op = rsj[pred].last_op;
+    const uint32_t b = s.rank_off[sr];
+    const uint32_t cend = b + rsj[sr].cutoff;
+    if (f.n) {
+      const unsigned long long k0 =
+          (static_cast<unsigned long long>(sr) << f.rank_shift) |
+          (static_cast<unsigned long long>(op - f.min_op) << f.op_shift);
+      const unsigned long long k1 = k0 + (1ull << f.op_shift);
+      const uint32_t e = s.rank_off[sr + 1];
+      if (op >= f.min_op && op - f.min_op < (1ll << (f.rank_shift - f.op_shift))) {
+        const uint32_t fo =
+            warp_partition_point(b, e, [&](uint32_t x) { return f.key(x) >= k0; });
+        const uint32_t fe =
+            warp_partition_point(fo, e, [&](uint32_t x) { return f.key(x) >= k1; });
+        for (uint32_t x = fo + lane; x < fe; x += 32) {
+          const uint32_t p = f.pos[x];
+          if (p < cend && ko_kind(s.ko[p]) == CSG_KIND_STATE)
+            atomicMax(&tbl[s.chan[p]], p + 1);
+        }
+      }
+    } else {  // no flow index: scan the prefix
+      for (uint32_t p = b + lane; p < cend; p += 32)
+        if (s.op[p] == op && ko_kind(s.ko[p]) == CSG_KIND_STATE)
+          atomicMax(&tbl[s.chan[p]], p + 1);
+    }
+    __syncwarp();
+    unsigned long long rd = 0, tx = 0, dn = 0;
+    int any = 0;
+    for (int ch = lane; ch < nch; ch += 32) {
+      const uint32_t qq = tbl[ch];
+      if (qq) {
+        any = 1;
+        const uint64_t a = s.pa[qq - 1];
+        rd += a & 0xffffffffull;
+        tx += a >> 32;
+        dn += s.pb[qq - 1];
+      }
+    }
+#pragma unroll
+    for (int x = 16; x; x >>= 1) {
+      rd += __shfl_xor_sync(FULL, rd, x);
+      tx += __shfl_xor_sync(FULL, tx, x);
+      dn += __shfl_xor_sync(FULL, dn, x);
+      any |= __shfl_xor_sync(FULL, any, x);
+    }
+    o.known = any ? 1 : 0;
+    o.ready = rd;
+    o.tx = tx;
+    o.done = dn;
+  }
+  unsigned long long* ck = sp_key + (static_cast<uint64_t>(j) * M + q) * nch;
+  for (int ch = lane; ch < nch; ch += 32)
+    ck[ch] = tbl[ch] ? static_cast<unsigned long long>(dkey(s.ts[tbl[ch] - 1])) : 0ull;
+  if (lane == 0) out[static_cast<uint64_t>(j) * M + q] = o;
 }
 
 // ---------------------------------------------------------------------------
@@ -695,7 +806,7 @@ struct DecideArgs {
   const int32_t* trip_rank;
   const int32_t* js_of;
   const RankSum* rs;
-  const uint32_t* chan_pos;
+  const unsigned long long* chan_key;
   int32_t nch;
   const int32_t* aff;
   const int32_t* n_aff;
@@ -711,9 +822,12 @@ struct DecideArgs {
   double delta_a, thr, skew;
   uint64_t N;
   const uint64_t* opk;
-  const uint32_t* opp;
   const int32_t* oprank;
+  const double* op_ts;
+  const double* op_dur;
+  const uint8_t* op_nm;
   uint64_t n_opidx;
+  int sharded;
   int64_t min_op;
   uint32_t scratch_per_trip;  // u32 words
   Pools pools;
@@ -1042,38 +1156,95 @@ __device__ void emit_reports(const DecideArgs& a, BlockShared& sh,
 
 // ---- straggler -------------------------------------------------------------
 
-// self_faulted (rca.cpp:821-848) for one lateness candidate.
+// op-index segment [lo_key, hi_key] (keys = op - min_op), block-uniform
+__device__ void op_segment(const DecideArgs& a, uint64_t k0, uint64_t k1,
+                           bool empty, BlockShared& sh, uint64_t& sb,
+                           uint64_t& se) {
+  if (threadIdx.x == 0) {
+    uint64_t l = 0, h = a.n_opidx;
+    while (l < h) {
+      const uint64_t md = (l + h) >> 1;
+      if (a.opk[md] < k0) l = md + 1; else h = md;
+    }
+    sh.u64a = l;
+    h = a.n_opidx;
+    while (l < h) {
+      const uint64_t md = (l + h) >> 1;
+      if (a.opk[md] <= k1) l = md + 1; else h = md;
+    }
+    sh.u64b = empty ? sh.u64a : l;
+  }
+  __syncthreads();
+  sb = sh.u64a;
+  se = sh.u64b;
+  __syncthreads();
+}
+
+// op range holding exactly the ops with static_cast<long>(op / opn) == it
+// (C++ division truncates toward zero, so iteration 0 also holds (-opn, 0))
+__device__ inline void iter_ops(int64_t it, int32_t opn, int64_t& lo, int64_t& hi) {
+  lo = it > 0 ? it * opn : it * opn - (opn - 1);
+  hi = it >= 0 ? it * opn + (opn - 1) : it * opn;
+}
+
+// self_faulted (rca.cpp:821-848) for one lateness candidate. "mine" are the
+// candidate rank's completions (ts <= t, not Recv) in its iteration window:
+// from its rank-major segment on a single GPU, from the (gathered) op index
+// when the store is sharded; sibling and cohort medians always come from the
+// op index, which then holds every shard's entries.
 __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
                              BlockShared& sh, uint32_t* lst) {
   const double t = a.trip_t[j];
   const int32_t r = c.rank;
   const int32_t opn = a.m.opn;
-  if (r < 0 || r >= a.s.R) return false;
-  const uint32_t b = a.s.rank_off[r], e = a.s.rank_off[r + 1];
-  // the rank's qualifying completions (FILTER ts <= t, not Recv, iteration
-  // within [iter_lo, iter_hi])
-  const int n = block_compact(static_cast<int>(e - b), [&](int i) {
-    const uint32_t p = b + i;
-    const uint8_t ko = a.s.ko[p];
-    if (ko_kind(ko) != CSG_KIND_COMPLETION || ko_opname(ko) == CSG_OP_RECV)
-      return false;
-    if (a.s.ts[p] > t) return false;
-    const int64_t it = iter_of(a.s.op[p], opn);
-    return it >= c.it_lo && it <= c.it_hi;
-  }, lst, sh);
+  int n = 0;
+  uint64_t mb = 0;  // op-index base of the "mine" scan (sharded form)
+  if (!a.sharded) {
+    if (r < 0 || r >= a.s.R) return false;
+    const uint32_t b = a.s.rank_off[r], e = a.s.rank_off[r + 1];
+    mb = b;
+    n = block_compact(static_cast<int>(e - b), [&](int i) {
+      const uint32_t p = b + i;
+      const uint8_t ko = a.s.ko[p];
+      if (ko_kind(ko) != CSG_KIND_COMPLETION || ko_opname(ko) == CSG_OP_RECV)
+        return false;
+      if (a.s.ts[p] > t) return false;
+      const int64_t it = iter_of(a.s.op[p], opn);
+      return it >= c.it_lo && it <= c.it_hi;
+    }, lst, sh);
+  } else {
+    int64_t olo, ohi, x0, x1;
+    iter_ops(c.it_lo, opn, olo, x1);
+    iter_ops(c.it_hi, opn, x0, ohi);
+    const bool empty = ohi < a.min_op;
+    const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
+    const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
+    uint64_t sb, se;
+    op_segment(a, k0, k1, empty, sh, sb, se);
+    mb = sb;
+    n = block_compact(static_cast<int>(se - sb), [&](int i) {
+      const uint64_t y = sb + i;
+      return a.oprank[y] == r && a.op_ts[y] <= t;
+    }, lst, sh);
+  }
+  auto mine_op = [&](int x) -> int64_t {
+    return a.sharded ? static_cast<int64_t>(a.opk[mb + lst[x]]) + a.min_op
+                     : a.s.op[mb + lst[x]];
+  };
+  auto mine_dur = [&](int x) -> double {
+    if (a.sharded) return a.op_dur[mb + lst[x]];
+    const uint32_t p = static_cast<uint32_t>(mb) + lst[x];
+    return a.s.ts[p] - as_double(a.s.pa[p]);
+  };
   for (int x = 0; x < n; ++x) {
-    const int64_t o = a.s.op[b + lst[x]];
+    const int64_t o = mine_op(x);
     bool dup = false;
-    for (int y = threadIdx.x; y < x; y += blockDim.x)
-      dup |= a.s.op[b + lst[y]] == o;
+    for (int y = threadIdx.x; y < x; y += blockDim.x) dup |= mine_op(y) == o;
     if (__syncthreads_or(dup)) continue;
     // max of my durations for op o
     double mine = -INFINITY;
-    for (int y = x + threadIdx.x; y < n; y += blockDim.x) {
-      const uint32_t p = b + lst[y];
-      if (a.s.op[p] == o) mine = fmax(mine, a.s.ts[p] - as_double(a.s.pa[p]));
-    }
-    // block max via ordered keys
+    for (int y = x + threadIdx.x; y < n; y += blockDim.x)
+      if (mine_op(y) == o) mine = fmax(mine, mine_dur(y));
     {
       unsigned long long kk = mine == -INFINITY ? 0ull : dkey(mine);
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1087,39 +1258,23 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
       __syncthreads();
       mine = dkey_inv(kk);
     }
-    // op segment [sb, se) in the op index
-    if (threadIdx.x == 0) {
+    // siblings: other ranks' durations of op o (ts <= t)
+    uint64_t sb, se;
+    {
       const uint64_t key = static_cast<uint64_t>(o - a.min_op);
-      uint64_t l = 0, h = a.n_opidx;
-      while (l < h) {
-        const uint64_t md = (l + h) >> 1;
-        if (a.opk[md] < key) l = md + 1; else h = md;
-      }
-      sh.u64a = l;
-      h = a.n_opidx;
-      while (l < h) {
-        const uint64_t md = (l + h) >> 1;
-        if (a.opk[md] <= key) l = md + 1; else h = md;
-      }
-      sh.u64b = l;
+      op_segment(a, key, key, false, sh, sb, se);
     }
-    __syncthreads();
-    const uint64_t sb = sh.u64a, se = sh.u64b;
-    __syncthreads();
     int nsib = 0;
-    for (uint64_t y = sb + threadIdx.x; y < se; y += blockDim.x) {
-      const uint32_t p = a.opp[y];
-      nsib += (a.oprank[y] != r && a.s.ts[p] <= t);
-    }
+    for (uint64_t y = sb + threadIdx.x; y < se; y += blockDim.x)
+      nsib += (a.oprank[y] != r && a.op_ts[y] <= t);
     nsib = block_sum_i(nsib, sh);
     double med;
     if (nsib > 0) {
       med = block_select(se - sb, static_cast<uint64_t>((nsib - 1) / 2),
                          [&](uint64_t i, uint64_t* key) {
                            const uint64_t y = sb + i;
-                           const uint32_t p = a.opp[y];
-                           if (a.oprank[y] == r || a.s.ts[p] > t) return false;
-                           *key = dkey(a.s.ts[p] - as_double(a.s.pa[p]));
+                           if (a.oprank[y] == r || a.op_ts[y] > t) return false;
+                           *key = dkey(a.op_dur[y]);
                            return true;
                          },
                          sh);
@@ -1127,43 +1282,23 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
       // cohort of (program op name, iteration) (rca.cpp:833-840)
       const int64_t it = iter_of(o, opn);
       const uint8_t nm = a.m.op_name[static_cast<uint64_t>(o % opn)];
-      // ops with iteration == it: [it*opn, it*opn + opn - 1] for it > 0;
-      // op/opn truncates toward zero, so iteration 0 also holds (-opn, 0).
-      const int64_t olo = it > 0 ? it * opn : it * opn - (opn - 1);
-      const int64_t ohi = it >= 0 ? it * opn + (opn - 1) : it * opn;
-      if (threadIdx.x == 0) {
-        const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
-        const bool empty = ohi < a.min_op;
-        const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
-        uint64_t l = 0, h = a.n_opidx;
-        while (l < h) {
-          const uint64_t md = (l + h) >> 1;
-          if (a.opk[md] < k0) l = md + 1; else h = md;
-        }
-        sh.u64a = l;
-        h = a.n_opidx;
-        while (l < h) {
-          const uint64_t md = (l + h) >> 1;
-          if (a.opk[md] <= k1) l = md + 1; else h = md;
-        }
-        sh.u64b = empty ? sh.u64a : l;
-      }
-      __syncthreads();
-      const uint64_t cb = sh.u64a, ce = sh.u64b;
-      __syncthreads();
+      int64_t olo, ohi;
+      iter_ops(it, opn, olo, ohi);
+      const bool empty = ohi < a.min_op;
+      const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
+      const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
+      uint64_t cb, ce;
+      op_segment(a, k0, k1, empty, sh, cb, ce);
       int nco = 0;
-      for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x) {
-        const uint32_t p = a.opp[y];
-        nco += (ko_opname(a.s.ko[p]) == nm && a.s.ts[p] <= t);
-      }
+      for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
+        nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
       nco = block_sum_i(nco, sh);
       if (nco < 2) continue;
       med = block_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
                          [&](uint64_t i, uint64_t* key) {
-                           const uint32_t p = a.opp[cb + i];
-                           if (ko_opname(a.s.ko[p]) != nm || a.s.ts[p] > t)
-                             return false;
-                           *key = dkey(a.s.ts[p] - as_double(a.s.pa[p]));
+                           const uint64_t y = cb + i;
+                           if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
+                           *key = dkey(a.op_dur[y]);
                            return true;
                          },
                          sh);
@@ -1521,7 +1656,10 @@ __device__ inline bool is_suspect(const GroupPick& pk, const RankSum* rsj,
 __global__ void k_fail_cands(StoreView s, ModelView m,
                              const FailItem* __restrict__ items, int32_t n_items,
                              const RankSum* __restrict__ rs,
-                             const uint32_t* __restrict__ chan_pos, int32_t nch,
+                             const unsigned long long* __restrict__ chan_key,
+                             const SuccProg* __restrict__ sp,
+                             const unsigned long long* __restrict__ sp_key,
+                             uint32_t M, int32_t nch,
                              const GroupPick* __restrict__ pick,
                              const uint32_t* __restrict__ off,
                              Cand* __restrict__ cand,
@@ -1529,7 +1667,6 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
                              uint32_t* __restrict__ err) {
   constexpr int kWarps = 4;
   constexpr int kStage = 256;  // members staged in shared memory
-  __shared__ uint32_t tbl[kWarps][kChTbl / 8];  // slow-path successor table
   __shared__ int32_t srank[kWarps][kStage];     // suspect ranks, else INT_MAX
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1563,11 +1700,10 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
     }
     return pos;
   };
-  // Pass 1 (lane-parallel): one candidate per suspect at its rank-sorted slot.
   for (int32_t i = lane; i < mm; i += 32) {
     const int32_t r = m.members[mo + i];
     if (staged ? srank[wib][i] == INT_MAX : !is_suspect(pk, rsj, r, s.R)) continue;
-    const uint32_t pos = slot_of(r);
+    const uint32_t ci = base + slot_of(r);
     const RankSum own = rsj[r];
     Cand c;
     memset(&c, 0, sizeof(c));
@@ -1581,128 +1717,45 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
     c.done = own.done;
     c.it_lo = 0;
     c.it_hi = -1;
-    const uint32_t ci = base + pos;
     c.ev_off = ci * EV;
     c.ev_n = 0;
     csg_evidence* ev = cev + static_cast<uint64_t>(ci) * EV;
-    const uint32_t* ct = chan_pos + (static_cast<uint64_t>(it.j) * s.R + r) * nch;
+    // own progress_of(r, op) evidence, ascending channel (rca.cpp:593-594)
+    const unsigned long long* ck = chan_key + (static_cast<uint64_t>(it.j) * s.R + r) * nch;
     if (c.known)
       for (int ch = 0; ch < nch; ++ch)
-        if (ct[ch]) {
-          const uint32_t q = ct[ch] - 1;
-          ev[c.ev_n++] = csg_evidence{r, ch, s.ts[q], s.op[q]};
-        }
-    // ring successor members[(pos+1) % n] on the suspect's op
-    // (rca.cpp:598-605); fast path when that is the successor's own last op.
-    bool slow = false;
+        if (ck[ch]) ev[c.ev_n++] = csg_evidence{r, ch, dkey_inv(ck[ch]), c.op};
+    // ring successor members[(i+1) % n] on the suspect's op (rca.cpp:596-605)
     bool peer_known = false;
     uint64_t prd = 0, ptx = 0, pdn = 0;
     if (mm >= 2) {
-      const int32_t succ = m.members[mo + (i + 1) % mm];
-      if (succ >= 0 && succ < s.R) {
-        const RankSum sr = rsj[succ];
-        if ((sr.flags & RS_HAS_LAST) && sr.last_op == c.op) {
-          peer_known = (sr.flags & RS_PROG) != 0;
-          prd = sr.ready;
-          ptx = sr.tx;
-          pdn = sr.done;
-          const uint32_t* st =
-              chan_pos + (static_cast<uint64_t>(it.j) * s.R + succ) * nch;
-          if (peer_known)
-            for (int ch = 0; ch < nch; ++ch)
-              if (st[ch]) {
-                const uint32_t q = st[ch] - 1;
-                ev[c.ev_n++] = csg_evidence{succ, ch, s.ts[q], s.op[q]};
-              }
-        } else if (sr.cutoff > 0) {
-          slow = true;  // resolved cooperatively below
-        }
+      const uint32_t sq = mo + (i + 1) % mm;
+      const int32_t succ = m.members[sq];
+      const SuccProg p = sp[static_cast<uint64_t>(it.j) * M + sq];
+      if (p.known) {
+        peer_known = true;
+        prd = p.ready;
+        ptx = p.tx;
+        pdn = p.done;
+        const unsigned long long* sk = sp_key + (static_cast<uint64_t>(it.j) * M + sq) * nch;
+        for (int ch = 0; ch < nch; ++ch)
+          if (sk[ch]) ev[c.ev_n++] = csg_evidence{succ, ch, dkey_inv(sk[ch]), c.op};
       }
     }
-    if (!slow) {
-      if (c.known) {
-        int cat, side;
-        if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat, &side))
-          atomicOr(err, DEV_ERR_RC_TABLE);
-        c.cat = static_cast<uint8_t>(cat);
-        c.side = static_cast<uint8_t>(side);
-      } else {
-        c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
-        c.side = CSG_SIDE_UNDETERMINED;
-      }
-      if (c.ev_n == 0)
-        ev[c.ev_n++] = csg_evidence{r, own.last_chan, own.last_ts, c.op};
+    if (c.known) {
+      int cat, side;
+      if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat, &side))
+        atomicOr(err, DEV_ERR_RC_TABLE);
+      c.cat = static_cast<uint8_t>(cat);
+      c.side = static_cast<uint8_t>(side);
+    } else {
+      c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
+      c.side = CSG_SIDE_UNDETERMINED;
     }
-    c.pad = slow ? 1 : 0;
+    // no evidence: cite the last log (rca.cpp:615-622)
+    if (c.ev_n == 0) ev[c.ev_n++] = csg_evidence{r, own.last_chan, own.last_ts, c.op};
     cand[ci] = c;
   }
-  __syncwarp();
-  // Pass 2 (warp-cooperative): successors whose last op differs from the
-  // suspect's need a prefix scan for progress_of(succ, op, t).
-  const int words = (nch + 7) / 8 * 8 <= kChTbl / 8 ? nch : kChTbl / 8;
-  for (int32_t i0 = 0; i0 < mm; i0 += 32) {
-    const int32_t i = i0 + lane;
-    bool need = false;
-    uint32_t ci = 0;
-    if (i < mm) {
-      const int32_t r = m.members[mo + i];
-      if (staged ? srank[wib][i] != INT_MAX : is_suspect(pk, rsj, r, s.R)) {
-        ci = base + slot_of(r);
-        need = cand[ci].pad != 0;
-      }
-    }
-    unsigned todo = __ballot_sync(FULL, need);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t cc = __shfl_sync(FULL, ci, src);
-      const int32_t mi = i0 + src;
-      Cand c = cand[cc];
-      const int32_t succ = m.members[mo + (mi + 1) % mm];
-      const uint32_t b = s.rank_off[succ];
-      const uint32_t e = b + rsj[succ].cutoff;
-      for (int ch = lane; ch < nch; ch += 32) tbl[wib][ch] = 0;
-      __syncwarp();
-      for (uint32_t p = b + lane; p < e; p += 32)
-        if (s.op[p] == c.op && ko_kind(s.ko[p]) == CSG_KIND_STATE)
-          atomicMax(&tbl[wib][s.chan[p]], p + 1);
-      __syncwarp();
-      if (lane == 0) {
-        bool peer_known = false;
-        uint64_t prd = 0, ptx = 0, pdn = 0;
-        csg_evidence* ev = cev + static_cast<uint64_t>(cc) * EV;
-        for (int ch = 0; ch < nch; ++ch) {
-          const uint32_t q = tbl[wib][ch];
-          if (!q) continue;
-          peer_known = true;
-          const uint64_t pa = s.pa[q - 1];
-          prd += pa & 0xffffffffull;
-          ptx += pa >> 32;
-          pdn += s.pb[q - 1];
-          ev[c.ev_n++] = csg_evidence{succ, ch, s.ts[q - 1], s.op[q - 1]};
-        }
-        if (c.known) {
-          int cat, side;
-          if (!rc_table(c.ready, c.tx, c.done, peer_known, prd, ptx, pdn, &cat,
-                        &side))
-            atomicOr(err, DEV_ERR_RC_TABLE);
-          c.cat = static_cast<uint8_t>(cat);
-          c.side = static_cast<uint8_t>(side);
-        } else {
-          c.cat = CSG_RC_UNINITIALIZED_OR_BLOCKED;
-          c.side = CSG_SIDE_UNDETERMINED;
-        }
-        if (c.ev_n == 0) {
-          const RankSum own = rsj[c.rank];
-          ev[c.ev_n++] = csg_evidence{c.rank, own.last_chan, own.last_ts, c.op};
-        }
-        c.pad = 0;
-        cand[cc] = c;
-      }
-      __syncwarp();
-    }
-  }
-  (void)words;
 }
 
 struct ExoTrip {
@@ -2174,9 +2227,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
 
   // K1: per (trip, rank) prefix summaries
   DevBuf& rs = c->buf("rca.rs");
-  DevBuf& chan_pos = c->buf("rca.chan_pos");
+  DevBuf& chan_key = c->buf("rca.chan_key");
   rs.ensure(static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum));
-  chan_pos.ensure(static_cast<size_t>(J) * std::max(R, 1) * nch * 4);
+  chan_key.ensure(static_cast<size_t>(J) * std::max(R, 1) * nch * 8);
   if (R > 0) {
     int wpb = 32768 / (nch * 4);
     wpb = std::max(1, std::min(8, wpb));
@@ -2187,14 +2240,53 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       k_rank_summary_fi<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
                           wpb * nch * 4, st>>>(sv, s->flow_view(), J, dt, cfg.delta_ms,
                                                rs.as<RankSum>(),
-                                               chan_pos.as<uint32_t>(), nch);
+                                               chan_key.as<unsigned long long>(), nch);
     } else {
       ProfScope ps_(c->lc, "k_rank_summary", st);
       k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
                        wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
                                             rs.as<RankSum>(),
-                                            chan_pos.as<uint32_t>(), nch);
+                                            chan_key.as<unsigned long long>(), nch);
     }
+  }
+  // sharded: every rank's summary lives on exactly one shard (zeros
+  // elsewhere), so a sum all-reduce assembles the global tables
+  comm_group_start(c);
+  comm_allreduce(c, rs.p, static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum) / 8,
+                 ncclUint64, ncclSum);
+  comm_allreduce(c, chan_key.p, static_cast<size_t>(J) * std::max(R, 1) * nch,
+                 ncclUint64, ncclSum);
+  comm_group_end(c);
+  // K1b: ring-successor progress per membership slot
+  DevBuf& slot_group = c->buf("rca.slot_group");
+  DevBuf& succ = c->buf("rca.succ");
+  DevBuf& succ_key = c->buf("rca.succ_key");
+  {
+    std::vector<uint32_t> h_sg(std::max<uint32_t>(M, 1));
+    for (int32_t g = 0; g < G; ++g)
+      for (uint32_t q = m->h_member_off[g]; q < m->h_member_off[g + 1]; ++q)
+        h_sg[q] = static_cast<uint32_t>(g);
+    upload(slot_group, h_sg, st);
+  }
+  succ.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * sizeof(SuccProg));
+  succ_key.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * nch * 8);
+  if (!affected_only && M > 0) {
+    int wpb = 32768 / (nch * 4);
+    wpb = std::max(1, std::min(8, wpb));
+    const uint64_t warps = static_cast<uint64_t>(M) * J;
+    ProfScope ps_(c->lc, "k_succ_prog", st);
+    k_succ_prog<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
+                  wpb * nch * 4, st>>>(sv, s->flow_view(), mv, J, M,
+                                       slot_group.as<uint32_t>(), rs.as<RankSum>(),
+                                       succ.as<SuccProg>(),
+                                       succ_key.as<unsigned long long>(), nch);
+  }
+  if (!affected_only && M > 0) {
+    comm_group_start(c);
+    comm_allreduce(c, succ.p, static_cast<size_t>(J) * M * sizeof(SuccProg) / 8,
+                   ncclUint64, ncclSum);
+    comm_allreduce(c, succ_key.p, static_cast<size_t>(J) * M * nch, ncclUint64, ncclSum);
+    comm_group_end(c);
   }
   // K2/K3: straggler iteration tables
   DevBuf& tbl_s = c->buf("rca.tbl_s");
@@ -2231,6 +2323,10 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                               M, tbl_s.as<unsigned long long>(),
                               tbl_e.as<unsigned long long>());
       }
+      comm_group_start(c);
+      comm_allreduce(c, tbl_s.p, cells, ncclUint64, ncclMin);
+      comm_allreduce(c, tbl_e.p, cells, ncclUint64, ncclMax);
+      comm_group_end(c);
       const uint64_t gw = static_cast<uint64_t>(G) * Js;
       ProfScope ps_(c->lc, "k_group_iters", st);
       k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
@@ -2270,21 +2366,17 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   CSG_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
   // K5: straggler flow rules
   DevBuf& fs = c->buf("rca.fs");
-  DevBuf& slot_group = c->buf("rca.slot_group");
   fs.ensure(static_cast<size_t>(std::max(Js, 1)) * std::max<uint32_t>(M, 1) * sizeof(FlowSum));
   if (Js > 0 && opn > 0 && M > 0) {
     store_build_op_index(s, opn);
-    std::vector<uint32_t> h_sg(M);
-    for (int32_t g = 0; g < G; ++g)
-      for (uint32_t q = m->h_member_off[g]; q < m->h_member_off[g + 1]; ++q)
-        h_sg[q] = static_cast<uint32_t>(g);
-    upload(slot_group, h_sg, st);
     const uint64_t warps = static_cast<uint64_t>(M) * Js;
     ProfScope ps_(c->lc, "k_flow", st);
     k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
         sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
         slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
         aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
+    comm_allreduce(c, fs.p, static_cast<size_t>(Js) * M * sizeof(FlowSum) / 8,
+                   ncclUint64, ncclSum);
   }
 
   // ---- failure trips: per-group candidates + per-trip exoneration ----
@@ -2363,7 +2455,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ProfScope ps_(c->lc, "k_fail_cands", st);
       k_fail_cands<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 127) / 128),
                      128, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
-                                   rs.as<RankSum>(), chan_pos.as<uint32_t>(), nch,
+                                   rs.as<RankSum>(), chan_key.as<unsigned long long>(),
+                                   succ.as<SuccProg>(), succ_key.as<unsigned long long>(),
+                                   M, nch,
                                    d_pick.as<GroupPick>(), d_off.as<uint32_t>(),
                                    d_cand.as<Cand>(), d_cev.as<csg_evidence>(),
                                    err.as<uint32_t>());
@@ -2409,7 +2503,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   a.trip_rank = drank;
   a.js_of = djs;
   a.rs = rs.as<RankSum>();
-  a.chan_pos = chan_pos.as<uint32_t>();
+  a.chan_key = chan_key.as<unsigned long long>();
   a.nch = nch;
   a.aff = aff.as<int32_t>();
   a.n_aff = n_aff.as<int32_t>();
@@ -2425,10 +2519,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   a.delta_a = cfg.delta_ms;
   a.thr = cfg.straggler_threshold_ms;
   a.skew = cfg.flow_skew_factor;
-  a.N = s->n;
+  a.N = s->n_global;
   a.opk = s->opidx_keys.as<uint64_t>();
-  a.opp = s->opidx_pos.as<uint32_t>();
   a.oprank = s->opidx_rank.as<int32_t>();
+  a.op_ts = s->opidx_ts.as<double>();
+  a.op_dur = s->opidx_dur.as<double>();
+  a.op_nm = s->opidx_nm.as<uint8_t>();
+  a.sharded = comm_active(c) ? 1 : 0;
   a.n_opidx = s->op_indexed ? s->n_opidx : 0;
   a.min_op = s->min_op;
   a.scratch_per_trip = static_cast<uint32_t>(spt);
@@ -2478,7 +2575,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ea.sus = p_sus.as<csg_suspect>();
       ea.ev = p_ev.as<csg_evidence>();
       ea.out = d_out.as<TripOut>();
-      ea.N = s->n;
+      ea.N = s->n_global;
       ea.err = err.as<uint32_t>();
       CSG_CUDA(cudaFuncSetAttribute(k_exonerate,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,

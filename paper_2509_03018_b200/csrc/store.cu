@@ -14,6 +14,7 @@
 #include <cstring>
 #include <vector>
 
+#include "comm.cuh"
 #include "objects.h"
 
 namespace csg {
@@ -195,17 +196,21 @@ __global__ void k_runmax(const double* __restrict__ ts,
   }
 }
 
-__global__ void k_opidx_rank(StoreView s, const uint32_t* __restrict__ pos,
-                             uint64_t n, int32_t* __restrict__ rank) {
+// Fill the op index's entry columns from the rank-major store.
+__global__ void k_opidx_fill(StoreView s, const uint32_t* __restrict__ pos,
+                             uint64_t n, int32_t* __restrict__ rank,
+                             double* __restrict__ ts, double* __restrict__ dur,
+                             uint8_t* __restrict__ nm) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t p = pos[i];
-    int32_t lo = 0, hi = s.R;  // last r with rank_off[r] <= p
-    while (hi - lo > 1) {
-      const int32_t md = (lo + hi) >> 1;
-      if (s.rank_off[md] <= p) lo = md; else hi = md;
-    }
-    rank[i] = lo;
+    rank[i] = static_cast<int32_t>(s.rank_of[p]);
+    const double t = s.ts[p];
+    double st;
+    memcpy(&st, &s.pa[p], 8);
+    ts[i] = t;
+    dur[i] = t - st;
+    nm[i] = static_cast<uint8_t>(ko_opname(s.ko[p]));
   }
 }
 
@@ -221,6 +226,30 @@ __global__ void k_flow_keys(StoreView s, int64_t min_op, int op_shift,
         static_cast<unsigned long long>(s.chan[p]));
     vals[p] = static_cast<uint32_t>(p);
   }
+}
+
+// Gathered-entry permutation into sorted order.
+__global__ void k_opidx_permute(const uint32_t* __restrict__ idx, uint64_t n,
+                                const int32_t* __restrict__ r0,
+                                const double* __restrict__ t0,
+                                const double* __restrict__ d0,
+                                const uint8_t* __restrict__ m0,
+                                int32_t* __restrict__ r1, double* __restrict__ t1,
+                                double* __restrict__ d1, uint8_t* __restrict__ m1) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = idx[i];
+    r1[i] = r0[k];
+    t1[i] = t0[k];
+    d1[i] = d0[k];
+    m1[i] = m0[k];
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = static_cast<uint32_t>(i);
 }
 
 // ---- query ---------------------------------------------------------------
@@ -366,6 +395,7 @@ void store_build_index(csg_store* s) {
   h.max_chan = INT32_MIN;
   h.min_op = INT64_MAX;
   h.max_op = INT64_MIN;
+  h.n_total = n;
   s->stats_dev.ensure(sizeof(StoreStats));
   CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
                            cudaMemcpyHostToDevice, st));
@@ -378,29 +408,46 @@ void store_build_index(csg_store* s) {
                                               s->keys.as<uint32_t>(),
                                               s->perm.as<uint32_t>());
   }
+  if (comm_active(c)) {
+    // global stats over the shards (identical rank space, ticks, op range)
+    StoreStats* d = s->stats_dev.as<StoreStats>();
+    comm_group_start(c);
+    comm_allreduce(c, &d->ts_max_key, 1, ncclUint64, ncclMax);
+    comm_allreduce(c, &d->min_rank, 1, ncclInt32, ncclMin);
+    comm_allreduce(c, &d->max_rank, 1, ncclInt32, ncclMax);
+    comm_allreduce(c, &d->min_chan, 1, ncclInt32, ncclMin);
+    comm_allreduce(c, &d->max_chan, 1, ncclInt32, ncclMax);
+    comm_allreduce(c, &d->min_op, 1, ncclInt64, ncclMin);
+    comm_allreduce(c, &d->max_op, 1, ncclInt64, ncclMax);
+    comm_allreduce(c, &d->n_nan, 1, ncclUint64, ncclSum);
+    comm_allreduce(c, &d->n_total, 1, ncclUint64, ncclSum);
+    comm_group_end(c);
+  }
   CSG_CUDA(cudaMemcpyAsync(&h, s->stats_dev.p, sizeof(h),
                            cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));
-  if (n && h.min_rank < 0)
+  const uint64_t ng = h.n_total;
+  s->n_global = ng;
+  if (ng && h.min_rank < 0)
     throw Error(CSG_ERR_RUNTIME,
                 "engine: negative rank in trace record (ranks must be >= 0)");
-  if (n && h.min_chan < 0)
+  if (ng && h.min_chan < 0)
     throw Error(CSG_ERR_RUNTIME,
                 "engine: negative channel in trace record (channels must be >= 0)");
-  if (n && h.max_chan >= 4096)
+  if (ng && h.max_chan >= 4096)
     throw Error(CSG_ERR_RUNTIME, "engine: channel id >= 4096 unsupported");
   if (h.n_nan)
     throw Error(CSG_ERR_RUNTIME, "engine: NaN timestamp in trace record");
   if (n > 0xFFFFFFF0ull)
     throw Error(CSG_ERR_RUNTIME, "engine: store exceeds 2^32 records");
-  const double mx = n ? dkey_inv(h.ts_max_key) : 0.0;
-  s->last_ts = (n && mx > 0.0) ? mx : 0.0;
-  s->min_rank = n ? h.min_rank : 0;
-  s->max_rank = n ? h.max_rank : -1;
-  s->min_chan = n ? h.min_chan : 0;
-  s->max_chan = n ? h.max_chan : -1;
-  s->min_op = n ? h.min_op : 0;
-  s->max_op = n ? h.max_op : -1;
+  const double mx = ng ? dkey_inv(h.ts_max_key) : 0.0;
+  s->last_ts = (ng && mx > 0.0) ? mx : 0.0;
+  s->min_rank = ng ? h.min_rank : 0;
+  s->max_rank = ng ? h.max_rank : -1;
+  s->min_chan = ng ? h.min_chan : 0;
+  s->max_chan = ng ? h.max_chan : -1;
+  s->min_op = ng ? h.min_op : 0;
+  s->max_op = ng ? h.max_op : -1;
   s->R = s->max_rank + 1;
   s->nch = s->max_chan + 1;
   const int32_t R = s->R;
@@ -469,7 +516,6 @@ void store_build_op_index(csg_store* s, int32_t opn) {
       ProfScope ps_(c->lc, "k_opidx_flags", st);
       k_opidx_flags<<<grid_for(n), 256, 0, st>>>(v, flags.as<uint32_t>());
     }
-    // total = last exclusive offset + last flag
     uint32_t last_flag = 0;
     CSG_CUDA(cudaMemcpyAsync(&last_flag, flags.as<uint32_t>() + n - 1, 4,
                              cudaMemcpyDeviceToHost, st));
@@ -480,28 +526,99 @@ void store_build_op_index(csg_store* s, int32_t opn) {
     CSG_CUDA(cudaStreamSynchronize(st));
     count = last_off + last_flag;
   }
-  s->n_opidx = count;
+  DevBuf& pos = c->buf("opidx.pos");
   s->opidx_keys.ensure(static_cast<size_t>(count) * 8 + 8);
-  s->opidx_pos.ensure(static_cast<size_t>(count) * 4 + 4);
+  pos.ensure(static_cast<size_t>(count) * 4 + 4);
   if (count) {
-    {
-      ProfScope ps_(c->lc, "k_opidx_scatter", st);
-      k_opidx_scatter<<<grid_for(n), 256, 0, st>>>(
-          v, flags.as<uint32_t>(), s->min_op, s->opidx_keys.as<uint64_t>(),
-          s->opidx_pos.as<uint32_t>());
-    }
-    const uint64_t range = static_cast<uint64_t>(s->max_op - s->min_op);
-    radix_sort_u64(s->opidx_keys.as<uint64_t>(), s->opidx_pos.as<uint32_t>(),
-                   count, bits_for(range), s->sort, st, c->lc);
+    ProfScope ps_(c->lc, "k_opidx_scatter", st);
+    k_opidx_scatter<<<grid_for(n), 256, 0, st>>>(
+        v, flags.as<uint32_t>(), s->min_op, s->opidx_keys.as<uint64_t>(),
+        pos.as<uint32_t>());
   }
+  const uint64_t range = static_cast<uint64_t>(s->max_op - s->min_op);
+  if (count)
+    radix_sort_u64(s->opidx_keys.as<uint64_t>(), pos.as<uint32_t>(), count,
+                   bits_for(range), s->sort, st, c->lc);
   s->opidx_rank.ensure(static_cast<size_t>(count) * 4 + 4);
+  s->opidx_ts.ensure(static_cast<size_t>(count) * 8 + 8);
+  s->opidx_dur.ensure(static_cast<size_t>(count) * 8 + 8);
+  s->opidx_nm.ensure(static_cast<size_t>(count) + 8);
   if (count) {
-    {
-      ProfScope ps_(c->lc, "k_opidx_rank", st);
-      k_opidx_rank<<<grid_for(count), 256, 0, st>>>(
-          s->view(), s->opidx_pos.as<uint32_t>(), count,
-          s->opidx_rank.as<int32_t>());
+    ProfScope ps_(c->lc, "k_opidx_fill", st);
+    k_opidx_fill<<<grid_for(count), 256, 0, st>>>(
+        v, pos.as<uint32_t>(), count, s->opidx_rank.as<int32_t>(),
+        s->opidx_ts.as<double>(), s->opidx_dur.as<double>(), s->opidx_nm.as<uint8_t>());
+  }
+  s->n_opidx = count;
+  if (comm_active(c)) {
+    // Sharded: every shard needs every rank's completions for the sibling /
+    // cohort medians. All-gather the (padded) entry columns, then re-sort.
+    DevBuf& dcnt = c->buf("opidx.cnt");
+    dcnt.ensure(static_cast<size_t>(c->nranks) * 8);
+    unsigned long long mine = count;
+    CSG_CUDA(cudaMemcpyAsync(dcnt.as<unsigned long long>() + c->rank, &mine, 8,
+                             cudaMemcpyHostToDevice, st));
+    comm_allgather(c, dcnt.as<unsigned long long>() + c->rank, dcnt.p, 1, ncclUint64);
+    std::vector<unsigned long long> cnts(c->nranks);
+    CSG_CUDA(cudaMemcpyAsync(cnts.data(), dcnt.p, c->nranks * 8, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaStreamSynchronize(st));
+    unsigned long long cmax = 0, total = 0;
+    for (auto x : cnts) {
+      cmax = std::max(cmax, x);
+      total += x;
     }
+    const size_t P = c->nranks;
+    DevBuf &gk = c->buf("opidx.gk"), &gr = c->buf("opidx.gr"), &gt = c->buf("opidx.gt"),
+           &gd = c->buf("opidx.gd"), &gm = c->buf("opidx.gm"), &gi = c->buf("opidx.gi");
+    DevBuf &lk = c->buf("opidx.lk"), &lr = c->buf("opidx.lr"), &lt = c->buf("opidx.lt"),
+           &ld = c->buf("opidx.ld"), &lm = c->buf("opidx.lm");
+    lk.ensure(cmax * 8 + 8);
+    lr.ensure(cmax * 4 + 4);
+    lt.ensure(cmax * 8 + 8);
+    ld.ensure(cmax * 8 + 8);
+    lm.ensure(cmax + 8);
+    // padding keys sort after every real key
+    CSG_CUDA(cudaMemsetAsync(lk.p, 0xff, cmax * 8 + 8, st));
+    if (count) {
+      CSG_CUDA(cudaMemcpyAsync(lk.p, s->opidx_keys.p, count * 8ull, cudaMemcpyDeviceToDevice, st));
+      CSG_CUDA(cudaMemcpyAsync(lr.p, s->opidx_rank.p, count * 4ull, cudaMemcpyDeviceToDevice, st));
+      CSG_CUDA(cudaMemcpyAsync(lt.p, s->opidx_ts.p, count * 8ull, cudaMemcpyDeviceToDevice, st));
+      CSG_CUDA(cudaMemcpyAsync(ld.p, s->opidx_dur.p, count * 8ull, cudaMemcpyDeviceToDevice, st));
+      CSG_CUDA(cudaMemcpyAsync(lm.p, s->opidx_nm.p, count, cudaMemcpyDeviceToDevice, st));
+    }
+    gk.ensure(P * cmax * 8 + 8);
+    gr.ensure(P * cmax * 4 + 4);
+    gt.ensure(P * cmax * 8 + 8);
+    gd.ensure(P * cmax * 8 + 8);
+    gm.ensure(P * cmax + 8);
+    gi.ensure(P * cmax * 4 + 4);
+    comm_group_start(c);
+    comm_allgather(c, lk.p, gk.p, cmax, ncclUint64);
+    comm_allgather(c, lr.p, gr.p, cmax, ncclInt32);
+    comm_allgather(c, lt.p, gt.p, cmax, ncclFloat64);
+    comm_allgather(c, ld.p, gd.p, cmax, ncclFloat64);
+    comm_allgather(c, lm.p, gm.p, cmax, ncclUint8);
+    comm_group_end(c);
+    const uint64_t ng = P * cmax;
+    {
+      ProfScope ps_(c->lc, "k_iota", st);
+      k_iota<<<grid_for(ng), 256, 0, st>>>(gi.as<uint32_t>(), ng);
+    }
+    radix_sort_u64(gk.as<uint64_t>(), gi.as<uint32_t>(), ng, 64, s->sort, st, c->lc);
+    s->opidx_keys.ensure(ng * 8 + 8);
+    s->opidx_rank.ensure(ng * 4 + 4);
+    s->opidx_ts.ensure(ng * 8 + 8);
+    s->opidx_dur.ensure(ng * 8 + 8);
+    s->opidx_nm.ensure(ng + 8);
+    CSG_CUDA(cudaMemcpyAsync(s->opidx_keys.p, gk.p, ng * 8, cudaMemcpyDeviceToDevice, st));
+    {
+      ProfScope ps_(c->lc, "k_opidx_permute", st);
+      k_opidx_permute<<<grid_for(ng), 256, 0, st>>>(
+          gi.as<uint32_t>(), ng, gr.as<int32_t>(), gt.as<double>(), gd.as<double>(),
+          gm.as<uint8_t>(), s->opidx_rank.as<int32_t>(), s->opidx_ts.as<double>(),
+          s->opidx_dur.as<double>(), s->opidx_nm.as<uint8_t>());
+    }
+    s->n_opidx = total;  // padding sorted to the end
   }
   CSG_CUDA(cudaGetLastError());
   s->op_indexed = true;

@@ -13,6 +13,7 @@
 // Floating point: the EMA and threshold products use explicit _rn intrinsics
 // (and the file is built with -fmad=false) so no FMA contraction happens,
 // matching the reference's SSE2 build.
+#include "comm.cuh"
 #include "objects.h"
 #include "trigger.cuh"
 
@@ -65,8 +66,8 @@ __global__ void k_window_stats(StoreView s, const double* __restrict__ ticks,
     ws.has_state = hstate;
     ws.pad = 0;
     ws.bytes = bytes;
-    ws.min_end = mn;
-    ws.max_end = mx;
+    ws.min_end = ncomp ? mn : 0.0;
+    ws.max_end = ncomp ? mx : 0.0;
     out[w] = ws;
   }
 }
@@ -124,14 +125,16 @@ __global__ void k_window_bins(StoreView s, const double* __restrict__ ticks,
   }
   __syncthreads();
   for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    // an empty window is all zeros: shards that do not own the sampled rank
+    // contribute nothing to the sum all-reduce
     WinStat w;
     w.n_rec = nrec[k];
     w.n_comp = ncomp[k];
     w.has_state = hstate[k];
     w.pad = 0;
     w.bytes = bytes[k];
-    w.min_end = ncomp[k] ? dkey_inv(mn[k]) : INFINITY;
-    w.max_end = ncomp[k] ? dkey_inv(mx[k]) : -INFINITY;
+    w.min_end = ncomp[k] ? dkey_inv(mn[k]) : 0.0;
+    w.max_end = ncomp[k] ? dkey_inv(mx[k]) : 0.0;
     out[static_cast<int64_t>(k) * S + si] = w;
   }
 }
@@ -351,6 +354,8 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
   trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
+  comm_allreduce(c, ws.p, static_cast<size_t>(T) * S * sizeof(WinStat) / 8, ncclUint64,
+                 ncclSum);
   {
     ProfScope ps_(c->lc, "k_ema_ticks", c->stream);
     k_ema_ticks<<<(S + 127) / 128, 128, 0, c->stream>>>(ws.as<WinStat>(), T, S, p,

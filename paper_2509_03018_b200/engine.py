@@ -118,6 +118,19 @@ class Context:
         return ({k: tuple(v) for k, v in json.loads(buf.value.decode()).items()},
                 h2d.value, d2h.value)
 
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """Join the NCCL communicator of a sharded store (csg_ctx_comm_init)."""
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id[:128])
+        _check(lib().csg_ctx_comm_init(self.h, buf, C.c_size_t(128), C.c_int(nranks),
+                                       C.c_int(rank)))
+
+    def comm_info(self):
+        nr = C.c_int()
+        rk = C.c_int()
+        coll = C.c_uint64()
+        _check(lib().csg_ctx_comm_info(self.h, C.byref(nr), C.byref(rk), C.byref(coll)))
+        return nr.value, rk.value, coll.value
+
     @classmethod
     def of_c_api(cls) -> "Context":
         """The context the collsight_* C API runs on (not owned)."""
@@ -514,12 +527,16 @@ def parse_trace(text: str) -> np.ndarray:
         lib().collsight_b200_free(out)
 
 
-def synthesize(scenario: Scenario, target_records: int = 0) -> np.ndarray:
-    """Synthetic trace for the scenario (benchmark generator, synth.cpp)."""
+def synthesize(scenario: Scenario, target_records: int = 0,
+               rank_range: Optional[Tuple[int, int]] = None) -> np.ndarray:
+    """Synthetic trace for the scenario (benchmark generator, synth.cpp);
+    rank_range=(lo, hi) keeps one shard's records."""
     out = C.c_void_p()
     n = C.c_size_t()
-    _ccheck(lib().collsight_b200_synthesize(scenario.h, C.c_uint64(target_records),
-                                            C.byref(out), C.byref(n)))
+    lo, hi = rank_range if rank_range else (0, 0x7FFFFFFF)
+    _ccheck(lib().collsight_b200_synthesize_ranks(scenario.h, C.c_uint64(target_records),
+                                                  C.c_int32(lo), C.c_int32(hi),
+                                                  C.byref(out), C.byref(n)))
     try:
         arr = np.empty(n.value, dtype=_abi.RECORD_DTYPE)
         if n.value:
@@ -527,3 +544,10 @@ def synthesize(scenario: Scenario, target_records: int = 0) -> np.ndarray:
         return arr
     finally:
         lib().collsight_b200_free(out)
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for csg_ctx_comm_init (call on one rank, broadcast)."""
+    buf = (C.c_ubyte * 128)()
+    _check(lib().csg_comm_unique_id(buf, C.c_size_t(128)))
+    return bytes(buf)

@@ -102,3 +102,25 @@ def test_prefix_scan_fallback_matches(name, tmp_path):
     env = dict(os.environ, CSG_DISABLE_FLOW_INDEX="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_c2_full_scale_window_matches_reference(eng):
+    """Full benchmark scale (1024 ranks, ~1e7 records): the reference's
+    report for one detection window (tests/golden/c2_window_22000.json, 11 min
+    of reference CPU time) against the engine's analyze on the same trigger."""
+    from paper_2509_03018_b200.model import TriggerEvent
+    from tests.golden.make_golden import fnv1a64
+    g = json.load(open(os.path.join(GOLDEN, "c2_window_22000.json")))
+    root = os.path.dirname(GOLDEN).rsplit("/tests", 1)[0]
+    scen = eng.Scenario.load(os.path.join(root, g["config"]))
+    recs = eng.synthesize(scen, g["target_records"])
+    assert len(recs) == g["records"]
+    assert fnv1a64(recs[:200000].tobytes()) == fnv1a64(recs[:200000].tobytes())
+    topo, prog = scen.layout()
+    tcfg, acfg, seed = scen.configs()
+    rep = g["report"]
+    store = eng.TraceStore(records=recs)
+    got = eng.analyze(store, eng.Model(topo, prog), acfg,
+                      TriggerEvent(rep["kind"], rep["suspect_rank"], rep["time_ms"]))
+    assert got == rep
