@@ -380,7 +380,7 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
   if (go) {
     const int64_t op = rsj[pred].last_op;
     const uint32_t b = s.rank_off[sr];
-    const uint32_t cend = b + rsj[sr].cutoff;
+    const uint32_t cend = min(b + rsj[sr].cutoff, s.rank_off[sr + 1]);
     if (f.n) {
       const unsigned long long k0 =
           (static_cast<unsigned long long>(sr) << f.rank_shift) |
@@ -455,7 +455,10 @@ __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
   if (g0 == g1) return;
   const int32_t j = strag_trip[js];
   const uint32_t b = s.rank_off[r];
-  const uint32_t cend = b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff;
+  // summaries are global after the shard all-reduce; only this shard's
+  // segment is walked (empty for ranks owned elsewhere)
+  const uint32_t cend =
+      min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, s.rank_off[r + 1]);
   for (uint32_t p = b + lane; p < cend; p += 32) {
     if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
     const int32_t cm = s.comm[p];
@@ -660,7 +663,8 @@ __global__ void k_flow(StoreView s, ModelView m, int32_t Js,
   const double t = trip_t[j];
   const double ws = t - delta_a;
   const uint32_t b = s.rank_off[r];
-  const uint32_t e = b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff;
+  const uint32_t e =
+      min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, s.rank_off[r + 1]);
   const double* rm = s.runmax;
   // records before p0 all have ts < ws (running max below ws)
   const uint32_t p0 =

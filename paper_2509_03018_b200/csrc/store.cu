@@ -493,6 +493,16 @@ void store_build_index(csg_store* s) {
     CSG_CUDA(cudaStreamSynchronize(st));
     uint64_t mx = 0;
     for (int32_t r = 0; r < R; ++r) mx = std::max<uint64_t>(mx, ro[r + 1] - ro[r]);
+    if (comm_active(c)) {  // scratch sized for the longest segment anywhere
+      DevBuf& d = c->buf("store.maxseg");
+      d.ensure(8);
+      unsigned long long v = mx;
+      CSG_CUDA(cudaMemcpyAsync(d.p, &v, 8, cudaMemcpyHostToDevice, st));
+      comm_allreduce(c, d.p, 1, ncclUint64, ncclMax);
+      CSG_CUDA(cudaMemcpyAsync(&v, d.p, 8, cudaMemcpyDeviceToHost, st));
+      CSG_CUDA(cudaStreamSynchronize(st));
+      mx = v;
+    }
     s->max_seg = mx;
   }
   CSG_CUDA(cudaGetLastError());
