@@ -66,6 +66,9 @@ def scaled_config(ngpus: int) -> str:
     every GPU owns 1024 ranks (~1e7 records) of a 1024N-rank trace."""
     cfg = json.load(open(CONFIG))
     cfg["layout"]["dp"] = cfg["layout"]["dp"] * ngpus
+    # one failing NIC per 1024-rank block (every 128 nodes), same onset
+    f0 = cfg["faults"][0]
+    cfg["faults"] = [dict(f0, node=f0["node"] + 128 * k) for k in range(ngpus)]
     return json.dumps(cfg)
 
 

@@ -107,11 +107,11 @@ def test_prefix_scan_fallback_matches(name, tmp_path):
 @pytest.mark.gpu
 def test_c2_full_scale_window_matches_reference(eng):
     """Full benchmark scale (1024 ranks, ~1e7 records): the reference's
-    report for one detection window (tests/golden/c2_window_22000.json, 11 min
+    report for one detection window (tests/golden/c2_window.json, 11 min
     of reference CPU time) against the engine's analyze on the same trigger."""
     from paper_2509_03018_b200.model import TriggerEvent
     from tests.golden.make_golden import fnv1a64
-    g = json.load(open(os.path.join(GOLDEN, "c2_window_22000.json")))
+    g = json.load(open(os.path.join(GOLDEN, "c2_window.json")))
     root = os.path.dirname(GOLDEN).rsplit("/tests", 1)[0]
     scen = eng.Scenario.load(os.path.join(root, g["config"]))
     recs = eng.synthesize(scen, g["target_records"])
