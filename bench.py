@@ -141,6 +141,17 @@ class Clocks:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture (profiles/ncu_traffic.json, written
+    by scripts/ncu_summary.py), or None when that kernel was not captured."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return t[kernel.split("<")[0]]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         return float(json.load(open(PEAKS))["hbm_gbs"]), "measured"
@@ -286,7 +297,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved,
                      "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": None, "launches": nl,
+                     "traffic": ncu_traffic(name),
+                     "algorithmic_bytes_per_launch": (ALGO_BYTES[name] * units_per_launch
+                                                      if achieved else None),
+                     "launches": nl,
                      "avg_launch_ms": tot_ms / nl, "share_of_step": step_share},
         "e2e": e2e,
         "cpu_baseline": cpu,
