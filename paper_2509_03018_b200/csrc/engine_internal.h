@@ -86,18 +86,16 @@ struct StoreView {
   const uint32_t* rank_of = nullptr;   // rank per rank-major position
 };
 
-// Flow index view (see store_build_flow_index).
+// Flow index view (see store_build_flow_index): inside each rank segment
+// [rank_off[r], rank_off[r+1]) the positions ordered by (op_seq, store
+// order). A segment whose op_seq is already non-decreasing in store order
+// (every simulator trace) is its own flow order: unsorted[r] == 0 and the
+// identity is used; otherwise pos[] holds that segment's permutation.
 struct FlowView {
-  uint64_t n = 0;
-  int op_shift = 0, rank_shift = 0;
-  int narrow = 0;  // keys stored as u32 (key bits <= 32)
-  int64_t min_op = 0;
-  const void* keys = nullptr;
-  const uint32_t* pos = nullptr;
-  __device__ unsigned long long key(uint64_t i) const {
-    return narrow ? static_cast<const uint32_t*>(keys)[i]
-                  : static_cast<const unsigned long long*>(keys)[i];
-  }
+  uint64_t n = 0;                      // 0: no flow index (prefix scans)
+  const uint8_t* unsorted = nullptr;   // per rank
+  const uint32_t* pos = nullptr;       // rank-major positions
+  __device__ uint32_t at(bool uns, uint32_t i) const { return uns ? pos[i] : i; }
 };
 
 __host__ __device__ inline int ko_kind(uint8_t ko) { return ko & 1; }

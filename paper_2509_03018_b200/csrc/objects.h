@@ -82,12 +82,12 @@ struct csg_store {
   csg::DevBuf opidx_dur;     // end_ms - start_ms
   csg::DevBuf opidx_nm;      // record op_name
   csg::DevBuf op_seg_off;    // dense [min_op, max_op+1] -> start in opidx
-  // flow index: rank-major positions ordered by (rank, op_seq, channel,
-  // store order); keys packed rank | op - min_op | channel
+  // flow index: per rank segment, positions ordered by (op_seq, store
+  // order); identity for segments already ordered (see FlowView)
   bool flow_indexed = false;
-  int flow_key_bits = 0, flow_op_shift = 0, flow_rank_shift = 0;
-  csg::DevBuf fl_keys;  // u64 keys (sorted)
-  csg::DevBuf fl_pos;   // u32 rank-major positions
+  csg::DevBuf fl_unsorted;  // u8 per rank
+  csg::DevBuf fl_pos;       // u32 rank-major positions (unsorted segments)
+  csg::DevBuf fl_keys;      // global-sort fallback scratch
   csg::DevBuf stats_dev;
 
   csg::StoreView view() const {
@@ -111,11 +111,7 @@ struct csg_store {
   csg::FlowView flow_view() const {
     csg::FlowView f;
     f.n = flow_indexed ? n : 0;
-    f.op_shift = flow_op_shift;
-    f.rank_shift = flow_rank_shift;
-    f.min_op = min_op;
-    f.narrow = flow_key_bits <= 32 ? 1 : 0;
-    f.keys = fl_keys.p;
+    f.unsorted = fl_unsorted.as<uint8_t>();
     f.pos = fl_pos.as<uint32_t>();
     return f;
   }

@@ -271,19 +271,16 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
       cand_stuck = true;
       stuck_op = s.op[found];
     }
-    const unsigned long long rk = static_cast<unsigned long long>(r) << f.rank_shift;
+    const bool uns = f.unsorted[r] != 0;
     auto range_of = [&](int64_t op, uint32_t& fo, uint32_t& fe) {
-      const unsigned long long k0 =
-          rk | (static_cast<unsigned long long>(op - f.min_op) << f.op_shift);
-      const unsigned long long k1 = k0 + (1ull << f.op_shift);
-      fo = warp_partition_point(b, e, [&](uint32_t i) { return f.key(i) >= k0; });
-      fe = warp_partition_point(fo, e, [&](uint32_t i) { return f.key(i) >= k1; });
+      fo = warp_partition_point(b, e, [&](uint32_t i) { return s.op[f.at(uns, i)] >= op; });
+      fe = warp_partition_point(fo, e, [&](uint32_t i) { return s.op[f.at(uns, i)] > op; });
     };
     uint32_t fo, fe;
     range_of(o.last_op, fo, fe);
     uint32_t first = 0xFFFFFFFFu;
     for (uint32_t i = fo + lane; i < fe; i += 32) {
-      const uint32_t p = f.pos[i];
+      const uint32_t p = f.at(uns, i);
       if (p >= cend) continue;
       first = min(first, p);
       if (ko_kind(s.ko[p]) == CSG_KIND_STATE) atomicMax(&tbl[s.chan[p]], p + 1);
@@ -296,7 +293,7 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
       if (stuck_op != o.last_op) range_of(stuck_op, so, se);
       bool hit = false;
       for (uint32_t i = so + lane; i < se && !hit; i += 32) {
-        const uint32_t p = f.pos[i];
+        const uint32_t p = f.at(uns, i);
         hit = p < cend && ko_kind(s.ko[p]) == CSG_KIND_COMPLETION;
       }
       if (!__any_sync(FULL, hit)) o.flags |= RS_STUCK;
@@ -382,21 +379,16 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
     const uint32_t b = s.rank_off[sr];
     const uint32_t cend = min(b + rsj[sr].cutoff, s.rank_off[sr + 1]);
     if (f.n) {
-      const unsigned long long k0 =
-          (static_cast<unsigned long long>(sr) << f.rank_shift) |
-          (static_cast<unsigned long long>(op - f.min_op) << f.op_shift);
-      const unsigned long long k1 = k0 + (1ull << f.op_shift);
       const uint32_t e = s.rank_off[sr + 1];
-      if (op >= f.min_op && op - f.min_op < (1ll << (f.rank_shift - f.op_shift))) {
-        const uint32_t fo =
-            warp_partition_point(b, e, [&](uint32_t x) { return f.key(x) >= k0; });
-        const uint32_t fe =
-            warp_partition_point(fo, e, [&](uint32_t x) { return f.key(x) >= k1; });
-        for (uint32_t x = fo + lane; x < fe; x += 32) {
-          const uint32_t p = f.pos[x];
-          if (p < cend && ko_kind(s.ko[p]) == CSG_KIND_STATE)
-            atomicMax(&tbl[s.chan[p]], p + 1);
-        }
+      const bool uns = f.unsorted[sr] != 0;
+      const uint32_t fo = warp_partition_point(
+          b, e, [&](uint32_t x) { return s.op[f.at(uns, x)] >= op; });
+      const uint32_t fe = warp_partition_point(
+          fo, e, [&](uint32_t x) { return s.op[f.at(uns, x)] > op; });
+      for (uint32_t x = fo + lane; x < fe; x += 32) {
+        const uint32_t p = f.at(uns, x);
+        if (p < cend && ko_kind(s.ko[p]) == CSG_KIND_STATE)
+          atomicMax(&tbl[s.chan[p]], p + 1);
       }
     } else {  // no flow index: scan the prefix
       for (uint32_t p = b + lane; p < cend; p += 32)

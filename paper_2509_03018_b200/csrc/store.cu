@@ -11,6 +11,7 @@
 // first ts > t" becomes one upper_bound over it.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -214,16 +215,96 @@ __global__ void k_opidx_fill(StoreView s, const uint32_t* __restrict__ pos,
   }
 }
 
+// Flow index, step 1: one warp per rank segment; flags segments whose
+// op_seq descends somewhere in store order (those need a permutation).
+__global__ void k_flow_check(StoreView s, uint8_t* __restrict__ unsorted,
+                             unsigned* __restrict__ n_unsorted) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= s.R) return;
+  const uint32_t b = s.rank_off[w], e = s.rank_off[w + 1];
+  bool desc = false;
+  for (uint32_t p = b + 1 + lane; p < e && !__any_sync(0xffffffffu, desc); p += 32)
+    desc = __ldg(s.op + p) < __ldg(s.op + p - 1);
+  desc = __any_sync(0xffffffffu, desc);
+  if (lane == 0) {
+    unsorted[w] = desc ? 1 : 0;
+    if (desc) atomicAdd(n_unsorted, 1u);
+  }
+}
+
+// Flow index, step 2: one block per flagged segment with at most
+// kFlowSmemMax records: stable sort by op_seq as a bitonic sort of unique
+// keys (op - segment min) << 14 | local index in shared memory. Longer
+// segments (or op spans >= 2^49) raise *overflow and the host falls back
+// to the device-wide radix sort.
+constexpr int kFlowSmemMax = 16384;
+__global__ void __launch_bounds__(1024)
+    k_flow_fix(StoreView s, const uint8_t* __restrict__ unsorted, int32_t P,
+               uint32_t* __restrict__ pos, unsigned* __restrict__ overflow) {
+  extern __shared__ unsigned long long fk[];
+  const int32_t r = blockIdx.x;
+  if (!unsorted[r]) return;
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  const uint32_t L = e - b;
+  if (L > static_cast<uint32_t>(P)) {
+    if (threadIdx.x == 0) atomicAdd(overflow, 1u);
+    return;
+  }
+  __shared__ long long smin, smax;
+  if (threadIdx.x == 0) {
+    smin = LLONG_MAX;
+    smax = LLONG_MIN;
+  }
+  __syncthreads();
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
+    const long long o = s.op[b + i];
+    mn = min(mn, o);
+    mx = max(mx, o);
+  }
+  atomicMin(&smin, mn);
+  atomicMax(&smax, mx);
+  __syncthreads();
+  if (static_cast<unsigned long long>(smax - smin) >= (1ull << 49)) {
+    if (threadIdx.x == 0) atomicAdd(overflow, 1u);
+    return;
+  }
+  for (int32_t i = threadIdx.x; i < P; i += blockDim.x)
+    fk[i] = i < static_cast<int32_t>(L)
+                ? (static_cast<unsigned long long>(s.op[b + i] - smin) << 14) |
+                      static_cast<unsigned long long>(i)
+                : ~0ull;
+  __syncthreads();
+  for (int32_t k = 2; k <= P; k <<= 1) {
+    for (int32_t j = k >> 1; j > 0; j >>= 1) {
+      for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const int32_t x = i ^ j;
+        if (x > i) {
+          const unsigned long long a = fk[i], c = fk[x];
+          const bool up = (i & k) == 0;
+          if ((a > c) == up) {
+            fk[i] = c;
+            fk[x] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < L; i += blockDim.x)
+    pos[b + i] = b + static_cast<uint32_t>(fk[i] & 0x3fffu);
+}
+
+// Global fallback: (rank, op - min_op) keys over the whole store.
 template <typename K>
-__global__ void k_flow_keys(StoreView s, int64_t min_op, int op_shift,
-                            int rank_shift, K* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+__global__ void k_flow_keys(StoreView s, int64_t min_op, int rank_shift,
+                            K* __restrict__ keys, uint32_t* __restrict__ vals) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     keys[p] = static_cast<K>(
         (static_cast<unsigned long long>(s.rank_of[p]) << rank_shift) |
-        (static_cast<unsigned long long>(s.op[p] - min_op) << op_shift) |
-        static_cast<unsigned long long>(s.chan[p]));
+        static_cast<unsigned long long>(s.op[p] - min_op));
     vals[p] = static_cast<uint32_t>(p);
   }
 }
@@ -637,36 +718,80 @@ void store_build_op_index(csg_store* s, int32_t opn) {
 bool store_build_flow_index(csg_store* s) {
   store_build_index(s);
   if (s->flow_indexed) return true;
-  const int cb = bits_for(static_cast<uint64_t>(std::max(s->nch, 1) - 1));
-  const int ob = bits_for(static_cast<uint64_t>(s->max_op - s->min_op));
-  const int rb = bits_for(static_cast<uint64_t>(std::max(s->R, 1) - 1));
-  if (cb + ob + rb > 64) return false;
   csg_ctx* c = s->ctx;
   cudaStream_t st = c->stream;
   const uint64_t n = s->n;
-  s->flow_op_shift = cb;
-  s->flow_rank_shift = cb + ob;
-  s->flow_key_bits = cb + ob + rb;
-  s->fl_keys.ensure(n * 8 + 8);
+  const int32_t R = s->R;
+  s->fl_unsorted.ensure(static_cast<size_t>(R) + 8);
   s->fl_pos.ensure(n * 4 + 4);
-  if (n && s->flow_key_bits <= 32) {
+  if (!n || !R) {
+    if (R) CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, R, st));
+    s->flow_indexed = true;
+    return true;
+  }
+  DevBuf& cnt = c->buf("flow.cnt");
+  cnt.ensure(8);
+  CSG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+  unsigned* d_uns = cnt.as<unsigned>();
+  unsigned* d_ovf = d_uns + 1;
+  static const bool force_global = std::getenv("CSG_FLOW_GLOBAL_SORT") != nullptr;
+  const uint64_t span = static_cast<uint64_t>(s->max_op - s->min_op);
+  bool global = force_global;
+  if (!global) {
     {
-      ProfScope ps_(c->lc, "k_flow_keys", st);
-      k_flow_keys<uint32_t><<<grid_for(n), 256, 0, st>>>(
-          s->view(), s->min_op, s->flow_op_shift, s->flow_rank_shift,
-          s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>());
+      ProfScope ps_(c->lc, "k_flow_check", st);
+      k_flow_check<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
+          s->view(), s->fl_unsorted.as<uint8_t>(), d_uns);
     }
-    radix_sort_u32(s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>(), n,
-                   s->flow_key_bits, s->sort, st, c->lc);
-  } else if (n) {
+    int32_t P = 64;
+    while (static_cast<uint64_t>(P) < s->max_seg && P < kFlowSmemMax) P <<= 1;
+    const size_t smem = static_cast<size_t>(P) * 8;
+    static bool attr = false;
+    if (!attr) {
+      CSG_CUDA(cudaFuncSetAttribute(k_flow_fix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kFlowSmemMax * 8));
+      attr = true;
+    }
     {
-      ProfScope ps_(c->lc, "k_flow_keys", st);
-      k_flow_keys<unsigned long long><<<grid_for(n), 256, 0, st>>>(
-          s->view(), s->min_op, s->flow_op_shift, s->flow_rank_shift,
-          s->fl_keys.as<unsigned long long>(), s->fl_pos.as<uint32_t>());
+      ProfScope ps_(c->lc, "k_flow_fix", st);
+      k_flow_fix<<<R, 1024, smem, st>>>(s->view(), s->fl_unsorted.as<uint8_t>(), P,
+                                        s->fl_pos.as<uint32_t>(), d_ovf);
     }
-    radix_sort_u64(reinterpret_cast<uint64_t*>(s->fl_keys.p), s->fl_pos.as<uint32_t>(),
-                   n, s->flow_key_bits, s->sort, st, c->lc);
+    // Without a segment longer than the shared-memory sort or a huge op
+    // span nothing can overflow: no host round trip on the common path.
+    if (s->max_seg > static_cast<uint64_t>(kFlowSmemMax) || span >= (1ull << 49)) {
+      unsigned h[2];
+      CSG_CUDA(cudaMemcpyAsync(h, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+      CSG_CUDA(cudaStreamSynchronize(st));
+      global = h[1] != 0;
+    }
+  }
+  if (global) {
+    // Device-wide stable radix sort by (rank, op): every segment permuted.
+    const int ob = bits_for(span);
+    const int rb = bits_for(static_cast<uint64_t>(std::max(R, 1) - 1));
+    if (ob + rb > 64) return false;
+    CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 1, R, st));
+    if (ob + rb <= 32) {
+      s->fl_keys.ensure(n * 4 + 4);
+      {
+        ProfScope ps_(c->lc, "k_flow_keys", st);
+        k_flow_keys<uint32_t><<<grid_for(n), 256, 0, st>>>(
+            s->view(), s->min_op, ob, s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>());
+      }
+      radix_sort_u32(s->fl_keys.as<uint32_t>(), s->fl_pos.as<uint32_t>(), n, ob + rb,
+                     s->sort, st, c->lc);
+    } else {
+      s->fl_keys.ensure(n * 8 + 8);
+      {
+        ProfScope ps_(c->lc, "k_flow_keys", st);
+        k_flow_keys<unsigned long long><<<grid_for(n), 256, 0, st>>>(
+            s->view(), s->min_op, ob, s->fl_keys.as<unsigned long long>(),
+            s->fl_pos.as<uint32_t>());
+      }
+      radix_sort_u64(s->fl_keys.as<uint64_t>(), s->fl_pos.as<uint32_t>(), n, ob + rb,
+                     s->sort, st, c->lc);
+    }
   }
   CSG_CUDA(cudaGetLastError());
   s->flow_indexed = true;

@@ -124,3 +124,56 @@ def test_c2_full_scale_window_matches_reference(eng):
     got = eng.analyze(store, eng.Model(topo, prog), acfg,
                       TriggerEvent(rep["kind"], rep["suspect_rank"], rep["time_ms"]))
     assert got == rep
+
+
+def shuffled_ops(recs, nranks=10, frac=0.1, seed=7):
+    """Store-order permutation inside a few ranks: swaps ~frac of the adjacent
+    record pairs of each chosen rank, so its op_seq descends in store order
+    (the flow index must then permute that segment)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    out = recs.copy()
+    ranks = rng.choice(np.unique(recs["rank"]), size=nranks, replace=False)
+    for r in ranks:
+        idx = np.flatnonzero(out["rank"] == r)
+        for i in rng.choice(len(idx) - 1, size=int(len(idx) * frac), replace=False):
+            a, b = idx[i], idx[i + 1]
+            out[a], out[b] = out[b].copy(), out[a].copy()
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["segment", "global"])
+@pytest.mark.parametrize("name", ["scenario1", "scenario5", "synth_hang_128"])
+def test_unsorted_flow_segments_match_reference(oracle, name, mode):
+    """Ranks whose op_seq is not monotone in store order: the per-segment
+    shared-memory flow sort (and the device-wide radix fallback) against the
+    reference run on the same permuted trace."""
+    import subprocess
+    import sys
+    recs, _, _ = golden(name)
+    recs = shuffled_ops(recs)
+    cfg = open(os.path.join(GOLDEN, "configs", name + ".json")).read()
+    _, want, _, _ = oracle.run_detection_cfg(cfg, recs)
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        recs.tofile(os.path.join(d, "r.bin"))
+        json.dump(want, open(os.path.join(d, "want.json"), "w"))
+        code = (
+            "import json,os,sys,numpy as np; sys.path.insert(0, %r);"
+            "from paper_2509_03018_b200 import engine as E;"
+            "from paper_2509_03018_b200._abi import RECORD_DTYPE;"
+            "from tests.conftest import GOLDEN;"
+            "recs = np.fromfile(os.path.join(%r,'r.bin'), dtype=RECORD_DTYPE);"
+            "s = E.Scenario.load(os.path.join(GOLDEN,'configs',%r+'.json'));"
+            "t,p = s.layout(); tc,ac,seed = s.configs();"
+            "got,_ = E.run_detection(E.TraceStore(records=recs), E.Model(t,p), tc, ac, seed);"
+            "want = json.load(open(os.path.join(%r,'want.json')));"
+            "assert got == want, [(a,b) for a,b in zip(got,want) if a!=b][:1]; print('ok', len(got))"
+            % (os.path.dirname(GOLDEN).rsplit('/tests', 1)[0], d, name, d))
+        env = dict(os.environ)
+        if mode == "global":
+            env["CSG_FLOW_GLOBAL_SORT"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                           text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
