@@ -93,7 +93,7 @@ struct StoreView {
 // identity is used; otherwise pos[] holds that segment's permutation.
 struct FlowView {
   uint64_t n = 0;                      // 0: no flow index (prefix scans)
-  const uint8_t* unsorted = nullptr;   // per rank
+  const uint32_t* unsorted = nullptr;  // per rank
   const uint32_t* pos = nullptr;       // rank-major positions
   __device__ uint32_t at(bool uns, uint32_t i) const { return uns ? pos[i] : i; }
 };

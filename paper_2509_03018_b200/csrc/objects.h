@@ -85,7 +85,7 @@ struct csg_store {
   // flow index: per rank segment, positions ordered by (op_seq, store
   // order); identity for segments already ordered (see FlowView)
   bool flow_indexed = false;
-  csg::DevBuf fl_unsorted;  // u8 per rank
+  csg::DevBuf fl_unsorted;  // u32 flag per rank
   csg::DevBuf fl_pos;       // u32 rank-major positions (unsorted segments)
   csg::DevBuf fl_keys;      // global-sort fallback scratch
   csg::DevBuf stats_dev;
@@ -111,7 +111,7 @@ struct csg_store {
   csg::FlowView flow_view() const {
     csg::FlowView f;
     f.n = flow_indexed ? n : 0;
-    f.unsorted = fl_unsorted.as<uint8_t>();
+    f.unsorted = fl_unsorted.as<uint32_t>();
     f.pos = fl_pos.as<uint32_t>();
     return f;
   }

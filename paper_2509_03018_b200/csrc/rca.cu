@@ -1829,6 +1829,17 @@ __device__ inline uint32_t pow2_ceil(uint32_t x) {
 
 constexpr int kExoThreads = 512;
 constexpr size_t kExoSmemMax = 192 * 1024;
+// Trips with at most kExoStage candidates keep the exoneration keys, the
+// (op, rank) order and the retained list in shared memory: the greedy sweep
+// is O(C x retained) dependent lookups, latency-bound from global memory.
+constexpr uint32_t kExoStage = 1024;
+struct ExoKey {
+  int64_t op;
+  int32_t rank;
+  uint32_t known;
+  uint64_t done, tx, ready;
+};
+constexpr size_t kExoStageBytes = kExoStage * (sizeof(ExoKey) + 8);
 
 __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   extern __shared__ __align__(16) unsigned long long exo_dyn[];
@@ -1861,19 +1872,41 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   // scratch layout (all 16-aligned)
   const uint32_t P = pow2_ceil(C);
   unsigned char* sp = a.scratch + tp.scratch_off;
-  uint32_t* ord = reinterpret_cast<uint32_t*>(sp);
+  const bool staged = C <= kExoStage;
+  unsigned char* dynb = reinterpret_cast<unsigned char*>(exo_dyn);
+  ExoKey* sk = reinterpret_cast<ExoKey*>(dynb);
+  uint32_t* ord = staged ? reinterpret_cast<uint32_t*>(dynb + kExoStage * sizeof(ExoKey))
+                         : reinterpret_cast<uint32_t*>(sp);
   int64_t* U = reinterpret_cast<int64_t*>(sp + ((P * 4 + 15) & ~15u));
-  uint32_t* ret = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(U) +
-                                              ((C * 8 + 15) & ~15u));
-  uint8_t* keep = reinterpret_cast<uint8_t*>(ret) + ((C * 4 + 15) & ~15u);
+  uint32_t* ret_g = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(U) +
+                                                ((C * 8 + 15) & ~15u));
+  uint32_t* ret = staged ? ord + kExoStage : ret_g;
+  uint8_t* keep = reinterpret_cast<uint8_t*>(ret_g) + ((C * 4 + 15) & ~15u);
   const uint32_t Rs = static_cast<uint32_t>(a.s.R > 0 ? a.s.R : 1);
   uint32_t* minpos = reinterpret_cast<uint32_t*>(keep + ((C + 15) & ~15u));
   uint32_t* rbits = minpos + ((Rs + 3) & ~3u);
   uint32_t* woff = rbits + (((Rs + 31) / 32 + 3) & ~3u);
   csg_suspect* stmp =
       reinterpret_cast<csg_suspect*>(woff + (((Rs + 31) / 32 + 3) & ~3u));
+  if (staged) {
+    for (uint32_t i = tid; i < C; i += blockDim.x) {
+      const Cand& c = cands[i];
+      sk[i] = ExoKey{c.op, c.rank, c.known, c.done, c.tx, c.ready};
+    }
+    __syncthreads();
+  }
+  auto key = [&](uint32_t i) -> ExoKey {
+    if (staged) return sk[i];
+    const Cand& c = cands[i];
+    return ExoKey{c.op, c.rank, c.known, c.done, c.tx, c.ready};
+  };
   // 1. stable (op, rank) order
-  block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) { return cand_before(cands, x, y); });
+  block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
+    const ExoKey kx = key(x), ky = key(y);
+    if (kx.op != ky.op) return kx.op < ky.op;
+    if (kx.rank != ky.rank) return kx.rank < ky.rank;
+    return x < y;
+  });
   // 2. distinct valid (>= 0) candidate ops, ascending (ordered compaction)
   {
     int Kc = 0;
@@ -1883,8 +1916,8 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       int64_t op = -1, prev = -1;
       bool fl = false;
       if (x < C) {
-        op = cands[ord[x]].op;
-        prev = x ? cands[ord[x - 1]].op : -1;
+        op = key(ord[x]).op;
+        prev = x ? key(ord[x - 1]).op : -1;
         fl = op >= 0 && (x == 0 || prev != op);
       }
       const unsigned bm = __ballot_sync(FULL, fl);
@@ -1924,8 +1957,9 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     if (a.debug && tid == 0)
       printf("exo trip %d C=%u K=%d V=%llu words=%d iters=%lld levels=%d\n", tp.j, C, K,
              V, words, (long long)(hi / opn - lo / opn + 1), a.m.n_levels);
-    if ((V * words + (V + 1) / 2) * 8 <= kExoSmemMax) {
-      bits = exo_dyn;  // ancestor bitsets resident in shared memory
+    const size_t stage_b = staged ? kExoStageBytes : 0;
+    if ((V * words + (V + 1) / 2) * 8 <= kExoSmemMax - stage_b) {
+      bits = exo_dyn + stage_b / 8;  // ancestor bitsets resident in shared memory
     } else {
       bits = a.bits + sh_u[0];
     }
@@ -1962,7 +1996,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       }
     }
   }
-  auto drops = [&](const Cand& c, const Cand& u) {
+  auto drops = [&](const ExoKey& c, const ExoKey& u) {
     if (u.rank == c.rank) return false;
     if (u.op == c.op)
       return u.known && c.known && prog_less(u.done, u.tx, u.ready, c.done, c.tx, c.ready);
@@ -1978,14 +2012,14 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     const uint32_t n_in = min(256u, C - base);
     const int nwg = 8;  // warps taking part in the 256-wide chunk
     if (tid < static_cast<int>(n_in)) {
-      const Cand c = cands[ord[base + tid]];
+      const ExoKey c = key(ord[base + tid]);
       bool p = false;
-      for (int q = 0; q < nret && !p; ++q) p = drops(c, cands[ret[q]]);
+      for (int q = 0; q < nret && !p; ++q) p = drops(c, key(ret[q]));
       pre[tid] = p;
       uint32_t row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (!p)
         for (int jj = 0; jj < tid; ++jj)
-          if (drops(c, cands[ord[base + jj]])) row[jj >> 5] |= 1u << (jj & 31);
+          if (drops(c, key(ord[base + jj]))) row[jj >> 5] |= 1u << (jj & 31);
       for (int q = 0; q < 8; ++q) rel[tid][q] = row[q];
     }
     __syncthreads();

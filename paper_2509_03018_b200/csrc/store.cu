@@ -215,85 +215,162 @@ __global__ void k_opidx_fill(StoreView s, const uint32_t* __restrict__ pos,
   }
 }
 
-// Flow index, step 1: one warp per rank segment; flags segments whose
-// op_seq descends somewhere in store order (those need a permutation).
-__global__ void k_flow_check(StoreView s, uint8_t* __restrict__ unsorted,
-                             unsigned* __restrict__ n_unsorted) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= s.R) return;
-  const uint32_t b = s.rank_off[w], e = s.rank_off[w + 1];
-  bool desc = false;
-  for (uint32_t p = b + 1 + lane; p < e && !__any_sync(0xffffffffu, desc); p += 32)
-    desc = __ldg(s.op + p) < __ldg(s.op + p - 1);
-  desc = __any_sync(0xffffffffu, desc);
-  if (lane == 0) {
-    unsorted[w] = desc ? 1 : 0;
-    if (desc) atomicAdd(n_unsorted, 1u);
+// Flow index, step 1: one streaming pass over the op column; a rank
+// segment whose op_seq descends somewhere in store order is flagged once and
+// appended to the work list of step 2.
+__global__ void k_flow_check(StoreView s, uint32_t* __restrict__ unsorted,
+                             uint32_t* __restrict__ list, unsigned* __restrict__ cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; p0 < s.n;
+       p0 += 4 * stride) {
+    int64_t a[4], c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t p = p0 + k * stride;
+      a[k] = p < s.n ? __ldg(s.op + p - 1) : 0;
+      c[k] = p < s.n ? __ldg(s.op + p) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t p = p0 + k * stride;
+      if (c[k] < a[k] && s.rank_of[p] == s.rank_of[p - 1]) {
+        const uint32_t r = s.rank_of[p];
+        if (atomicExch(&unsorted[r], 1u) == 0u) list[atomicAdd(cnt, 1u)] = r;
+      }
+    }
   }
 }
 
-// Flow index, step 2: one block per flagged segment with at most
-// kFlowSmemMax records: stable sort by op_seq as a bitonic sort of unique
-// keys (op - segment min) << 14 | local index in shared memory. Longer
-// segments (or op spans >= 2^49) raise *overflow and the host falls back
-// to the device-wide radix sort.
+// Flow index, step 2: persistent blocks over the flagged segments (at most
+// P <= kFlowSmemMax records each), ops staged in shared memory. A segment
+// made of k <= kFlowRuns ascending runs is merged directly: an element's
+// output position is its offset in its run plus, for every other run, the
+// number of elements ordered before it there (binary search; earlier runs
+// win ties, so the order is stable). Otherwise a bitonic sort of the unique
+// keys (op - segment min) << 14 | local index. Longer segments (or op spans
+// >= 2^49) count into *overflow and the host falls back to the device-wide
+// radix sort.
 constexpr int kFlowSmemMax = 16384;
+constexpr int kFlowRuns = 8;
 __global__ void __launch_bounds__(1024)
-    k_flow_fix(StoreView s, const uint8_t* __restrict__ unsorted, int32_t P,
+    k_flow_fix(StoreView s, const uint32_t* __restrict__ list,
+               const unsigned* __restrict__ cnt, int32_t P,
                uint32_t* __restrict__ pos, unsigned* __restrict__ overflow) {
-  extern __shared__ unsigned long long fk[];
-  const int32_t r = blockIdx.x;
-  if (!unsorted[r]) return;
-  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
-  const uint32_t L = e - b;
-  if (L > static_cast<uint32_t>(P)) {
-    if (threadIdx.x == 0) atomicAdd(overflow, 1u);
-    return;
-  }
-  __shared__ long long smin, smax;
-  if (threadIdx.x == 0) {
-    smin = LLONG_MAX;
-    smax = LLONG_MIN;
-  }
-  __syncthreads();
-  long long mn = LLONG_MAX, mx = LLONG_MIN;
-  for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
-    const long long o = s.op[b + i];
-    mn = min(mn, o);
-    mx = max(mx, o);
-  }
-  atomicMin(&smin, mn);
-  atomicMax(&smax, mx);
-  __syncthreads();
-  if (static_cast<unsigned long long>(smax - smin) >= (1ull << 49)) {
-    if (threadIdx.x == 0) atomicAdd(overflow, 1u);
-    return;
-  }
-  for (int32_t i = threadIdx.x; i < P; i += blockDim.x)
-    fk[i] = i < static_cast<int32_t>(L)
-                ? (static_cast<unsigned long long>(s.op[b + i] - smin) << 14) |
-                      static_cast<unsigned long long>(i)
-                : ~0ull;
-  __syncthreads();
-  for (int32_t k = 2; k <= P; k <<= 1) {
-    for (int32_t j = k >> 1; j > 0; j >>= 1) {
-      for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
-        const int32_t x = i ^ j;
-        if (x > i) {
-          const unsigned long long a = fk[i], c = fk[x];
-          const bool up = (i & k) == 0;
-          if ((a > c) == up) {
-            fk[i] = c;
-            fk[x] = a;
+  extern __shared__ long long so[];
+  __shared__ uint32_t rs[kFlowRuns + 1];
+  __shared__ int nrun;
+  __shared__ long long wmin[32], wmax[32];
+  const unsigned total = *cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (unsigned w = blockIdx.x; w < total; w += gridDim.x) {
+    const uint32_t r = list[w];
+    const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+    const uint32_t L = e - b;
+    if (L > static_cast<uint32_t>(P)) {
+      if (threadIdx.x == 0) atomicAdd(overflow, 1u);
+      continue;  // uniform over the block
+    }
+    if (threadIdx.x == 0) nrun = 0;
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) so[i] = s.op[b + i];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x)
+      if (i == 0 || so[i] < so[i - 1]) {
+        const int q = atomicAdd(&nrun, 1);
+        if (q < kFlowRuns) rs[q] = i;
+      }
+    __syncthreads();
+    const int k = nrun;
+    if (k <= kFlowRuns) {
+      if (threadIdx.x == 0) {  // order the <= 8 run starts, close the last run
+        for (int x = 1; x < k; ++x)
+          for (int y = x; y > 0 && rs[y] < rs[y - 1]; --y) {
+            const uint32_t t = rs[y];
+            rs[y] = rs[y - 1];
+            rs[y - 1] = t;
           }
-        }
+        rs[k] = L;
       }
       __syncthreads();
+      for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
+        const long long x = so[i];
+        int ra = 0;
+        while (i >= rs[ra + 1]) ++ra;
+        uint32_t out = i - rs[ra];
+        for (int j = 0; j < k; ++j) {
+          if (j == ra) continue;
+          uint32_t lo = rs[j], hi = rs[j + 1];
+          if (j < ra) {  // elements <= x come first (earlier in store order)
+            while (lo < hi) {
+              const uint32_t m = (lo + hi) >> 1;
+              if (so[m] <= x) lo = m + 1; else hi = m;
+            }
+          } else {
+            while (lo < hi) {
+              const uint32_t m = (lo + hi) >> 1;
+              if (so[m] < x) lo = m + 1; else hi = m;
+            }
+          }
+          out += lo - rs[j];
+        }
+        pos[b + out] = b + i;
+      }
+      __syncthreads();
+      continue;
     }
+    // general case: bitonic sort of unique keys
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
+      mn = min(mn, so[i]);
+      mx = max(mx, so[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      wmin[warp] = mn;
+      wmax[warp] = mx;
+    }
+    __syncthreads();
+    mn = LLONG_MAX;
+    mx = LLONG_MIN;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+      mn = min(mn, wmin[q]);
+      mx = max(mx, wmax[q]);
+    }
+    if (static_cast<unsigned long long>(mx - mn) >= (1ull << 49)) {
+      if (threadIdx.x == 0) atomicAdd(overflow, 1u);
+      __syncthreads();
+      continue;
+    }
+    unsigned long long* fk = reinterpret_cast<unsigned long long*>(so);
+    for (int32_t i = threadIdx.x; i < P; i += blockDim.x)
+      fk[i] = i < static_cast<int32_t>(L)
+                  ? (static_cast<unsigned long long>(so[i] - mn) << 14) |
+                        static_cast<unsigned long long>(i)
+                  : ~0ull;
+    __syncthreads();
+    for (int32_t kk = 2; kk <= P; kk <<= 1) {
+      for (int32_t j = kk >> 1; j > 0; j >>= 1) {
+        for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+          const int32_t x = i ^ j;
+          if (x > i) {
+            const unsigned long long av = fk[i], cv = fk[x];
+            const bool up = (i & kk) == 0;
+            if ((av > cv) == up) {
+              fk[i] = cv;
+              fk[x] = av;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x)
+      pos[b + i] = b + static_cast<uint32_t>(fk[i] & 0x3fffu);
+    __syncthreads();
   }
-  for (uint32_t i = threadIdx.x; i < L; i += blockDim.x)
-    pos[b + i] = b + static_cast<uint32_t>(fk[i] & 0x3fffu);
 }
 
 // Global fallback: (rank, op - min_op) keys over the whole store.
@@ -325,6 +402,12 @@ __global__ void k_opidx_permute(const uint32_t* __restrict__ idx, uint64_t n,
     d1[i] = d0[k];
     m1[i] = m0[k];
   }
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ v, uint64_t n, uint32_t x) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = x;
 }
 
 __global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
@@ -722,15 +805,17 @@ bool store_build_flow_index(csg_store* s) {
   cudaStream_t st = c->stream;
   const uint64_t n = s->n;
   const int32_t R = s->R;
-  s->fl_unsorted.ensure(static_cast<size_t>(R) + 8);
+  s->fl_unsorted.ensure((static_cast<size_t>(R) + 2) * 4);
   s->fl_pos.ensure(n * 4 + 4);
+  CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4 + 4, st));
   if (!n || !R) {
-    if (R) CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, R, st));
     s->flow_indexed = true;
     return true;
   }
   DevBuf& cnt = c->buf("flow.cnt");
+  DevBuf& list = c->buf("flow.list");
   cnt.ensure(8);
+  list.ensure(static_cast<size_t>(R) * 4 + 4);
   CSG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
   unsigned* d_uns = cnt.as<unsigned>();
   unsigned* d_ovf = d_uns + 1;
@@ -740,11 +825,18 @@ bool store_build_flow_index(csg_store* s) {
   if (!global) {
     {
       ProfScope ps_(c->lc, "k_flow_check", st);
-      k_flow_check<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
-          s->view(), s->fl_unsorted.as<uint8_t>(), d_uns);
+      k_flow_check<<<grid_for(n / 4 + 1), 256, 0, st>>>(
+          s->view(), s->fl_unsorted.as<uint32_t>(), list.as<uint32_t>(), d_uns);
     }
+    // CSG_FLOW_SMEM_CAP (power of two) lowers the shared-memory segment cap
+    // so tests can drive the overflow -> device-wide fallback on small traces
+    static const int32_t cap = [] {
+      const char* e = std::getenv("CSG_FLOW_SMEM_CAP");
+      int32_t v = e ? std::atoi(e) : kFlowSmemMax;
+      return (v >= 64 && v <= kFlowSmemMax) ? v : kFlowSmemMax;
+    }();
     int32_t P = 64;
-    while (static_cast<uint64_t>(P) < s->max_seg && P < kFlowSmemMax) P <<= 1;
+    while (static_cast<uint64_t>(P) < s->max_seg && P < cap) P <<= 1;
     const size_t smem = static_cast<size_t>(P) * 8;
     static bool attr = false;
     if (!attr) {
@@ -754,12 +846,12 @@ bool store_build_flow_index(csg_store* s) {
     }
     {
       ProfScope ps_(c->lc, "k_flow_fix", st);
-      k_flow_fix<<<R, 1024, smem, st>>>(s->view(), s->fl_unsorted.as<uint8_t>(), P,
-                                        s->fl_pos.as<uint32_t>(), d_ovf);
+      k_flow_fix<<<static_cast<unsigned>(std::min<int32_t>(R, 148)), 1024, smem, st>>>(
+          s->view(), list.as<uint32_t>(), d_uns, P, s->fl_pos.as<uint32_t>(), d_ovf);
     }
     // Without a segment longer than the shared-memory sort or a huge op
     // span nothing can overflow: no host round trip on the common path.
-    if (s->max_seg > static_cast<uint64_t>(kFlowSmemMax) || span >= (1ull << 49)) {
+    if (s->max_seg > static_cast<uint64_t>(P) || span >= (1ull << 49)) {
       unsigned h[2];
       CSG_CUDA(cudaMemcpyAsync(h, cnt.p, 8, cudaMemcpyDeviceToHost, st));
       CSG_CUDA(cudaStreamSynchronize(st));
@@ -771,7 +863,10 @@ bool store_build_flow_index(csg_store* s) {
     const int ob = bits_for(span);
     const int rb = bits_for(static_cast<uint64_t>(std::max(R, 1) - 1));
     if (ob + rb > 64) return false;
-    CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 1, R, st));
+    {
+      ProfScope ps_(c->lc, "k_fill_u32", st);
+      k_fill_u32<<<grid_for(R), 256, 0, st>>>(s->fl_unsorted.as<uint32_t>(), R, 1u);
+    }
     if (ob + rb <= 32) {
       s->fl_keys.ensure(n * 4 + 4);
       {

@@ -126,7 +126,7 @@ def test_c2_full_scale_window_matches_reference(eng):
     assert got == rep
 
 
-def shuffled_ops(recs, nranks=10, frac=0.1, seed=7):
+def shuffled_ops(recs, nranks=10, frac=0.1, seed=7, swaps=None):
     """Store-order permutation inside a few ranks: swaps ~frac of the adjacent
     record pairs of each chosen rank, so its op_seq descends in store order
     (the flow index must then permute that segment)."""
@@ -136,23 +136,25 @@ def shuffled_ops(recs, nranks=10, frac=0.1, seed=7):
     ranks = rng.choice(np.unique(recs["rank"]), size=nranks, replace=False)
     for r in ranks:
         idx = np.flatnonzero(out["rank"] == r)
-        for i in rng.choice(len(idx) - 1, size=int(len(idx) * frac), replace=False):
+        k = swaps if swaps is not None else int(len(idx) * frac)
+        for i in rng.choice(len(idx) - 1, size=k, replace=False):
             a, b = idx[i], idx[i + 1]
             out[a], out[b] = out[b].copy(), out[a].copy()
     return out
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["segment", "global"])
+@pytest.mark.parametrize("mode", ["segment", "global", "overflow"])
+@pytest.mark.parametrize("swaps", [3, None])
 @pytest.mark.parametrize("name", ["scenario1", "scenario5", "synth_hang_128"])
-def test_unsorted_flow_segments_match_reference(oracle, name, mode):
+def test_unsorted_flow_segments_match_reference(oracle, name, mode, swaps):
     """Ranks whose op_seq is not monotone in store order: the per-segment
     shared-memory flow sort (and the device-wide radix fallback) against the
     reference run on the same permuted trace."""
     import subprocess
     import sys
     recs, _, _ = golden(name)
-    recs = shuffled_ops(recs)
+    recs = shuffled_ops(recs, swaps=swaps)  # 3 swaps: <= 7 ascending runs (merge path)
     cfg = open(os.path.join(GOLDEN, "configs", name + ".json")).read()
     _, want, _, _ = oracle.run_detection_cfg(cfg, recs)
     import tempfile
@@ -174,6 +176,8 @@ def test_unsorted_flow_segments_match_reference(oracle, name, mode):
         env = dict(os.environ)
         if mode == "global":
             env["CSG_FLOW_GLOBAL_SORT"] = "1"
+        elif mode == "overflow":  # segments longer than the smem sort
+            env["CSG_FLOW_SMEM_CAP"] = "64"
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                            text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
