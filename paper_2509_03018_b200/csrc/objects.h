@@ -53,6 +53,7 @@ struct StoreStats {
   long long min_op, max_op;
   unsigned long long n_nan;
   unsigned long long n_total;  // records over all shards
+  int lmin_rank, lmax_rank;    // this shard's own rank range (not reduced)
 };
 
 struct csg_store {

@@ -2016,21 +2016,38 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       bool p = false;
       for (int q = 0; q < nret && !p; ++q) p = drops(c, key(ret[q]));
       pre[tid] = p;
-      uint32_t row[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (!p)
-        for (int jj = 0; jj < tid; ++jj)
-          if (drops(c, key(ord[base + jj]))) row[jj >> 5] |= 1u << (jj & 31);
-      for (int q = 0; q < 8; ++q) rel[tid][q] = row[q];
+      for (int q = 0; q < 8; ++q) {
+        uint32_t w = 0;
+        if (!p)
+          for (int jj = q * 32; jj < min(q * 32 + 32, tid); ++jj)
+            if (drops(c, key(ord[base + jj]))) w |= 1u << (jj & 31);
+        rel[tid][q] = w;
+      }
     }
     __syncthreads();
-    if (tid == 0) {
-      uint32_t mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (uint32_t i = 0; i < n_in; ++i) {
-        bool dropped = pre[i];
-        for (int q = 0; q < 8 && !dropped; ++q) dropped = (rel[i][q] & mask[q]) != 0;
-        if (!dropped) mask[i >> 5] |= 1u << (i & 31);
+    if (tid < 32) {
+      // In-chunk greedy, one warp: 32-candidate groups in order; a lane is
+      // dropped by kept candidates of earlier groups (final masks, one AND
+      // per word), then the group resolves lane by lane with a ballot-free
+      // broadcast of each lane's verdict.
+      const int lane = tid;
+      for (uint32_t g = 0; g * 32 < n_in; ++g) {
+        const uint32_t i = g * 32 + lane;
+        bool dropped = i >= n_in || pre[i];
+        uint32_t row = 0;
+        if (!dropped) {
+          for (uint32_t q = 0; q < g && !dropped; ++q)
+            dropped = (rel[i][q] & keepmask[q]) != 0;
+          row = rel[i][g];
+        }
+        uint32_t kept = 0;
+        for (int t = 0; t < 32; ++t) {
+          const bool me = !dropped && (row & kept) == 0;
+          if (__shfl_sync(FULL, me ? 1 : 0, t)) kept |= 1u << t;
+        }
+        if (lane == 0) keepmask[g] = kept;
+        __syncwarp();
       }
-      for (int q = 0; q < 8; ++q) keepmask[q] = mask[q];
     }
     __syncthreads();
     const bool k = tid < static_cast<int>(n_in) &&

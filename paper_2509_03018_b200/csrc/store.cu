@@ -25,16 +25,78 @@ __device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long 
   atomicMax(a, v);
 }
 
-// One pass over the packed records: store statistics (max timestamp, rank /
-// channel / op ranges, NaN count) and the (rank, store index) sort pairs.
+// Store statistics accumulated per thread, reduced per block, committed with
+// one set of global atomics per block: max timestamp (ordered key), rank /
+// channel / op ranges, NaN count.
+struct StatAcc {
+  unsigned long long tsk = 0, nan = 0;
+  int mnr = INT_MAX, mxr = INT_MIN, mnc = INT_MAX, mxc = INT_MIN;
+  long long mno = LLONG_MAX, mxo = LLONG_MIN;
+  __device__ void add(double t, long long op, int rank, int chan) {
+    if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
+    mnr = min(mnr, rank);
+    mxr = max(mxr, rank);
+    mnc = min(mnc, chan);
+    mxc = max(mxc, chan);
+    mno = min(mno, op);
+    mxo = max(mxo, op);
+  }
+  __device__ void commit(StoreStats* st) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      tsk = max(tsk, __shfl_xor_sync(0xffffffffu, tsk, o));
+      mnr = min(mnr, __shfl_xor_sync(0xffffffffu, mnr, o));
+      mxr = max(mxr, __shfl_xor_sync(0xffffffffu, mxr, o));
+      mnc = min(mnc, __shfl_xor_sync(0xffffffffu, mnc, o));
+      mxc = max(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
+      mno = min(mno, __shfl_xor_sync(0xffffffffu, mno, o));
+      mxo = max(mxo, __shfl_xor_sync(0xffffffffu, mxo, o));
+      nan += __shfl_xor_sync(0xffffffffu, nan, o);
+    }
+    __shared__ StatAcc sw[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sw[warp] = *this;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        tsk = max(tsk, sw[w].tsk);
+        nan += sw[w].nan;
+        mnr = min(mnr, sw[w].mnr);
+        mxr = max(mxr, sw[w].mxr);
+        mnc = min(mnc, sw[w].mnc);
+        mxc = max(mxc, sw[w].mxc);
+        mno = min(mno, sw[w].mno);
+        mxo = max(mxo, sw[w].mxo);
+      }
+      atomic_max_u64(&st->ts_max_key, tsk);
+      atomicMin(&st->min_rank, mnr);
+      atomicMax(&st->max_rank, mxr);
+      atomicMin(&st->lmin_rank, mnr);
+      atomicMax(&st->lmax_rank, mxr);
+      atomicMin(&st->min_chan, mnc);
+      atomicMax(&st->max_chan, mxc);
+      atomicMin(&st->min_op, mno);
+      atomicMax(&st->max_op, mxo);
+      if (nan) atomicAdd(&st->n_nan, nan);
+    }
+  }
+};
+
+// Fields the index reads from one packed record's first 32 bytes.
+__device__ inline void rec_head(const csg_packed_record* r, uint64_t i, ulonglong2& h0,
+                                ulonglong2& hm) {
+  const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + i);
+  h0 = __ldg(rec);
+  hm = __ldg(rec + 1);
+}
+
+// One pass over the packed records: store statistics and the (rank, store
+// index) sort pairs (general index path, rank spans > kHistDigits).
 __global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n,
                              StoreStats* __restrict__ st,
                              uint32_t* __restrict__ keys,
                              uint32_t* __restrict__ vals) {
-  unsigned long long tsk = 0;
-  int mnr = INT_MAX, mxr = INT_MIN, mnc = INT_MAX, mxc = INT_MIN;
-  long long mno = LLONG_MAX, mxo = LLONG_MIN;
-  unsigned long long nan = 0;
+  StatAcc acc;
   // 4 records in flight per thread (independent 16-byte loads) to keep
   // enough bytes outstanding for HBM.
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -44,11 +106,7 @@ __global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint64_t i = i0 + k * stride;
-      if (i < n) {
-        const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + i);
-        h0[k] = __ldg(rec);
-        hm[k] = __ldg(rec + 1);
-      }
+      if (i < n) rec_head(r, i, h0[k], hm[k]);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -56,67 +114,307 @@ __global__ void k_stats_keys(const csg_packed_record* __restrict__ r, uint64_t n
       if (i >= n) break;
       double t;
       memcpy(&t, &h0[k].x, 8);
-      const long long op = static_cast<long long>(h0[k].y);
       const int rank = static_cast<int>(hm[k].x & 0xffffffffu);
-      const int chan = static_cast<int>(hm[k].y & 0xffffffffu);
-      if (t != t) ++nan; else tsk = max(tsk, (unsigned long long)dkey(t));
-      mnr = min(mnr, rank);
-      mxr = max(mxr, rank);
-      mnc = min(mnc, chan);
-      mxc = max(mxc, chan);
-      mno = min(mno, op);
-      mxo = max(mxo, op);
+      acc.add(t, static_cast<long long>(h0[k].y), rank,
+              static_cast<int>(hm[k].y & 0xffffffffu));
       keys[i] = static_cast<uint32_t>(rank);
       vals[i] = static_cast<uint32_t>(i);
     }
   }
+  acc.commit(st);
+}
+
+// ---- fused rank-major index (rank span <= kHistDigits) ----------------------
+//
+// The reference's RankIndex (proj/src/rca.cpp:77-90: every rank's records in
+// store order) as ONE stable counting-sort pass over 11-bit rank digits:
+//   k_stats_hist  statistics + per-tile digit histogram (digit = rank & 2047),
+//                 written digit-major (L2-resident, 2048 x tiles words)
+//   k_hist_scan*  exclusive scan in (rank - min_rank, tile) order (the
+//                 rotation by min_rank & 2047 makes the digit order the rank
+//                 order for any span <= 2048, e.g. a shard's rank range)
+//   k_scatter     per tile: stable local ranking (warp match_any), digit-
+//                 ordered staging of tile indices in shared memory, then each
+//                 record is read once and written once into the rank-major
+//                 SoA columns in contiguous digit runs.
+constexpr int kHistDigits = 2048;
+constexpr int kTileThreads = 256;
+constexpr int kTileItems = 16;
+constexpr int kTile = kTileThreads * kTileItems;  // 4096 records
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_stats_hist(const csg_packed_record* __restrict__ r, uint64_t n,
+                 StoreStats* __restrict__ st, uint32_t* __restrict__ counts,
+                 uint32_t ntiles) {
+  __shared__ uint32_t hist[kHistDigits];
+  for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads) hist[d] = 0;
+  __syncthreads();
+  StatAcc acc;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTile;
+#pragma unroll 1
+  for (int k0 = 0; k0 < kTileItems; k0 += 4) {
+    ulonglong2 h0[4], hm[4];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    tsk = max(tsk, __shfl_xor_sync(0xffffffffu, tsk, o));
-    mnr = min(mnr, __shfl_xor_sync(0xffffffffu, mnr, o));
-    mxr = max(mxr, __shfl_xor_sync(0xffffffffu, mxr, o));
-    mnc = min(mnc, __shfl_xor_sync(0xffffffffu, mnc, o));
-    mxc = max(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
-    mno = min(mno, __shfl_xor_sync(0xffffffffu, mno, o));
-    mxo = max(mxo, __shfl_xor_sync(0xffffffffu, mxo, o));
-    nan += __shfl_xor_sync(0xffffffffu, nan, o);
-  }
-  // block reduction, then one set of global atomics per block (hundreds of
-  // blocks, not tens of thousands of warps, contend on the 8 counters)
-  __shared__ unsigned long long s_tsk[32], s_nan[32];
-  __shared__ int s_mnr[32], s_mxr[32], s_mnc[32], s_mxc[32];
-  __shared__ long long s_mno[32], s_mxo[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    s_tsk[warp] = tsk;
-    s_nan[warp] = nan;
-    s_mnr[warp] = mnr;
-    s_mxr[warp] = mxr;
-    s_mnc[warp] = mnc;
-    s_mxc[warp] = mxc;
-    s_mno[warp] = mno;
-    s_mxo[warp] = mxo;
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = base + (k0 + k) * kTileThreads + threadIdx.x;
+      if (i < n) rec_head(r, i, h0[k], hm[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = base + (k0 + k) * kTileThreads + threadIdx.x;
+      const bool valid = i < n;
+      double t = 0;
+      int rank = 0;
+      if (valid) {
+        memcpy(&t, &h0[k].x, 8);
+        rank = static_cast<int>(hm[k].x & 0xffffffffu);
+        acc.add(t, static_cast<long long>(h0[k].y), rank,
+                static_cast<int>(hm[k].y & 0xffffffffu));
+      }
+      const uint32_t d = valid ? static_cast<uint32_t>(rank) & (kHistDigits - 1)
+                               : 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (valid && (threadIdx.x & 31) == __ffs(peers) - 1)
+        atomicAdd(&hist[d], __popc(peers));
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      tsk = max(tsk, s_tsk[w]);
-      nan += s_nan[w];
-      mnr = min(mnr, s_mnr[w]);
-      mxr = max(mxr, s_mxr[w]);
-      mnc = min(mnc, s_mnc[w]);
-      mxc = max(mxc, s_mxc[w]);
-      mno = min(mno, s_mno[w]);
-      mxo = max(mxo, s_mxo[w]);
+  for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads)
+    counts[static_cast<uint64_t>(d) * ntiles + blockIdx.x] = hist[d];
+  acc.commit(st);
+}
+
+// Exclusive scan of the virtual array v[i] = counts[((i / T + d0) & 2047) * T
+// + i % T], i < D * T: block sums, then per-block scan with the carried base.
+constexpr int kHScanPer = 4;
+constexpr int kHScanTile = kTileThreads * kHScanPer;  // 1024
+
+__device__ inline uint32_t hv(const uint32_t* counts, uint64_t i, uint32_t T, uint32_t d0) {
+  const uint64_t d = (i / T + d0) & (kHistDigits - 1);
+  return counts[d * T + i % T];
+}
+
+__device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
     }
-    atomic_max_u64(&st->ts_max_key, tsk);
-    atomicMin(&st->min_rank, mnr);
-    atomicMax(&st->max_rank, mxr);
-    atomicMin(&st->min_chan, mnc);
-    atomicMax(&st->max_chan, mxc);
-    atomicMin(&st->min_op, mno);
-    atomicMax(&st->max_op, mxo);
-    if (nan) atomicAdd(&st->n_nan, nan);
+    if (lane < nw) wsum[lane] = s;
+  }
+  __syncthreads();
+  if (total) *total = wsum[nw - 1];
+  const uint32_t before = warp ? wsum[warp - 1] : 0;
+  const uint32_t r = before + x - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_hist_scan_sums(const uint32_t* __restrict__ counts, uint64_t M, uint32_t T,
+                     uint32_t d0, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t wsum[32];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kHScanTile;
+  uint32_t t = 0;
+#pragma unroll
+  for (int k = 0; k < kHScanPer; ++k) {
+    const uint64_t i = base + k * kTileThreads + threadIdx.x;
+    if (i < M) t += hv(counts, i, T, d0);
+  }
+  uint32_t tot;
+  block_excl_scan_u32(t, wsum, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_hist_scan_apply(const uint32_t* __restrict__ counts, uint64_t M, uint32_t T,
+                      uint32_t d0, const uint32_t* __restrict__ sums,
+                      uint32_t* __restrict__ out) {
+  __shared__ uint32_t wsum[32];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kHScanTile +
+                        static_cast<uint64_t>(threadIdx.x) * kHScanPer;
+  uint32_t x[kHScanPer];
+  uint32_t t = 0;
+#pragma unroll
+  for (int k = 0; k < kHScanPer; ++k) {
+    x[k] = base + k < M ? hv(counts, base + k, T, d0) : 0u;
+    t += x[k];
+  }
+  uint32_t run = block_excl_scan_u32(t, wsum, nullptr) + sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kHScanPer; ++k) {
+    if (base + k < M) out[base + k] = run;
+    run += x[k];
+  }
+}
+
+// rank_off over absolute ranks [0, R] from the scanned tile offsets.
+__global__ void k_rank_off_hist(const uint32_t* __restrict__ goff, uint32_t T,
+                                int32_t min_rank, int32_t max_rank, int32_t R,
+                                uint64_t n, uint32_t* __restrict__ off) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > R) return;
+  uint32_t v;
+  if (r < min_rank) v = 0;
+  else if (r > max_rank) v = static_cast<uint32_t>(n);
+  else v = goff[static_cast<uint64_t>(r - min_rank) * T];
+  off[r] = v;
+}
+
+struct ScatterOut {
+  double* ts;
+  int64_t* op;
+  int32_t* comm;
+  int32_t* chan;
+  uint8_t* ko;
+  uint64_t* pa;
+  uint64_t* pb;
+  uint32_t* perm;   // store index per rank-major position
+  uint32_t* rank;   // rank per rank-major position
+};
+
+__global__ void __launch_bounds__(kTileThreads, 3)
+    k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
+              const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
+              int32_t D, ScatterOut o) {
+  constexpr int kW = kTileThreads / 32;
+  extern __shared__ uint16_t wc[];             // [kW][D] per-warp digit counts
+  __shared__ uint32_t bm[kHistDigits];         // global base - tile start
+  __shared__ uint16_t sidx[kTile];             // tile indices in digit order
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kW * D; i += kTileThreads) wc[i] = 0;
+  __syncthreads();
+  const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
+  const uint32_t tn = static_cast<uint32_t>(n - tb < kTile ? n - tb : kTile);
+  // Phase A: digit of every item (warp w owns tile records [512w, 512w+512),
+  // item k of lane l is record 512w + 32k + l: warp order, then k, then lane
+  // is record order), ranked inside the warp with match_any.
+  uint32_t d[kTileItems];
+  uint16_t rk[kTileItems];
+#pragma unroll
+  for (int k = 0; k < kTileItems; ++k) {
+    const uint32_t li = warp * (32 * kTileItems) + k * 32 + lane;
+    d[k] = li < tn ? static_cast<uint32_t>(
+                         __ldg(reinterpret_cast<const int32_t*>(r + tb + li) + 4) - min_rank)
+                   : 0xFFFFFFFFu;
+  }
+  uint16_t* mine = wc + warp * D;
+#pragma unroll
+  for (int k = 0; k < kTileItems; ++k) {
+    const bool valid = d[k] != 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d[k]);
+    const uint32_t before = valid ? mine[d[k]] : 0u;
+    rk[k] = static_cast<uint16_t>(before + __popc(peers & ((1u << lane) - 1u)));
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1)
+      mine[d[k]] = static_cast<uint16_t>(before + __popc(peers));
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: cross-warp prefix + tile digit start (block scan) folded into
+  // the warp counters; bm = global base of the tile's run - its tile start
+  uint32_t carry = 0;
+  for (int d0 = 0; d0 < D; d0 += kTileThreads) {
+    const int dd = d0 + tid;
+    uint32_t tot = 0;
+    uint16_t pre[kW];
+    if (dd < D) {
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        pre[w] = static_cast<uint16_t>(tot);
+        tot += wc[w * D + dd];
+      }
+    }
+    uint32_t all;
+    const uint32_t ts0 = carry + block_excl_scan_u32(tot, wsum, &all);
+    if (dd < D) {
+#pragma unroll
+      for (int w = 0; w < kW; ++w) wc[w * D + dd] = static_cast<uint16_t>(ts0 + pre[w]);
+      bm[dd] = goff[static_cast<uint64_t>(dd) * T + blockIdx.x] - ts0;
+    }
+    carry += all;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kTileItems; ++k)
+    if (d[k] != 0xFFFFFFFFu)
+      sidx[mine[d[k]] + rk[k]] =
+          static_cast<uint16_t>(warp * (32 * kTileItems) + k * 32 + lane);
+  __syncthreads();
+  // Phase B: digit order; consecutive threads write consecutive positions of
+  // one digit run.
+  for (uint32_t p = tid; p < tn; p += kTileThreads) {
+    const uint32_t li = sidx[p];
+    const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + tb + li);
+    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1), h1 = __ldg(rec + 2);
+    const int32_t rank = static_cast<int32_t>(hm.x & 0xffffffffu);
+    const uint32_t q = bm[static_cast<uint32_t>(rank - min_rank)] + p;
+    double t;
+    memcpy(&t, &h0.x, 8);
+    o.ts[q] = t;
+    o.op[q] = static_cast<int64_t>(h0.y);
+    o.comm[q] = static_cast<int32_t>(hm.x >> 32);
+    o.chan[q] = static_cast<int32_t>(hm.y & 0xffffffffu);
+    const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
+    const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
+    o.ko[q] = static_cast<uint8_t>((kind & 1) | (name << 1));
+    o.pa[q] = h1.x;
+    o.pb[q] = (kind & 1) ? (h1.y & 0xffffffffull) : h1.y;
+    o.perm[q] = static_cast<uint32_t>(tb + li);
+    o.rank[q] = static_cast<uint32_t>(rank);
+  }
+}
+
+// Per-rank running max of ts: one block per rank segment, the segment split
+// into one contiguous part per warp; part maxima exchanged through shared
+// memory give every warp its carry-in (all warps of all ranks stream at
+// once instead of one warp walking a whole segment).
+__global__ void __launch_bounds__(1024)
+    k_runmax_blk(const double* __restrict__ ts, const uint32_t* __restrict__ off,
+                 double* __restrict__ out) {
+  __shared__ double pmax[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const uint32_t b = off[blockIdx.x], e = off[blockIdx.x + 1];
+  const uint32_t L = e - b;
+  const uint32_t per = ((L + nw - 1) / nw + 31) & ~31u;
+  const uint32_t pb = min(e, b + warp * per), pe = min(e, pb + per);
+  double m = -INFINITY;
+  for (uint32_t p = pb + lane; p < pe; p += 32) {
+    const double x = __ldg(ts + p);
+    if (x == x) m = fmax(m, x);  // NaN never breaks a prefix
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) pmax[warp] = m;
+  __syncthreads();
+  double carry = -INFINITY;
+  for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
+  for (uint32_t base = pb; base < pe; base += 32) {
+    const uint32_t p = base + lane;
+    double x = p < pe ? __ldg(ts + p) : -INFINITY;
+    if (x != x) x = -INFINITY;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = fmax(x, y);
+    }
+    x = fmax(x, carry);
+    carry = __shfl_sync(0xffffffffu, x, 31);
+    if (p < pe) out[p] = x;
   }
 }
 
@@ -159,41 +457,6 @@ __global__ void k_gather(const csg_packed_record* __restrict__ r,
     pa[p] = h1.x;  // start_ms bits | ready | tx << 32
     pb[p] = h1.y;  // msg_bytes | done (| reserved << 32)
     if (kind & 1) pb[p] = h1.y & 0xffffffffull;
-  }
-}
-
-// Per-rank inclusive running max of ts: one warp per rank, 8 chunks of 32
-// records loaded per step (independent loads in flight), scanned in
-// registers with the carry chained through the chunks.
-__global__ void k_runmax(const double* __restrict__ ts,
-                         const uint32_t* __restrict__ off, int32_t R,
-                         double* __restrict__ out) {
-  constexpr int kChunks = 8;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= R) return;
-  const uint32_t b = off[w], e = off[w + 1];
-  double carry = -INFINITY;
-  for (uint32_t base = b; base < e; base += 32 * kChunks) {
-    double x[kChunks];
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) {
-      const uint32_t p = base + k * 32 + lane;
-      x[k] = p < e ? __ldg(ts + p) : -INFINITY;
-      if (x[k] != x[k]) x[k] = -INFINITY;  // NaN never breaks a prefix
-    }
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) {
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, x[k], o);
-        if (lane >= o) x[k] = fmax(x[k], y);
-      }
-      x[k] = fmax(x[k], carry);
-      carry = __shfl_sync(0xffffffffu, x[k], 31);
-      const uint32_t p = base + k * 32 + lane;
-      if (p < e) out[p] = x[k];
-    }
   }
 }
 
@@ -560,17 +823,20 @@ void store_build_index(csg_store* s) {
   h.min_op = INT64_MAX;
   h.max_op = INT64_MIN;
   h.n_total = n;
+  h.lmin_rank = INT32_MAX;
+  h.lmax_rank = INT32_MIN;
   s->stats_dev.ensure(sizeof(StoreStats));
   CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
                            cudaMemcpyHostToDevice, st));
   s->perm.ensure(n * 4 + 4);
   s->keys.ensure(n * 4 + 4);
+  const uint32_t ntiles = static_cast<uint32_t>((n + kTile - 1) / kTile);
+  DevBuf& hcnt = c->buf("index.hist");
+  hcnt.ensure(static_cast<size_t>(kHistDigits) * ntiles * 4 + 4);
   if (n) {
-    ProfScope ps_(c->lc, "k_stats_keys", st);
-    const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, 148ull * 8));
-    k_stats_keys<<<g, 256, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
-                                              s->keys.as<uint32_t>(),
-                                              s->perm.as<uint32_t>());
+    ProfScope ps_(c->lc, "k_stats_hist", st);
+    k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
+                                                  hcnt.as<uint32_t>(), ntiles);
   }
   if (comm_active(c)) {
     // global stats over the shards (identical rank space, ticks, op range)
@@ -625,30 +891,84 @@ void store_build_index(csg_store* s) {
   s->ko.ensure(n + 8);
   s->pa.ensure(n * 8 + 8);
   s->pb.ensure(n * 8 + 8);
-  if (n) {
-    radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
-                   bits_for(static_cast<uint64_t>(R > 0 ? R - 1 : 0)), s->sort,
-                   st, c->lc);
+  static const bool force_general = std::getenv("CSG_INDEX_RADIX") != nullptr;
+  const bool fused = n && !force_general &&
+                     static_cast<int64_t>(h.lmax_rank) - h.lmin_rank < kHistDigits;
+  if (fused) {
+    // one stable counting-sort pass over the rank digits (see k_scatter)
+    const int32_t lmin = h.lmin_rank;
+    const int32_t D = h.lmax_rank - lmin + 1;
+    const uint64_t M = static_cast<uint64_t>(D) * ntiles;
+    const uint32_t d0 = static_cast<uint32_t>(lmin) & (kHistDigits - 1);
+    DevBuf& goff = c->buf("index.goff");
+    DevBuf& sums = c->buf("index.sums");
+    goff.ensure(M * 4 + 4);
+    const uint64_t nb = (M + kHScanTile - 1) / kHScanTile;
+    sums.ensure(nb * 4 + 4);
     {
-      ProfScope ps_(c->lc, "k_gather", st);
-      k_gather<<<grid_for(n), 256, 0, st>>>(
-          recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
-          s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
-          s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
+      ProfScope ps_(c->lc, "k_hist_scan_sums", st);
+      k_hist_scan_sums<<<static_cast<unsigned>(nb), kTileThreads, 0, st>>>(
+          hcnt.as<uint32_t>(), M, ntiles, d0, sums.as<uint32_t>());
     }
-  }
-  {
-    ProfScope ps_(c->lc, "k_rank_off", st);
-    k_rank_off<<<(R + 1 + 255) / 256, 256, 0, st>>>(s->keys.as<uint32_t>(), n, R,
-                                                   s->rank_off.as<uint32_t>());
+    exclusive_scan_u32(sums.as<uint32_t>(), nb, c->scratch_a, st, c->lc);
+    {
+      ProfScope ps_(c->lc, "k_hist_scan_apply", st);
+      k_hist_scan_apply<<<static_cast<unsigned>(nb), kTileThreads, 0, st>>>(
+          hcnt.as<uint32_t>(), M, ntiles, d0, sums.as<uint32_t>(), goff.as<uint32_t>());
+    }
+    ScatterOut o{s->ts.as<double>(), s->op.as<int64_t>(), s->comm.as<int32_t>(),
+                 s->chan.as<int32_t>(), s->ko.as<uint8_t>(), s->pa.as<uint64_t>(),
+                 s->pb.as<uint64_t>(), s->perm.as<uint32_t>(), s->keys.as<uint32_t>()};
+    const size_t smem = static_cast<size_t>(kTileThreads / 32) * D * 2;
+    static bool attr = false;
+    if (!attr) {
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (kTileThreads / 32) * kHistDigits * 2));
+      attr = true;
+    }
+    {
+      ProfScope ps_(c->lc, "k_scatter", st);
+      k_scatter<<<ntiles, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
+                                                   lmin, D, o);
+    }
+    {
+      ProfScope ps_(c->lc, "k_rank_off", st);
+      k_rank_off_hist<<<(R + 1 + 255) / 256, 256, 0, st>>>(
+          goff.as<uint32_t>(), ntiles, lmin, h.lmax_rank, R, n, s->rank_off.as<uint32_t>());
+    }
+  } else {
+    // general path: (rank, store index) pairs, LSD radix sort, gather
+    if (n) {
+      DevBuf& st2 = c->buf("index.stats2");
+      st2.ensure(sizeof(StoreStats));
+      CSG_CUDA(cudaMemcpyAsync(st2.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+      ProfScope ps_(c->lc, "k_stats_keys", st);
+      const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, 148ull * 8));
+      k_stats_keys<<<g, 256, 0, st>>>(recs, n, st2.as<StoreStats>(), s->keys.as<uint32_t>(),
+                                      s->perm.as<uint32_t>());
+    }
+    if (n) {
+      radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
+                     bits_for(static_cast<uint64_t>(R > 0 ? R - 1 : 0)), s->sort,
+                     st, c->lc);
+      {
+        ProfScope ps_(c->lc, "k_gather", st);
+        k_gather<<<grid_for(n), 256, 0, st>>>(
+            recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
+            s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
+            s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
+      }
+    }
+    {
+      ProfScope ps_(c->lc, "k_rank_off", st);
+      k_rank_off<<<(R + 1 + 255) / 256, 256, 0, st>>>(s->keys.as<uint32_t>(), n, R,
+                                                     s->rank_off.as<uint32_t>());
+    }
   }
   if (n && R) {
-    {
-      ProfScope ps_(c->lc, "k_runmax", st);
-      k_runmax<<<(static_cast<uint64_t>(R) * 32 + 255) / 256, 256, 0, st>>>(
-          s->ts.as<double>(), s->rank_off.as<uint32_t>(), R,
-          s->runmax.as<double>());
-    }
+    ProfScope ps_(c->lc, "k_runmax", st);
+    k_runmax_blk<<<R, 1024, 0, st>>>(s->ts.as<double>(), s->rank_off.as<uint32_t>(),
+                                     s->runmax.as<double>());
   }
   {
     std::vector<uint32_t> ro(static_cast<size_t>(R) + 1);
