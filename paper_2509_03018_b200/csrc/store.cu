@@ -285,96 +285,193 @@ struct ScatterOut {
   uint32_t* rank;   // rank per rank-major position
 };
 
-__global__ void __launch_bounds__(kTileThreads, 3)
+// --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
+__device__ inline uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ inline void mbar_init(unsigned long long* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ inline void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                 unsigned long long* m) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+      "r"(bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m))
+      : "memory");
+}
+__device__ inline void mbar_wait(unsigned long long* m, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(m)), "r"(parity)
+        : "memory");
+  }
+}
+
+// Persistent scatter: every block walks its histogram tiles (kTile records)
+// as sub-tiles of 256 x ITEMS records, double-buffered in shared memory by
+// bulk async copies, so each packed record is read from HBM exactly once and
+// coalesced. Per sub-tile: digits from shared memory, stable warp ranking
+// (match_any), digit-ordered staging of sub-tile indices, then every record
+// is written once into the rank-major SoA columns in contiguous digit runs.
+// bx[d] carries the running global base of digit d through the sub-tiles of
+// one histogram tile.
+template <int ITEMS>
+__global__ void __launch_bounds__(kTileThreads, 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
               int32_t D, ScatterOut o) {
   constexpr int kW = kTileThreads / 32;
-  extern __shared__ uint16_t wc[];             // [kW][D] per-warp digit counts
-  __shared__ uint32_t bm[kHistDigits];         // global base - tile start
-  __shared__ uint16_t sidx[kTile];             // tile indices in digit order
+  constexpr int TR = kTileThreads * ITEMS;
+  constexpr int SUB = kTile / TR;
+  constexpr int kMaxPer = kHistDigits / kTileThreads;  // digits per thread
+  extern __shared__ __align__(128) unsigned char dyn[];
+  unsigned char* buf0 = dyn;
+  uint16_t* wc = reinterpret_cast<uint16_t*>(dyn + 2 * TR * 48);  // [kW][D]
+  uint32_t* bx = reinterpret_cast<uint32_t*>(wc + kW * ((D + 1) & ~1));
+  __shared__ uint16_t sidx[TR];
   __shared__ uint32_t wsum[32];
+  __shared__ __align__(8) unsigned long long mbar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kW * D; i += kTileThreads) wc[i] = 0;
-  __syncthreads();
-  const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
-  const uint32_t tn = static_cast<uint32_t>(n - tb < kTile ? n - tb : kTile);
-  // Phase A: digit of every item (warp w owns tile records [512w, 512w+512),
-  // item k of lane l is record 512w + 32k + l: warp order, then k, then lane
-  // is record order), ranked inside the warp with match_any.
-  uint32_t d[kTileItems];
-  uint16_t rk[kTileItems];
-#pragma unroll
-  for (int k = 0; k < kTileItems; ++k) {
-    const uint32_t li = warp * (32 * kTileItems) + k * 32 + lane;
-    d[k] = li < tn ? static_cast<uint32_t>(
-                         __ldg(reinterpret_cast<const int32_t*>(r + tb + li) + 4) - min_rank)
-                   : 0xFFFFFFFFu;
-  }
-  uint16_t* mine = wc + warp * D;
-#pragma unroll
-  for (int k = 0; k < kTileItems; ++k) {
-    const bool valid = d[k] != 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xffffffffu, d[k]);
-    const uint32_t before = valid ? mine[d[k]] : 0u;
-    rk[k] = static_cast<uint16_t>(before + __popc(peers & ((1u << lane) - 1u)));
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1)
-      mine[d[k]] = static_cast<uint16_t>(before + __popc(peers));
-    __syncwarp();
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
   }
   __syncthreads();
-  // per digit: cross-warp prefix + tile digit start (block scan) folded into
-  // the warp counters; bm = global base of the tile's run - its tile start
-  uint32_t carry = 0;
-  for (int d0 = 0; d0 < D; d0 += kTileThreads) {
-    const int dd = d0 + tid;
-    uint32_t tot = 0;
-    uint16_t pre[kW];
-    if (dd < D) {
+  auto sub_of = [&](uint32_t j, uint32_t& t, uint64_t& first, uint32_t& cnt) {
+    t = blockIdx.x + (j / SUB) * gridDim.x;
+    first = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(j % SUB) * TR;
+    cnt = first < n ? static_cast<uint32_t>(n - first < static_cast<uint64_t>(TR) ? n - first : static_cast<uint64_t>(TR)) : 0u;
+    return t < T;
+  };
+  auto issue = [&](uint32_t j) {
+    uint32_t t, cnt;
+    uint64_t first;
+    if (tid == 0 && sub_of(j, t, first, cnt) && cnt)
+      bulk_load(buf0 + (j & 1) * TR * 48, r + first, cnt * 48, &mbar[j & 1]);
+  };
+  uint32_t par0 = 0, par1 = 0;
+  issue(0);
+  for (uint32_t j = 0;; ++j) {
+    uint32_t t, cnt;
+    uint64_t first;
+    if (!sub_of(j, t, first, cnt)) break;
+    issue(j + 1);  // its buffer was released by the barrier ending j - 1
+    if (j % SUB == 0)
+      for (int dd = tid; dd < D; dd += kTileThreads)
+        bx[dd] = goff[static_cast<uint64_t>(dd) * T + t];
+    if (cnt == 0) {
+      __syncthreads();
+      continue;
+    }
+    const unsigned char* sb = buf0 + (j & 1) * TR * 48;
+    for (int i = tid; i < kW * D; i += kTileThreads) wc[i] = 0;
+    if (j & 1) {
+      mbar_wait(&mbar[1], par1);
+      par1 ^= 1;
+    } else {
+      mbar_wait(&mbar[0], par0);
+      par0 ^= 1;
+    }
+    __syncthreads();
+    // Phase A: warp w owns sub-tile records [32*ITEMS*w, 32*ITEMS*(w+1)),
+    // item k of lane l is record 32*ITEMS*w + 32k + l (record order).
+    uint32_t d[ITEMS];
+    uint16_t rk[ITEMS];
 #pragma unroll
-      for (int w = 0; w < kW; ++w) {
-        pre[w] = static_cast<uint16_t>(tot);
-        tot += wc[w * D + dd];
+    for (int k = 0; k < ITEMS; ++k) {
+      const uint32_t li = warp * (32 * ITEMS) + k * 32 + lane;
+      d[k] = li < cnt ? static_cast<uint32_t>(
+                            *reinterpret_cast<const int32_t*>(sb + li * 48 + 16) - min_rank)
+                      : 0xFFFFFFFFu;
+    }
+    uint16_t* mine = wc + warp * D;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const bool valid = d[k] != 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d[k]);
+      const uint32_t before = valid ? mine[d[k]] : 0u;
+      rk[k] = static_cast<uint16_t>(before + __popc(peers & ((1u << lane) - 1u)));
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1)
+        mine[d[k]] = static_cast<uint16_t>(before + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit: cross-warp prefix + sub-tile start folded into the warp
+    // counters; bx becomes (running base - sub-tile start) for phase B
+    uint32_t nxt[kMaxPer];
+    uint32_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int dd = i * kTileThreads + tid;
+      if (i * kTileThreads >= D) break;  // block-uniform
+      uint32_t tot = 0;
+      uint16_t pre[kW];
+      if (dd < D) {
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+          pre[w] = static_cast<uint16_t>(tot);
+          tot += wc[w * D + dd];
+        }
       }
-    }
-    uint32_t all;
-    const uint32_t ts0 = carry + block_excl_scan_u32(tot, wsum, &all);
-    if (dd < D) {
+      uint32_t all;
+      const uint32_t ts0 = carry + block_excl_scan_u32(tot, wsum, &all);
+      if (dd < D) {
 #pragma unroll
-      for (int w = 0; w < kW; ++w) wc[w * D + dd] = static_cast<uint16_t>(ts0 + pre[w]);
-      bm[dd] = goff[static_cast<uint64_t>(dd) * T + blockIdx.x] - ts0;
+        for (int w = 0; w < kW; ++w) wc[w * D + dd] = static_cast<uint16_t>(ts0 + pre[w]);
+        const uint32_t rb = bx[dd];
+        nxt[i] = rb + tot;
+        bx[dd] = rb - ts0;
+      }
+      carry += all;
     }
-    carry += all;
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kTileItems; ++k)
-    if (d[k] != 0xFFFFFFFFu)
-      sidx[mine[d[k]] + rk[k]] =
-          static_cast<uint16_t>(warp * (32 * kTileItems) + k * 32 + lane);
-  __syncthreads();
-  // Phase B: digit order; consecutive threads write consecutive positions of
-  // one digit run.
-  for (uint32_t p = tid; p < tn; p += kTileThreads) {
-    const uint32_t li = sidx[p];
-    const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(r + tb + li);
-    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1), h1 = __ldg(rec + 2);
-    const int32_t rank = static_cast<int32_t>(hm.x & 0xffffffffu);
-    const uint32_t q = bm[static_cast<uint32_t>(rank - min_rank)] + p;
-    double t;
-    memcpy(&t, &h0.x, 8);
-    o.ts[q] = t;
-    o.op[q] = static_cast<int64_t>(h0.y);
-    o.comm[q] = static_cast<int32_t>(hm.x >> 32);
-    o.chan[q] = static_cast<int32_t>(hm.y & 0xffffffffu);
-    const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
-    const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
-    o.ko[q] = static_cast<uint8_t>((kind & 1) | (name << 1));
-    o.pa[q] = h1.x;
-    o.pb[q] = (kind & 1) ? (h1.y & 0xffffffffull) : h1.y;
-    o.perm[q] = static_cast<uint32_t>(tb + li);
-    o.rank[q] = static_cast<uint32_t>(rank);
+    for (int k = 0; k < ITEMS; ++k)
+      if (d[k] != 0xFFFFFFFFu)
+        sidx[mine[d[k]] + rk[k]] = static_cast<uint16_t>(warp * (32 * ITEMS) + k * 32 + lane);
+    __syncthreads();
+    // Phase B: digit order; consecutive threads write consecutive positions
+    // of one digit run.
+    for (uint32_t p = tid; p < cnt; p += kTileThreads) {
+      const uint32_t li = sidx[p];
+      const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(sb + li * 48);
+      const ulonglong2 h0 = rec[0], hm = rec[1], h1 = rec[2];
+      const int32_t rank = static_cast<int32_t>(hm.x & 0xffffffffu);
+      const uint32_t q = bx[static_cast<uint32_t>(rank - min_rank)] + p;
+      double tv;
+      memcpy(&tv, &h0.x, 8);
+      o.ts[q] = tv;
+      o.op[q] = static_cast<int64_t>(h0.y);
+      o.comm[q] = static_cast<int32_t>(hm.x >> 32);
+      o.chan[q] = static_cast<int32_t>(hm.y & 0xffffffffu);
+      const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
+      const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
+      o.ko[q] = static_cast<uint8_t>((kind & 1) | (name << 1));
+      o.pa[q] = h1.x;
+      o.pb[q] = (kind & 1) ? (h1.y & 0xffffffffull) : h1.y;
+      o.perm[q] = static_cast<uint32_t>(first + li);
+      o.rank[q] = static_cast<uint32_t>(rank);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int dd = i * kTileThreads + tid;
+      if (i * kTileThreads >= D) break;
+      if (dd < D) bx[dd] = nxt[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -919,17 +1016,28 @@ void store_build_index(csg_store* s) {
     ScatterOut o{s->ts.as<double>(), s->op.as<int64_t>(), s->comm.as<int32_t>(),
                  s->chan.as<int32_t>(), s->ko.as<uint8_t>(), s->pa.as<uint64_t>(),
                  s->pb.as<uint64_t>(), s->perm.as<uint32_t>(), s->keys.as<uint32_t>()};
-    const size_t smem = static_cast<size_t>(kTileThreads / 32) * D * 2;
+    // sub-tiles of 2048 records (1024 when the digit span needs the room)
+    const bool wide = D > 1024;
+    const int TR = wide ? 1024 : 2048;
+    const size_t smem = 2ull * TR * 48 + (kTileThreads / 32) * ((D + 1) & ~1) * 2 +
+                        static_cast<size_t>(D) * 4;
     static bool attr = false;
     if (!attr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (kTileThreads / 32) * kHistDigits * 2));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * 1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
       attr = true;
     }
+    const unsigned grid = std::min<unsigned>(ntiles, 148);
     {
       ProfScope ps_(c->lc, "k_scatter", st);
-      k_scatter<<<ntiles, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
-                                                   lmin, D, o);
+      if (wide)
+        k_scatter<4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
+                                                       lmin, D, o);
+      else
+        k_scatter<8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
+                                                       lmin, D, o);
     }
     {
       ProfScope ps_(c->lc, "k_rank_off", st);
