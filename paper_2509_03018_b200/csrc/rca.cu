@@ -1839,13 +1839,10 @@ struct ExoKey {
   uint32_t known;
   uint64_t done, tx, ready;
 };
-constexpr size_t kExoStageBytes = kExoStage * (sizeof(ExoKey) + 8);
+constexpr size_t kExoStageBytes = kExoStage * (sizeof(ExoKey) + 4);
 
 __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   extern __shared__ __align__(16) unsigned long long exo_dyn[];
-  __shared__ uint32_t rel[256][8];
-  __shared__ uint8_t pre[256];
-  __shared__ uint32_t keepmask[8];
   __shared__ int32_t sh_i[8];
   __shared__ unsigned long long sh_u[2];
   __shared__ uint32_t wsum[16];
@@ -1880,7 +1877,6 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   int64_t* U = reinterpret_cast<int64_t*>(sp + ((P * 4 + 15) & ~15u));
   uint32_t* ret_g = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(U) +
                                                 ((C * 8 + 15) & ~15u));
-  uint32_t* ret = staged ? ord + kExoStage : ret_g;
   uint8_t* keep = reinterpret_cast<uint8_t*>(ret_g) + ((C * 4 + 15) & ~15u);
   const uint32_t Rs = static_cast<uint32_t>(a.s.R > 0 ? a.s.R : 1);
   uint32_t* minpos = reinterpret_cast<uint32_t*>(keep + ((C + 15) & ~15u));
@@ -1996,76 +1992,119 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       }
     }
   }
-  auto drops = [&](const ExoKey& c, const ExoKey& u) {
-    if (u.rank == c.rank) return false;
-    if (u.op == c.op)
-      return u.known && c.known && prog_less(u.done, u.tx, u.ready, c.done, c.tx, c.ready);
-    if (c.op < 0 || u.op < 0 || K < 2) return false;
-    const int l = cidx[u.op - lo];
-    return ((bits[(c.op - lo) * words + (l >> 6)] >> (l & 63)) & 1ull) != 0;
-  };
-  // 3. greedy exoneration (rca.cpp:487-514) in chunks of 256: drops by
-  //    retained candidates of earlier chunks in parallel, then the in-chunk
-  //    order resolved with bit masks by one thread.
-  int nret = 0;
-  for (uint32_t base = 0; base < C; base += 256) {
-    const uint32_t n_in = min(256u, C - base);
-    const int nwg = 8;  // warps taking part in the 256-wide chunk
-    if (tid < static_cast<int>(n_in)) {
-      const ExoKey c = key(ord[base + tid]);
-      bool p = false;
-      for (int q = 0; q < nret && !p; ++q) p = drops(c, key(ret[q]));
-      pre[tid] = p;
-      for (int q = 0; q < 8; ++q) {
-        uint32_t w = 0;
-        if (!p)
-          for (int jj = q * 32; jj < min(q * 32 + 32, tid); ++jj)
-            if (drops(c, key(ord[base + jj]))) w |= 1u << (jj & 31);
-        rel[tid][q] = w;
-      }
-    }
-    __syncthreads();
-    if (tid < 32) {
-      // In-chunk greedy, one warp: 32-candidate groups in order; a lane is
-      // dropped by kept candidates of earlier groups (final masks, one AND
-      // per word), then the group resolves lane by lane with a ballot-free
-      // broadcast of each lane's verdict.
-      const int lane = tid;
-      for (uint32_t g = 0; g * 32 < n_in; ++g) {
-        const uint32_t i = g * 32 + lane;
-        bool dropped = i >= n_in || pre[i];
-        uint32_t row = 0;
-        if (!dropped) {
-          for (uint32_t q = 0; q < g && !dropped; ++q)
-            dropped = (rel[i][q] & keepmask[q]) != 0;
-          row = rel[i][g];
+  // 3. greedy exoneration (rca.cpp:487-514). In (op, rank) order a
+  //    candidate c is dropped by an already-retained u of another rank when
+  //    u has the same op and strictly less progress (done, tx, ready), or
+  //    when c's op depends on u's op. Both relations only look backwards in
+  //    op order, so the sweep runs op group by op group (one warp):
+  //    * dependency drops: a group's candidates test, in parallel, the
+  //      ancestor bitset of their op against a summary of every earlier
+  //      group's retained ranks (rsum[l]: -1 none, the single rank, or -2
+  //      for two or more ranks; NE / MU bitsets of non-empty / multi-rank
+  //      groups), i.e. "some retained u there has a rank != c.rank";
+  //    * same-op drops: the group walks in rank order keeping the least
+  //      retained progress m1 (rank rk1) and the least progress of a retained
+  //      rank != rk1 (m2); c is dropped iff the least retained progress among
+  //      OTHER ranks is below its own.
+  //    Exactly the reference's O(C x retained) greedy, in O(C + K) steps.
+  constexpr int kMaskWords = 64;
+  __shared__ unsigned long long NE[kMaskWords], MU[kMaskWords];
+  int32_t* rsum = reinterpret_cast<int32_t*>(ret_g);  // [K] retained-rank summary
+  if (tid < 32) {
+    const int lane = tid;
+    const bool masks = words <= kMaskWords;
+    for (int l = lane; l < K; l += 32) rsum[l] = -1;
+    for (int w = lane; w < kMaskWords; w += 32) NE[w] = MU[w] = 0;
+    __syncwarp();
+    auto plt = [](uint64_t d0, uint64_t t0, uint64_t r0, uint64_t d1, uint64_t t1,
+                  uint64_t r1) { return prog_less(d0, t0, r0, d1, t1, r1); };
+    uint32_t x = 0;
+    while (x < C) {
+      const int64_t op = key(ord[x]).op;
+      // group end: first sorted position with a different op
+      uint32_t y = x + 1;
+      for (uint32_t b0 = x + 1; b0 < C; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        const unsigned mm = __ballot_sync(FULL, i < C && key(ord[i]).op != op);
+        if (mm) {
+          y = b0 + __ffs(mm) - 1;
+          break;
         }
-        uint32_t kept = 0;
-        for (int t = 0; t < 32; ++t) {
-          const bool me = !dropped && (row & kept) == 0;
-          if (__shfl_sync(FULL, me ? 1 : 0, t)) kept |= 1u << t;
-        }
-        if (lane == 0) keepmask[g] = kept;
-        __syncwarp();
+        y = min(C, b0 + 32);
       }
+      const bool dag = op >= 0 && K >= 2;
+      const int g = dag ? cidx[op - lo] : -1;
+      const unsigned long long* row = dag ? bits + (op - lo) * words : nullptr;
+      const uint64_t INF = ~0ull;
+      uint64_t m1d = INF, m1t = INF, m1r = INF, m2d = INF, m2t = INF, m2r = INF;
+      int32_t rk1 = INT_MIN;
+      int32_t gs = -1;  // this group's retained-rank summary
+      for (uint32_t base = x; base < y; base += 32) {
+        const uint32_t i = base + lane;
+        bool dd = false;
+        if (i < y && dag) {
+          const int32_t r = key(ord[i]).rank;
+          for (int w = 0; w < words && !dd; ++w) {
+            unsigned long long av = row[w];
+            if (masks) {
+              if (av & MU[w]) {
+                dd = true;
+                break;
+              }
+              av &= NE[w];
+            }
+            while (av && !dd) {
+              const int l = w * 64 + __ffsll(av) - 1;
+              const int32_t q = rsum[l];
+              dd = q != -1 && q != r;
+              av &= av - 1;
+            }
+          }
+        }
+        const uint32_t nt = min(32u, y - base);
+        for (uint32_t t = 0; t < nt; ++t) {
+          const bool ddt = __shfl_sync(FULL, dd ? 1 : 0, t) != 0;
+          const ExoKey c = key(ord[base + t]);
+          bool kept = !ddt;
+          if (kept && c.known) {
+            if (rk1 != c.rank) kept = !plt(m1d, m1t, m1r, c.done, c.tx, c.ready);
+            else kept = !plt(m2d, m2t, m2r, c.done, c.tx, c.ready);
+          }
+          if (lane == 0) keep[base + t] = kept ? 1 : 0;
+          if (kept) {
+            gs = gs == -1 ? c.rank : (gs == c.rank ? gs : -2);
+            if (c.known) {
+              if (plt(c.done, c.tx, c.ready, m1d, m1t, m1r)) {
+                if (c.rank != rk1) {
+                  m2d = m1d;
+                  m2t = m1t;
+                  m2r = m1r;
+                }
+                m1d = c.done;
+                m1t = c.tx;
+                m1r = c.ready;
+                rk1 = c.rank;
+              } else if (c.rank != rk1 && plt(c.done, c.tx, c.ready, m2d, m2t, m2r)) {
+                m2d = c.done;
+                m2t = c.tx;
+                m2r = c.ready;
+              }
+            }
+          }
+        }
+      }
+      if (g >= 0 && lane == 0) {
+        rsum[g] = gs;
+        if (masks && gs != -1) {
+          NE[g >> 6] |= 1ull << (g & 63);
+          if (gs == -2) MU[g >> 6] |= 1ull << (g & 63);
+        }
+      }
+      __syncwarp();
+      x = y;
     }
-    __syncthreads();
-    const bool k = tid < static_cast<int>(n_in) &&
-                   ((keepmask[tid >> 5] >> (tid & 31)) & 1u);
-    if (tid < static_cast<int>(n_in)) keep[base + tid] = k ? 1 : 0;
-    // ordered append of this chunk's retained candidates
-    const unsigned bm = __ballot_sync(FULL, k);
-    if ((tid & 31) == 0 && (tid >> 5) < nwg) wsum[tid >> 5] = __popc(bm);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int q = 0; q < nwg; ++q) {
-      if (q < (tid >> 5)) before += wsum[q];
-      total += wsum[q];
-    }
-    if (k) ret[nret + before + __popc(bm & ((1u << (tid & 31)) - 1u))] = ord[base + tid];
-    nret += total;
-    __syncthreads();
   }
+  __syncthreads();
   // 4. report: exonerated in sorted order; suspects = first retained entry
   //    per rank (its evidence in that order); suspects sorted by rank.
   const int32_t R = a.s.R > 0 ? a.s.R : 1;

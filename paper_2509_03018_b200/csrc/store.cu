@@ -367,10 +367,21 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     uint64_t first;
     if (!sub_of(j, t, first, cnt)) break;
     issue(j + 1);  // its buffer was released by the barrier ending j - 1
-    if (j % SUB == 0)
-      for (int dd = tid; dd < D; dd += kTileThreads)
-        bx[dd] = goff[static_cast<uint64_t>(dd) * T + t];
+    // a new histogram tile starts from its scanned global bases: loaded now,
+    // consumed after phase A (latency hidden)
+    const bool fresh = j % SUB == 0;
+    uint32_t g0[kMaxPer];
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int dd = i * kTileThreads + tid;
+      g0[i] = (fresh && dd < D) ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
+    }
     if (cnt == 0) {
+#pragma unroll
+      for (int i = 0; i < kMaxPer; ++i) {
+        const int dd = i * kTileThreads + tid;
+        if (fresh && dd < D) bx[dd] = g0[i];
+      }
       __syncthreads();
       continue;
     }
@@ -430,7 +441,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (dd < D) {
 #pragma unroll
         for (int w = 0; w < kW; ++w) wc[w * D + dd] = static_cast<uint16_t>(ts0 + pre[w]);
-        const uint32_t rb = bx[dd];
+        const uint32_t rb = fresh ? g0[i] : bx[dd];
         nxt[i] = rb + tot;
         bx[dd] = rb - ts0;
       }
@@ -443,26 +454,49 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         sidx[mine[d[k]] + rk[k]] = static_cast<uint16_t>(warp * (32 * ITEMS) + k * 32 + lane);
     __syncthreads();
     // Phase B: digit order; consecutive threads write consecutive positions
-    // of one digit run.
-    for (uint32_t p = tid; p < cnt; p += kTileThreads) {
-      const uint32_t li = sidx[p];
-      const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(sb + li * 48);
-      const ulonglong2 h0 = rec[0], hm = rec[1], h1 = rec[2];
-      const int32_t rank = static_cast<int32_t>(hm.x & 0xffffffffu);
-      const uint32_t q = bx[static_cast<uint32_t>(rank - min_rank)] + p;
-      double tv;
-      memcpy(&tv, &h0.x, 8);
-      o.ts[q] = tv;
-      o.op[q] = static_cast<int64_t>(h0.y);
-      o.comm[q] = static_cast<int32_t>(hm.x >> 32);
-      o.chan[q] = static_cast<int32_t>(hm.y & 0xffffffffu);
-      const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
-      const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
-      o.ko[q] = static_cast<uint8_t>((kind & 1) | (name << 1));
-      o.pa[q] = h1.x;
-      o.pb[q] = (kind & 1) ? (h1.y & 0xffffffffull) : h1.y;
-      o.perm[q] = static_cast<uint32_t>(first + li);
-      o.rank[q] = static_cast<uint32_t>(rank);
+    // of one digit run. Four records per thread in flight (independent
+    // shared-memory chains; 8 warps per SM leave little else to hide them).
+    constexpr int kB = 4;
+    for (uint32_t p0 = tid; p0 < cnt; p0 += kB * kTileThreads) {
+      uint32_t li[kB], q[kB];
+      ulonglong2 h0[kB], hm[kB], h1[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const uint32_t p = p0 + k * kTileThreads;
+        li[k] = p < cnt ? sidx[p] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(sb + li[k] * 48);
+        h0[k] = rec[0];
+        hm[k] = rec[1];
+        h1[k] = rec[2];
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const uint32_t p = p0 + k * kTileThreads;
+        const int32_t rank = static_cast<int32_t>(hm[k].x & 0xffffffffu);
+        q[k] = bx[static_cast<uint32_t>(rank - min_rank)] + p;
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const uint32_t p = p0 + k * kTileThreads;
+        if (p >= cnt) break;
+        const uint32_t qq = q[k];
+        double tv;
+        memcpy(&tv, &h0[k].x, 8);
+        o.ts[qq] = tv;
+        o.op[qq] = static_cast<int64_t>(h0[k].y);
+        o.comm[qq] = static_cast<int32_t>(hm[k].x >> 32);
+        o.chan[qq] = static_cast<int32_t>(hm[k].y & 0xffffffffu);
+        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
+        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
+        o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
+        o.pa[qq] = h1[k].x;
+        o.pb[qq] = (kind & 1) ? (h1[k].y & 0xffffffffull) : h1[k].y;
+        o.perm[qq] = static_cast<uint32_t>(first + li[k]);
+        o.rank[qq] = static_cast<uint32_t>(hm[k].x & 0xffffffffu);
+      }
     }
     __syncthreads();
 #pragma unroll

@@ -181,3 +181,32 @@ def test_unsorted_flow_segments_match_reference(oracle, name, mode, swaps):
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                            text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,shuffle", [("scenario1", False), ("scenario2", False),
+                                          ("scenario5", False), ("scenario7", False),
+                                          ("synth_hang_128", False), ("scenario5", True),
+                                          ("synth_hang_128", True)])
+def test_random_windows_match_reference(eng, oracle, name, shuffle):
+    """analyze() (failure and straggler modes) at random (time, suspect rank)
+    triggers against the reference: candidate sets of every size and op mix
+    reach the exoneration sweep, not only the ones run_detection trips on."""
+    import numpy as np
+    from paper_2509_03018_b200.model import FAILURE, STRAGGLER, TriggerEvent
+    recs, _, _ = golden(name)
+    if shuffle:
+        recs = shuffled_ops(recs, swaps=3)
+    scen = eng.Scenario.load(os.path.join(GOLDEN, "configs", name + ".json"))
+    topo, prog = scen.layout()
+    _, acfg, _ = scen.configs()
+    store, model = eng.TraceStore(records=recs), eng.Model(topo, prog)
+    rng = np.random.default_rng(11)
+    last = float(recs["ts"].max())
+    ranks = np.unique(recs["rank"])
+    for k in range(12):
+        t = float(rng.uniform(acfg.delta_ms, last + 50.0))
+        trig = TriggerEvent(FAILURE if k % 3 else STRAGGLER, int(rng.choice(ranks)), t)
+        got = eng.analyze(store, model, acfg, trig)
+        want = oracle.analyze(topo, prog, acfg, recs, trig)
+        assert got == want, (k, trig)
