@@ -565,6 +565,12 @@ csg_status csg_model_create(csg_ctx* ctx, const csg_topology_desc* td,
     put(m->par_it, par_it, st);
     put(m->lvl_off, lvl_off, st);
     put(m->lvl_ops, lvl_ops, st);
+    put(m->op_level, level, st);
+    {
+      uint32_t md = 0;
+      for (int32_t s2 = 0; s2 < opn; ++s2) md = std::max(md, par_off[s2 + 1] - par_off[s2]);
+      m->max_deg = static_cast<int32_t>(md);
+    }
     CSG_CUDA(cudaStreamSynchronize(st));
     *out = m.release();
     return CSG_OK;

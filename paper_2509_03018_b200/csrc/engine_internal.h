@@ -83,8 +83,17 @@ struct StoreView {
   const uint8_t* ko = nullptr;         // kind | op_name << 1
   const uint64_t* pa = nullptr;        // start_ms bits | ready | tx << 32
   const uint64_t* pb = nullptr;        // msg_bytes | done
-  const uint32_t* rank_of = nullptr;   // rank per rank-major position
 };
+
+// Rank owning rank-major position p (p < n): upper_bound over rank_off.
+__device__ inline int32_t rank_at(const StoreView& s, uint32_t p) {
+  int32_t lo = 0, hi = s.R;  // rank_off[lo] <= p < rank_off[hi]
+  while (hi - lo > 1) {
+    const int32_t m = (lo + hi) >> 1;
+    if (s.rank_off[m] <= p) lo = m; else hi = m;
+  }
+  return lo;
+}
 
 // Flow index view (see store_build_flow_index): inside each rank segment
 // [rank_off[r], rank_off[r+1]) the positions ordered by (op_seq, store
@@ -123,6 +132,8 @@ struct ModelView {
   int32_t n_levels = 0;
   const uint32_t* lvl_off = nullptr;     // [n_levels+1]
   const int32_t* lvl_ops = nullptr;      // ops ordered by level
+  const int32_t* op_level = nullptr;     // level of each program op [opn]
+  int32_t max_deg = 0;                   // most parents of one program op
 };
 
 // Ordered-key transform for doubles (non-NaN): unsigned compare == double

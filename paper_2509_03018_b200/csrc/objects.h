@@ -87,6 +87,8 @@ struct csg_store {
   // order); identity for segments already ordered (see FlowView)
   bool flow_indexed = false;
   csg::DevBuf fl_unsorted;  // u32 flag per rank
+  csg::DevBuf fl_list;      // ranks with a descending op_seq (work list)
+  csg::DevBuf fl_cnt;       // [0] list length, [1] overflow count
   csg::DevBuf fl_pos;       // u32 rank-major positions (unsorted segments)
   csg::DevBuf fl_keys;      // global-sort fallback scratch
   csg::DevBuf stats_dev;
@@ -106,7 +108,6 @@ struct csg_store {
     v.ko = ko.as<uint8_t>();
     v.pa = pa.as<uint64_t>();
     v.pb = pb.as<uint64_t>();
-    v.rank_of = keys.as<uint32_t>();
     return v;
   }
   csg::FlowView flow_view() const {
@@ -131,10 +132,11 @@ struct csg_model {
   std::vector<int32_t> h_rg_group;
   std::vector<uint8_t> h_op_name;
   int32_t n_levels = 0;
+  int32_t max_deg = 0;  // most parents of one program op
   // device copies
   csg::DevBuf group_kind, member_off, members, member_slot, comp,
       group_first_op, rg_off, rg_group, rg_slot, op_name, par_off, par_op,
-      par_it, lvl_off, lvl_ops;
+      par_it, lvl_off, lvl_ops, op_level;
   csg::ModelView view() const {
     csg::ModelView v;
     v.world_size = world_size;
@@ -157,6 +159,8 @@ struct csg_model {
     v.n_levels = n_levels;
     v.lvl_off = lvl_off.as<uint32_t>();
     v.lvl_ops = lvl_ops.as<int32_t>();
+    v.op_level = op_level.as<int32_t>();
+    v.max_deg = max_deg;
     return v;
   }
 };

@@ -1847,6 +1847,8 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   __shared__ unsigned long long sh_u[2];
   __shared__ uint32_t wsum[16];
   __shared__ uint32_t scan3[16][3];
+  __shared__ int32_t s_rsum[kExoStage];
+  __shared__ uint8_t s_keep[kExoStage];
   ExoTrip& tp = a.trips[blockIdx.x];
   const int tid = threadIdx.x;
   const uint32_t cbase = a.off[tp.first_item];
@@ -1877,9 +1879,10 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   int64_t* U = reinterpret_cast<int64_t*>(sp + ((P * 4 + 15) & ~15u));
   uint32_t* ret_g = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(U) +
                                                 ((C * 8 + 15) & ~15u));
-  uint8_t* keep = reinterpret_cast<uint8_t*>(ret_g) + ((C * 4 + 15) & ~15u);
+  uint8_t* keep_g = reinterpret_cast<uint8_t*>(ret_g) + ((C * 4 + 15) & ~15u);
   const uint32_t Rs = static_cast<uint32_t>(a.s.R > 0 ? a.s.R : 1);
-  uint32_t* minpos = reinterpret_cast<uint32_t*>(keep + ((C + 15) & ~15u));
+  uint32_t* minpos = reinterpret_cast<uint32_t*>(keep_g + ((C + 15) & ~15u));
+  uint8_t* keep = staged ? s_keep : keep_g;
   uint32_t* rbits = minpos + ((Rs + 3) & ~3u);
   uint32_t* woff = rbits + (((Rs + 31) / 32 + 3) & ~3u);
   csg_suspect* stmp =
@@ -1896,6 +1899,9 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     const Cand& c = cands[i];
     return ExoKey{c.op, c.rank, c.known, c.done, c.tx, c.ready};
   };
+  long long clk[8];
+  int nclk = 0;
+  clk[nclk++] = clock64();
   // 1. stable (op, rank) order
   block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
     const ExoKey kx = key(x), ky = key(y);
@@ -1903,6 +1909,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     if (kx.rank != ky.rank) return kx.rank < ky.rank;
     return x < y;
   });
+  clk[nclk++] = clock64();
   // 2. distinct valid (>= 0) candidate ops, ascending (ordered compaction)
   {
     int Kc = 0;
@@ -1931,6 +1938,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     if (tid == 0) sh_i[0] = Kc;
   }
   __syncthreads();
+  clk[nclk++] = clock64();
   const int K = sh_i[0];
   const int words = (K + 63) / 64;
   const int32_t opn = a.m.opn;
@@ -1966,6 +1974,56 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     for (int i = tid; i < K; i += blockDim.x) cidx[U[i] - lo] = i;
     __syncthreads();
     // ancestor bitsets over [lo, hi] in (iteration, level) order
+    const bool in_smem = bits == exo_dyn + stage_b / 8;
+    const size_t used_b = (V * words + (V + 1) / 2) * 8;
+    const size_t small_b = V * 8 + 4 + V * static_cast<size_t>(a.m.max_deg) * 4;
+    if (in_smem && V <= 4096 && used_b + small_b <= kExoSmemMax - stage_b) {
+      // Small window: the parent lists of every op in [lo, hi] are gathered
+      // into shared memory once (one round of independent global loads),
+      // then the (iteration, level) wavefront runs on shared memory only.
+      int32_t* vlv = cidx + ((V + 1) & ~1ull);
+      uint32_t* vpo = reinterpret_cast<uint32_t*>(vlv + V);
+      int32_t* vpl = reinterpret_cast<int32_t*>(vpo + V + 1);
+      const uint32_t md = static_cast<uint32_t>(a.m.max_deg);
+      for (unsigned long long v = tid; v < V; v += blockDim.x) {
+        const int64_t gv = lo + static_cast<int64_t>(v);
+        const int64_t it = gv / opn;
+        const int32_t sop = static_cast<int32_t>(gv - it * opn);
+        vlv[v] = __ldg(a.m.op_level + sop);
+        const uint32_t pe0 = __ldg(a.m.par_off + sop), pe1 = __ldg(a.m.par_off + sop + 1);
+        vpo[v] = pe1 - pe0;
+        for (uint32_t k = 0; k < md; ++k) {
+          int32_t lp = -1;
+          if (pe0 + k < pe1) {
+            const int64_t pit = it + __ldg(a.m.par_it + pe0 + k);
+            const int64_t pv = pit * opn + __ldg(a.m.par_op + pe0 + k);
+            if (pit >= 0 && pv >= lo) lp = static_cast<int32_t>(pv - lo);
+          }
+          vpl[v * md + k] = lp;
+        }
+      }
+      __syncthreads();
+      for (int64_t it = lo / opn; it <= hi / opn; ++it) {
+        for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
+          for (unsigned long long q = tid; q < V * words; q += blockDim.x) {
+            const unsigned long long v = q / words;
+            const int wd = static_cast<int>(q % words);
+            if (vlv[v] != lv || (lo + static_cast<int64_t>(v)) / opn != it) continue;
+            unsigned long long acc = 0;
+            const uint32_t np = vpo[v];
+            for (uint32_t k = 0; k < np; ++k) {
+              const int32_t lp = vpl[v * md + k];
+              if (lp < 0) continue;
+              acc |= bits[static_cast<uint64_t>(lp) * words + wd];
+              const int l = cidx[lp];
+              if (l >= 0 && (l >> 6) == wd) acc |= 1ull << (l & 63);
+            }
+            bits[v * words + wd] = acc;
+          }
+          __syncthreads();
+        }
+      }
+    } else
     for (int64_t it = lo / opn; it <= hi / opn; ++it) {
       for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
         const uint32_t l0 = a.m.lvl_off[lv];
@@ -1992,6 +2050,8 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       }
     }
   }
+  __syncthreads();
+  clk[nclk++] = clock64();
   // 3. greedy exoneration (rca.cpp:487-514). In (op, rank) order a
   //    candidate c is dropped by an already-retained u of another rank when
   //    u has the same op and strictly less progress (done, tx, ready), or
@@ -2009,7 +2069,8 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   //    Exactly the reference's O(C x retained) greedy, in O(C + K) steps.
   constexpr int kMaskWords = 64;
   __shared__ unsigned long long NE[kMaskWords], MU[kMaskWords];
-  int32_t* rsum = reinterpret_cast<int32_t*>(ret_g);  // [K] retained-rank summary
+  // [K] retained-rank summary (K <= C)
+  int32_t* rsum = staged ? s_rsum : reinterpret_cast<int32_t*>(ret_g);
   if (tid < 32) {
     const int lane = tid;
     const bool masks = words <= kMaskWords;
@@ -2105,6 +2166,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     }
   }
   __syncthreads();
+  clk[nclk++] = clock64();
   // 4. report: exonerated in sorted order; suspects = first retained entry
   //    per rank (its evidence in that order); suspects sorted by rank.
   const int32_t R = a.s.R > 0 ? a.s.R : 1;
@@ -2174,6 +2236,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     run_v += tv;
     __syncthreads();
   }
+  clk[nclk++] = clock64();
   // suspect ranks are unique: rank-sorted position = number of suspect ranks
   // below it (prefix popcount over the rank bitmap)
   if (tid == 0) {
@@ -2193,6 +2256,11 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   __syncthreads();
   for (uint32_t i = tid; i < run_s; i += blockDim.x) sus[i] = stmp[i];
   if (tid == 0) {
+    clk[nclk++] = clock64();
+    if (a.debug)
+      printf("exo trip %d phases (cycles): sort %lld ops %lld dag %lld sweep %lld report %lld "
+             "order %lld\n", tp.j, clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2],
+             clk[4] - clk[3], clk[5] - clk[4], clk[6] - clk[5]);
     o.verdict = run_s ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED;
     o.n_sus = run_s;
     o.exo_off = tp.sus_off + C;

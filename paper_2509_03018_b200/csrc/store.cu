@@ -282,7 +282,6 @@ struct ScatterOut {
   uint64_t* pa;
   uint64_t* pb;
   uint32_t* perm;   // store index per rank-major position
-  uint32_t* rank;   // rank per rank-major position
 };
 
 // --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
@@ -371,10 +370,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     // consumed after phase A (latency hidden)
     const bool fresh = j % SUB == 0;
     uint32_t g0[kMaxPer];
+    if (fresh) {
 #pragma unroll
-    for (int i = 0; i < kMaxPer; ++i) {
-      const int dd = i * kTileThreads + tid;
-      g0[i] = (fresh && dd < D) ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
+      for (int i = 0; i < kMaxPer; ++i) {
+        const int dd = i * kTileThreads + tid;
+        g0[i] = dd < D ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
+      }
     }
     if (cnt == 0) {
 #pragma unroll
@@ -386,7 +387,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       continue;
     }
     const unsigned char* sb = buf0 + (j & 1) * TR * 48;
-    for (int i = tid; i < kW * D; i += kTileThreads) wc[i] = 0;
+    {  // clear the warp counters, 16 bytes per store
+      uint4* w4 = reinterpret_cast<uint4*>(wc);
+      const int n4 = (kW * ((D + 1) & ~1) * 2 + 15) / 16;
+      for (int i = tid; i < n4; i += kTileThreads) w4[i] = make_uint4(0, 0, 0, 0);
+    }
     if (j & 1) {
       mbar_wait(&mbar[1], par1);
       par1 ^= 1;
@@ -495,7 +500,6 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         o.pa[qq] = h1[k].x;
         o.pb[qq] = (kind & 1) ? (h1[k].y & 0xffffffffull) : h1[k].y;
         o.perm[qq] = static_cast<uint32_t>(first + li[k]);
-        o.rank[qq] = static_cast<uint32_t>(hm[k].x & 0xffffffffu);
       }
     }
     __syncthreads();
@@ -512,26 +516,35 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // Per-rank running max of ts: one block per rank segment, the segment split
 // into one contiguous part per warp; part maxima exchanged through shared
 // memory give every warp its carry-in (all warps of all ranks stream at
-// once instead of one warp walking a whole segment).
+// once instead of one warp walking a whole segment). The same pass flags
+// segments whose op_seq descends in store order (the flow index permutes
+// only those, see k_flow_fix) and appends them to a work list.
 __global__ void __launch_bounds__(1024)
-    k_runmax_blk(const double* __restrict__ ts, const uint32_t* __restrict__ off,
-                 double* __restrict__ out) {
+    k_runmax_blk(const double* __restrict__ ts, const int64_t* __restrict__ op,
+                 const uint32_t* __restrict__ off, double* __restrict__ out,
+                 uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
+                 unsigned* __restrict__ cnt) {
   __shared__ double pmax[32];
+  __shared__ int desc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   const uint32_t b = off[blockIdx.x], e = off[blockIdx.x + 1];
   const uint32_t L = e - b;
+  if (threadIdx.x == 0) desc = 0;
   const uint32_t per = ((L + nw - 1) / nw + 31) & ~31u;
   const uint32_t pb = min(e, b + warp * per), pe = min(e, pb + per);
   double m = -INFINITY;
+  bool dsc = false;
   for (uint32_t p = pb + lane; p < pe; p += 32) {
     const double x = __ldg(ts + p);
     if (x == x) m = fmax(m, x);  // NaN never breaks a prefix
+    if (p > b) dsc |= __ldg(op + p) < __ldg(op + p - 1);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) pmax[warp] = m;
   __syncthreads();
+  if (dsc) desc = 1;
   double carry = -INFINITY;
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
   for (uint32_t base = pb; base < pe; base += 32) {
@@ -546,6 +559,11 @@ __global__ void __launch_bounds__(1024)
     x = fmax(x, carry);
     carry = __shfl_sync(0xffffffffu, x, 31);
     if (p < pe) out[p] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsorted[blockIdx.x] = desc ? 1u : 0u;
+    if (desc) list[atomicAdd(cnt, 1u)] = blockIdx.x;
   }
 }
 
@@ -599,39 +617,13 @@ __global__ void k_opidx_fill(StoreView s, const uint32_t* __restrict__ pos,
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t p = pos[i];
-    rank[i] = static_cast<int32_t>(s.rank_of[p]);
+    rank[i] = rank_at(s, p);
     const double t = s.ts[p];
     double st;
     memcpy(&st, &s.pa[p], 8);
     ts[i] = t;
     dur[i] = t - st;
     nm[i] = static_cast<uint8_t>(ko_opname(s.ko[p]));
-  }
-}
-
-// Flow index, step 1: one streaming pass over the op column; a rank
-// segment whose op_seq descends somewhere in store order is flagged once and
-// appended to the work list of step 2.
-__global__ void k_flow_check(StoreView s, uint32_t* __restrict__ unsorted,
-                             uint32_t* __restrict__ list, unsigned* __restrict__ cnt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t p0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; p0 < s.n;
-       p0 += 4 * stride) {
-    int64_t a[4], c[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t p = p0 + k * stride;
-      a[k] = p < s.n ? __ldg(s.op + p - 1) : 0;
-      c[k] = p < s.n ? __ldg(s.op + p) : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t p = p0 + k * stride;
-      if (c[k] < a[k] && s.rank_of[p] == s.rank_of[p - 1]) {
-        const uint32_t r = s.rank_of[p];
-        if (atomicExch(&unsorted[r], 1u) == 0u) list[atomicAdd(cnt, 1u)] = r;
-      }
-    }
   }
 }
 
@@ -774,7 +766,7 @@ __global__ void k_flow_keys(StoreView s, int64_t min_op, int rank_shift,
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < s.n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     keys[p] = static_cast<K>(
-        (static_cast<unsigned long long>(s.rank_of[p]) << rank_shift) |
+        (static_cast<unsigned long long>(rank_at(s, static_cast<uint32_t>(p))) << rank_shift) |
         static_cast<unsigned long long>(s.op[p] - min_op));
     vals[p] = static_cast<uint32_t>(p);
   }
@@ -1049,7 +1041,7 @@ void store_build_index(csg_store* s) {
     }
     ScatterOut o{s->ts.as<double>(), s->op.as<int64_t>(), s->comm.as<int32_t>(),
                  s->chan.as<int32_t>(), s->ko.as<uint8_t>(), s->pa.as<uint64_t>(),
-                 s->pb.as<uint64_t>(), s->perm.as<uint32_t>(), s->keys.as<uint32_t>()};
+                 s->pb.as<uint64_t>(), s->perm.as<uint32_t>()};
     // sub-tiles of 2048 records (1024 when the digit span needs the room)
     const bool wide = D > 1024;
     const int TR = wide ? 1024 : 2048;
@@ -1107,10 +1099,21 @@ void store_build_index(csg_store* s) {
                                                      s->rank_off.as<uint32_t>());
     }
   }
+  // flow-index descent flags + work list, filled by k_runmax_blk
+  s->fl_unsorted.ensure((static_cast<size_t>(R) + 2) * 4);
+  DevBuf& flist = s->fl_list;
+  DevBuf& fcnt = s->fl_cnt;
+  flist.ensure(static_cast<size_t>(R) * 4 + 4);
+  fcnt.ensure(8);
+  CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
   if (n && R) {
     ProfScope ps_(c->lc, "k_runmax", st);
-    k_runmax_blk<<<R, 1024, 0, st>>>(s->ts.as<double>(), s->rank_off.as<uint32_t>(),
-                                     s->runmax.as<double>());
+    k_runmax_blk<<<R, 1024, 0, st>>>(s->ts.as<double>(), s->op.as<int64_t>(),
+                                     s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
+                                     s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(),
+                                     fcnt.as<unsigned>());
+  } else if (R) {
+    CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4, st));
   }
   {
     std::vector<uint32_t> ro(static_cast<size_t>(R) + 1);
@@ -1267,29 +1270,20 @@ bool store_build_flow_index(csg_store* s) {
   cudaStream_t st = c->stream;
   const uint64_t n = s->n;
   const int32_t R = s->R;
-  s->fl_unsorted.ensure((static_cast<size_t>(R) + 2) * 4);
   s->fl_pos.ensure(n * 4 + 4);
-  CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4 + 4, st));
   if (!n || !R) {
     s->flow_indexed = true;
     return true;
   }
-  DevBuf& cnt = c->buf("flow.cnt");
-  DevBuf& list = c->buf("flow.list");
-  cnt.ensure(8);
-  list.ensure(static_cast<size_t>(R) * 4 + 4);
-  CSG_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+  // descent flags, work list and its count come from k_runmax_blk
+  DevBuf& cnt = s->fl_cnt;
+  DevBuf& list = s->fl_list;
   unsigned* d_uns = cnt.as<unsigned>();
   unsigned* d_ovf = d_uns + 1;
   static const bool force_global = std::getenv("CSG_FLOW_GLOBAL_SORT") != nullptr;
   const uint64_t span = static_cast<uint64_t>(s->max_op - s->min_op);
   bool global = force_global;
   if (!global) {
-    {
-      ProfScope ps_(c->lc, "k_flow_check", st);
-      k_flow_check<<<grid_for(n / 4 + 1), 256, 0, st>>>(
-          s->view(), s->fl_unsorted.as<uint32_t>(), list.as<uint32_t>(), d_uns);
-    }
     // CSG_FLOW_SMEM_CAP (power of two) lowers the shared-memory segment cap
     // so tests can drive the overflow -> device-wide fallback on small traces
     static const int32_t cap = [] {
