@@ -1841,7 +1841,7 @@ struct ExoKey {
 };
 constexpr size_t kExoStageBytes = kExoStage * (sizeof(ExoKey) + 4);
 
-__global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
+__global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   extern __shared__ __align__(16) unsigned long long exo_dyn[];
   __shared__ int32_t sh_i[8];
   __shared__ unsigned long long sh_u[2];
@@ -1899,9 +1899,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     const Cand& c = cands[i];
     return ExoKey{c.op, c.rank, c.known, c.done, c.tx, c.ready};
   };
-  long long clk[8];
-  int nclk = 0;
-  clk[nclk++] = clock64();
+  long long clk0 = clock64(), clk1 = 0, clk2 = 0, clk3 = 0, clk4 = 0, clk5 = 0;
   // 1. stable (op, rank) order
   block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
     const ExoKey kx = key(x), ky = key(y);
@@ -1909,7 +1907,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     if (kx.rank != ky.rank) return kx.rank < ky.rank;
     return x < y;
   });
-  clk[nclk++] = clock64();
+  clk1 = clock64();
   // 2. distinct valid (>= 0) candidate ops, ascending (ordered compaction)
   {
     int Kc = 0;
@@ -1938,7 +1936,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     if (tid == 0) sh_i[0] = Kc;
   }
   __syncthreads();
-  clk[nclk++] = clock64();
+  clk2 = clock64();
   const int K = sh_i[0];
   const int words = (K + 63) / 64;
   const int32_t opn = a.m.opn;
@@ -1987,38 +1985,47 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
       const uint32_t md = static_cast<uint32_t>(a.m.max_deg);
       for (unsigned long long v = tid; v < V; v += blockDim.x) {
         const int64_t gv = lo + static_cast<int64_t>(v);
+        const int32_t sop = static_cast<int32_t>(gv - (gv / opn) * opn);
+        vlv[v] = __ldg(a.m.op_level + sop);
+        vpo[v] = __ldg(a.m.par_off + sop + 1) - __ldg(a.m.par_off + sop);
+      }
+      // one (op, parent slot) per thread: independent loads, one latency
+      for (unsigned long long q = tid; q < V * md; q += blockDim.x) {
+        const unsigned long long v = q / md;
+        const uint32_t k = static_cast<uint32_t>(q % md);
+        const int64_t gv = lo + static_cast<int64_t>(v);
         const int64_t it = gv / opn;
         const int32_t sop = static_cast<int32_t>(gv - it * opn);
-        vlv[v] = __ldg(a.m.op_level + sop);
         const uint32_t pe0 = __ldg(a.m.par_off + sop), pe1 = __ldg(a.m.par_off + sop + 1);
-        vpo[v] = pe1 - pe0;
-        for (uint32_t k = 0; k < md; ++k) {
-          int32_t lp = -1;
-          if (pe0 + k < pe1) {
-            const int64_t pit = it + __ldg(a.m.par_it + pe0 + k);
-            const int64_t pv = pit * opn + __ldg(a.m.par_op + pe0 + k);
-            if (pit >= 0 && pv >= lo) lp = static_cast<int32_t>(pv - lo);
-          }
-          vpl[v * md + k] = lp;
+        int32_t lp = -1;
+        if (pe0 + k < pe1) {
+          const int64_t pit = it + __ldg(a.m.par_it + pe0 + k);
+          const int64_t pv = pit * opn + __ldg(a.m.par_op + pe0 + k);
+          if (pit >= 0 && pv >= lo) lp = static_cast<int32_t>(pv - lo);
         }
+        vpl[q] = lp;
       }
       __syncthreads();
+      // wavefront: one warp per (op, word), lanes over the parent slots
+      const int lane = tid & 31, nwarps = blockDim.x >> 5;
       for (int64_t it = lo / opn; it <= hi / opn; ++it) {
         for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
-          for (unsigned long long q = tid; q < V * words; q += blockDim.x) {
+          for (unsigned long long q = tid >> 5; q < V * words; q += nwarps) {
             const unsigned long long v = q / words;
             const int wd = static_cast<int>(q % words);
             if (vlv[v] != lv || (lo + static_cast<int64_t>(v)) / opn != it) continue;
             unsigned long long acc = 0;
             const uint32_t np = vpo[v];
-            for (uint32_t k = 0; k < np; ++k) {
+            for (uint32_t k = lane; k < np; k += 32) {
               const int32_t lp = vpl[v * md + k];
               if (lp < 0) continue;
               acc |= bits[static_cast<uint64_t>(lp) * words + wd];
               const int l = cidx[lp];
               if (l >= 0 && (l >> 6) == wd) acc |= 1ull << (l & 63);
             }
-            bits[v * words + wd] = acc;
+            const uint32_t lo32 = __reduce_or_sync(FULL, static_cast<uint32_t>(acc));
+            const uint32_t hi32 = __reduce_or_sync(FULL, static_cast<uint32_t>(acc >> 32));
+            if (lane == 0) bits[v * words + wd] = (static_cast<unsigned long long>(hi32) << 32) | lo32;
           }
           __syncthreads();
         }
@@ -2051,7 +2058,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     }
   }
   __syncthreads();
-  clk[nclk++] = clock64();
+  clk3 = clock64();
   // 3. greedy exoneration (rca.cpp:487-514). In (op, rank) order a
   //    candidate c is dropped by an already-retained u of another rank when
   //    u has the same op and strictly less progress (done, tx, ready), or
@@ -2122,37 +2129,48 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
             }
           }
         }
+        // sequential greedy over the batch; each lane holds its own key and
+        // the walk broadcasts lane t's fields (independent of the state, so
+        // the shuffles pipeline; only the two-minimum state is carried)
         const uint32_t nt = min(32u, y - base);
+        ExoKey mk{};
+        if (i < y) mk = key(ord[i]);
+        unsigned keptm = 0;
         for (uint32_t t = 0; t < nt; ++t) {
           const bool ddt = __shfl_sync(FULL, dd ? 1 : 0, t) != 0;
-          const ExoKey c = key(ord[base + t]);
+          const int32_t crank = __shfl_sync(FULL, mk.rank, t);
+          const bool cknown = __shfl_sync(FULL, mk.known, t) != 0;
+          const uint64_t cd = __shfl_sync(FULL, mk.done, t);
+          const uint64_t ct = __shfl_sync(FULL, mk.tx, t);
+          const uint64_t cr = __shfl_sync(FULL, mk.ready, t);
           bool kept = !ddt;
-          if (kept && c.known) {
-            if (rk1 != c.rank) kept = !plt(m1d, m1t, m1r, c.done, c.tx, c.ready);
-            else kept = !plt(m2d, m2t, m2r, c.done, c.tx, c.ready);
+          if (kept && cknown) {
+            if (rk1 != crank) kept = !plt(m1d, m1t, m1r, cd, ct, cr);
+            else kept = !plt(m2d, m2t, m2r, cd, ct, cr);
           }
-          if (lane == 0) keep[base + t] = kept ? 1 : 0;
           if (kept) {
-            gs = gs == -1 ? c.rank : (gs == c.rank ? gs : -2);
-            if (c.known) {
-              if (plt(c.done, c.tx, c.ready, m1d, m1t, m1r)) {
-                if (c.rank != rk1) {
+            keptm |= 1u << t;
+            gs = gs == -1 ? crank : (gs == crank ? gs : -2);
+            if (cknown) {
+              if (plt(cd, ct, cr, m1d, m1t, m1r)) {
+                if (crank != rk1) {
                   m2d = m1d;
                   m2t = m1t;
                   m2r = m1r;
                 }
-                m1d = c.done;
-                m1t = c.tx;
-                m1r = c.ready;
-                rk1 = c.rank;
-              } else if (c.rank != rk1 && plt(c.done, c.tx, c.ready, m2d, m2t, m2r)) {
-                m2d = c.done;
-                m2t = c.tx;
-                m2r = c.ready;
+                m1d = cd;
+                m1t = ct;
+                m1r = cr;
+                rk1 = crank;
+              } else if (crank != rk1 && plt(cd, ct, cr, m2d, m2t, m2r)) {
+                m2d = cd;
+                m2t = ct;
+                m2r = cr;
               }
             }
           }
         }
+        if (i < y) keep[i] = (keptm >> lane) & 1u;
       }
       if (g >= 0 && lane == 0) {
         rsum[g] = gs;
@@ -2166,7 +2184,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     }
   }
   __syncthreads();
-  clk[nclk++] = clock64();
+  clk4 = clock64();
   // 4. report: exonerated in sorted order; suspects = first retained entry
   //    per rank (its evidence in that order); suspects sorted by rank.
   const int32_t R = a.s.R > 0 ? a.s.R : 1;
@@ -2236,7 +2254,7 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
     run_v += tv;
     __syncthreads();
   }
-  clk[nclk++] = clock64();
+  clk5 = clock64();
   // suspect ranks are unique: rank-sorted position = number of suspect ranks
   // below it (prefix popcount over the rank bitmap)
   if (tid == 0) {
@@ -2256,11 +2274,10 @@ __global__ void __launch_bounds__(kExoThreads) k_exonerate(ExoArgs a) {
   __syncthreads();
   for (uint32_t i = tid; i < run_s; i += blockDim.x) sus[i] = stmp[i];
   if (tid == 0) {
-    clk[nclk++] = clock64();
     if (a.debug)
       printf("exo trip %d phases (cycles): sort %lld ops %lld dag %lld sweep %lld report %lld "
-             "order %lld\n", tp.j, clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2],
-             clk[4] - clk[3], clk[5] - clk[4], clk[6] - clk[5]);
+             "order %lld\n", tp.j, clk1 - clk0, clk2 - clk1, clk3 - clk2, clk4 - clk3,
+             clk5 - clk4, (long long)clock64() - clk5);
     o.verdict = run_s ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED;
     o.n_sus = run_s;
     o.exo_off = tp.sus_off + C;
