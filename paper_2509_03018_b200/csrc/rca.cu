@@ -1900,6 +1900,7 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
     return ExoKey{c.op, c.rank, c.known, c.done, c.tx, c.ready};
   };
   long long clk0 = clock64(), clk1 = 0, clk2 = 0, clk3 = 0, clk4 = 0, clk5 = 0;
+  long long cy_y = 0, cy_dd = 0, cy_walk = 0;
   // 1. stable (op, rank) order
   block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
     const ExoKey kx = key(x), ky = key(y);
@@ -1956,9 +1957,6 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
     }
     __syncthreads();
     if (!sh_i[1]) return;
-    if (a.debug && tid == 0)
-      printf("exo trip %d C=%u K=%d V=%llu words=%d iters=%lld levels=%d\n", tp.j, C, K,
-             V, words, (long long)(hi / opn - lo / opn + 1), a.m.n_levels);
     const size_t stage_b = staged ? kExoStageBytes : 0;
     if ((V * words + (V + 1) / 2) * 8 <= kExoSmemMax - stage_b) {
       bits = exo_dyn + stage_b / 8;  // ancestor bitsets resident in shared memory
@@ -2088,6 +2086,7 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
                   uint64_t r1) { return prog_less(d0, t0, r0, d1, t1, r1); };
     uint32_t x = 0;
     while (x < C) {
+      long long c0 = clock64();
       const int64_t op = key(ord[x]).op;
       // group end: first sorted position with a different op
       uint32_t y = x + 1;
@@ -2100,16 +2099,28 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
         }
         y = min(C, b0 + 32);
       }
+      cy_y += clock64() - c0;
       const bool dag = op >= 0 && K >= 2;
       const int g = dag ? cidx[op - lo] : -1;
       const unsigned long long* row = dag ? bits + (op - lo) * words : nullptr;
+      // Same-op rule, in parallel. Inside a group the candidates run in rank
+      // order and equal ranks are adjacent, so "retained u of another rank
+      // before c" = retained candidates before c's rank run. A candidate
+      // with progress above the least retained progress is dropped, so the
+      // least RETAINED progress before a run equals the least progress of
+      // ALL dependency-surviving known candidates before it (the minimum
+      // itself is always retained). Hence c survives iff !dd and
+      // !(KM(run start) < prog(c)), KM = exclusive prefix minimum over the
+      // group at run granularity — no step depends on another's verdict.
       const uint64_t INF = ~0ull;
-      uint64_t m1d = INF, m1t = INF, m1r = INF, m2d = INF, m2t = INF, m2r = INF;
-      int32_t rk1 = INT_MIN;
-      int32_t gs = -1;  // this group's retained-rank summary
+      uint64_t kcd = INF, kct = INF, kcr = INF;  // min before the open run
+      uint64_t kod = INF, kot = INF, kor = INF;  // min inside the open run
+      int32_t orank = INT_MIN;                   // rank of the open run
+      int32_t kmin = INT_MAX, kmax = INT_MIN;    // retained ranks of the group
       for (uint32_t base = x; base < y; base += 32) {
         const uint32_t i = base + lane;
         bool dd = false;
+        long long c1 = clock64();
         if (i < y && dag) {
           const int32_t r = key(ord[i]).rank;
           for (int w = 0; w < words && !dd; ++w) {
@@ -2129,49 +2140,120 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
             }
           }
         }
-        // sequential greedy over the batch; each lane holds its own key and
-        // the walk broadcasts lane t's fields (independent of the state, so
-        // the shuffles pipeline; only the two-minimum state is carried)
-        const uint32_t nt = min(32u, y - base);
+        long long c2 = clock64();
+        cy_dd += c2 - c1;
+        const bool in = i < y;
         ExoKey mk{};
-        if (i < y) mk = key(ord[i]);
-        unsigned keptm = 0;
-        for (uint32_t t = 0; t < nt; ++t) {
-          const bool ddt = __shfl_sync(FULL, dd ? 1 : 0, t) != 0;
-          const int32_t crank = __shfl_sync(FULL, mk.rank, t);
-          const bool cknown = __shfl_sync(FULL, mk.known, t) != 0;
-          const uint64_t cd = __shfl_sync(FULL, mk.done, t);
-          const uint64_t ct = __shfl_sync(FULL, mk.tx, t);
-          const uint64_t cr = __shfl_sync(FULL, mk.ready, t);
-          bool kept = !ddt;
-          if (kept && cknown) {
-            if (rk1 != crank) kept = !plt(m1d, m1t, m1r, cd, ct, cr);
-            else kept = !plt(m2d, m2t, m2r, cd, ct, cr);
+        if (in) mk = key(ord[i]);
+        const int32_t rk = in ? mk.rank : INT_MAX;
+        // this lane's contribution to the minimum
+        uint64_t vd = INF, vt = INF, vr = INF;
+        if (in && !dd && mk.known) {
+          vd = mk.done;
+          vt = mk.tx;
+          vr = mk.ready;
+        }
+        // exclusive prefix minimum over lanes (lexicographic triples)
+        uint64_t pd = vd, pt = vt, pr = vr;  // inclusive first
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t qd = __shfl_up_sync(FULL, pd, o), qt = __shfl_up_sync(FULL, pt, o),
+                         qr = __shfl_up_sync(FULL, pr, o);
+          if (lane >= o && plt(qd, qt, qr, pd, pt, pr)) {
+            pd = qd;
+            pt = qt;
+            pr = qr;
           }
-          if (kept) {
-            keptm |= 1u << t;
-            gs = gs == -1 ? crank : (gs == crank ? gs : -2);
-            if (cknown) {
-              if (plt(cd, ct, cr, m1d, m1t, m1r)) {
-                if (crank != rk1) {
-                  m2d = m1d;
-                  m2t = m1t;
-                  m2r = m1r;
-                }
-                m1d = cd;
-                m1t = ct;
-                m1r = cr;
-                rk1 = crank;
-              } else if (crank != rk1 && plt(cd, ct, cr, m2d, m2t, m2r)) {
-                m2d = cd;
-                m2t = ct;
-                m2r = cr;
-              }
+        }
+        // run starts inside the batch
+        const int32_t prev_rank = __shfl_up_sync(FULL, rk, 1);
+        const bool start = in && (lane == 0 ? rk != orank : rk != prev_rank);
+        const unsigned sm = __ballot_sync(FULL, start);
+        const unsigned upto = sm & (lane == 31 ? FULL : ((2u << lane) - 1u));
+        // KM for this lane's run
+        uint64_t md = kcd, mt = kct, mr = kcr;
+        {
+          const int s = upto ? 31 - __clz(upto) : -1;  // start of my run in batch
+          // min over batch lanes [0, s) = inclusive prefix at s - 1
+          const int src = s > 0 ? s - 1 : 0;
+          const uint64_t bd = __shfl_sync(FULL, pd, src), bt = __shfl_sync(FULL, pt, src),
+                         br = __shfl_sync(FULL, pr, src);
+          if (s >= 0) {  // my run starts in this batch: closed + open run + lanes before s
+            if (plt(kod, kot, kor, md, mt, mr)) {
+              md = kod;
+              mt = kot;
+              mr = kor;
+            }
+            if (s > 0 && plt(bd, bt, br, md, mt, mr)) {
+              md = bd;
+              mt = bt;
+              mr = br;
             }
           }
         }
-        if (i < y) keep[i] = (keptm >> lane) & 1u;
+        bool kept = in && !dd;
+        if (kept && mk.known) kept = !plt(md, mt, mr, mk.done, mk.tx, mk.ready);
+        if (in) keep[i] = kept ? 1 : 0;
+        if (kept) {
+          kmin = min(kmin, rk);
+          kmax = max(kmax, rk);
+        }
+        // carry: the open run after this batch is the last lane's run
+        const unsigned last = __ballot_sync(FULL, in);
+        const int ll = 31 - __clz(last);
+        const int ls = __shfl_sync(FULL, upto ? 31 - __clz(upto) : -1, ll);
+        const uint64_t ad = __shfl_sync(FULL, pd, ll), at = __shfl_sync(FULL, pt, ll),
+                       ar = __shfl_sync(FULL, pr, ll);  // min over the whole batch
+        if (ls >= 0) {
+          // closed = everything before the last run's start
+          const int src = ls > 0 ? ls - 1 : 0;
+          const uint64_t bd = __shfl_sync(FULL, pd, src), bt = __shfl_sync(FULL, pt, src),
+                         br = __shfl_sync(FULL, pr, src);
+          if (plt(kod, kot, kor, kcd, kct, kcr)) {
+            kcd = kod;
+            kct = kot;
+            kcr = kor;
+          }
+          if (ls > 0 && plt(bd, bt, br, kcd, kct, kcr)) {
+            kcd = bd;
+            kct = bt;
+            kcr = br;
+          }
+          // open run = lanes [ls, ll]: min of their values
+          uint64_t od = INF, ot = INF, orr = INF;
+          if (lane >= ls && lane <= ll) {
+            od = vd;
+            ot = vt;
+            orr = vr;
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const uint64_t qd = __shfl_xor_sync(FULL, od, o), qt = __shfl_xor_sync(FULL, ot, o),
+                           qr = __shfl_xor_sync(FULL, orr, o);
+            if (plt(qd, qt, qr, od, ot, orr)) {
+              od = qd;
+              ot = qt;
+              orr = qr;
+            }
+          }
+          kod = od;
+          kot = ot;
+          kor = orr;
+        } else if (plt(ad, at, ar, kod, kot, kor)) {  // the open run continues
+          kod = ad;
+          kot = at;
+          kor = ar;
+        }
+        orank = __shfl_sync(FULL, rk, ll);
+        cy_walk += clock64() - c2;
       }
+      // retained-rank summary: -1 none, the single rank, -2 several
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+      }
+      const int32_t gs = kmin == INT_MAX ? -1 : (kmin == kmax ? kmin : -2);
       if (g >= 0 && lane == 0) {
         rsum[g] = gs;
         if (masks && gs != -1) {
@@ -2275,9 +2357,11 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   for (uint32_t i = tid; i < run_s; i += blockDim.x) sus[i] = stmp[i];
   if (tid == 0) {
     if (a.debug)
-      printf("exo trip %d phases (cycles): sort %lld ops %lld dag %lld sweep %lld report %lld "
-             "order %lld\n", tp.j, clk1 - clk0, clk2 - clk1, clk3 - clk2, clk4 - clk3,
-             clk5 - clk4, (long long)clock64() - clk5);
+      printf("exo trip %d C=%u K=%d lo=%lld hi=%lld words=%d phases (cycles): sort %lld "
+             "ops %lld dag %lld sweep %lld [y %lld dd %lld walk %lld] report %lld order %lld\n",
+             tp.j, C, K, (long long)lo, (long long)hi, words, clk1 - clk0, clk2 - clk1,
+             clk3 - clk2, clk4 - clk3, cy_y, cy_dd, cy_walk, clk5 - clk4,
+             (long long)clock64() - clk5);
     o.verdict = run_s ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_UNDETERMINED;
     o.n_sus = run_s;
     o.exo_off = tp.sus_off + C;
