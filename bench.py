@@ -39,15 +39,17 @@ METRIC = "trace records/s through trigger+RCA"
 UNIT = "records/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
-# Algorithmic bytes per unit for the roofline:
-#  k_gather:        read the 48 B packed record + 4 B permutation entry,
-#                   write 41 B of rank-major columns            -> 93 B/record
-#  k_downsweep:     one LSD pass, read key+value, write key+value -> 16 B/record
-#  k_rank_summary:  one read of the prefix's op(8)+kind(1)+channel(4)
-#                   per (trip, rank) prefix record               -> 13 B/record
-ALGO_BYTES = {"k_gather": 93.0, "k_downsweep": 16.0, "k_rank_summary": 13.0,
-              "k_upsweep": 4.0, "k_window_stats": 17.0, "k_runmax": 16.0,
-              "k_stats": 48.0, "k_rank_keys": 56.0}
+# Algorithmic bytes per record for the roofline, per launch
+# = bytes/record x records in the store:
+#  k_scatter:     read the 48 B packed record once (bulk copy into shared
+#                 memory), write ts 8 + op 8 + comm 4 + chan 4 + kind|op_name 1
+#                 + payload 16 + store index 4 = 45 B of rank-major columns
+#  k_stats_hist:  read the record's first 32 B (ts, op_seq, rank, comm,
+#                 channel, kind)
+#  k_runmax:      read ts 8 + op_seq 8, write the running max 8
+#  k_gather/k_downsweep/k_upsweep: general (rank span > 2048) index path
+ALGO_BYTES = {"k_scatter": 93.0, "k_stats_hist": 32.0, "k_runmax": 24.0,
+              "k_gather": 93.0, "k_downsweep": 16.0, "k_upsweep": 4.0}
 
 
 def log(*a):
@@ -187,7 +189,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         reports, sampled = step()
     ctx.reset_stats()
-    ctx.profile(True)
+    ctx.profile(False)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -198,8 +200,6 @@ def run_ours(args):
         wall = time.perf_counter() - t0
     torch.cuda.synchronize()
     dev_ms, launches = ctx.stats()
-    kstats, _, _ = ctx.kernel_stats()
-    ctx.profile(False)
     ms_step = dev_ms / args.steps
     n_total = n
     if ws > 1:
@@ -211,19 +211,27 @@ def run_ours(args):
         n_total = int(nt.item())
     value = n_total / (ms_step / 1e3)
 
-    # roofline of the dominant kernel (largest share of device time)
+    # per-kernel CUDA-event times from separate profiled steps (the events
+    # between launches are kept out of the timed steps above)
+    ctx.reset_stats()
+    ctx.profile(True)
+    prof_steps = 3
+    for _ in range(prof_steps):
+        step()
+    prof_ms, _ = ctx.stats()
+    kstats, _, _ = ctx.kernel_stats()
+    ctx.profile(False)
+
+    # roofline of the dominant HBM kernel (largest share of device time among
+    # the kernels with an algorithmic byte count)
     peak, peak_kind = hbm_peak()
-    dom = max(kstats.items(), key=lambda kv: kv[1][0])
-    name, (tot_ms, nl) = dom
     trips = len(reports)
-    units_per_launch = {"k_gather": n, "k_downsweep": n, "k_upsweep": n,
-                        "k_window_stats": None, "k_rank_summary": n * max(trips, 1),
-                        "k_runmax": n, "k_stats": n, "k_rank_keys": n}.get(name)
-    achieved = None
-    if units_per_launch and name in ALGO_BYTES:
-        per_launch_bytes = ALGO_BYTES[name] * units_per_launch
-        achieved = per_launch_bytes / (tot_ms / nl / 1e3) / 1e9
-    step_share = {k: round(v[0] / (dev_ms or 1), 4) for k, v in
+    cand = {k: v for k, v in kstats.items() if k in ALGO_BYTES}
+    name, (tot_ms, nl) = max(cand.items(), key=lambda kv: kv[1][0])
+    per_launch_bytes = ALGO_BYTES[name] * n
+    achieved = per_launch_bytes / (tot_ms / nl / 1e3) / 1e9
+    kern_ms = sum(v[0] for v in kstats.values())
+    step_share = {k: round(v[0] / (prof_ms or 1), 4) for k, v in
                   sorted(kstats.items(), key=lambda kv: -kv[1][0])}
 
     # e2e through the public API from pinned host memory
@@ -296,12 +304,14 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved,
                      "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None,
+                     "frac": achieved / peak,
                      "traffic": ncu_traffic(name),
-                     "algorithmic_bytes_per_launch": (ALGO_BYTES[name] * units_per_launch
-                                                      if achieved else None),
+                     "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "algorithmic_bytes_per_record": ALGO_BYTES[name],
                      "launches": nl,
-                     "avg_launch_ms": tot_ms / nl, "share_of_step": step_share},
+                     "avg_launch_ms": tot_ms / nl,
+                     "kernel_ms_per_step": kern_ms / prof_steps,
+                     "share_of_step": step_share},
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

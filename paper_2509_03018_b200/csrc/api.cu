@@ -692,13 +692,8 @@ csg_status csg_run_detection(csg_store* store, const csg_model* model,
                                     d_s.as<int32_t>(),
                                     static_cast<int32_t>(sampled.size()),
                                     trig_params(*tcfg), events);
-      trips.resize(n);
-      if (n)
-        CSG_CUDA(cudaMemcpyAsync(trips.data(), events.p,
-                                 n * sizeof(csg_trigger_event),
-                                 cudaMemcpyDeviceToHost, c->stream));
-      c->d2h_bytes += n * sizeof(csg_trigger_event);
-      CSG_CUDA(cudaStreamSynchronize(c->stream));
+      trips.assign(c->h_events.begin(), c->h_events.begin() + n);
+      c->d2h_bytes += static_cast<uint64_t>(T) * sizeof(csg_trigger_event) + 4;
     }
     RcaResult r;
     rca_batch(store, model, *acfg, trips.data(),

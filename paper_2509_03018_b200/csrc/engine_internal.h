@@ -28,6 +28,32 @@ struct Error : std::runtime_error {
   } while (0)
 
 // Growable device buffer (bytes).
+// Grow-only pinned host buffer mapped into the device address space
+// (kernels write results straight into it; no separate copy-back).
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    const size_t want = b < 4096 ? 4096 : b + b / 2;
+    CSG_CUDA(cudaHostAlloc(&p, want, cudaHostAllocMapped));
+    bytes = want;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;

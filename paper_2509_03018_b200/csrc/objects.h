@@ -20,6 +20,8 @@ struct csg_ctx {
   int nranks = 1, rank = 0;
   uint64_t collectives = 0;
   csg::LaunchCounter lc;
+  std::vector<double> h_ticks;  // detection tick times (host-computed)
+  std::vector<csg_trigger_event> h_events;  // trips of the last trigger_run
   // shared scratch
   csg::DevBuf scratch_a, scratch_b, scratch_c, pinned_flag_dev;
   uint32_t* host_flag = nullptr;  // pinned
@@ -27,6 +29,8 @@ struct csg_ctx {
   // cudaFree on the analysis path once warm).
   std::map<std::string, csg::DevBuf> arena;
   csg::DevBuf& buf(const char* name) { return arena[name]; }
+  std::map<std::string, csg::HostBuf> host_arena;  // mapped pinned buffers
+  csg::HostBuf& hbuf(const char* name) { return host_arena[name]; }
 
   // Times an engine phase on the context stream with CUDA events.
   struct Timed {

@@ -2371,19 +2371,47 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   }
 }
 
-struct PackSeg {
-  uint32_t src, dst, n, kind;  // kind 0 suspects, 1 evidence
-};
+// Dense packing of every trip's suspects, exonerated and evidence, planned
+// and copied on the device straight into mapped pinned host memory: the
+// host learns sizes and receives the data in the same round trip.
+// out[j] offsets are rewritten to the packed positions; tot = {sus, ev}.
+__global__ void k_pack_plan(TripOut* __restrict__ out, int32_t J,
+                            uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                            unsigned long long* __restrict__ tot) {
+  if (threadIdx.x || blockIdx.x) return;
+  uint64_t ns = 0, ne = 0;
+  for (int32_t j = 0; j < J; ++j) {
+    TripOut& t = out[j];
+    src[3 * j + 0] = t.sus_off;
+    dst[3 * j + 0] = static_cast<uint32_t>(ns);
+    t.sus_off = static_cast<uint32_t>(ns);
+    ns += t.n_sus;
+    src[3 * j + 1] = t.exo_off;
+    dst[3 * j + 1] = static_cast<uint32_t>(ns);
+    t.exo_off = static_cast<uint32_t>(ns);
+    ns += t.n_exo;
+    src[3 * j + 2] = t.ev_off;
+    dst[3 * j + 2] = static_cast<uint32_t>(ne);
+    t.ev_off = static_cast<uint32_t>(ne);
+    ne += t.n_ev;
+  }
+  tot[0] = ns;
+  tot[1] = ne;
+}
 
-__global__ void k_pack(const PackSeg* __restrict__ segs,
+__global__ void k_pack(const TripOut* __restrict__ out, const uint32_t* __restrict__ src,
+                       const uint32_t* __restrict__ dst,
                        const csg_suspect* __restrict__ sus,
                        const csg_evidence* __restrict__ ev,
                        csg_suspect* __restrict__ osus,
                        csg_evidence* __restrict__ oev) {
-  const PackSeg sg = segs[blockIdx.x];
-  for (uint32_t i = threadIdx.x; i < sg.n; i += blockDim.x) {
-    if (sg.kind == 0) osus[sg.dst + i] = sus[sg.src + i];
-    else oev[sg.dst + i] = ev[sg.src + i];
+  const int32_t j = blockIdx.x / 3, kind = blockIdx.x % 3;
+  const TripOut& t = out[j];
+  const uint32_t n = kind == 0 ? t.n_sus : kind == 1 ? t.n_exo : t.n_ev;
+  const uint32_t s0 = src[blockIdx.x], d0 = dst[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    if (kind < 2) osus[d0 + i] = sus[s0 + i];
+    else oev[d0 + i] = ev[s0 + i];
   }
 }
 
@@ -2791,6 +2819,16 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                                 static_cast<int>(shm)));
   uint32_t h_err = 0;
   unsigned long long used[8];
+  std::vector<TripOut> to(J);
+  unsigned long long ptot[2] = {0, 0};
+  DevBuf& d_psrc = c->buf("rca.pack_src");
+  DevBuf& d_pdst = c->buf("rca.pack_dst");
+  DevBuf& d_ptot = c->buf("rca.pack_tot");
+  d_psrc.ensure(static_cast<size_t>(J) * 12 + 4);
+  d_pdst.ensure(static_cast<size_t>(J) * 12 + 4);
+  d_ptot.ensure(16);
+  HostBuf& h_sus = c->hbuf("rca.packed_sus");
+  HostBuf& h_ev = c->hbuf("rca.packed_ev");
   for (int attempt = 0;; ++attempt) {
     p_cand.ensure(cand_cap * sizeof(Cand));
     p_cev.ensure(cev_cap * sizeof(csg_evidence));
@@ -2842,8 +2880,27 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ProfScope ps_(c->lc, "k_decide", st);
       k_decide<<<J, kDecideThreads, shm, st>>>(a);
     }
+    // pack straight into mapped host memory; the results, the trip table,
+    // the pool usage and the error word all come back in ONE round trip
+    {
+      ProfScope ps_(c->lc, "k_pack_plan", st);
+      k_pack_plan<<<1, 1, 0, st>>>(d_out.as<TripOut>(), J, d_psrc.as<uint32_t>(),
+                                   d_pdst.as<uint32_t>(), d_ptot.as<unsigned long long>());
+    }
+    h_sus.ensure(sus_cap * sizeof(csg_suspect) + 64);
+    h_ev.ensure(ev_cap * sizeof(csg_evidence) + 64);
+    if (J > 0) {
+      ProfScope ps_(c->lc, "k_pack", st);
+      k_pack<<<static_cast<unsigned>(3 * J), 128, 0, st>>>(
+          d_out.as<TripOut>(), d_psrc.as<uint32_t>(), d_pdst.as<uint32_t>(),
+          p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(), h_sus.as<csg_suspect>(),
+          h_ev.as<csg_evidence>());
+    }
     CSG_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
     CSG_CUDA(cudaMemcpyAsync(used, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(to.data(), d_out.p, J * sizeof(TripOut),
+                             cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(ptot, d_ptot.p, 16, cudaMemcpyDeviceToHost, st));
     CSG_CUDA(cudaStreamSynchronize(st));
     CSG_CUDA(cudaGetLastError());
     if (h_err & DEV_ERR_RC_TABLE)
@@ -2867,46 +2924,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     h_err &= ~(DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH);
     CSG_CUDA(cudaMemcpyAsync(err.p, &h_err, 4, cudaMemcpyHostToDevice, st));
   }
-  // ---- pack the reports densely and bring them back in three copies
-  std::vector<TripOut> to(J);
-  CSG_CUDA(cudaMemcpyAsync(to.data(), d_out.p, J * sizeof(TripOut),
-                           cudaMemcpyDeviceToHost, st));
-  CSG_CUDA(cudaStreamSynchronize(st));
-  std::vector<PackSeg> segs;
-  uint64_t ns_tot = 0, ne_tot = 0;
-  for (int32_t j = 0; j < J; ++j) {
-    TripOut& t = to[j];
-    segs.push_back(PackSeg{t.sus_off, static_cast<uint32_t>(ns_tot), t.n_sus, 0});
-    t.sus_off = static_cast<uint32_t>(ns_tot);
-    ns_tot += t.n_sus;
-    segs.push_back(PackSeg{t.exo_off, static_cast<uint32_t>(ns_tot), t.n_exo, 0});
-    t.exo_off = static_cast<uint32_t>(ns_tot);
-    ns_tot += t.n_exo;
-    segs.push_back(PackSeg{t.ev_off, static_cast<uint32_t>(ne_tot), t.n_ev, 1});
-    t.ev_off = static_cast<uint32_t>(ne_tot);
-    ne_tot += t.n_ev;
-  }
-  DevBuf& d_segs = c->buf("rca.segs");
-  DevBuf& d_psus = c->buf("rca.packed_sus");
-  DevBuf& d_pev = c->buf("rca.packed_ev");
-  upload(d_segs, segs, st);
-  d_psus.ensure(ns_tot * sizeof(csg_suspect) + 32);
-  d_pev.ensure(ne_tot * sizeof(csg_evidence) + 32);
-  {
-    ProfScope ps_(c->lc, "k_pack", st);
-    k_pack<<<static_cast<unsigned>(segs.size()), 128, 0, st>>>(
-        d_segs.as<PackSeg>(), p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
-        d_psus.as<csg_suspect>(), d_pev.as<csg_evidence>());
-  }
-  out.sus.resize(ns_tot);
-  out.ev.resize(ne_tot);
-  if (ns_tot)
-    CSG_CUDA(cudaMemcpyAsync(out.sus.data(), d_psus.p, ns_tot * sizeof(csg_suspect),
-                             cudaMemcpyDeviceToHost, st));
-  if (ne_tot)
-    CSG_CUDA(cudaMemcpyAsync(out.ev.data(), d_pev.p, ne_tot * sizeof(csg_evidence),
-                             cudaMemcpyDeviceToHost, st));
-  CSG_CUDA(cudaStreamSynchronize(st));
+  const uint64_t ns_tot = ptot[0], ne_tot = ptot[1];
+  out.sus.assign(h_sus.as<csg_suspect>(), h_sus.as<csg_suspect>() + ns_tot);
+  out.ev.assign(h_ev.as<csg_evidence>(), h_ev.as<csg_evidence>() + ne_tot);
   c->d2h_bytes += J * sizeof(TripOut) + ns_tot * sizeof(csg_suspect) +
                   ne_tot * sizeof(csg_evidence) + 8 * 8 + 4;
   out.trips = to;

@@ -7,6 +7,8 @@
 // serves the straggler self-evidence pass (proj/src/rca.cpp:803-815).
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -35,8 +37,22 @@ struct Profiler {
     }
     return pool[used++];
   }
-  // Call after the stream has been synchronized.
+  // Call after the stream has been synchronized. CSG_TIMELINE=1 prints
+  // every launch (start offset, duration, idle gap before it) to stderr.
   void collect() {
+    static const bool tl = std::getenv("CSG_TIMELINE") != nullptr;
+    if (tl && !pending.empty()) {
+      float prev_end = 0;
+      for (const Rec& r : pending) {
+        float s0 = 0, e0 = 0;
+        if (!r.b || cudaEventElapsedTime(&s0, pending[0].a, r.a) != cudaSuccess ||
+            cudaEventElapsedTime(&e0, pending[0].a, r.b) != cudaSuccess)
+          continue;
+        fprintf(stderr, "timeline %-22s start %9.1f us  dur %8.1f us  gap %8.1f us\n",
+                r.name, s0 * 1e3, (e0 - s0) * 1e3, (s0 - prev_end) * 1e3);
+        prev_end = e0;
+      }
+    }
     for (const Rec& r : pending) {
       float ms = 0;
       if (r.b && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {

@@ -278,20 +278,6 @@ __global__ void k_ema_single(const WinStat* __restrict__ ws,
   *tripped = hit;
 }
 
-// Tick times by FP accumulation exactly as runner.cpp:69-71:
-// for (t = I; t <= last_ts; t += I) if (t >= delta) evaluate.
-__global__ void k_ticks(double I, double last_ts, double delta, int64_t cap,
-                        double* __restrict__ ticks, int32_t* __restrict__ n) {
-  if (threadIdx.x || blockIdx.x) return;
-  int64_t c = 0;
-  for (double t = I; t <= last_ts; t = __dadd_rn(t, I)) {
-    if (t < delta) continue;
-    if (c < cap) ticks[c] = t;
-    ++c;
-  }
-  *n = static_cast<int32_t>(c < cap ? c : cap);
-}
-
 }  // namespace
 
 void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
@@ -320,25 +306,26 @@ void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
   CSG_CUDA(cudaGetLastError());
 }
 
+// Tick times by FP accumulation exactly as runner.cpp:69-71:
+// for (t = I; t <= last_ts; t += I) if (t >= delta) evaluate.
+// Computed on the host (plain IEEE adds, no contraction: the same doubles as
+// the reference's SSE2 loop) and uploaded without a device round trip.
 int32_t trigger_ticks(csg_store* s, double I, double delta, DevBuf& ticks) {
   csg_ctx* c = s->ctx;
-  // The loop runs while t <= last_ts; bound the tick count generously.
   const double est = s->last_ts / I;
   if (!(est < 5e7))
     throw Error(CSG_ERR_RUNTIME, "run_detection: too many detection ticks");
-  const int64_t cap = static_cast<int64_t>(est) + 4;
-  ticks.ensure(static_cast<size_t>(cap) * 8 + 8);
-  DevBuf& dn = c->buf("trig.ticks_n");
-  dn.ensure(4);
-  {
-    ProfScope ps_(c->lc, "k_ticks", c->stream);
-    k_ticks<<<1, 1, 0, c->stream>>>(I, s->last_ts, delta, cap, ticks.as<double>(),
-                                    dn.as<int32_t>());
+  std::vector<double>& h = c->h_ticks;
+  h.clear();
+  for (double t = I; t <= s->last_ts; t += I) {
+    if (t < delta) continue;
+    h.push_back(t);
   }
-  int32_t n = 0;
-  CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  CSG_CUDA(cudaStreamSynchronize(c->stream));
-  return n;
+  ticks.ensure(h.size() * 8 + 8);
+  if (!h.empty())
+    CSG_CUDA(cudaMemcpyAsync(ticks.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice,
+                             c->stream));
+  return static_cast<int32_t>(h.size());
 }
 
 int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
@@ -368,9 +355,15 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
                                             events.as<csg_trigger_event>(),
                                             dn.as<int32_t>());
   }
+  // one round trip: the trip count and every possible event slot together
+  c->h_events.resize(static_cast<size_t>(T) + 1);
   int32_t n = 0;
   CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CSG_CUDA(cudaMemcpyAsync(c->h_events.data(), events.p,
+                           static_cast<size_t>(T) * sizeof(csg_trigger_event),
+                           cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaStreamSynchronize(c->stream));
+  c->h_events.resize(static_cast<size_t>(n));
   return n;
 }
 
