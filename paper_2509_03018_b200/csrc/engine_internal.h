@@ -95,20 +95,32 @@ constexpr int kFlowBuf = 256;     // completions per (rank, op) in a window
 constexpr uint32_t kNoPos = 0xFFFFFFFFu;
 
 // Rank-major, structure-of-arrays view of the store built by the index.
+// Interleaved column: element i is field OFF of a STRIDE-wide rank-major
+// record. The index builder writes {ts, op_seq}, {comm, channel} and the
+// 16-byte payload with one wide store each (fewer, fuller sectors on the
+// scattered write side); readers index columns as before.
+template <typename T, int STRIDE, int OFF>
+struct ColView {
+  const T* p = nullptr;
+  __host__ __device__ __forceinline__ T operator[](uint64_t i) const {
+    return p[i * STRIDE + OFF];
+  }
+};
+
 struct StoreView {
   uint64_t n = 0;          // records
   int32_t R = 0;           // rank space [0, R)
   int32_t nch = 0;         // channel space [0, nch)
   const uint32_t* rank_off = nullptr;  // [R+1]
   const uint32_t* perm = nullptr;      // rank-major pos -> store index
-  const double* ts = nullptr;
   const double* runmax = nullptr;      // per-rank running max of ts
-  const int64_t* op = nullptr;
-  const int32_t* comm = nullptr;
-  const int32_t* chan = nullptr;
+  ColView<double, 2, 0> ts;            // {ts, op_seq} pairs
+  ColView<int64_t, 2, 1> op;
+  ColView<int32_t, 2, 0> comm;         // {comm, channel} pairs
+  ColView<int32_t, 2, 1> chan;
   const uint8_t* ko = nullptr;         // kind | op_name << 1
-  const uint64_t* pa = nullptr;        // start_ms bits | ready | tx << 32
-  const uint64_t* pb = nullptr;        // msg_bytes | done
+  ColView<uint64_t, 2, 0> pa;          // payload pairs: start_ms bits | ready | tx << 32
+  ColView<uint64_t, 2, 1> pb;          //                msg_bytes | done
 };
 
 // Rank owning rank-major position p (p < n): upper_bound over rank_off.

@@ -74,7 +74,10 @@ struct csg_store {
   // rank-major index
   int32_t R = 0, nch = 0;
   uint64_t max_seg = 0;  // longest rank segment
-  csg::DevBuf rank_off, perm, keys, ts, runmax, op, comm, chan, ko, pa, pb;
+  csg::DevBuf rank_off, perm, keys, runmax, ko;
+  csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
+  csg::DevBuf cc;   // {comm, channel} (8 B)
+  csg::DevBuf pay;  // {start_ms | ready,tx ; msg_bytes | done} (16 B)
   csg::SortScratch sort;
   // op-ordered completion index for the straggler self-evidence pass
   bool op_indexed = false;
@@ -104,14 +107,14 @@ struct csg_store {
     v.nch = nch;
     v.rank_off = rank_off.as<uint32_t>();
     v.perm = perm.as<uint32_t>();
-    v.ts = ts.as<double>();
     v.runmax = runmax.as<double>();
-    v.op = op.as<int64_t>();
-    v.comm = comm.as<int32_t>();
-    v.chan = chan.as<int32_t>();
+    v.ts.p = tso.as<double>();
+    v.op.p = tso.as<int64_t>();
+    v.comm.p = cc.as<int32_t>();
+    v.chan.p = cc.as<int32_t>();
     v.ko = ko.as<uint8_t>();
-    v.pa = pa.as<uint64_t>();
-    v.pb = pb.as<uint64_t>();
+    v.pa.p = pay.as<uint64_t>();
+    v.pb.p = pay.as<uint64_t>();
     return v;
   }
   csg::FlowView flow_view() const {

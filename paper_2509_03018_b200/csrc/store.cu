@@ -274,13 +274,10 @@ __global__ void k_rank_off_hist(const uint32_t* __restrict__ goff, uint32_t T,
 }
 
 struct ScatterOut {
-  double* ts;
-  int64_t* op;
-  int32_t* comm;
-  int32_t* chan;
-  uint8_t* ko;
-  uint64_t* pa;
-  uint64_t* pb;
+  ulonglong2* tso;  // {ts, op_seq}
+  int2* cc;         // {comm, channel}
+  uint8_t* ko;      // kind | op_name << 1
+  ulonglong2* pay;  // payload pair
   uint32_t* perm;   // store index per rank-major position
 };
 
@@ -329,7 +326,7 @@ template <int ITEMS>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
-              int32_t D, ScatterOut o) {
+              int32_t D, ScatterOut o, int mode) {
   constexpr int kW = kTileThreads / 32;
   constexpr int TR = kTileThreads * ITEMS;
   constexpr int SUB = kTile / TR;
@@ -462,6 +459,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     // of one digit run. Four records per thread in flight (independent
     // shared-memory chains; 8 warps per SM leave little else to hide them).
     constexpr int kB = 4;
+    if (mode != 2)
     for (uint32_t p0 = tid; p0 < cnt; p0 += kB * kTileThreads) {
       uint32_t li[kB], q[kB];
       ulonglong2 h0[kB], hm[kB], h1[kB];
@@ -488,17 +486,17 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         const uint32_t p = p0 + k * kTileThreads;
         if (p >= cnt) break;
         const uint32_t qq = q[k];
-        double tv;
-        memcpy(&tv, &h0[k].x, 8);
-        o.ts[qq] = tv;
-        o.op[qq] = static_cast<int64_t>(h0[k].y);
-        o.comm[qq] = static_cast<int32_t>(hm[k].x >> 32);
-        o.chan[qq] = static_cast<int32_t>(hm[k].y & 0xffffffffu);
+        if (mode == 1) {
+          if (qq == 0xFFFFFFFFu) o.ko[0] = static_cast<uint8_t>(h0[k].x + hm[k].y + h1[k].x);
+          continue;
+        }
+        o.tso[qq] = h0[k];
+        o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
+                             static_cast<int32_t>(hm[k].y & 0xffffffffu));
         const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
         const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
         o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
-        o.pa[qq] = h1[k].x;
-        o.pb[qq] = (kind & 1) ? (h1[k].y & 0xffffffffull) : h1[k].y;
+        o.pay[qq] = make_ulonglong2(h1[k].x, (kind & 1) ? (h1[k].y & 0xffffffffull) : h1[k].y);
         o.perm[qq] = static_cast<uint32_t>(first + li[k]);
       }
     }
@@ -520,7 +518,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // segments whose op_seq descends in store order (the flow index permutes
 // only those, see k_flow_fix) and appends them to a work list.
 __global__ void __launch_bounds__(1024)
-    k_runmax_blk(const double* __restrict__ ts, const int64_t* __restrict__ op,
+    k_runmax_blk(const ulonglong2* __restrict__ tso,
                  const uint32_t* __restrict__ off, double* __restrict__ out,
                  uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
                  unsigned* __restrict__ cnt) {
@@ -536,9 +534,12 @@ __global__ void __launch_bounds__(1024)
   double m = -INFINITY;
   bool dsc = false;
   for (uint32_t p = pb + lane; p < pe; p += 32) {
-    const double x = __ldg(ts + p);
+    const ulonglong2 v = __ldg(tso + p);
+    double x;
+    memcpy(&x, &v.x, 8);
     if (x == x) m = fmax(m, x);  // NaN never breaks a prefix
-    if (p > b) dsc |= __ldg(op + p) < __ldg(op + p - 1);
+    if (p > b) dsc |= static_cast<long long>(v.y) <
+                      static_cast<long long>(__ldg(&tso[p - 1].y));
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -549,7 +550,11 @@ __global__ void __launch_bounds__(1024)
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
   for (uint32_t base = pb; base < pe; base += 32) {
     const uint32_t p = base + lane;
-    double x = p < pe ? __ldg(ts + p) : -INFINITY;
+    double x = -INFINITY;
+    if (p < pe) {
+      const unsigned long long u = __ldg(&tso[p].x);
+      memcpy(&x, &u, 8);
+    }
     if (x != x) x = -INFINITY;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -580,32 +585,22 @@ __global__ void k_rank_off(const uint32_t* __restrict__ keys, uint64_t n,
   off[r] = static_cast<uint32_t>(lo);
 }
 
-// Gather packed AoS records into rank-major SoA columns.
+// Gather packed AoS records into rank-major columns (general index path).
 __global__ void k_gather(const csg_packed_record* __restrict__ r,
-                         const uint32_t* __restrict__ perm, uint64_t n,
-                         double* __restrict__ ts, int64_t* __restrict__ op,
-                         int32_t* __restrict__ comm, int32_t* __restrict__ chan,
-                         uint8_t* __restrict__ ko, uint64_t* __restrict__ pa,
-                         uint64_t* __restrict__ pb) {
+                         const uint32_t* __restrict__ perm, uint64_t n, ScatterOut o) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     // 48-byte records are 16-byte aligned: three 16-byte vector loads.
     const ulonglong2* rec =
         reinterpret_cast<const ulonglong2*>(r + perm[p]);
     const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1), h1 = __ldg(rec + 2);
-    double t;
-    memcpy(&t, &h0.x, 8);
-    ts[p] = t;
-    op[p] = static_cast<int64_t>(h0.y);
-    const uint64_t w2 = hm.x, w3 = hm.y;
-    comm[p] = static_cast<int32_t>(w2 >> 32);
-    chan[p] = static_cast<int32_t>(w3 & 0xffffffffu);
-    const uint8_t kind = static_cast<uint8_t>((w3 >> 32) & 0xff);
-    const uint8_t name = static_cast<uint8_t>((w3 >> 40) & 0xff);
-    ko[p] = static_cast<uint8_t>((kind & 1) | (name << 1));
-    pa[p] = h1.x;  // start_ms bits | ready | tx << 32
-    pb[p] = h1.y;  // msg_bytes | done (| reserved << 32)
-    if (kind & 1) pb[p] = h1.y & 0xffffffffull;
+    o.tso[p] = h0;
+    o.cc[p] = make_int2(static_cast<int32_t>(hm.x >> 32),
+                        static_cast<int32_t>(hm.y & 0xffffffffu));
+    const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
+    const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
+    o.ko[p] = static_cast<uint8_t>((kind & 1) | (name << 1));
+    o.pay[p] = make_ulonglong2(h1.x, (kind & 1) ? (h1.y & 0xffffffffull) : h1.y);
   }
 }
 
@@ -620,7 +615,8 @@ __global__ void k_opidx_fill(StoreView s, const uint32_t* __restrict__ pos,
     rank[i] = rank_at(s, p);
     const double t = s.ts[p];
     double st;
-    memcpy(&st, &s.pa[p], 8);
+    const uint64_t pa = s.pa[p];
+    memcpy(&st, &pa, 8);
     ts[i] = t;
     dur[i] = t - st;
     nm[i] = static_cast<uint8_t>(ko_opname(s.ko[p]));
@@ -1006,14 +1002,11 @@ void store_build_index(csg_store* s) {
   const int32_t R = s->R;
 
   s->rank_off.ensure((static_cast<size_t>(R) + 1) * 4);
-  s->ts.ensure(n * 8 + 8);
+  s->tso.ensure(n * 16 + 16);
   s->runmax.ensure(n * 8 + 8);
-  s->op.ensure(n * 8 + 8);
-  s->comm.ensure(n * 4 + 4);
-  s->chan.ensure(n * 4 + 4);
+  s->cc.ensure(n * 8 + 8);
   s->ko.ensure(n + 8);
-  s->pa.ensure(n * 8 + 8);
-  s->pb.ensure(n * 8 + 8);
+  s->pay.ensure(n * 16 + 16);
   static const bool force_general = std::getenv("CSG_INDEX_RADIX") != nullptr;
   const bool fused = n && !force_general &&
                      static_cast<int64_t>(h.lmax_rank) - h.lmin_rank < kHistDigits;
@@ -1039,9 +1032,8 @@ void store_build_index(csg_store* s) {
       k_hist_scan_apply<<<static_cast<unsigned>(nb), kTileThreads, 0, st>>>(
           hcnt.as<uint32_t>(), M, ntiles, d0, sums.as<uint32_t>(), goff.as<uint32_t>());
     }
-    ScatterOut o{s->ts.as<double>(), s->op.as<int64_t>(), s->comm.as<int32_t>(),
-                 s->chan.as<int32_t>(), s->ko.as<uint8_t>(), s->pa.as<uint64_t>(),
-                 s->pb.as<uint64_t>(), s->perm.as<uint32_t>()};
+    ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
+                 s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
     // sub-tiles of 2048 records (1024 when the digit span needs the room)
     const bool wide = D > 1024;
     const int TR = wide ? 1024 : 2048;
@@ -1056,14 +1048,15 @@ void store_build_index(csg_store* s) {
       attr = true;
     }
     const unsigned grid = std::min<unsigned>(ntiles, 148);
+    static const int smode = std::getenv("CSG_SCATTER_MODE") ? std::atoi(std::getenv("CSG_SCATTER_MODE")) : 0;
     {
       ProfScope ps_(c->lc, "k_scatter", st);
       if (wide)
         k_scatter<4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
-                                                       lmin, D, o);
+                                                       lmin, D, o, smode);
       else
         k_scatter<8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
-                                                       lmin, D, o);
+                                                       lmin, D, o, smode);
     }
     {
       ProfScope ps_(c->lc, "k_rank_off", st);
@@ -1087,10 +1080,9 @@ void store_build_index(csg_store* s) {
                      st, c->lc);
       {
         ProfScope ps_(c->lc, "k_gather", st);
-        k_gather<<<grid_for(n), 256, 0, st>>>(
-            recs, s->perm.as<uint32_t>(), n, s->ts.as<double>(),
-            s->op.as<int64_t>(), s->comm.as<int32_t>(), s->chan.as<int32_t>(),
-            s->ko.as<uint8_t>(), s->pa.as<uint64_t>(), s->pb.as<uint64_t>());
+        ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
+                     s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
+        k_gather<<<grid_for(n), 256, 0, st>>>(recs, s->perm.as<uint32_t>(), n, o);
       }
     }
     {
@@ -1108,7 +1100,7 @@ void store_build_index(csg_store* s) {
   CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
   if (n && R) {
     ProfScope ps_(c->lc, "k_runmax", st);
-    k_runmax_blk<<<R, 1024, 0, st>>>(s->ts.as<double>(), s->op.as<int64_t>(),
+    k_runmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(),
                                      s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
                                      s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(),
                                      fcnt.as<unsigned>());
