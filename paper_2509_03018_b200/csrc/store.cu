@@ -13,6 +13,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "comm.cuh"
@@ -322,19 +323,19 @@ __device__ inline void mbar_wait(unsigned long long* m, uint32_t parity) {
 // is written once into the rank-major SoA columns in contiguous digit runs.
 // bx[d] carries the running global base of digit d through the sub-tiles of
 // one histogram tile.
-template <int ITEMS>
-__global__ void __launch_bounds__(kTileThreads, 1)
+template <int ITEMS, int NBUF, int DPT>
+__global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
               int32_t D, ScatterOut o, int mode) {
   constexpr int kW = kTileThreads / 32;
   constexpr int TR = kTileThreads * ITEMS;
   constexpr int SUB = kTile / TR;
-  constexpr int kMaxPer = kHistDigits / kTileThreads;  // digits per thread
+  constexpr int Dp = DPT * kTileThreads;  // padded digit stride (DPT per thread)
   extern __shared__ __align__(128) unsigned char dyn[];
   unsigned char* buf0 = dyn;
-  uint16_t* wc = reinterpret_cast<uint16_t*>(dyn + 2 * TR * 48);  // [kW][D]
-  uint32_t* bx = reinterpret_cast<uint32_t*>(wc + kW * ((D + 1) & ~1));
+  uint16_t* wc = reinterpret_cast<uint16_t*>(dyn + NBUF * TR * 48);  // [kW][Dp]
+  uint32_t* bx = reinterpret_cast<uint32_t*>(wc + kW * Dp);           // [Dp]
   __shared__ uint16_t sidx[TR];
   __shared__ uint32_t wsum[32];
   __shared__ __align__(8) unsigned long long mbar[2];
@@ -353,43 +354,45 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   auto issue = [&](uint32_t j) {
     uint32_t t, cnt;
     uint64_t first;
+    const int b = NBUF == 2 ? (j & 1) : 0;
     if (tid == 0 && sub_of(j, t, first, cnt) && cnt)
-      bulk_load(buf0 + (j & 1) * TR * 48, r + first, cnt * 48, &mbar[j & 1]);
+      bulk_load(buf0 + b * TR * 48, r + first, cnt * 48, &mbar[b]);
   };
   uint32_t par0 = 0, par1 = 0;
-  issue(0);
+  if (NBUF == 2) issue(0);
   for (uint32_t j = 0;; ++j) {
     uint32_t t, cnt;
     uint64_t first;
     if (!sub_of(j, t, first, cnt)) break;
-    issue(j + 1);  // its buffer was released by the barrier ending j - 1
+    // double buffer: prefetch the next sub-tile into the buffer released by
+    // the barrier ending j - 1; single buffer (several CTAs per SM cover
+    // each other's load latency): load this one now
+    issue(NBUF == 2 ? j + 1 : j);
     // a new histogram tile starts from its scanned global bases: loaded now,
     // consumed after phase A (latency hidden)
     const bool fresh = j % SUB == 0;
-    uint32_t g0[kMaxPer];
+    uint32_t g0[DPT];
     if (fresh) {
 #pragma unroll
-      for (int i = 0; i < kMaxPer; ++i) {
-        const int dd = i * kTileThreads + tid;
-        g0[i] = dd < D ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
+      for (int k = 0; k < DPT; ++k) {
+        const int dd = tid * DPT + k;
+        g0[k] = dd < D ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
       }
     }
     if (cnt == 0) {
+      if (fresh)
 #pragma unroll
-      for (int i = 0; i < kMaxPer; ++i) {
-        const int dd = i * kTileThreads + tid;
-        if (fresh && dd < D) bx[dd] = g0[i];
-      }
+        for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = g0[k];
       __syncthreads();
       continue;
     }
-    const unsigned char* sb = buf0 + (j & 1) * TR * 48;
+    const unsigned char* sb = buf0 + (NBUF == 2 ? (j & 1) : 0) * TR * 48;
     {  // clear the warp counters, 16 bytes per store
       uint4* w4 = reinterpret_cast<uint4*>(wc);
-      const int n4 = (kW * ((D + 1) & ~1) * 2 + 15) / 16;
+      constexpr int n4 = kW * Dp * 2 / 16;
       for (int i = tid; i < n4; i += kTileThreads) w4[i] = make_uint4(0, 0, 0, 0);
     }
-    if (j & 1) {
+    if (NBUF == 2 && (j & 1)) {
       mbar_wait(&mbar[1], par1);
       par1 ^= 1;
     } else {
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                             *reinterpret_cast<const int32_t*>(sb + li * 48 + 16) - min_rank)
                       : 0xFFFFFFFFu;
     }
-    uint16_t* mine = wc + warp * D;
+    uint16_t* mine = wc + warp * Dp;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const bool valid = d[k] != 0xFFFFFFFFu;
@@ -421,33 +424,54 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
     }
     __syncthreads();
-    // per digit: cross-warp prefix + sub-tile start folded into the warp
-    // counters; bx becomes (running base - sub-tile start) for phase B
-    uint32_t nxt[kMaxPer];
-    uint32_t carry = 0;
+    // per digit (thread t owns digits [DPT*t, DPT*t + DPT), one vector load
+    // per warp row): cross-warp prefix + sub-tile start folded into the
+    // warp counters; bx becomes (running base - sub-tile start) for phase B
+    using VecT = typename std::conditional<DPT == 8, uint4, uint2>::type;
+    union DV {
+      VecT v;
+      uint16_t h[DPT];
+    };
+    uint32_t tot[DPT];
 #pragma unroll
-    for (int i = 0; i < kMaxPer; ++i) {
-      const int dd = i * kTileThreads + tid;
-      if (i * kTileThreads >= D) break;  // block-uniform
-      uint32_t tot = 0;
-      uint16_t pre[kW];
-      if (dd < D) {
+    for (int k = 0; k < DPT; ++k) tot[k] = 0;
 #pragma unroll
-        for (int w = 0; w < kW; ++w) {
-          pre[w] = static_cast<uint16_t>(tot);
-          tot += wc[w * D + dd];
+    for (int w = 0; w < kW; ++w) {
+      DV x;
+      x.v = *reinterpret_cast<const VecT*>(wc + w * Dp + tid * DPT);
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) tot[k] += x.h[k];
+    }
+    uint32_t mysum = 0;
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) mysum += tot[k];
+    uint32_t ts0[DPT];
+    ts0[0] = block_excl_scan_u32(mysum, wsum, nullptr);
+#pragma unroll
+    for (int k = 1; k < DPT; ++k) ts0[k] = ts0[k - 1] + tot[k - 1];
+    {
+      uint32_t run[DPT];
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) run[k] = ts0[k];
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        DV x, y;
+        x.v = *reinterpret_cast<const VecT*>(wc + w * Dp + tid * DPT);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+          y.h[k] = static_cast<uint16_t>(run[k]);
+          run[k] += x.h[k];
         }
+        *reinterpret_cast<VecT*>(wc + w * Dp + tid * DPT) = y.v;
       }
-      uint32_t all;
-      const uint32_t ts0 = carry + block_excl_scan_u32(tot, wsum, &all);
-      if (dd < D) {
+    }
+    uint32_t nxt[DPT];
 #pragma unroll
-        for (int w = 0; w < kW; ++w) wc[w * D + dd] = static_cast<uint16_t>(ts0 + pre[w]);
-        const uint32_t rb = fresh ? g0[i] : bx[dd];
-        nxt[i] = rb + tot;
-        bx[dd] = rb - ts0;
-      }
-      carry += all;
+    for (int k = 0; k < DPT; ++k) {
+      const int dd = tid * DPT + k;
+      const uint32_t rb = fresh ? g0[k] : bx[dd];
+      nxt[k] = rb + tot[k];
+      bx[dd] = rb - ts0[k];
     }
     __syncthreads();
 #pragma unroll
@@ -502,11 +526,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kMaxPer; ++i) {
-      const int dd = i * kTileThreads + tid;
-      if (i * kTileThreads >= D) break;
-      if (dd < D) bx[dd] = nxt[i];
-    }
+    for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = nxt[k];
     __syncthreads();
   }
 }
@@ -1034,29 +1054,44 @@ void store_build_index(csg_store* s) {
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
                  s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
-    // sub-tiles of 2048 records (1024 when the digit span needs the room)
-    const bool wide = D > 1024;
-    const int TR = wide ? 1024 : 2048;
-    const size_t smem = 2ull * TR * 48 + (kTileThreads / 32) * ((D + 1) & ~1) * 2 +
-                        static_cast<size_t>(D) * 4;
+    // Rank spans <= 1024: 2048-record sub-tiles double-buffered in one CTA
+    // per SM. Wider spans (or CSG_SCATTER_CFG=2): 1024-record sub-tiles, one
+    // bulk-copy buffer per CTA, several CTAs per SM.
+    static const int cfg = std::getenv("CSG_SCATTER_CFG") ? std::atoi(std::getenv("CSG_SCATTER_CFG")) : 0;
+    const bool dbl = cfg != 2 && D <= 1024;
+    const int TR = dbl ? 2048 : 1024;
+    const int nbuf = dbl ? 2 : 1;
+    const int Dp = (D <= 1024 ? 4 : 8) * kTileThreads;
+    const size_t smem = static_cast<size_t>(nbuf) * TR * 48 +
+                        (kTileThreads / 32) * static_cast<size_t>(Dp) * 2 +
+                        static_cast<size_t>(Dp) * 4;
     static bool attr = false;
     if (!attr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * 1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    1024 * 48 + 8 * 1024 * 2 + 1024 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
       attr = true;
     }
-    const unsigned grid = std::min<unsigned>(ntiles, 148);
+    int per_sm = 1;
+    if (!dbl)
+      CSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, D <= 1024 ? k_scatter<4, 1, 4> : k_scatter<4, 1, 8>, kTileThreads, smem));
+    const unsigned grid = std::min<unsigned>(ntiles, 148u * std::max(per_sm, 1));
     static const int smode = std::getenv("CSG_SCATTER_MODE") ? std::atoi(std::getenv("CSG_SCATTER_MODE")) : 0;
     {
       ProfScope ps_(c->lc, "k_scatter", st);
-      if (wide)
-        k_scatter<4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
-                                                       lmin, D, o, smode);
+      if (dbl)
+        k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
+                                                             ntiles, lmin, D, o, smode);
+      else if (D <= 1024)
+        k_scatter<4, 1, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
+                                                             ntiles, lmin, D, o, smode);
       else
-        k_scatter<8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(), ntiles,
-                                                       lmin, D, o, smode);
+        k_scatter<4, 1, 8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
+                                                             ntiles, lmin, D, o, smode);
     }
     {
       ProfScope ps_(c->lc, "k_rank_off", st);
