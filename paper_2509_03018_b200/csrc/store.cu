@@ -568,22 +568,36 @@ __global__ void __launch_bounds__(1024)
   if (dsc) desc = 1;
   double carry = -INFINITY;
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
-  for (uint32_t base = pb; base < pe; base += 32) {
-    const uint32_t p = base + lane;
-    double x = -INFINITY;
-    if (p < pe) {
-      const unsigned long long u = __ldg(&tso[p].x);
-      memcpy(&x, &u, 8);
+  // 256-element chunks: each lane scans 8 consecutive elements sequentially,
+  // one warp scan of the lane maxima, then the lane's carry-in is applied
+  // (one shuffle scan per 256 elements instead of per 32)
+  constexpr int kE = 8;
+  for (uint32_t base = pb; base < pe; base += 32 * kE) {
+    const uint32_t q0 = base + lane * kE;
+    double x[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      x[k] = -INFINITY;
+      if (q0 + k < pe) {
+        const unsigned long long u = __ldg(&tso[q0 + k].x);
+        memcpy(&x[k], &u, 8);
+        if (x[k] != x[k]) x[k] = -INFINITY;
+      }
     }
-    if (x != x) x = -INFINITY;
+#pragma unroll
+    for (int k = 1; k < kE; ++k) x[k] = fmax(x[k], x[k - 1]);
+    double m = x[kE - 1];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x = fmax(x, y);
+      const double y = __shfl_up_sync(0xffffffffu, m, o);
+      if (lane >= o) m = fmax(m, y);
     }
-    x = fmax(x, carry);
-    carry = __shfl_sync(0xffffffffu, x, 31);
-    if (p < pe) out[p] = x;
+    double cin = __shfl_up_sync(0xffffffffu, m, 1);
+    cin = lane ? fmax(cin, carry) : carry;
+#pragma unroll
+    for (int k = 0; k < kE; ++k)
+      if (q0 + k < pe) out[q0 + k] = fmax(x[k], cin);
+    carry = fmax(carry, __shfl_sync(0xffffffffu, m, 31));
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -255,6 +255,176 @@ __global__ void k_pick_trips(const uint8_t* __restrict__ trip,
   if (threadIdx.x == 0) *n_events = base;
 }
 
+// Whole trigger stage of run_detection in one launch (unsharded stores):
+//   1. window statistics: grid (B, S); block (b, s) bins chunk b of sampled
+//      rank s's segment into per-tick shared-memory bins (as k_window_bins)
+//      and merges them into zero-initialised global accumulators (ordered
+//      timestamp keys: max via atomicMax, min via atomicMax of the
+//      complemented key);
+//   2. the last block of each sampled rank runs its EMA recurrence over all
+//      ticks (evaluate, trigger.cpp:57-136) from the accumulators staged in
+//      shared memory;
+//   3. the last rank to finish picks the lowest tripped rank of every tick
+//      and compacts the trips in tick order (runner.cpp:72-79).
+struct WinAcc {
+  unsigned int n_rec, n_comp, has_state, pad;
+  unsigned long long bytes, mn_inv, mx;
+};
+
+__global__ void __launch_bounds__(512)
+    k_trigger(StoreView s, const double* __restrict__ ticks, int32_t T,
+              const int32_t* __restrict__ sampled, int32_t S, TrigParams p, int32_t B,
+              WinAcc* __restrict__ acc, unsigned* __restrict__ done,
+              uint8_t* __restrict__ trip, csg_trigger_event* __restrict__ events,
+              int32_t* __restrict__ n_events) {
+  extern __shared__ __align__(16) unsigned char tg_dyn[];
+  double* st = reinterpret_cast<double*>(tg_dyn);                       // [T]
+  unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
+  unsigned long long* mn = bytes + T;  // complemented keys (max = min)
+  unsigned long long* mx = mn + T;
+  uint32_t* nrec = reinterpret_cast<uint32_t*>(mx + T);
+  uint32_t* ncomp = nrec + T;
+  uint32_t* hstate = ncomp + T;
+  __shared__ int last;
+  const int32_t si = blockIdx.y, bi = blockIdx.x;
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    st[k] = ticks[k];
+    bytes[k] = mn[k] = mx[k] = 0;
+    nrec[k] = ncomp[k] = hstate[k] = 0;
+  }
+  __syncthreads();
+  const double delta = p.delta;
+  const int32_t r = sampled[si];
+  if (r >= 0 && r < s.R) {
+    const uint32_t b0 = s.rank_off[r], L = s.rank_off[r + 1] - b0;
+    const uint32_t cb = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * bi / B);
+    const uint32_t ce = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * (bi + 1) / B);
+    for (uint32_t q = cb + threadIdx.x; q < ce; q += blockDim.x) {
+      const double x = s.ts[q];
+      int32_t lo = 0, hi = T;  // first tick with t_k >= x
+      while (lo < hi) {
+        const int32_t md = (lo + hi) >> 1;
+        if (st[md] < x) lo = md + 1; else hi = md;
+      }
+      const bool comp = ko_kind(s.ko[q]) == CSG_KIND_COMPLETION;
+      for (int32_t k = lo; k < T && !(x < st[k] - delta); ++k) {
+        if (x > st[k]) continue;
+        atomicAdd(&nrec[k], 1u);
+        if (comp) {
+          atomicAdd(&ncomp[k], 1u);
+          atomicAdd(&bytes[k], static_cast<unsigned long long>(s.pb[q]));
+          const unsigned long long kk = dkey(x);
+          atomicMax(&mn[k], ~kk);
+          atomicMax(&mx[k], kk);
+        } else {
+          hstate[k] = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    if (!nrec[k]) continue;
+    WinAcc& a = acc[static_cast<int64_t>(k) * S + si];
+    atomicAdd(&a.n_rec, nrec[k]);
+    if (hstate[k]) atomicOr(&a.has_state, 1u);
+    if (ncomp[k]) {
+      atomicAdd(&a.n_comp, ncomp[k]);
+      atomicAdd(&a.bytes, bytes[k]);
+      atomicMax(&a.mn_inv, mn[k]);
+      atomicMax(&a.mx, mx[k]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&done[si], 1u) == static_cast<unsigned>(B - 1);
+  __syncthreads();
+  if (!last) return;
+  // ---- last block of sampled rank si: EMA over the ticks
+  __threadfence();
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    const WinAcc* a = acc + static_cast<int64_t>(k) * S + si;
+    nrec[k] = __ldcg(&a->n_rec);
+    ncomp[k] = __ldcg(&a->n_comp);
+    hstate[k] = __ldcg(&a->has_state);
+    bytes[k] = __ldcg(&a->bytes);
+    mn[k] = __ldcg(&a->mn_inv);
+    mx[k] = __ldcg(&a->mx);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TrigSlot b{0, 0, 0, 0, 0, 0};
+    for (int32_t k = 0; k < T; ++k) {
+      WinStat w;
+      w.n_rec = nrec[k];
+      w.n_comp = ncomp[k];
+      w.has_state = hstate[k];
+      w.pad = 0;
+      w.bytes = bytes[k];
+      w.min_end = ncomp[k] ? dkey_inv(~mn[k]) : 0.0;
+      w.max_end = ncomp[k] ? dkey_inv(mx[k]) : 0.0;
+      trip[static_cast<int64_t>(k) * S + si] = static_cast<uint8_t>(ema_step(b, w, p));
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&done[S], 1u) == static_cast<unsigned>(S - 1);
+  __syncthreads();
+  if (!last) return;
+  // ---- last rank: lowest tripped sampled rank per tick, compacted in order
+  __threadfence();
+  __shared__ int32_t base;
+  __shared__ int32_t wsum[32];
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t k0 = 0; k0 < T; k0 += blockDim.x) {
+    const int32_t k = k0 + threadIdx.x;
+    int kind = -1, rank = -1;
+    if (k < T) {
+      for (int32_t q = 0; q < S; ++q) {
+        const uint8_t c = __ldcg(trip + static_cast<int64_t>(k) * S + q);
+        if (c) {
+          kind = c == 1 ? CSG_TRIGGER_FAILURE : CSG_TRIGGER_STRAGGLER;
+          rank = sampled[q];
+          break;
+        }
+      }
+    }
+    const int hit = kind >= 0;
+    int x = hit;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const int excl = (warp ? wsum[warp - 1] : 0) + x - hit;
+    if (hit) {
+      csg_trigger_event e;
+      e.kind = kind;
+      e.suspect_rank = rank;
+      e.time_ms = st[k];
+      events[base + excl] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_events = base;
+}
+
 // csg_evaluate: one tick, the caller's sampled list in order (duplicates
 // allowed, exactly like the reference loop), baselines persisted in the
 // state's per-rank slots.
@@ -340,6 +510,28 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
+  const size_t tsmem = static_cast<size_t>(T) * 44;
+  if (!comm_active(c) && tsmem <= 200 * 1024) {
+    DevBuf& acc = c->buf("trig.acc");
+    const size_t abytes = static_cast<size_t>(T) * S * sizeof(WinAcc);
+    acc.ensure(abytes + (static_cast<size_t>(S) + 1) * 4 + 16);
+    CSG_CUDA(cudaMemsetAsync(acc.p, 0, abytes + (static_cast<size_t>(S) + 1) * 4, c->stream));
+    // about 2k records per block of a sampled rank's segment
+    const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, s->max_seg / 2048)));
+    static bool attr = false;
+    if (!attr) {
+      CSG_CUDA(cudaFuncSetAttribute(k_trigger, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
+      attr = true;
+    }
+    {
+      ProfScope ps_(c->lc, "k_trigger", c->stream);
+      k_trigger<<<dim3(B, S), 512, tsmem, c->stream>>>(
+          s->view(), d_ticks, T, d_sampled, S, p, B, acc.as<WinAcc>(),
+          reinterpret_cast<unsigned*>(acc.as<unsigned char>() + abytes), trip.as<uint8_t>(),
+          events.as<csg_trigger_event>(), dn.as<int32_t>());
+    }
+  } else {
   trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
   comm_allreduce(c, ws.p, static_cast<size_t>(T) * S * sizeof(WinStat) / 8, ncclUint64,
                  ncclSum);
@@ -354,6 +546,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
                                             d_sampled, S,
                                             events.as<csg_trigger_event>(),
                                             dn.as<int32_t>());
+  }
   }
   // one round trip: the trip count and every possible event slot together
   c->h_events.resize(static_cast<size_t>(T) + 1);
