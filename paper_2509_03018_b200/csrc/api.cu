@@ -3,6 +3,7 @@
 // crosses this boundary; every entry point maps failures to csg_status and
 // the thread-local message of csg_last_error().
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -420,6 +421,8 @@ csg_status csg_model_create(csg_ctx* ctx, const csg_topology_desc* td,
     CSG_CUDA(cudaSetDevice(ctx->device));
     auto m = std::make_unique<csg_model>();
     m->ctx = ctx;
+    static std::atomic<uint64_t> next_uid{1};
+    m->uid = next_uid++;
     const int32_t G = td->n_groups;
     const int32_t opn = pd->n_ops;
     if (G < 0 || opn < 0) throw Error(CSG_ERR_ARG, "negative table size");

@@ -57,6 +57,7 @@ struct HostBuf {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  HostBuf stage;  // pinned staging for asynchronous uploads (see upload())
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;

@@ -30,6 +30,7 @@ struct csg_ctx {
   std::map<std::string, csg::DevBuf> arena;
   csg::DevBuf& buf(const char* name) { return arena[name]; }
   std::map<std::string, csg::HostBuf> host_arena;  // mapped pinned buffers
+  uint64_t slot_group_uid = 0;  // model whose slot -> group table is in "rca.slot_group"
   csg::HostBuf& hbuf(const char* name) { return host_arena[name]; }
 
   // Times an engine phase on the context stream with CUDA events.
@@ -58,6 +59,7 @@ struct StoreStats {
   unsigned long long n_nan;
   unsigned long long n_total;  // records over all shards
   int lmin_rank, lmax_rank;    // this shard's own rank range (not reduced)
+  unsigned long long max_seg;  // longest rank segment (k_runmax_blk)
 };
 
 struct csg_store {
@@ -74,6 +76,7 @@ struct csg_store {
   // rank-major index
   int32_t R = 0, nch = 0;
   uint64_t max_seg = 0;  // longest rank segment
+  bool max_seg_pending = false;  // still on the device (stats_dev->max_seg)
   csg::DevBuf rank_off, perm, keys, runmax, ko;
   csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
   csg::DevBuf cc;   // {comm, channel} (8 B)
@@ -140,6 +143,7 @@ struct csg_model {
   std::vector<uint8_t> h_op_name;
   int32_t n_levels = 0;
   int32_t max_deg = 0;  // most parents of one program op
+  uint64_t uid = 0;  // unique per model object (context-side table caches)
   // device copies
   csg::DevBuf group_kind, member_off, members, member_slot, comp,
       group_first_op, rg_off, rg_group, rg_slot, op_name, par_off, par_op,
@@ -209,6 +213,8 @@ void store_build_index(csg_store* s);
 void store_build_op_index(csg_store* s, int32_t opn);
 // Returns false (and builds nothing) when the packed key exceeds 64 bits.
 bool store_build_flow_index(csg_store* s);
+// Brings stats_dev->max_seg to the host if still pending (one round trip).
+void store_resolve_max_seg(csg_store* s);
 
 // Per-thread error text for csg_last_error.
 void set_error(const std::string& msg);

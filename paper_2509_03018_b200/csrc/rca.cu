@@ -2444,12 +2444,18 @@ namespace csg {
 
 namespace {
 
+// Host vector -> device buffer through the buffer's pinned staging area
+// (a truly asynchronous copy; the staging area is only rewritten by the
+// next call, after the stream has been synchronised in between).
 template <typename T>
 T* upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   b.ensure(v.size() * sizeof(T) + sizeof(T));
-  if (!v.empty())
-    CSG_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T),
+  if (!v.empty()) {
+    b.stage.ensure(v.size() * sizeof(T));
+    std::memcpy(b.stage.p, v.data(), v.size() * sizeof(T));
+    CSG_CUDA(cudaMemcpyAsync(b.p, b.stage.p, v.size() * sizeof(T),
                              cudaMemcpyHostToDevice, st));
+  }
   return b.as<T>();
 }
 
@@ -2479,6 +2485,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     throw Error(CSG_ERR_RUNTIME,
                 "engine: consecutive_iterations_k > 64 is not supported");
   store_build_index(s);
+  store_resolve_max_seg(s);
   csg_ctx* c = s->ctx;
   cudaStream_t st = c->stream;
   const StoreView sv = s->view();
@@ -2544,12 +2551,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   DevBuf& slot_group = c->buf("rca.slot_group");
   DevBuf& succ = c->buf("rca.succ");
   DevBuf& succ_key = c->buf("rca.succ_key");
-  {
+  if (c->slot_group_uid != m->uid) {  // group of every membership slot
     std::vector<uint32_t> h_sg(std::max<uint32_t>(M, 1));
     for (int32_t g = 0; g < G; ++g)
       for (uint32_t q = m->h_member_off[g]; q < m->h_member_off[g + 1]; ++q)
         h_sg[q] = static_cast<uint32_t>(g);
     upload(slot_group, h_sg, st);
+    c->slot_group_uid = m->uid;
   }
   succ.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * sizeof(SuccProg));
   succ_key.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * nch * 8);

@@ -541,14 +541,17 @@ __global__ void __launch_bounds__(1024)
     k_runmax_blk(const ulonglong2* __restrict__ tso,
                  const uint32_t* __restrict__ off, double* __restrict__ out,
                  uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
-                 unsigned* __restrict__ cnt) {
+                 unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg) {
   __shared__ double pmax[32];
   __shared__ int desc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   const uint32_t b = off[blockIdx.x], e = off[blockIdx.x + 1];
   const uint32_t L = e - b;
-  if (threadIdx.x == 0) desc = 0;
+  if (threadIdx.x == 0) {
+    desc = 0;
+    if (L) atomicMax(max_seg, static_cast<unsigned long long>(L));
+  }
   const uint32_t per = ((L + nw - 1) / nw + 31) & ~31u;
   const uint32_t pb = min(e, b + warp * per), pe = min(e, pb + per);
   double m = -INFINITY;
@@ -568,22 +571,29 @@ __global__ void __launch_bounds__(1024)
   if (dsc) desc = 1;
   double carry = -INFINITY;
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
-  // 256-element chunks: each lane scans 8 consecutive elements sequentially,
-  // one warp scan of the lane maxima, then the lane's carry-in is applied
+  // 256-element chunks: coalesced loads, a padded shared-memory transpose
+  // so each lane scans 8 consecutive elements sequentially, one warp scan of
+  // the lane maxima, carry applied, transposed back for coalesced stores
   // (one shuffle scan per 256 elements instead of per 32)
   constexpr int kE = 8;
+  extern __shared__ double rm_tr[];
+  double* tr = rm_tr + warp * (32 * (kE + 1));
   for (uint32_t base = pb; base < pe; base += 32 * kE) {
-    const uint32_t q0 = base + lane * kE;
-    double x[kE];
 #pragma unroll
     for (int k = 0; k < kE; ++k) {
-      x[k] = -INFINITY;
-      if (q0 + k < pe) {
-        const unsigned long long u = __ldg(&tso[q0 + k].x);
-        memcpy(&x[k], &u, 8);
-        if (x[k] != x[k]) x[k] = -INFINITY;
+      const uint32_t e = k * 32 + lane;
+      double v = -INFINITY;
+      if (base + e < pe) {
+        const unsigned long long u = __ldg(&tso[base + e].x);
+        memcpy(&v, &u, 8);
+        if (v != v) v = -INFINITY;
       }
+      tr[(e / kE) * (kE + 1) + e % kE] = v;
     }
+    __syncwarp();
+    double x[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) x[k] = tr[lane * (kE + 1) + k];
 #pragma unroll
     for (int k = 1; k < kE; ++k) x[k] = fmax(x[k], x[k - 1]);
     double m = x[kE - 1];
@@ -595,9 +605,15 @@ __global__ void __launch_bounds__(1024)
     double cin = __shfl_up_sync(0xffffffffu, m, 1);
     cin = lane ? fmax(cin, carry) : carry;
 #pragma unroll
-    for (int k = 0; k < kE; ++k)
-      if (q0 + k < pe) out[q0 + k] = fmax(x[k], cin);
+    for (int k = 0; k < kE; ++k) tr[lane * (kE + 1) + k] = fmax(x[k], cin);
     carry = fmax(carry, __shfl_sync(0xffffffffu, m, 31));
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const uint32_t e = k * 32 + lane;
+      if (base + e < pe) out[base + e] = tr[(e / kE) * (kE + 1) + e % kE];
+    }
+    __syncwarp();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -978,6 +994,7 @@ void store_build_index(csg_store* s) {
   h.n_total = n;
   h.lmin_rank = INT32_MAX;
   h.lmax_rank = INT32_MIN;
+  h.max_seg = 0;
   s->stats_dev.ensure(sizeof(StoreStats));
   CSG_CUDA(cudaMemcpyAsync(s->stats_dev.p, &h, sizeof(h),
                            cudaMemcpyHostToDevice, st));
@@ -1149,31 +1166,31 @@ void store_build_index(csg_store* s) {
   CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
   if (n && R) {
     ProfScope ps_(c->lc, "k_runmax", st);
-    k_runmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(),
+    static bool rattr = false;
+    if (!rattr) {
+      CSG_CUDA(cudaFuncSetAttribute(k_runmax_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    32 * 32 * 9 * 8));
+      rattr = true;
+    }
+    k_runmax_blk<<<R, 1024, 32 * 32 * 9 * 8, st>>>(s->tso.as<ulonglong2>(),
                                      s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
                                      s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(),
-                                     fcnt.as<unsigned>());
+                                     fcnt.as<unsigned>(), &s->stats_dev.as<StoreStats>()->max_seg);
   } else if (R) {
     CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4, st));
   }
-  {
-    std::vector<uint32_t> ro(static_cast<size_t>(R) + 1);
-    CSG_CUDA(cudaMemcpyAsync(ro.data(), s->rank_off.p, ro.size() * 4,
-                             cudaMemcpyDeviceToHost, st));
+  // the longest segment stays on the device until the next host round trip
+  // (trigger_run picks it up with the trips); shards agree on it over NCCL
+  s->max_seg = 0;
+  s->max_seg_pending = n && R;
+  if (comm_active(c)) {
+    unsigned long long* d = &s->stats_dev.as<StoreStats>()->max_seg;
+    comm_allreduce(c, d, 1, ncclUint64, ncclMax);
+    unsigned long long v = 0;
+    CSG_CUDA(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, st));
     CSG_CUDA(cudaStreamSynchronize(st));
-    uint64_t mx = 0;
-    for (int32_t r = 0; r < R; ++r) mx = std::max<uint64_t>(mx, ro[r + 1] - ro[r]);
-    if (comm_active(c)) {  // scratch sized for the longest segment anywhere
-      DevBuf& d = c->buf("store.maxseg");
-      d.ensure(8);
-      unsigned long long v = mx;
-      CSG_CUDA(cudaMemcpyAsync(d.p, &v, 8, cudaMemcpyHostToDevice, st));
-      comm_allreduce(c, d.p, 1, ncclUint64, ncclMax);
-      CSG_CUDA(cudaMemcpyAsync(&v, d.p, 8, cudaMemcpyDeviceToHost, st));
-      CSG_CUDA(cudaStreamSynchronize(st));
-      mx = v;
-    }
-    s->max_seg = mx;
+    s->max_seg = v;
+    s->max_seg_pending = false;
   }
   CSG_CUDA(cudaGetLastError());
   s->indexed = true;
@@ -1304,9 +1321,20 @@ void store_build_op_index(csg_store* s, int32_t opn) {
   s->op_indexed = true;
 }
 
+void store_resolve_max_seg(csg_store* s) {
+  if (!s->max_seg_pending) return;
+  unsigned long long v = 0;
+  CSG_CUDA(cudaMemcpyAsync(&v, &s->stats_dev.as<StoreStats>()->max_seg, 8,
+                           cudaMemcpyDeviceToHost, s->ctx->stream));
+  CSG_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  s->max_seg = v;
+  s->max_seg_pending = false;
+}
+
 bool store_build_flow_index(csg_store* s) {
   store_build_index(s);
   if (s->flow_indexed) return true;
+  store_resolve_max_seg(s);
   csg_ctx* c = s->ctx;
   cudaStream_t st = c->stream;
   const uint64_t n = s->n;

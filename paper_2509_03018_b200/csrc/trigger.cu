@@ -516,8 +516,9 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     const size_t abytes = static_cast<size_t>(T) * S * sizeof(WinAcc);
     acc.ensure(abytes + (static_cast<size_t>(S) + 1) * 4 + 16);
     CSG_CUDA(cudaMemsetAsync(acc.p, 0, abytes + (static_cast<size_t>(S) + 1) * 4, c->stream));
-    // about 2k records per block of a sampled rank's segment
-    const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, s->max_seg / 2048)));
+    // about 2k records per block of a sampled rank's (average) segment
+    const uint64_t avg = s->R > 0 ? s->n / static_cast<uint64_t>(s->R) : 0;
+    const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, avg / 2048)));
     static bool attr = false;
     if (!attr) {
       CSG_CUDA(cudaFuncSetAttribute(k_trigger, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -555,7 +556,18 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   CSG_CUDA(cudaMemcpyAsync(c->h_events.data(), events.p,
                            static_cast<size_t>(T) * sizeof(csg_trigger_event),
                            cudaMemcpyDeviceToHost, c->stream));
+  // the store's longest segment rides on the same round trip
+  HostBuf& hm = c->hbuf("store.max_seg");
+  hm.ensure(8);
+  const bool ms = s->max_seg_pending;
+  if (ms)
+    CSG_CUDA(cudaMemcpyAsync(hm.p, &s->stats_dev.as<StoreStats>()->max_seg, 8,
+                             cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaStreamSynchronize(c->stream));
+  if (ms) {
+    s->max_seg = *hm.as<unsigned long long>();
+    s->max_seg_pending = false;
+  }
   c->h_events.resize(static_cast<size_t>(n));
   return n;
 }
