@@ -571,49 +571,22 @@ __global__ void __launch_bounds__(1024)
   if (dsc) desc = 1;
   double carry = -INFINITY;
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
-  // 256-element chunks: coalesced loads, a padded shared-memory transpose
-  // so each lane scans 8 consecutive elements sequentially, one warp scan of
-  // the lane maxima, carry applied, transposed back for coalesced stores
-  // (one shuffle scan per 256 elements instead of per 32)
-  constexpr int kE = 8;
-  extern __shared__ double rm_tr[];
-  double* tr = rm_tr + warp * (32 * (kE + 1));
-  for (uint32_t base = pb; base < pe; base += 32 * kE) {
-#pragma unroll
-    for (int k = 0; k < kE; ++k) {
-      const uint32_t e = k * 32 + lane;
-      double v = -INFINITY;
-      if (base + e < pe) {
-        const unsigned long long u = __ldg(&tso[base + e].x);
-        memcpy(&v, &u, 8);
-        if (v != v) v = -INFINITY;
-      }
-      tr[(e / kE) * (kE + 1) + e % kE] = v;
+  for (uint32_t base = pb; base < pe; base += 32) {
+    const uint32_t p = base + lane;
+    double x = -INFINITY;
+    if (p < pe) {
+      const unsigned long long u = __ldg(&tso[p].x);
+      memcpy(&x, &u, 8);
     }
-    __syncwarp();
-    double x[kE];
-#pragma unroll
-    for (int k = 0; k < kE; ++k) x[k] = tr[lane * (kE + 1) + k];
-#pragma unroll
-    for (int k = 1; k < kE; ++k) x[k] = fmax(x[k], x[k - 1]);
-    double m = x[kE - 1];
+    if (x != x) x = -INFINITY;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, m, o);
-      if (lane >= o) m = fmax(m, y);
+      const double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = fmax(x, y);
     }
-    double cin = __shfl_up_sync(0xffffffffu, m, 1);
-    cin = lane ? fmax(cin, carry) : carry;
-#pragma unroll
-    for (int k = 0; k < kE; ++k) tr[lane * (kE + 1) + k] = fmax(x[k], cin);
-    carry = fmax(carry, __shfl_sync(0xffffffffu, m, 31));
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kE; ++k) {
-      const uint32_t e = k * 32 + lane;
-      if (base + e < pe) out[base + e] = tr[(e / kE) * (kE + 1) + e % kE];
-    }
-    __syncwarp();
+    x = fmax(x, carry);
+    carry = __shfl_sync(0xffffffffu, x, 31);
+    if (p < pe) out[p] = x;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1166,13 +1139,7 @@ void store_build_index(csg_store* s) {
   CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
   if (n && R) {
     ProfScope ps_(c->lc, "k_runmax", st);
-    static bool rattr = false;
-    if (!rattr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_runmax_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    32 * 32 * 9 * 8));
-      rattr = true;
-    }
-    k_runmax_blk<<<R, 1024, 32 * 32 * 9 * 8, st>>>(s->tso.as<ulonglong2>(),
+    k_runmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(),
                                      s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
                                      s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(),
                                      fcnt.as<unsigned>(), &s->stats_dev.as<StoreStats>()->max_seg);
