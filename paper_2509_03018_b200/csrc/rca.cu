@@ -2509,11 +2509,29 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
   }
   const int32_t Js = static_cast<int32_t>(h_strag.size());
-  const double* dt = upload(c->buf("rca.t"), h_t, st);
-  const int32_t* dkind = upload(c->buf("rca.kind"), h_kind, st);
-  const int32_t* drank = upload(c->buf("rca.rank"), h_rank, st);
-  const int32_t* djs = upload(c->buf("rca.js"), h_js, st);
-  const int32_t* dstrag = upload(c->buf("rca.strag"), h_strag, st);
+  // the five per-trip arrays go up in one pinned copy (each API call costs
+  // microseconds of host time on the critical path)
+  DevBuf& targ = c->buf("rca.trip_args");
+  const size_t nb_t = static_cast<size_t>(J) * 8, nb_i = static_cast<size_t>(J) * 4;
+  const size_t o_kind = nb_t, o_rank = o_kind + nb_i, o_js = o_rank + nb_i,
+               o_strag = o_js + nb_i, tbytes = o_strag + static_cast<size_t>(Js) * 4 + 8;
+  targ.ensure(tbytes);
+  targ.stage.ensure(tbytes);
+  {
+    unsigned char* h = targ.stage.as<unsigned char>();
+    std::memcpy(h, h_t.data(), nb_t);
+    std::memcpy(h + o_kind, h_kind.data(), nb_i);
+    std::memcpy(h + o_rank, h_rank.data(), nb_i);
+    std::memcpy(h + o_js, h_js.data(), nb_i);
+    if (Js) std::memcpy(h + o_strag, h_strag.data(), static_cast<size_t>(Js) * 4);
+    CSG_CUDA(cudaMemcpyAsync(targ.p, h, tbytes, cudaMemcpyHostToDevice, st));
+  }
+  unsigned char* tb = targ.as<unsigned char>();
+  const double* dt = reinterpret_cast<const double*>(tb);
+  const int32_t* dkind = reinterpret_cast<const int32_t*>(tb + o_kind);
+  const int32_t* drank = reinterpret_cast<const int32_t*>(tb + o_rank);
+  const int32_t* djs = reinterpret_cast<const int32_t*>(tb + o_js);
+  const int32_t* dstrag = reinterpret_cast<const int32_t*>(tb + o_strag);
 
   // K1: per (trip, rank) prefix summaries
   DevBuf& rs = c->buf("rca.rs");
@@ -2639,13 +2657,17 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                                   gi.as<GroupIter>(), aff.as<int32_t>(),
                                   aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
   }
-  std::vector<int32_t> h_naff(J);
-  out.aff.assign(static_cast<size_t>(J) * G, 0);
-  CSG_CUDA(cudaMemcpyAsync(h_naff.data(), n_aff.p, J * 4, cudaMemcpyDeviceToHost, st));
+  HostBuf& h_affb = c->hbuf("rca.aff");
+  h_affb.ensure(static_cast<size_t>(J) * (static_cast<size_t>(G) + 1) * 4 + 16);
+  int32_t* h_na = h_affb.as<int32_t>();
+  int32_t* h_ag = h_na + J;
+  CSG_CUDA(cudaMemcpyAsync(h_na, n_aff.p, J * 4, cudaMemcpyDeviceToHost, st));
   if (G)
-    CSG_CUDA(cudaMemcpyAsync(out.aff.data(), aff.p, static_cast<size_t>(J) * G * 4,
+    CSG_CUDA(cudaMemcpyAsync(h_ag, aff.p, static_cast<size_t>(J) * G * 4,
                              cudaMemcpyDeviceToHost, st));
   CSG_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> h_naff(h_na, h_na + J);
+  out.aff.assign(h_ag, h_ag + static_cast<size_t>(J) * G);
   CSG_CUDA(cudaGetLastError());
   c->d2h_bytes += static_cast<uint64_t>(J) * 4 + static_cast<uint64_t>(J) * G * 4;
   out.trips.assign(J, TripOut{});
@@ -2722,16 +2744,26 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   DevBuf& d_off = c->buf("rca.off");
   DevBuf& d_cand = c->buf("rca.cand");
   DevBuf& d_cev = c->buf("rca.cev");
-  DevBuf& d_exo = c->buf("rca.exo");
+  ExoTrip* d_exo_ptr = nullptr;
   DevBuf& d_exs = c->buf("rca.exo_scratch");
   if (n_items > 0) {
-    upload(d_items, items, st);
+    // items, exoneration trips and the zero closing the offset scan: one
+    // pinned upload
+    const size_t ib = items.size() * sizeof(FailItem), xb = exo.size() * sizeof(ExoTrip);
+    const size_t xo = (ib + 15) & ~size_t(15), zo = (xo + xb + 15) & ~size_t(15);
+    d_items.ensure(zo + 16);
+    d_items.stage.ensure(zo + 16);
+    std::memcpy(d_items.stage.p, items.data(), ib);
+    std::memcpy(d_items.stage.as<unsigned char>() + xo, exo.data(), xb);
+    std::memset(d_items.stage.as<unsigned char>() + zo, 0, 4);
+    CSG_CUDA(cudaMemcpyAsync(d_items.p, d_items.stage.p, zo + 4, cudaMemcpyHostToDevice, st));
     d_pick.ensure(static_cast<size_t>(n_items) * sizeof(GroupPick));
     d_off.ensure(static_cast<size_t>(n_items + 1) * 4);
-    CSG_CUDA(cudaMemsetAsync(d_off.as<uint32_t>() + n_items, 0, 4, st));
+    CSG_CUDA(cudaMemcpyAsync(d_off.as<uint32_t>() + n_items, d_items.as<unsigned char>() + zo, 4,
+                             cudaMemcpyDeviceToDevice, st));
     d_cand.ensure(cand_ub * sizeof(Cand) + sizeof(Cand));
     d_cev.ensure(cand_ub * EV * sizeof(csg_evidence) + sizeof(csg_evidence));
-    upload(d_exo, exo, st);
+    d_exo_ptr = reinterpret_cast<ExoTrip*>(d_items.as<unsigned char>() + xo);
     d_exs.ensure(scratch_bytes + 256);
     {
       ProfScope ps_(c->lc, "k_fail_count", st);
@@ -2867,7 +2899,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ea.cev = d_cev.as<csg_evidence>();
       ea.EV = EV;
       ea.off = d_off.as<uint32_t>();
-      ea.trips = d_exo.as<ExoTrip>();
+      ea.trips = d_exo_ptr;
       ea.n_trips = static_cast<int32_t>(exo.size());
       ea.scratch = d_exs.as<unsigned char>();
       ea.bits = p_bits.as<unsigned long long>();

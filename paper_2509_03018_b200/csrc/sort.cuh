@@ -7,6 +7,7 @@
 // serves the straggler self-evidence pass (proj/src/rca.cpp:803-815).
 #pragma once
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -26,6 +27,7 @@ struct Profiler {
   struct Rec {
     const char* name;
     cudaEvent_t a, b;
+    double host_us;  // host clock at launch (CSG_TIMELINE)
   };
   std::vector<Rec> pending;
   std::map<std::string, std::pair<double, uint64_t>> totals;
@@ -48,8 +50,10 @@ struct Profiler {
         if (!r.b || cudaEventElapsedTime(&s0, pending[0].a, r.a) != cudaSuccess ||
             cudaEventElapsedTime(&e0, pending[0].a, r.b) != cudaSuccess)
           continue;
-        fprintf(stderr, "timeline %-22s start %9.1f us  dur %8.1f us  gap %8.1f us\n",
-                r.name, s0 * 1e3, (e0 - s0) * 1e3, (s0 - prev_end) * 1e3);
+        fprintf(stderr,
+                "timeline %-22s start %9.1f us  dur %8.1f us  gap %8.1f us  host %9.1f us\n",
+                r.name, s0 * 1e3, (e0 - s0) * 1e3, (s0 - prev_end) * 1e3,
+                r.host_us - pending[0].host_us);
         prev_end = e0;
       }
     }
@@ -84,7 +88,10 @@ struct ProfScope {
     if (on) {
       cudaEvent_t a = lc.prof.take();
       cudaEventRecord(a, st);
-      lc.prof.pending.push_back({name, a, nullptr});
+      const double hus = std::chrono::duration<double, std::micro>(
+                             std::chrono::steady_clock::now().time_since_epoch())
+                             .count();
+      lc.prof.pending.push_back({name, a, nullptr, hus});
     }
   }
   ~ProfScope() {
