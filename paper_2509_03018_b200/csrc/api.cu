@@ -4,6 +4,7 @@
 // the thread-local message of csg_last_error().
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -173,6 +174,38 @@ csg_results* package(const RcaResult& r, const csg_trigger_event* trips,
 }
 
 }  // namespace
+
+namespace csg {
+namespace {
+__global__ void k_signal(unsigned long long* flag, unsigned long long v) {
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(flag) = v;
+  __threadfence_system();
+}
+}  // namespace
+
+void ctx_sync(csg_ctx* c) {
+  c->sig.ensure(64);
+  volatile unsigned long long* f = c->sig.as<volatile unsigned long long>();
+  const unsigned long long v = ++c->sig_seq;
+  k_signal<<<1, 1, 0, c->stream>>>(c->sig.as<unsigned long long>(), v);
+  CSG_CUDA(cudaGetLastError());
+  ++c->lc.launches;
+  // spin briefly (the short waits of the analysis path), then let the
+  // driver block; either way surface stream errors
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*f < v) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(500)) {
+      CSG_CUDA(cudaStreamSynchronize(c->stream));
+      break;
+    }
+  }
+  const cudaError_t e = cudaStreamQuery(c->stream);
+  if (e != cudaSuccess && e != cudaErrorNotReady) CSG_CUDA(e);
+  if (e == cudaErrorNotReady) CSG_CUDA(cudaStreamSynchronize(c->stream));
+}
+}  // namespace csg
+
 
 extern "C" {
 
@@ -699,6 +732,7 @@ csg_status csg_run_detection(csg_store* store, const csg_model* model,
       c->d2h_bytes += static_cast<uint64_t>(T) * sizeof(csg_trigger_event) + 4;
     }
     RcaResult r;
+    tl_mark("run_detection -> rca_batch");
     rca_batch(store, model, *acfg, trips.data(),
               static_cast<int32_t>(trips.size()), false, r);
     *out = package(r, trips.data(), static_cast<int32_t>(trips.size()));

@@ -30,7 +30,11 @@ struct csg_ctx {
   std::map<std::string, csg::DevBuf> arena;
   csg::DevBuf& buf(const char* name) { return arena[name]; }
   std::map<std::string, csg::HostBuf> host_arena;  // mapped pinned buffers
-  uint64_t slot_group_uid = 0;  // model whose slot -> group table is in "rca.slot_group"
+  uint64_t slot_group_uid = 0;
+  // low-latency host wait (ctx_sync): a mapped pinned word the stream's
+  // last kernel sets; the host polls it instead of sleeping in the driver
+  csg::HostBuf sig;
+  uint64_t sig_seq = 0;  // model whose slot -> group table is in "rca.slot_group"
   csg::HostBuf& hbuf(const char* name) { return host_arena[name]; }
 
   // Times an engine phase on the context stream with CUDA events.
@@ -213,6 +217,10 @@ void store_build_index(csg_store* s);
 void store_build_op_index(csg_store* s, int32_t opn);
 // Returns false (and builds nothing) when the packed key exceeds 64 bits.
 bool store_build_flow_index(csg_store* s);
+// Waits until everything enqueued on the context stream has completed
+// (spins on a mapped flag, falls back to cudaStreamSynchronize; errors are
+// reported like cudaStreamSynchronize's).
+void ctx_sync(csg_ctx* c);
 // Brings stats_dev->max_seg to the host if still pending (one round trip).
 void store_resolve_max_seg(csg_store* s);
 

@@ -2484,6 +2484,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   if (cfg.consecutive_iterations_k > kMaxK)
     throw Error(CSG_ERR_RUNTIME,
                 "engine: consecutive_iterations_k > 64 is not supported");
+  tl_mark("rca_batch entry");
   store_build_index(s);
   store_resolve_max_seg(s);
   csg_ctx* c = s->ctx;
@@ -2526,6 +2527,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (Js) std::memcpy(h + o_strag, h_strag.data(), static_cast<size_t>(Js) * 4);
     CSG_CUDA(cudaMemcpyAsync(targ.p, h, tbytes, cudaMemcpyHostToDevice, st));
   }
+  tl_mark("rca trip args uploaded");
   unsigned char* tb = targ.as<unsigned char>();
   const double* dt = reinterpret_cast<const double*>(tb);
   const int32_t* dkind = reinterpret_cast<const int32_t*>(tb + o_kind);
@@ -2665,7 +2667,8 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   if (G)
     CSG_CUDA(cudaMemcpyAsync(h_ag, aff.p, static_cast<size_t>(J) * G * 4,
                              cudaMemcpyDeviceToHost, st));
-  CSG_CUDA(cudaStreamSynchronize(st));
+  ctx_sync(c);
+  tl_mark("affected sync returned");
   std::vector<int32_t> h_naff(h_na, h_na + J);
   out.aff.assign(h_ag, h_ag + static_cast<size_t>(J) * G);
   CSG_CUDA(cudaGetLastError());
@@ -2746,6 +2749,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   DevBuf& d_cev = c->buf("rca.cev");
   ExoTrip* d_exo_ptr = nullptr;
   DevBuf& d_exs = c->buf("rca.exo_scratch");
+  tl_mark("fail items planned");
   if (n_items > 0) {
     // items, exoneration trips and the zero closing the offset scan: one
     // pinned upload
@@ -2936,12 +2940,20 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
           p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(), h_sus.as<csg_suspect>(),
           h_ev.as<csg_evidence>());
     }
-    CSG_CUDA(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(used, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(to.data(), d_out.p, J * sizeof(TripOut),
-                             cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(ptot, d_ptot.p, 16, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaStreamSynchronize(st));
+    // pinned: [0] error word, [16] pool usage, [80] packed totals, [96..) trips
+    HostBuf& hr = c->hbuf("rca.tail");
+    hr.ensure(96 + static_cast<size_t>(J) * sizeof(TripOut));
+    unsigned char* hrp = hr.as<unsigned char>();
+    CSG_CUDA(cudaMemcpyAsync(hrp, err.p, 4, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(hrp + 16, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(hrp + 80, d_ptot.p, 16, cudaMemcpyDeviceToHost, st));
+    CSG_CUDA(cudaMemcpyAsync(hrp + 96, d_out.p, J * sizeof(TripOut), cudaMemcpyDeviceToHost,
+                             st));
+    ctx_sync(c);
+    std::memcpy(&h_err, hrp, 4);
+    std::memcpy(used, hrp + 16, 8 * 8);
+    std::memcpy(ptot, hrp + 80, 16);
+    std::memcpy(to.data(), hrp + 96, J * sizeof(TripOut));
     CSG_CUDA(cudaGetLastError());
     if (h_err & DEV_ERR_RC_TABLE)
       throw Error(CSG_ERR_RUNTIME,

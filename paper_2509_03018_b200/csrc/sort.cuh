@@ -51,9 +51,10 @@ struct Profiler {
             cudaEventElapsedTime(&e0, pending[0].a, r.b) != cudaSuccess)
           continue;
         fprintf(stderr,
-                "timeline %-22s start %9.1f us  dur %8.1f us  gap %8.1f us  host %9.1f us\n",
+                "timeline %-22s start %9.1f us  dur %8.1f us  gap %8.1f us  host %9.1f us"
+                "  abs %14.1f\n",
                 r.name, s0 * 1e3, (e0 - s0) * 1e3, (s0 - prev_end) * 1e3,
-                r.host_us - pending[0].host_us);
+                r.host_us - pending[0].host_us, r.host_us);
         prev_end = e0;
       }
     }
@@ -72,6 +73,16 @@ struct Profiler {
     for (cudaEvent_t e : pool) cudaEventDestroy(e);
   }
 };
+
+// CSG_TIMELINE=1: host-side marks on the same clock as the launch records.
+inline void tl_mark(const char* what) {
+  static const bool tl = std::getenv("CSG_TIMELINE") != nullptr;
+  if (!tl) return;
+  const double hus = std::chrono::duration<double, std::micro>(
+                         std::chrono::steady_clock::now().time_since_epoch())
+                         .count();
+  fprintf(stderr, "hostmark %-28s %14.1f us\n", what, hus);
+}
 
 struct LaunchCounter {
   uint64_t launches = 0;

@@ -996,9 +996,13 @@ void store_build_index(csg_store* s) {
     comm_allreduce(c, &d->n_total, 1, ncclUint64, ncclSum);
     comm_group_end(c);
   }
-  CSG_CUDA(cudaMemcpyAsync(&h, s->stats_dev.p, sizeof(h),
-                           cudaMemcpyDeviceToHost, st));
-  CSG_CUDA(cudaStreamSynchronize(st));
+  {
+    HostBuf& hs = c->hbuf("store.stats");
+    hs.ensure(sizeof(h));
+    CSG_CUDA(cudaMemcpyAsync(hs.p, s->stats_dev.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    ctx_sync(c);
+    std::memcpy(&h, hs.p, sizeof(h));
+  }
   const uint64_t ng = h.n_total;
   s->n_global = ng;
   if (ng && h.min_rank < 0)
@@ -1301,6 +1305,7 @@ void store_resolve_max_seg(csg_store* s) {
 bool store_build_flow_index(csg_store* s) {
   store_build_index(s);
   if (s->flow_indexed) return true;
+  tl_mark("flow index entry");
   store_resolve_max_seg(s);
   csg_ctx* c = s->ctx;
   cudaStream_t st = c->stream;

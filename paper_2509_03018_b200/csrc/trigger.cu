@@ -13,6 +13,8 @@
 // Floating point: the EMA and threshold products use explicit _rn intrinsics
 // (and the file is built with -fmad=false) so no FMA contraction happens,
 // matching the reference's SSE2 build.
+#include <cstring>
+
 #include "comm.cuh"
 #include "objects.h"
 #include "trigger.cuh"
@@ -550,25 +552,27 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   }
   }
   // one round trip: the trip count and every possible event slot together
-  c->h_events.resize(static_cast<size_t>(T) + 1);
-  int32_t n = 0;
-  CSG_CUDA(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  CSG_CUDA(cudaMemcpyAsync(c->h_events.data(), events.p,
-                           static_cast<size_t>(T) * sizeof(csg_trigger_event),
+  // pinned: [0] trip count, [8] longest store segment, [16..) event slots
+  HostBuf& hb = c->hbuf("trig.out");
+  hb.ensure(16 + static_cast<size_t>(T) * sizeof(csg_trigger_event));
+  unsigned char* h = hb.as<unsigned char>();
+  CSG_CUDA(cudaMemcpyAsync(h, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CSG_CUDA(cudaMemcpyAsync(h + 16, events.p, static_cast<size_t>(T) * sizeof(csg_trigger_event),
                            cudaMemcpyDeviceToHost, c->stream));
-  // the store's longest segment rides on the same round trip
-  HostBuf& hm = c->hbuf("store.max_seg");
-  hm.ensure(8);
-  const bool ms = s->max_seg_pending;
+  const bool ms = s->max_seg_pending;  // rides on the same round trip
   if (ms)
-    CSG_CUDA(cudaMemcpyAsync(hm.p, &s->stats_dev.as<StoreStats>()->max_seg, 8,
+    CSG_CUDA(cudaMemcpyAsync(h + 8, &s->stats_dev.as<StoreStats>()->max_seg, 8,
                              cudaMemcpyDeviceToHost, c->stream));
-  CSG_CUDA(cudaStreamSynchronize(c->stream));
+  ctx_sync(c);
+  tl_mark("trigger sync returned");
   if (ms) {
-    s->max_seg = *hm.as<unsigned long long>();
+    std::memcpy(&s->max_seg, h + 8, 8);
     s->max_seg_pending = false;
   }
-  c->h_events.resize(static_cast<size_t>(n));
+  int32_t n = 0;
+  std::memcpy(&n, h, 4);
+  const csg_trigger_event* ev = reinterpret_cast<const csg_trigger_event*>(h + 16);
+  c->h_events.assign(ev, ev + n);
   return n;
 }
 
@@ -606,7 +610,7 @@ void trigger_evaluate_single(csg_store* s, const int32_t* sampled, int32_t S,
   CSG_CUDA(cudaMemcpyAsync(tripped, tr.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CSG_CUDA(cudaMemcpyAsync(event, ev.p, sizeof(*event), cudaMemcpyDeviceToHost,
                            c->stream));
-  CSG_CUDA(cudaStreamSynchronize(c->stream));
+  ctx_sync(c);
   CSG_CUDA(cudaGetLastError());
 }
 
