@@ -220,7 +220,23 @@ bool store_build_flow_index(csg_store* s);
 // Waits until everything enqueued on the context stream has completed
 // (spins on a mapped flag, falls back to cudaStreamSynchronize; errors are
 // reported like cudaStreamSynchronize's).
-void ctx_sync(csg_ctx* c);
+// fetch (optional): small device regions copied into mapped host memory by
+// the same kernel that publishes completion.
+struct FetchSeg {
+  const unsigned char* src;
+  unsigned char* dst;
+  uint32_t bytes;
+};
+constexpr int kFetchSegs = 6;
+struct FetchArgs {
+  FetchSeg seg[kFetchSegs];
+  int n;
+  void add(const void* src, void* dst, size_t bytes) {
+    seg[n++] = FetchSeg{static_cast<const unsigned char*>(src),
+                        static_cast<unsigned char*>(dst), static_cast<uint32_t>(bytes)};
+  }
+};
+void ctx_sync(csg_ctx* c, const FetchArgs* fetch = nullptr);
 // Brings stats_dev->max_seg to the host if still pending (one round trip).
 void store_resolve_max_seg(csg_store* s);
 

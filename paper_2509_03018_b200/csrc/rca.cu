@@ -2663,11 +2663,12 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   h_affb.ensure(static_cast<size_t>(J) * (static_cast<size_t>(G) + 1) * 4 + 16);
   int32_t* h_na = h_affb.as<int32_t>();
   int32_t* h_ag = h_na + J;
-  CSG_CUDA(cudaMemcpyAsync(h_na, n_aff.p, J * 4, cudaMemcpyDeviceToHost, st));
-  if (G)
-    CSG_CUDA(cudaMemcpyAsync(h_ag, aff.p, static_cast<size_t>(J) * G * 4,
-                             cudaMemcpyDeviceToHost, st));
-  ctx_sync(c);
+  {
+    FetchArgs fa{};
+    fa.add(n_aff.p, h_na, static_cast<size_t>(J) * 4);
+    if (G) fa.add(aff.p, h_ag, static_cast<size_t>(J) * G * 4);
+    ctx_sync(c, &fa);
+  }
   tl_mark("affected sync returned");
   std::vector<int32_t> h_naff(h_na, h_na + J);
   out.aff.assign(h_ag, h_ag + static_cast<size_t>(J) * G);
@@ -2944,12 +2945,14 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     HostBuf& hr = c->hbuf("rca.tail");
     hr.ensure(96 + static_cast<size_t>(J) * sizeof(TripOut));
     unsigned char* hrp = hr.as<unsigned char>();
-    CSG_CUDA(cudaMemcpyAsync(hrp, err.p, 4, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(hrp + 16, p_used.p, 8 * 8, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(hrp + 80, d_ptot.p, 16, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaMemcpyAsync(hrp + 96, d_out.p, J * sizeof(TripOut), cudaMemcpyDeviceToHost,
-                             st));
-    ctx_sync(c);
+    {
+      FetchArgs fa{};
+      fa.add(err.p, hrp, 4);
+      fa.add(p_used.p, hrp + 16, 8 * 8);
+      fa.add(d_ptot.p, hrp + 80, 16);
+      fa.add(d_out.p, hrp + 96, static_cast<size_t>(J) * sizeof(TripOut));
+      ctx_sync(c, &fa);
+    }
     std::memcpy(&h_err, hrp, 4);
     std::memcpy(used, hrp + 16, 8 * 8);
     std::memcpy(ptot, hrp + 80, 16);

@@ -999,8 +999,9 @@ void store_build_index(csg_store* s) {
   {
     HostBuf& hs = c->hbuf("store.stats");
     hs.ensure(sizeof(h));
-    CSG_CUDA(cudaMemcpyAsync(hs.p, s->stats_dev.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    ctx_sync(c);
+    FetchArgs fa{};
+    fa.add(s->stats_dev.p, hs.p, sizeof(h));
+    ctx_sync(c, &fa);
     std::memcpy(&h, hs.p, sizeof(h));
   }
   const uint64_t ng = h.n_total;

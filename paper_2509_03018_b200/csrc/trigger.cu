@@ -556,14 +556,12 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   HostBuf& hb = c->hbuf("trig.out");
   hb.ensure(16 + static_cast<size_t>(T) * sizeof(csg_trigger_event));
   unsigned char* h = hb.as<unsigned char>();
-  CSG_CUDA(cudaMemcpyAsync(h, dn.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  CSG_CUDA(cudaMemcpyAsync(h + 16, events.p, static_cast<size_t>(T) * sizeof(csg_trigger_event),
-                           cudaMemcpyDeviceToHost, c->stream));
+  FetchArgs fa{};
+  fa.add(dn.p, h, 4);
+  fa.add(events.p, h + 16, static_cast<size_t>(T) * sizeof(csg_trigger_event));
   const bool ms = s->max_seg_pending;  // rides on the same round trip
-  if (ms)
-    CSG_CUDA(cudaMemcpyAsync(h + 8, &s->stats_dev.as<StoreStats>()->max_seg, 8,
-                             cudaMemcpyDeviceToHost, c->stream));
-  ctx_sync(c);
+  if (ms) fa.add(&s->stats_dev.as<StoreStats>()->max_seg, h + 8, 8);
+  ctx_sync(c, &fa);
   tl_mark("trigger sync returned");
   if (ms) {
     std::memcpy(&s->max_seg, h + 8, 8);
