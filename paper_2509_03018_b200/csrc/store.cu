@@ -143,41 +143,40 @@ constexpr int kTileThreads = 256;
 constexpr int kTileItems = 16;
 constexpr int kTile = kTileThreads * kTileItems;  // 4096 records
 
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, 2)
     k_stats_hist(const csg_packed_record* __restrict__ r, uint64_t n,
                  StoreStats* __restrict__ st, uint32_t* __restrict__ counts,
                  uint32_t ntiles) {
   __shared__ uint32_t hist[kHistDigits];
   for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads) hist[d] = 0;
-  __syncthreads();
   StatAcc acc;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTile;
-#pragma unroll 1
-  for (int k0 = 0; k0 < kTileItems; k0 += 4) {
-    ulonglong2 h0[4], hm[4];
+  // every load of the tile issued before the first use (32 x 16 B per thread
+  // in flight: the kernel is a pure HBM stream)
+  ulonglong2 h0[kTileItems], hm[kTileItems];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t i = base + (k0 + k) * kTileThreads + threadIdx.x;
-      if (i < n) rec_head(r, i, h0[k], hm[k]);
-    }
+  for (int k = 0; k < kTileItems; ++k) {
+    const uint64_t i = base + k * kTileThreads + threadIdx.x;
+    if (i < n) rec_head(r, i, h0[k], hm[k]);
+  }
+  __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t i = base + (k0 + k) * kTileThreads + threadIdx.x;
-      const bool valid = i < n;
-      double t = 0;
-      int rank = 0;
-      if (valid) {
-        memcpy(&t, &h0[k].x, 8);
-        rank = static_cast<int>(hm[k].x & 0xffffffffu);
-        acc.add(t, static_cast<long long>(h0[k].y), rank,
-                static_cast<int>(hm[k].y & 0xffffffffu));
-      }
-      const uint32_t d = valid ? static_cast<uint32_t>(rank) & (kHistDigits - 1)
-                               : 0xFFFFFFFFu;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      if (valid && (threadIdx.x & 31) == __ffs(peers) - 1)
-        atomicAdd(&hist[d], __popc(peers));
+  for (int k = 0; k < kTileItems; ++k) {
+    const uint64_t i = base + k * kTileThreads + threadIdx.x;
+    const bool valid = i < n;
+    double t = 0;
+    int rank = 0;
+    if (valid) {
+      memcpy(&t, &h0[k].x, 8);
+      rank = static_cast<int>(hm[k].x & 0xffffffffu);
+      acc.add(t, static_cast<long long>(h0[k].y), rank,
+              static_cast<int>(hm[k].y & 0xffffffffu));
     }
+    const uint32_t d = valid ? static_cast<uint32_t>(rank) & (kHistDigits - 1)
+                             : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(&hist[d], __popc(peers));
   }
   __syncthreads();
   for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads)
