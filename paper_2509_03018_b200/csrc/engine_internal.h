@@ -114,7 +114,8 @@ struct StoreView {
   int32_t nch = 0;         // channel space [0, nch)
   const uint32_t* rank_off = nullptr;  // [R+1]
   const uint32_t* perm = nullptr;      // rank-major pos -> store index
-  const double* runmax = nullptr;      // per-rank running max of ts
+  const double* cmax = nullptr;        // per-rank chunked prefix max of ts
+                                       // (chunk c of rank r at r + off[r]/128 + c)
   ColView<double, 2, 0> ts;            // {ts, op_seq} pairs
   ColView<int64_t, 2, 1> op;
   ColView<int32_t, 2, 0> comm;         // {comm, channel} pairs
@@ -123,6 +124,8 @@ struct StoreView {
   ColView<uint64_t, 2, 0> pa;          // payload pairs: start_ms bits | ready | tx << 32
   ColView<uint64_t, 2, 1> pb;          //                msg_bytes | done
 };
+
+constexpr uint32_t kCmChunk = 128;  // records per cmax chunk
 
 // Rank owning rank-major position p (p < n): upper_bound over rank_off.
 __device__ inline int32_t rank_at(const StoreView& s, uint32_t p) {

@@ -81,7 +81,8 @@ struct csg_store {
   int32_t R = 0, nch = 0;
   uint64_t max_seg = 0;  // longest rank segment
   bool max_seg_pending = false;  // still on the device (stats_dev->max_seg)
-  csg::DevBuf rank_off, perm, keys, runmax, ko;
+  csg::DevBuf rank_off, perm, keys, ko;
+  csg::DevBuf runmax;  // chunked prefix max of ts (StoreView::cmax)
   csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
   csg::DevBuf cc;   // {comm, channel} (8 B)
   csg::DevBuf pay;  // {start_ms | ready,tx ; msg_bytes | done} (16 B)
@@ -114,7 +115,7 @@ struct csg_store {
     v.nch = nch;
     v.rank_off = rank_off.as<uint32_t>();
     v.perm = perm.as<uint32_t>();
-    v.runmax = runmax.as<double>();
+    v.cmax = runmax.as<double>();
     v.ts.p = tso.as<double>();
     v.op.p = tso.as<int64_t>();
     v.comm.p = cc.as<int32_t>();

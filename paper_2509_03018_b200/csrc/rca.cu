@@ -67,6 +67,35 @@ __device__ uint32_t warp_partition_point(uint32_t lo, uint32_t hi, P pred) {
   return mm ? lo + __ffs(mm) - 1 : hi;
 }
 
+// First rank-major position of rank r's segment whose ts is > x (strict)
+// or >= x, else the segment end; warp-collective. Binary search over the
+// chunked prefix maxima (store.cu k_chunkmax_blk), then one 128-record
+// chunk scan. This is the reference's store-order prefix cut-off (the first
+// record with ts > t ends the prefix, rca.cpp:156 / :174 / :207 / :225).
+__device__ uint32_t seg_first(const StoreView& s, int32_t r, double x, bool strict) {
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  const uint32_t nc = (e - b + kCmChunk - 1) / kCmChunk;
+  const double* cm = s.cmax + (b / kCmChunk + r);
+  const uint32_t c = warp_partition_point(0, nc, [&](uint32_t k) {
+    const double m = cm[k];
+    return strict ? m > x : m >= x;
+  });
+  if (c == nc) return e;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 0; k < kCmChunk / 32; ++k) {
+    const uint32_t p = b + c * kCmChunk + k * 32 + lane;
+    bool hit = false;
+    if (p < e) {
+      const double t = s.ts[p];
+      hit = strict ? t > x : t >= x;
+    }
+    const unsigned mm = __ballot_sync(FULL, hit);
+    if (mm) return b + c * kCmChunk + k * 32 + __ffs(mm) - 1;
+  }
+  return e;  // unreachable: the chunk's maximum satisfies the predicate
+}
+
 // Lower median sorted[(n-1)/2] of n virtual values (warp; O(n^2/32)).
 template <typename V>
 __device__ double warp_lower_median(int n, V val) {
@@ -114,9 +143,7 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
   const double t = trip_t[j];
   const double ws = t - delta_a;  // window_start, rca.cpp:405
   const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
-  const double* rm = s.runmax;
-  const uint32_t cend =
-      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
+  const uint32_t cend = seg_first(s, r, t, true);
   const uint32_t c = cend - b;
   // A rank without prefix records leaves an all-zero summary, so summaries
   // of ranks owned by other shards combine by summation (see comm.cu).
@@ -139,8 +166,9 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
     int64_t found = -1;
     // The prefix's running max bounds every timestamp in it: a rank that
     // has been silent since before the window has nothing to scan.
-    const int64_t scan_from =
-        rm[cend - 1] >= ws ? static_cast<int64_t>(cend) - 1 : static_cast<int64_t>(b) - 1;
+    const int64_t scan_from = seg_first(s, r, ws, false) < cend
+                                  ? static_cast<int64_t>(cend) - 1
+                                  : static_cast<int64_t>(b) - 1;
     for (int64_t top = scan_from;
          top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
       const int64_t p = top - lane;
@@ -233,9 +261,7 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
   const double t = trip_t[j];
   const double ws = t - delta_a;
   const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
-  const double* rm = s.runmax;
-  const uint32_t cend =
-      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] > t; });
+  const uint32_t cend = seg_first(s, r, t, true);
   const uint32_t c = cend - b;
   // A rank without prefix records leaves an all-zero summary, so summaries
   // of ranks owned by other shards combine by summation (see comm.cu).
@@ -256,8 +282,9 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
     int64_t found = -1;
     // The prefix's running max bounds every timestamp in it: a rank that
     // has been silent since before the window has nothing to scan.
-    const int64_t scan_from =
-        rm[cend - 1] >= ws ? static_cast<int64_t>(cend) - 1 : static_cast<int64_t>(b) - 1;
+    const int64_t scan_from = seg_first(s, r, ws, false) < cend
+                                  ? static_cast<int64_t>(cend) - 1
+                                  : static_cast<int64_t>(b) - 1;
     for (int64_t top = scan_from;
          top >= static_cast<int64_t>(b) && found < 0; top -= 32) {
       const int64_t p = top - lane;
@@ -657,10 +684,8 @@ __global__ void k_flow(StoreView s, ModelView m, int32_t Js,
   const uint32_t b = s.rank_off[r];
   const uint32_t e =
       min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, s.rank_off[r + 1]);
-  const double* rm = s.runmax;
   // records before p0 all have ts < ws (running max below ws)
-  const uint32_t p0 =
-      warp_partition_point(b, e, [&](uint32_t p) { return rm[p] >= ws; });
+  const uint32_t p0 = min(seg_first(s, r, ws, false), e);
   auto win_comp = [&](uint32_t p) {
     const uint8_t ko = s.ko[p];
     return ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV &&

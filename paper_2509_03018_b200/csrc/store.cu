@@ -530,54 +530,66 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
   }
 }
 
-// Per-rank running max of ts: one block per rank segment, the segment split
-// into one contiguous part per warp; part maxima exchanged through shared
-// memory give every warp its carry-in (all warps of all ranks stream at
-// once instead of one warp walking a whole segment). The same pass flags
-// segments whose op_seq descends in store order (the flow index permutes
-// only those, see k_flow_fix) and appends them to a work list.
+// Per-rank chunked prefix maximum of ts (StoreView::cmax): one block per rank
+// segment, the segment split into one contiguous run of 128-record chunks
+// per warp. Each warp reduces its chunks (4 coalesced loads per lane, one
+// warp reduction per chunk), warps exchange their part maxima through shared
+// memory, and each warp turns its chunk maxima into running maxima with one
+// warp scan per 32 chunks. Every reference "prefix scan that stops at the
+// first ts > t" (rca.cpp:146-237) becomes a binary search over the chunk
+// maxima plus one chunk scan (seg_first), without materialising a running
+// maximum per record. The same pass flags segments whose op_seq descends in
+// store order (the flow index permutes only those, see k_flow_fix).
 __global__ void __launch_bounds__(1024)
-    k_runmax_blk(const ulonglong2* __restrict__ tso,
-                 const uint32_t* __restrict__ off, double* __restrict__ out,
-                 uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
-                 unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg) {
+    k_chunkmax_blk(const ulonglong2* __restrict__ tso,
+                   const uint32_t* __restrict__ off, double* __restrict__ cm,
+                   uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
+                   unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg) {
   __shared__ double pmax[32];
   __shared__ int desc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const uint32_t b = off[blockIdx.x], e = off[blockIdx.x + 1];
+  const int32_t r = blockIdx.x;
+  const uint32_t b = off[r], e = off[r + 1];
   const uint32_t L = e - b;
   if (threadIdx.x == 0) {
     desc = 0;
     if (L) atomicMax(max_seg, static_cast<unsigned long long>(L));
   }
-  const uint32_t per = ((L + nw - 1) / nw + 31) & ~31u;
-  const uint32_t pb = min(e, b + warp * per), pe = min(e, pb + per);
+  const uint32_t nc = (L + kCmChunk - 1) / kCmChunk;
+  const uint32_t cper = (nc + nw - 1) / nw;  // chunks per warp
+  const uint32_t c0 = min(nc, warp * cper), c1 = min(nc, c0 + cper);
+  double* cmr = cm + (b / kCmChunk + r);
   double m = -INFINITY;
   bool dsc = false;
-  for (uint32_t p = pb + lane; p < pe; p += 32) {
-    const ulonglong2 v = __ldg(tso + p);
-    double x;
-    memcpy(&x, &v.x, 8);
-    if (x == x) m = fmax(m, x);  // NaN never breaks a prefix
-    if (p > b) dsc |= static_cast<long long>(v.y) <
-                      static_cast<long long>(__ldg(&tso[p - 1].y));
-  }
+  for (uint32_t c = c0; c < c1; ++c) {
+    double x = -INFINITY;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int k = 0; k < kCmChunk / 32; ++k) {
+      const uint32_t p = b + c * kCmChunk + k * 32 + lane;
+      if (p < e) {
+        const ulonglong2 v = __ldg(tso + p);
+        double t;
+        memcpy(&t, &v.x, 8);
+        if (t == t) x = fmax(x, t);  // NaN never breaks a prefix
+        if (p > b) dsc |= static_cast<long long>(v.y) <
+                          static_cast<long long>(__ldg(&tso[p - 1].y));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) cmr[c] = x;
+    m = fmax(m, x);
+  }
   if (lane == 0) pmax[warp] = m;
   __syncthreads();
   if (dsc) desc = 1;
   double carry = -INFINITY;
   for (int w = 0; w < warp; ++w) carry = fmax(carry, pmax[w]);
-  for (uint32_t base = pb; base < pe; base += 32) {
-    const uint32_t p = base + lane;
-    double x = -INFINITY;
-    if (p < pe) {
-      const unsigned long long u = __ldg(&tso[p].x);
-      memcpy(&x, &u, 8);
-    }
-    if (x != x) x = -INFINITY;
+  __syncwarp();
+  for (uint32_t cb = c0; cb < c1; cb += 32) {
+    const uint32_t c = cb + lane;
+    double x = c < c1 ? cmr[c] : -INFINITY;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double y = __shfl_up_sync(0xffffffffu, x, o);
@@ -585,12 +597,12 @@ __global__ void __launch_bounds__(1024)
     }
     x = fmax(x, carry);
     carry = __shfl_sync(0xffffffffu, x, 31);
-    if (p < pe) out[p] = x;
+    if (c < c1) cmr[c] = x;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsorted[blockIdx.x] = desc ? 1u : 0u;
-    if (desc) list[atomicAdd(cnt, 1u)] = blockIdx.x;
+    unsorted[r] = desc ? 1u : 0u;
+    if (desc) list[atomicAdd(cnt, 1u)] = r;
   }
 }
 
@@ -1031,7 +1043,7 @@ void store_build_index(csg_store* s) {
 
   s->rank_off.ensure((static_cast<size_t>(R) + 1) * 4);
   s->tso.ensure(n * 16 + 16);
-  s->runmax.ensure(n * 8 + 8);
+  s->runmax.ensure((n / kCmChunk + static_cast<size_t>(R) + 2) * 8);
   s->cc.ensure(n * 8 + 8);
   s->ko.ensure(n + 8);
   s->pay.ensure(n * 16 + 16);
@@ -1142,11 +1154,11 @@ void store_build_index(csg_store* s) {
   fcnt.ensure(8);
   CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
   if (n && R) {
-    ProfScope ps_(c->lc, "k_runmax", st);
-    k_runmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(),
-                                     s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
-                                     s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(),
-                                     fcnt.as<unsigned>(), &s->stats_dev.as<StoreStats>()->max_seg);
+    ProfScope ps_(c->lc, "k_chunkmax", st);
+    k_chunkmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(), s->rank_off.as<uint32_t>(),
+                                       s->runmax.as<double>(), s->fl_unsorted.as<uint32_t>(),
+                                       flist.as<uint32_t>(), fcnt.as<unsigned>(),
+                                       &s->stats_dev.as<StoreStats>()->max_seg);
   } else if (R) {
     CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4, st));
   }
