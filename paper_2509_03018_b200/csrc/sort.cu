@@ -249,8 +249,15 @@ void radix_sort_u64(uint64_t* keys, uint32_t* vals, uint64_t n, int nbits,
 
 void exclusive_scan_u32(uint32_t* data, uint64_t n, DevBuf& tmp,
                         cudaStream_t st, LaunchCounter& lc) {
-  tmp.ensure((n / (kScanTile - 1) + 64) * sizeof(uint32_t));
-  scan_rec(data, n, tmp.as<uint32_t>(), st, lc);
+  if (n == 0) return;
+  const uint32_t nt = static_cast<uint32_t>((n + kLbTile - 1) / kLbTile);
+  tmp.ensure((static_cast<size_t>(nt) + 1) * 8);
+  CSG_CUDA(cudaMemsetAsync(tmp.p, 0, (static_cast<size_t>(nt) + 1) * 8, st));
+  {
+    ProfScope ps_(lc, "k_scan_lookback", st);
+    k_scan_lookback<<<nt, kLbThreads, 0, st>>>(LoadU32{data}, n, data,
+                                               tmp.as<unsigned long long>(), nt);
+  }
   CSG_CUDA(cudaGetLastError());
 }
 

@@ -136,3 +136,108 @@ inline int bits_for(uint64_t max_value) {
 }
 
 }  // namespace csg
+
+namespace csg {
+
+// ---- single-pass exclusive scan (decoupled look-back) -----------------------
+// out[i] = sum of ld(0 .. i-1) for i < n. Tiles of 4096 values claim an
+// order through an atomic ticket, publish their aggregate, look back over
+// their predecessors' published aggregates / inclusive prefixes with one warp
+// and publish their inclusive prefix: one launch instead of reduce + scan +
+// apply. flags: (ntiles + 1) zeroed u64 words (the last one is the ticket).
+constexpr int kLbThreads = 256;
+constexpr int kLbItems = 16;
+constexpr int kLbTile = kLbThreads * kLbItems;
+
+__device__ inline uint32_t lb_block_excl(uint32_t v, uint32_t* wsum, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = lane < kLbThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < kLbThreads / 32) wsum[lane] = s;
+  }
+  __syncthreads();
+  *total = wsum[kLbThreads / 32 - 1];
+  return (warp ? wsum[warp - 1] : 0) + x - v;
+}
+
+template <typename Load>
+__global__ void __launch_bounds__(kLbThreads)
+    k_scan_lookback(Load ld, uint64_t n, uint32_t* __restrict__ out,
+                    unsigned long long* __restrict__ flags, uint32_t ntiles) {
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ uint32_t wsum[32];
+  constexpr unsigned long long AGG = 1ull << 62, INC = 2ull << 62;
+  if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<unsigned*>(flags + ntiles), 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = static_cast<uint64_t>(tile) * kLbTile + threadIdx.x * kLbItems;
+  uint32_t x[kLbItems];
+  uint32_t t = 0;
+#pragma unroll
+  for (int k = 0; k < kLbItems; ++k) {
+    x[k] = base + k < n ? ld(base + k) : 0u;
+    t += x[k];
+  }
+  uint32_t agg;
+  const uint32_t off = lb_block_excl(t, wsum, &agg);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(flags + tile, INC | agg);
+      }
+    } else {
+      if (lane == 0) atomicExch(flags + tile, AGG | agg);
+      int64_t w = static_cast<int64_t>(tile) - 1;  // window end (closest predecessor)
+      while (true) {
+        const int64_t q = w - lane;
+        unsigned long long f = INC;  // before tile 0: nothing left to add
+        if (q >= 0) {
+          do {
+            f = atomicAdd(flags + q, 0ull);
+          } while ((f >> 62) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (f >> 62) == 2);
+        // lanes up to and including the first inclusive one contribute
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        uint32_t v = lane <= stop ? static_cast<uint32_t>(f & 0xffffffffull) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (inc) break;
+        w -= 32;
+      }
+      if (lane == 0) atomicExch(flags + tile, INC | static_cast<unsigned long long>(prefix + agg));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + off;
+#pragma unroll
+  for (int k = 0; k < kLbItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += x[k];
+  }
+}
+
+struct LoadU32 {
+  const uint32_t* p;
+  __device__ uint32_t operator()(uint64_t i) const { return p[i]; }
+};
+
+}  // namespace csg

@@ -184,10 +184,8 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   acc.commit(st);
 }
 
-// Exclusive scan of the virtual array v[i] = counts[((i / T + d0) & 2047) * T
-// + i % T], i < D * T: block sums, then per-block scan with the carried base.
-constexpr int kHScanPer = 4;
-constexpr int kHScanTile = kTileThreads * kHScanPer;  // 1024
+// The scan input is the virtual array v[i] = counts[((i / T + d0) & 2047) *
+// T + i % T], i < D * T (k_scan_lookback with HistLoad).
 
 __device__ inline uint32_t hv(const uint32_t* counts, uint64_t i, uint32_t T, uint32_t d0) {
   const uint64_t d = (i / T + d0) & (kHistDigits - 1);
@@ -222,43 +220,11 @@ __device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint3
   return r;
 }
 
-__global__ void __launch_bounds__(kTileThreads)
-    k_hist_scan_sums(const uint32_t* __restrict__ counts, uint64_t M, uint32_t T,
-                     uint32_t d0, uint32_t* __restrict__ sums) {
-  __shared__ uint32_t wsum[32];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kHScanTile;
-  uint32_t t = 0;
-#pragma unroll
-  for (int k = 0; k < kHScanPer; ++k) {
-    const uint64_t i = base + k * kTileThreads + threadIdx.x;
-    if (i < M) t += hv(counts, i, T, d0);
-  }
-  uint32_t tot;
-  block_excl_scan_u32(t, wsum, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(kTileThreads)
-    k_hist_scan_apply(const uint32_t* __restrict__ counts, uint64_t M, uint32_t T,
-                      uint32_t d0, const uint32_t* __restrict__ sums,
-                      uint32_t* __restrict__ out) {
-  __shared__ uint32_t wsum[32];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kHScanTile +
-                        static_cast<uint64_t>(threadIdx.x) * kHScanPer;
-  uint32_t x[kHScanPer];
-  uint32_t t = 0;
-#pragma unroll
-  for (int k = 0; k < kHScanPer; ++k) {
-    x[k] = base + k < M ? hv(counts, base + k, T, d0) : 0u;
-    t += x[k];
-  }
-  uint32_t run = block_excl_scan_u32(t, wsum, nullptr) + sums[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < kHScanPer; ++k) {
-    if (base + k < M) out[base + k] = run;
-    run += x[k];
-  }
-}
+struct HistLoad {
+  const uint32_t* counts;
+  uint32_t T, d0;
+  __device__ uint32_t operator()(uint64_t i) const { return hv(counts, i, T, d0); }
+};
 
 // rank_off over absolute ranks [0, R] from the scanned tile offsets.
 __global__ void k_rank_off_hist(const uint32_t* __restrict__ goff, uint32_t T,
@@ -562,24 +528,40 @@ __global__ void __launch_bounds__(1024)
   double* cmr = cm + (b / kCmChunk + r);
   double m = -INFINITY;
   bool dsc = false;
-  for (uint32_t c = c0; c < c1; ++c) {
-    double x = -INFINITY;
+  constexpr int G = kCmChunk / 32;  // 32-record groups per chunk
+  // op_seq of the record before the current group (descent check)
+  long long prev = LLONG_MIN;
+  if (c0 < c1 && c0 > 0) prev = static_cast<long long>(__ldg(&tso[b + c0 * kCmChunk - 1].y));
+  for (uint32_t c = c0; c < c1; c += 2) {
+    // two chunks' loads in flight before any use
+    ulonglong2 v[2 * G];
 #pragma unroll
-    for (int k = 0; k < kCmChunk / 32; ++k) {
+    for (int k = 0; k < 2 * G; ++k) {
       const uint32_t p = b + c * kCmChunk + k * 32 + lane;
-      if (p < e) {
-        const ulonglong2 v = __ldg(tso + p);
-        double t;
-        memcpy(&t, &v.x, 8);
-        if (t == t) x = fmax(x, t);  // NaN never breaks a prefix
-        if (p > b) dsc |= static_cast<long long>(v.y) <
-                          static_cast<long long>(__ldg(&tso[p - 1].y));
-      }
+      v[k] = (c + k / G < c1 && p < e) ? __ldg(tso + p)
+                                         : make_ulonglong2(0xFFF0000000000000ull, 0);
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-    if (lane == 0) cmr[c] = x;
-    m = fmax(m, x);
+    for (int h = 0; h < 2; ++h) {
+      if (c + h >= c1) break;
+      double x = -INFINITY;
+#pragma unroll
+      for (int k = h * G; k < h * G + G; ++k) {
+        const uint32_t p = b + c * kCmChunk + k * 32 + lane;
+        double t;
+        memcpy(&t, &v[k].x, 8);
+        if (p < e && t == t) x = fmax(x, t);  // NaN never breaks a prefix
+        const long long op = static_cast<long long>(v[k].y);
+        long long pv = __shfl_up_sync(0xffffffffu, op, 1);
+        if (lane == 0) pv = prev;
+        if (p < e && p > b) dsc |= op < pv;
+        prev = __shfl_sync(0xffffffffu, op, 31);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (lane == 0) cmr[c + h] = x;
+      m = fmax(m, x);
+    }
   }
   if (lane == 0) pmax[warp] = m;
   __syncthreads();
@@ -1059,18 +1041,15 @@ void store_build_index(csg_store* s) {
     DevBuf& goff = c->buf("index.goff");
     DevBuf& sums = c->buf("index.sums");
     goff.ensure(M * 4 + 4);
-    const uint64_t nb = (M + kHScanTile - 1) / kHScanTile;
-    sums.ensure(nb * 4 + 4);
     {
-      ProfScope ps_(c->lc, "k_hist_scan_sums", st);
-      k_hist_scan_sums<<<static_cast<unsigned>(nb), kTileThreads, 0, st>>>(
-          hcnt.as<uint32_t>(), M, ntiles, d0, sums.as<uint32_t>());
-    }
-    exclusive_scan_u32(sums.as<uint32_t>(), nb, c->scratch_a, st, c->lc);
-    {
-      ProfScope ps_(c->lc, "k_hist_scan_apply", st);
-      k_hist_scan_apply<<<static_cast<unsigned>(nb), kTileThreads, 0, st>>>(
-          hcnt.as<uint32_t>(), M, ntiles, d0, sums.as<uint32_t>(), goff.as<uint32_t>());
+      // single-pass decoupled look-back scan over the rotated digit-major view
+      const uint32_t nt = static_cast<uint32_t>((M + kLbTile - 1) / kLbTile);
+      sums.ensure((static_cast<size_t>(nt) + 1) * 8);
+      CSG_CUDA(cudaMemsetAsync(sums.p, 0, (static_cast<size_t>(nt) + 1) * 8, st));
+      ProfScope ps_(c->lc, "k_hist_scan", st);
+      k_scan_lookback<<<nt, kLbThreads, 0, st>>>(HistLoad{hcnt.as<uint32_t>(), ntiles, d0}, M,
+                                                 goff.as<uint32_t>(),
+                                                 sums.as<unsigned long long>(), nt);
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
                  s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
