@@ -74,16 +74,31 @@ void comm_allreduce(csg_ctx* c, void* ptr, size_t count, ncclDataType_t t,
                     ncclRedOp_t op) {
   if (!comm_active(c) || count == 0) return;
   ++c->collectives;
+  ProfScope ps_(c->lc, c->comm_group_depth ? "nccl_in_group" : "nccl_allreduce", c->stream,
+                false);
   check(nccl().AllReduce(ptr, ptr, count, t, op, static_cast<ncclComm_t>(c->comm),
                          c->stream),
         "allreduce");
 }
 
 void comm_group_start(csg_ctx* c) {
-  if (comm_active(c)) check(nccl().GroupStart(), "group start");
+  if (!comm_active(c)) return;
+  if (c->comm_group_depth++ == 0 && c->lc.prof.enabled) {
+    cudaEvent_t a = c->lc.prof.take();
+    cudaEventRecord(a, c->stream);
+    c->lc.prof.pending.push_back({"nccl_group", a, nullptr, 0.0});
+    c->group_rec = c->lc.prof.pending.size() - 1;
+  }
+  check(nccl().GroupStart(), "group start");
 }
 void comm_group_end(csg_ctx* c) {
-  if (comm_active(c)) check(nccl().GroupEnd(), "group end");
+  if (!comm_active(c)) return;
+  check(nccl().GroupEnd(), "group end");
+  if (--c->comm_group_depth == 0 && c->lc.prof.enabled && c->group_rec < c->lc.prof.pending.size()) {
+    cudaEvent_t b = c->lc.prof.take();
+    cudaEventRecord(b, c->stream);
+    c->lc.prof.pending[c->group_rec].b = b;
+  }
 }
 
 void comm_allgather(csg_ctx* c, const void* send, void* recv, size_t count,
@@ -95,6 +110,8 @@ void comm_allgather(csg_ctx* c, const void* send, void* recv, size_t count,
     return;
   }
   ++c->collectives;
+  ProfScope ps_(c->lc, c->comm_group_depth ? "nccl_in_group" : "nccl_allgather", c->stream,
+                false);
   check(nccl().AllGather(send, recv, count, t, static_cast<ncclComm_t>(c->comm),
                          c->stream),
         "allgather");

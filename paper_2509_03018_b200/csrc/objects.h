@@ -19,6 +19,8 @@ struct csg_ctx {
   void* comm = nullptr;
   int nranks = 1, rank = 0;
   uint64_t collectives = 0;
+  int comm_group_depth = 0;   // NCCL group nesting (timeline records)
+  size_t group_rec = ~size_t(0);
   csg::LaunchCounter lc;
   std::vector<double> h_ticks;  // detection tick times (host-computed)
   std::vector<csg_trigger_event> h_events;  // trips of the last trigger_run

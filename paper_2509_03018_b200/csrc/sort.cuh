@@ -93,9 +93,9 @@ struct ProfScope {
   LaunchCounter& lc;
   cudaStream_t st;
   bool on;
-  ProfScope(LaunchCounter& l, const char* name, cudaStream_t s)
+  ProfScope(LaunchCounter& l, const char* name, cudaStream_t s, bool ours = true)
       : lc(l), st(s), on(l.prof.enabled) {
-    ++lc.launches;
+    if (ours) ++lc.launches;  // NCCL collectives are timed, not counted
     if (on) {
       cudaEvent_t a = lc.prof.take();
       cudaEventRecord(a, st);
