@@ -65,12 +65,10 @@ def dist_env():
 
 def scaled_config(ngpus: int) -> str:
     """Weak scaling: N GPUs analyze an N x larger job — DP grows to 32N, so
-    every GPU owns 1024 ranks (~1e7 records) of a 1024N-rank trace."""
+    every GPU owns 1024 ranks (~1e7 records) of a 1024N-rank trace with the
+    same single injected hang (BASELINE C4: one fault in the whole job)."""
     cfg = json.load(open(CONFIG))
     cfg["layout"]["dp"] = cfg["layout"]["dp"] * ngpus
-    # one failing NIC per 1024-rank block (every 128 nodes), same onset
-    f0 = cfg["faults"][0]
-    cfg["faults"] = [dict(f0, node=f0["node"] + 128 * k) for k in range(ngpus)]
     return json.dumps(cfg)
 
 
@@ -196,6 +194,8 @@ def run_ours(args):
     with Clocks(local) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
+            if ws > 1:  # shards analyze each window in lockstep
+                dist.barrier()
             reports, sampled = step()
         wall = time.perf_counter() - t0
     torch.cuda.synchronize()

@@ -184,6 +184,16 @@ namespace {
 __global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long long v) {
   for (int sgi = 0; sgi < a.n; ++sgi) {
     const FetchSeg& g = a.seg[sgi];
+    if (g.row_len) {  // rows with device-side lengths, one warp per row
+      const int lane = threadIdx.x & 31;
+      for (uint32_t rw = threadIdx.x >> 5; rw < g.nrows; rw += blockDim.x >> 5) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(g.src + rw * g.bytes);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(g.dst + rw * g.bytes);
+        const int32_t len = g.row_len[rw];
+        for (int32_t i = lane; i < len; i += 32) d4[i] = s4[i];
+      }
+      continue;
+    }
     const bool vec = ((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) |
                        g.bytes) & 15) == 0;
     if (vec) {

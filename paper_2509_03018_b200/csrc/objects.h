@@ -229,6 +229,10 @@ struct FetchSeg {
   const unsigned char* src;
   unsigned char* dst;
   uint32_t bytes;
+  // row mode (row_len != nullptr): nrows rows of stride `bytes`, row i holds
+  // row_len[i] (device) 4-byte elements — only those are copied
+  const int32_t* row_len;
+  uint32_t nrows;
 };
 constexpr int kFetchSegs = 6;
 struct FetchArgs {
@@ -236,7 +240,14 @@ struct FetchArgs {
   int n;
   void add(const void* src, void* dst, size_t bytes) {
     seg[n++] = FetchSeg{static_cast<const unsigned char*>(src),
-                        static_cast<unsigned char*>(dst), static_cast<uint32_t>(bytes)};
+                        static_cast<unsigned char*>(dst), static_cast<uint32_t>(bytes),
+                        nullptr, 0};
+  }
+  void add_rows(const void* src, void* dst, size_t stride, const int32_t* lens,
+                uint32_t nrows) {
+    seg[n++] = FetchSeg{static_cast<const unsigned char*>(src),
+                        static_cast<unsigned char*>(dst), static_cast<uint32_t>(stride),
+                        lens, nrows};
   }
 };
 void ctx_sync(csg_ctx* c, const FetchArgs* fetch = nullptr);

@@ -2691,12 +2691,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   {
     FetchArgs fa{};
     fa.add(n_aff.p, h_na, static_cast<size_t>(J) * 4);
-    if (G) fa.add(aff.p, h_ag, static_cast<size_t>(J) * G * 4);
+    // only each trip's affected groups cross PCIe, not the J x G matrix
+    if (G) fa.add_rows(aff.p, h_ag, static_cast<size_t>(G) * 4, n_aff.as<int32_t>(), J);
     ctx_sync(c, &fa);
   }
   tl_mark("affected sync returned");
   std::vector<int32_t> h_naff(h_na, h_na + J);
-  out.aff.assign(h_ag, h_ag + static_cast<size_t>(J) * G);
+  out.aff = h_ag;
   CSG_CUDA(cudaGetLastError());
   c->d2h_bytes += static_cast<uint64_t>(J) * 4 + static_cast<uint64_t>(J) * G * 4;
   out.trips.assign(J, TripOut{});

@@ -77,7 +77,10 @@ struct RcaResult {
   std::vector<TripOut> trips;
   std::vector<csg_suspect> sus;
   std::vector<csg_evidence> ev;
-  std::vector<int32_t> aff;  // [J * G]
+  // [J * G] row j: trip j's affected groups (first trips[j].n_aff valid);
+  // points into the context's pinned read-back buffer (valid until the
+  // next analysis on the context)
+  const int32_t* aff = nullptr;
   int32_t G = 0;
 };
 

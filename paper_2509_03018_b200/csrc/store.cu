@@ -226,6 +226,41 @@ struct HistLoad {
   __device__ uint32_t operator()(uint64_t i) const { return hv(counts, i, T, d0); }
 };
 
+// Packs the store statistics into order-preserving u64 images (dir 0) so
+// one MAX all-reduce combines every extremum across shards (minima travel
+// as complements), counts into a SUM pair; dir 1 unpacks the reduced
+// values (the shard's own lmin/lmax_rank stay local).
+__device__ inline unsigned long long i64_key(long long v) {
+  return static_cast<unsigned long long>(v) ^ 0x8000000000000000ull;
+}
+__device__ inline long long key_i64(unsigned long long k) {
+  return static_cast<long long>(k ^ 0x8000000000000000ull);
+}
+__global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (dir == 0) {
+    pk[0] = st->ts_max_key;
+    pk[1] = ~i64_key(st->min_rank);
+    pk[2] = i64_key(st->max_rank);
+    pk[3] = ~i64_key(st->min_chan);
+    pk[4] = i64_key(st->max_chan);
+    pk[5] = ~i64_key(st->min_op);
+    pk[6] = i64_key(st->max_op);
+    pk[8] = st->n_nan;
+    pk[9] = st->n_total;
+  } else {
+    st->ts_max_key = pk[0];
+    st->min_rank = static_cast<int>(key_i64(~pk[1]));
+    st->max_rank = static_cast<int>(key_i64(pk[2]));
+    st->min_chan = static_cast<int>(key_i64(~pk[3]));
+    st->max_chan = static_cast<int>(key_i64(pk[4]));
+    st->min_op = key_i64(~pk[5]);
+    st->max_op = key_i64(pk[6]);
+    st->n_nan = pk[8];
+    st->n_total = pk[9];
+  }
+}
+
 // rank_off over absolute ranks [0, R] from the scanned tile offsets.
 __global__ void k_rank_off_hist(const uint32_t* __restrict__ goff, uint32_t T,
                                 int32_t min_rank, int32_t max_rank, int32_t R,
@@ -976,18 +1011,24 @@ void store_build_index(csg_store* s) {
   }
   if (comm_active(c)) {
     // global stats over the shards (identical rank space, ticks, op range)
-    StoreStats* d = s->stats_dev.as<StoreStats>();
+    // one MAX all-reduce over order-preserving u64 images (minima as
+    // complements) and one SUM all-reduce for the counts
+    DevBuf& pk = c->buf("store.stats_pack");
+    pk.ensure(16 * 8);
+    {
+      ProfScope ps_(c->lc, "k_stats_pack", st);
+      k_stats_pack<<<1, 32, 0, st>>>(s->stats_dev.as<StoreStats>(),
+                                     pk.as<unsigned long long>(), 0);
+    }
     comm_group_start(c);
-    comm_allreduce(c, &d->ts_max_key, 1, ncclUint64, ncclMax);
-    comm_allreduce(c, &d->min_rank, 1, ncclInt32, ncclMin);
-    comm_allreduce(c, &d->max_rank, 1, ncclInt32, ncclMax);
-    comm_allreduce(c, &d->min_chan, 1, ncclInt32, ncclMin);
-    comm_allreduce(c, &d->max_chan, 1, ncclInt32, ncclMax);
-    comm_allreduce(c, &d->min_op, 1, ncclInt64, ncclMin);
-    comm_allreduce(c, &d->max_op, 1, ncclInt64, ncclMax);
-    comm_allreduce(c, &d->n_nan, 1, ncclUint64, ncclSum);
-    comm_allreduce(c, &d->n_total, 1, ncclUint64, ncclSum);
+    comm_allreduce(c, pk.p, 7, ncclUint64, ncclMax);
+    comm_allreduce(c, pk.as<unsigned long long>() + 8, 2, ncclUint64, ncclSum);
     comm_group_end(c);
+    {
+      ProfScope ps_(c->lc, "k_stats_pack", st);
+      k_stats_pack<<<1, 32, 0, st>>>(s->stats_dev.as<StoreStats>(),
+                                     pk.as<unsigned long long>(), 1);
+    }
   }
   {
     HostBuf& hs = c->hbuf("store.stats");

@@ -268,112 +268,54 @@ __global__ void k_pick_trips(const uint8_t* __restrict__ trip,
 //      shared memory;
 //   3. the last rank to finish picks the lowest tripped rank of every tick
 //      and compacts the trips in tick order (runner.cpp:72-79).
-struct WinAcc {
+// Accumulators of the trigger windows, zero-initialised; split by the
+// reduction they need so a sharded store combines them with one SUM and one
+// MAX all-reduce (complemented min key: max = min).
+struct WinSum {
   unsigned int n_rec, n_comp, has_state, pad;
-  unsigned long long bytes, mn_inv, mx;
+  unsigned long long bytes;
+};
+struct WinMax {
+  unsigned long long mn_inv, mx;
 };
 
-__global__ void __launch_bounds__(512)
-    k_trigger(StoreView s, const double* __restrict__ ticks, int32_t T,
-              const int32_t* __restrict__ sampled, int32_t S, TrigParams p, int32_t B,
-              WinAcc* __restrict__ acc, unsigned* __restrict__ done,
-              uint8_t* __restrict__ trip, csg_trigger_event* __restrict__ events,
-              int32_t* __restrict__ n_events) {
-  extern __shared__ __align__(16) unsigned char tg_dyn[];
-  double* st = reinterpret_cast<double*>(tg_dyn);                       // [T]
-  unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
-  unsigned long long* mn = bytes + T;  // complemented keys (max = min)
-  unsigned long long* mx = mn + T;
-  uint32_t* nrec = reinterpret_cast<uint32_t*>(mx + T);
-  uint32_t* ncomp = nrec + T;
-  uint32_t* hstate = ncomp + T;
+// EMA of sampled rank si over all ticks (evaluate, trigger.cpp:57-136) from
+// the accumulated windows staged in shared memory, then — in the last block
+// to finish (done[S] ticket) — the lowest tripped rank of every tick,
+// compacted in tick order (runner.cpp:72-79). Block-collective.
+__device__ void trigger_ema_pick(int32_t si, int32_t T, const double* st, int32_t S,
+                                 const int32_t* __restrict__ sampled, const TrigParams& p,
+                                 const WinSum* __restrict__ asum,
+                                 const WinMax* __restrict__ amax, unsigned* __restrict__ done,
+                                 uint8_t* __restrict__ trip,
+                                 csg_trigger_event* __restrict__ events,
+                                 int32_t* __restrict__ n_events, WinStat* ws) {
   __shared__ int last;
-  const int32_t si = blockIdx.y, bi = blockIdx.x;
-  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
-    st[k] = ticks[k];
-    bytes[k] = mn[k] = mx[k] = 0;
-    nrec[k] = ncomp[k] = hstate[k] = 0;
-  }
-  __syncthreads();
-  const double delta = p.delta;
-  const int32_t r = sampled[si];
-  if (r >= 0 && r < s.R) {
-    const uint32_t b0 = s.rank_off[r], L = s.rank_off[r + 1] - b0;
-    const uint32_t cb = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * bi / B);
-    const uint32_t ce = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * (bi + 1) / B);
-    for (uint32_t q = cb + threadIdx.x; q < ce; q += blockDim.x) {
-      const double x = s.ts[q];
-      int32_t lo = 0, hi = T;  // first tick with t_k >= x
-      while (lo < hi) {
-        const int32_t md = (lo + hi) >> 1;
-        if (st[md] < x) lo = md + 1; else hi = md;
-      }
-      const bool comp = ko_kind(s.ko[q]) == CSG_KIND_COMPLETION;
-      for (int32_t k = lo; k < T && !(x < st[k] - delta); ++k) {
-        if (x > st[k]) continue;
-        atomicAdd(&nrec[k], 1u);
-        if (comp) {
-          atomicAdd(&ncomp[k], 1u);
-          atomicAdd(&bytes[k], static_cast<unsigned long long>(s.pb[q]));
-          const unsigned long long kk = dkey(x);
-          atomicMax(&mn[k], ~kk);
-          atomicMax(&mx[k], kk);
-        } else {
-          hstate[k] = 1;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
-    if (!nrec[k]) continue;
-    WinAcc& a = acc[static_cast<int64_t>(k) * S + si];
-    atomicAdd(&a.n_rec, nrec[k]);
-    if (hstate[k]) atomicOr(&a.has_state, 1u);
-    if (ncomp[k]) {
-      atomicAdd(&a.n_comp, ncomp[k]);
-      atomicAdd(&a.bytes, bytes[k]);
-      atomicMax(&a.mn_inv, mn[k]);
-      atomicMax(&a.mx, mx[k]);
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&done[si], 1u) == static_cast<unsigned>(B - 1);
-  __syncthreads();
-  if (!last) return;
-  // ---- last block of sampled rank si: EMA over the ticks
   __threadfence();
   for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
-    const WinAcc* a = acc + static_cast<int64_t>(k) * S + si;
-    nrec[k] = __ldcg(&a->n_rec);
-    ncomp[k] = __ldcg(&a->n_comp);
-    hstate[k] = __ldcg(&a->has_state);
-    bytes[k] = __ldcg(&a->bytes);
-    mn[k] = __ldcg(&a->mn_inv);
-    mx[k] = __ldcg(&a->mx);
+    const WinSum* a = asum + static_cast<int64_t>(k) * S + si;
+    const WinMax* m = amax + static_cast<int64_t>(k) * S + si;
+    WinStat w;
+    w.n_rec = __ldcg(&a->n_rec);
+    w.n_comp = __ldcg(&a->n_comp);
+    w.has_state = __ldcg(&a->has_state);
+    w.pad = 0;
+    w.bytes = __ldcg(&a->bytes);
+    w.min_end = w.n_comp ? dkey_inv(~__ldcg(&m->mn_inv)) : 0.0;
+    w.max_end = w.n_comp ? dkey_inv(__ldcg(&m->mx)) : 0.0;
+    ws[k] = w;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     TrigSlot b{0, 0, 0, 0, 0, 0};
-    for (int32_t k = 0; k < T; ++k) {
-      WinStat w;
-      w.n_rec = nrec[k];
-      w.n_comp = ncomp[k];
-      w.has_state = hstate[k];
-      w.pad = 0;
-      w.bytes = bytes[k];
-      w.min_end = ncomp[k] ? dkey_inv(~mn[k]) : 0.0;
-      w.max_end = ncomp[k] ? dkey_inv(mx[k]) : 0.0;
-      trip[static_cast<int64_t>(k) * S + si] = static_cast<uint8_t>(ema_step(b, w, p));
-    }
+    for (int32_t k = 0; k < T; ++k)
+      trip[static_cast<int64_t>(k) * S + si] = static_cast<uint8_t>(ema_step(b, ws[k], p));
   }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&done[S], 1u) == static_cast<unsigned>(S - 1);
   __syncthreads();
   if (!last) return;
-  // ---- last rank: lowest tripped sampled rank per tick, compacted in order
   __threadfence();
   __shared__ int32_t base;
   __shared__ int32_t wsum[32];
@@ -425,6 +367,105 @@ __global__ void __launch_bounds__(512)
     __syncthreads();
   }
   if (threadIdx.x == 0) *n_events = base;
+}
+
+// Whole trigger stage of run_detection in one launch:
+//   1. window statistics: grid (B, S); block (b, s) bins chunk b of sampled
+//      rank s's segment into per-tick shared-memory bins (as k_window_bins)
+//      and merges them into the zero-initialised accumulators;
+//   2. (chain != 0) the last block of each sampled rank runs trigger_ema_pick
+//      for it. Sharded stores stop after step 1 (chain == 0), all-reduce the
+//      accumulators and finish with k_trigger_ema.
+__global__ void __launch_bounds__(512)
+    k_trigger(StoreView s, const double* __restrict__ ticks, int32_t T,
+              const int32_t* __restrict__ sampled, int32_t S, TrigParams p, int32_t B,
+              WinSum* __restrict__ asum, WinMax* __restrict__ amax, unsigned* __restrict__ done,
+              uint8_t* __restrict__ trip, csg_trigger_event* __restrict__ events,
+              int32_t* __restrict__ n_events, int chain) {
+  extern __shared__ __align__(16) unsigned char tg_dyn[];
+  double* st = reinterpret_cast<double*>(tg_dyn);                       // [T]
+  unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
+  unsigned long long* mn = bytes + T;  // complemented keys (max = min)
+  unsigned long long* mx = mn + T;
+  uint32_t* nrec = reinterpret_cast<uint32_t*>(mx + T);
+  uint32_t* ncomp = nrec + T;
+  uint32_t* hstate = ncomp + T;
+  __shared__ int last;
+  const int32_t si = blockIdx.y, bi = blockIdx.x;
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    st[k] = ticks[k];
+    bytes[k] = mn[k] = mx[k] = 0;
+    nrec[k] = ncomp[k] = hstate[k] = 0;
+  }
+  __syncthreads();
+  const double delta = p.delta;
+  const int32_t r = sampled[si];
+  if (r >= 0 && r < s.R) {
+    const uint32_t b0 = s.rank_off[r], L = s.rank_off[r + 1] - b0;
+    const uint32_t cb = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * bi / B);
+    const uint32_t ce = b0 + static_cast<uint32_t>(static_cast<uint64_t>(L) * (bi + 1) / B);
+    for (uint32_t q = cb + threadIdx.x; q < ce; q += blockDim.x) {
+      const double x = s.ts[q];
+      int32_t lo = 0, hi = T;  // first tick with t_k >= x
+      while (lo < hi) {
+        const int32_t md = (lo + hi) >> 1;
+        if (st[md] < x) lo = md + 1; else hi = md;
+      }
+      const bool comp = ko_kind(s.ko[q]) == CSG_KIND_COMPLETION;
+      for (int32_t k = lo; k < T && !(x < st[k] - delta); ++k) {
+        if (x > st[k]) continue;
+        atomicAdd(&nrec[k], 1u);
+        if (comp) {
+          atomicAdd(&ncomp[k], 1u);
+          atomicAdd(&bytes[k], static_cast<unsigned long long>(s.pb[q]));
+          const unsigned long long kk = dkey(x);
+          atomicMax(&mn[k], ~kk);
+          atomicMax(&mx[k], kk);
+        } else {
+          hstate[k] = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+    if (!nrec[k]) continue;
+    WinSum& a = asum[static_cast<int64_t>(k) * S + si];
+    WinMax& m = amax[static_cast<int64_t>(k) * S + si];
+    atomicAdd(&a.n_rec, nrec[k]);
+    if (hstate[k]) atomicOr(&a.has_state, 1u);
+    if (ncomp[k]) {
+      atomicAdd(&a.n_comp, ncomp[k]);
+      atomicAdd(&a.bytes, bytes[k]);
+      atomicMax(&m.mn_inv, mn[k]);
+      atomicMax(&m.mx, mx[k]);
+    }
+  }
+  if (!chain) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&done[si], 1u) == static_cast<unsigned>(B - 1);
+  __syncthreads();
+  if (!last) return;
+  // the bins are merged: their 36 T bytes stage the T window statistics
+  trigger_ema_pick(si, T, st, S, sampled, p, asum, amax, done, trip, events, n_events,
+                   reinterpret_cast<WinStat*>(bytes));
+}
+
+// Sharded finish: one block per sampled rank over the all-reduced windows.
+__global__ void __launch_bounds__(512)
+    k_trigger_ema(const double* __restrict__ ticks, int32_t T,
+                  const int32_t* __restrict__ sampled, int32_t S, TrigParams p,
+                  const WinSum* __restrict__ asum, const WinMax* __restrict__ amax,
+                  unsigned* __restrict__ done, uint8_t* __restrict__ trip,
+                  csg_trigger_event* __restrict__ events, int32_t* __restrict__ n_events) {
+  extern __shared__ __align__(16) unsigned char te_dyn[];
+  double* st = reinterpret_cast<double*>(te_dyn);       // [T]
+  WinStat* ws = reinterpret_cast<WinStat*>(st + T);      // [T]
+  for (int32_t k = threadIdx.x; k < T; k += blockDim.x) st[k] = ticks[k];
+  __syncthreads();
+  trigger_ema_pick(blockIdx.x, T, st, S, sampled, p, asum, amax, done, trip, events,
+                   n_events, ws);
 }
 
 // csg_evaluate: one tick, the caller's sampled list in order (duplicates
@@ -512,12 +553,18 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
-  const size_t tsmem = static_cast<size_t>(T) * 44;
-  if (!comm_active(c) && tsmem <= 200 * 1024) {
+  const size_t tsmem = std::max<size_t>(static_cast<size_t>(T) * 44,
+                                        static_cast<size_t>(T) * (8 + sizeof(WinStat)));
+  if (tsmem <= 200 * 1024) {
     DevBuf& acc = c->buf("trig.acc");
-    const size_t abytes = static_cast<size_t>(T) * S * sizeof(WinAcc);
-    acc.ensure(abytes + (static_cast<size_t>(S) + 1) * 4 + 16);
-    CSG_CUDA(cudaMemsetAsync(acc.p, 0, abytes + (static_cast<size_t>(S) + 1) * 4, c->stream));
+    const size_t sb = static_cast<size_t>(T) * S * sizeof(WinSum);
+    const size_t mb = static_cast<size_t>(T) * S * sizeof(WinMax);
+    const size_t db = (static_cast<size_t>(S) + 1) * 4;
+    acc.ensure(sb + mb + db + 16);
+    CSG_CUDA(cudaMemsetAsync(acc.p, 0, sb + mb + db, c->stream));
+    WinSum* asum = acc.as<WinSum>();
+    WinMax* amax = reinterpret_cast<WinMax*>(acc.as<unsigned char>() + sb);
+    unsigned* done = reinterpret_cast<unsigned*>(acc.as<unsigned char>() + sb + mb);
     // about 2k records per block of a sampled rank's (average) segment
     const uint64_t avg = s->R > 0 ? s->n / static_cast<uint64_t>(s->R) : 0;
     const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, avg / 2048)));
@@ -525,13 +572,26 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     if (!attr) {
       CSG_CUDA(cudaFuncSetAttribute(k_trigger, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     200 * 1024));
+      CSG_CUDA(cudaFuncSetAttribute(k_trigger_ema, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
       attr = true;
     }
+    const bool sharded = comm_active(c);
     {
       ProfScope ps_(c->lc, "k_trigger", c->stream);
-      k_trigger<<<dim3(B, S), 512, tsmem, c->stream>>>(
-          s->view(), d_ticks, T, d_sampled, S, p, B, acc.as<WinAcc>(),
-          reinterpret_cast<unsigned*>(acc.as<unsigned char>() + abytes), trip.as<uint8_t>(),
+      k_trigger<<<dim3(B, S), 512, static_cast<size_t>(T) * 44, c->stream>>>(
+          s->view(), d_ticks, T, d_sampled, S, p, B, asum, amax, done, trip.as<uint8_t>(),
+          events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1);
+    }
+    if (sharded) {
+      // shards own disjoint rank ranges: windows combine by sum / max
+      comm_group_start(c);
+      comm_allreduce(c, asum, sb / 8, ncclUint64, ncclSum);
+      comm_allreduce(c, amax, mb / 8, ncclUint64, ncclMax);
+      comm_group_end(c);
+      ProfScope ps_(c->lc, "k_trigger_ema", c->stream);
+      k_trigger_ema<<<S, 512, static_cast<size_t>(T) * (8 + sizeof(WinStat)), c->stream>>>(
+          d_ticks, T, d_sampled, S, p, asum, amax, done, trip.as<uint8_t>(),
           events.as<csg_trigger_event>(), dn.as<int32_t>());
     }
   } else {

@@ -34,4 +34,18 @@ for i in range(4):
         if rank == 0:
             print("---- last step", file=sys.stderr, flush=True)
         ctx.kernel_stats()
+
+# per-rank device time per step, back to back (as bench.py) and barrier-separated
+for mode in ("back-to-back", "barrier"):
+    ctx.reset_stats()
+    ctx.profile(False)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(10):
+        if mode == "barrier":
+            dist.barrier()
+        store.invalidate()
+        E.run_detection(store, model, tcfg, acfg, seed)
+    ms, _ = ctx.stats()
+    print(f"rank {rank} {mode}: {ms / 10:.3f} ms/step", file=sys.stderr, flush=True)
 dist.destroy_process_group()
