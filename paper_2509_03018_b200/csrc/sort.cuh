@@ -93,8 +93,9 @@ struct ProfScope {
   LaunchCounter& lc;
   cudaStream_t st;
   bool on;
+  const char* name_;
   ProfScope(LaunchCounter& l, const char* name, cudaStream_t s, bool ours = true)
-      : lc(l), st(s), on(l.prof.enabled) {
+      : lc(l), st(s), on(l.prof.enabled), name_(name) {
     if (ours) ++lc.launches;  // NCCL collectives are timed, not counted
     if (on) {
       cudaEvent_t a = lc.prof.take();
@@ -106,6 +107,12 @@ struct ProfScope {
     }
   }
   ~ProfScope() {
+    static const bool sync_each = std::getenv("CSG_SYNC_EACH") != nullptr;
+    if (sync_each) {  // debugging aid: name the kernel that faulted
+      const cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) fprintf(stderr, "CSG_SYNC_EACH: %s after %s\n",
+                                    cudaGetErrorString(e), name_);
+    }
     if (on) {
       cudaEvent_t b = lc.prof.take();
       cudaEventRecord(b, st);

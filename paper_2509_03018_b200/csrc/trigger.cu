@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(512)
   if (threadIdx.x == 0) last = atomicAdd(&done[si], 1u) == static_cast<unsigned>(B - 1);
   __syncthreads();
   if (!last) return;
-  // the bins are merged: their 36 T bytes stage the T window statistics
+  // the bins are merged: the 40 T bytes behind the tick times (launched with
+  // T * (8 + sizeof(WinStat)) bytes) stage the T window statistics
   trigger_ema_pick(si, T, st, S, sampled, p, asum, amax, done, trip, events, n_events,
                    reinterpret_cast<WinStat*>(bytes));
 }
@@ -553,8 +554,10 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
-  const size_t tsmem = std::max<size_t>(static_cast<size_t>(T) * 44,
-                                        static_cast<size_t>(T) * (8 + sizeof(WinStat)));
+  // bins need 44 B per tick; after the merge the last block of a sampled
+  // rank stages its window statistics behind the tick times (8 + 40 B)
+  static_assert(sizeof(WinStat) == 40, "WinStat layout");
+  const size_t tsmem = static_cast<size_t>(T) * (8 + sizeof(WinStat));
   if (tsmem <= 200 * 1024) {
     DevBuf& acc = c->buf("trig.acc");
     const size_t sb = static_cast<size_t>(T) * S * sizeof(WinSum);
@@ -579,7 +582,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     const bool sharded = comm_active(c);
     {
       ProfScope ps_(c->lc, "k_trigger", c->stream);
-      k_trigger<<<dim3(B, S), 512, static_cast<size_t>(T) * 44, c->stream>>>(
+      k_trigger<<<dim3(B, S), 512, tsmem, c->stream>>>(
           s->view(), d_ticks, T, d_sampled, S, p, B, asum, amax, done, trip.as<uint8_t>(),
           events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1);
     }
@@ -590,7 +593,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
       comm_allreduce(c, amax, mb / 8, ncclUint64, ncclMax);
       comm_group_end(c);
       ProfScope ps_(c->lc, "k_trigger_ema", c->stream);
-      k_trigger_ema<<<S, 512, static_cast<size_t>(T) * (8 + sizeof(WinStat)), c->stream>>>(
+      k_trigger_ema<<<S, 512, tsmem, c->stream>>>(
           d_ticks, T, d_sampled, S, p, asum, amax, done, trip.as<uint8_t>(),
           events.as<csg_trigger_event>(), dn.as<int32_t>());
     }
