@@ -35,6 +35,25 @@ sys.path.insert(0, ROOT)
 
 CONFIG = os.path.join(ROOT, "configs", "c2_hang_1024.json")
 TARGET_RECORDS = 10_000_000
+# --workload c3: BASELINE configs[2] (8192 ranks, 16 channels, 1e8 records,
+# mixed fail-slow faults) — the "per 1e8-record window" latency
+WORKLOADS = {
+    "c2": ("configs/c2_hang_1024.json", 10_000_000,
+           "C2: 1024-rank DP32xPP4xTP8 hybrid trace, injected hang (nic_shutdown), "
+           "full run_detection replay"),
+    "c3": ("configs/c3_8192.json", 100_000_000,
+           "C3: 8192-rank DP128xPP8xTP8 trace, 16 channels, mixed fail-slow "
+           "(gpu_power_limit, pcie_downgrade, background_traffic), full run_detection replay"),
+}
+WORKLOAD_DESC = WORKLOADS["c2"][2]
+
+
+def select_workload(name):
+    global CONFIG, TARGET_RECORDS, WORKLOAD_DESC
+    cfg, target, desc = WORKLOADS[name]
+    CONFIG = os.path.join(ROOT, cfg)
+    TARGET_RECORDS = target
+    WORKLOAD_DESC = desc
 METRIC = "trace records/s through trigger+RCA"
 UNIT = "records/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -79,7 +98,7 @@ def load_workload(ngpus: int = 1, shard: int = 0):
     scen = E.Scenario.parse(scaled_config(ngpus))
     world = 1024 * ngpus
     lo, hi = D.shard_bounds(world, ngpus)[shard]
-    cache = f"/tmp/collsight_c2_{TARGET_RECORDS}_n{ngpus}_s{shard}.rec"
+    cache = f"/tmp/collsight_{os.path.basename(CONFIG)}_{TARGET_RECORDS}_n{ngpus}_s{shard}.rec"
     if os.path.exists(cache):
         recs = np.fromfile(cache, dtype=np.uint8).view(RECORD_DTYPE)
     else:
@@ -293,14 +312,14 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+int64",
         "data": "synthetic (csrc/host/synth.cpp, seed 42)",
-        "config": {"workload": "C2: 1024-rank DP32xPP4xTP8 hybrid trace, injected "
-                               "hang (nic_shutdown), full run_detection replay",
-                   "records": n_total, "records_per_gpu": n, "ranks": 1024 * ws,
-                   "channels_per_pair": 4,
+        "config": {"workload": WORKLOAD_DESC,
+                   "records": n_total, "records_per_gpu": n,
+                   "ranks": topo.world_size,
+                   "channels_per_pair": json.load(open(CONFIG))["layout"]["channels_per_pair"],
                    "ticks_tripped": trips, "sampled_ranks": len(sampled),
                    "parallelism": f"rank-range shards x{ws}, NCCL all-reduce of "
                                   "per-rank summaries" if ws > 1 else "single",
-                   "l2": "inputs (480 MB store) larger than the 126 MB L2"},
+                   "l2": f"inputs ({n * 48 / 1e6:.0f} MB store) larger than the 126 MB L2"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved,
                      "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
@@ -443,7 +462,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    select_workload(args.workload)
     if args.impl == "reference":
         run_reference(args)
     else:

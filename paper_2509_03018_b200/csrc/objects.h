@@ -77,6 +77,7 @@ struct csg_store {
   // stats (valid when indexed)
   double last_ts = 0;  // max(0, max timestamp), runner.cpp:51-56
   int32_t min_rank = 0, max_rank = -1;
+  int32_t own_lo = 0, own_hi = -1;  // this shard's own rank range (local records)
   int32_t min_chan = 0, max_chan = -1;
   int64_t min_op = 0, max_op = -1;
   // rank-major index

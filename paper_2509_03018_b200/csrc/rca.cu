@@ -128,13 +128,13 @@ __global__ void k_rank_summary(StoreView s, int32_t J,
                                const double* __restrict__ trip_t,
                                double delta_a, RankSum* __restrict__ out,
                                unsigned long long* __restrict__ chan_key,
-                               int32_t nch) {
+                               int32_t nch, int32_t r0, int32_t nr) {
   extern __shared__ uint32_t sm_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const bool active = w < static_cast<int64_t>(s.R) * J;
-  const int32_t r = active ? static_cast<int32_t>(w / J) : 0;
+  const bool active = w < static_cast<int64_t>(nr) * J;
+  const int32_t r = active ? r0 + static_cast<int32_t>(w / J) : 0;
   const int32_t j = active ? static_cast<int32_t>(w % J) : 0;
   uint32_t* tbl = sm_tbl + wib * nch;
   if (!active) return;
@@ -247,13 +247,13 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
                                   const double* __restrict__ trip_t,
                                   double delta_a, RankSum* __restrict__ out,
                                   unsigned long long* __restrict__ chan_key,
-                                  int32_t nch) {
+                                  int32_t nch, int32_t r0, int32_t nr) {
   extern __shared__ uint32_t sm_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= static_cast<int64_t>(s.R) * J) return;
-  const int32_t r = static_cast<int32_t>(w / J);
+  if (w >= static_cast<int64_t>(nr) * J) return;
+  const int32_t r = r0 + static_cast<int32_t>(w / J);
   const int32_t j = static_cast<int32_t>(w % J);
   uint32_t* tbl = sm_tbl + wib * nch;
   for (int c = lane; c < nch; c += 32) tbl[c] = 0;
@@ -377,14 +377,17 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
                             const RankSum* __restrict__ rs,
                             SuccProg* __restrict__ out,
                             unsigned long long* __restrict__ sp_key,
-                            int32_t nch) {
+                            int32_t nch, const uint32_t* __restrict__ slots,
+                            uint32_t nslots) {
   extern __shared__ uint32_t sp_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= static_cast<int64_t>(M) * J) return;
-  const int32_t j = static_cast<int32_t>(w / M);
-  const uint32_t q = static_cast<uint32_t>(w % M);
+  // slots (sharded stores): only the membership slots of owned ranks
+  const uint32_t E = slots ? nslots : M;
+  if (w >= static_cast<int64_t>(E) * J) return;
+  const int32_t j = static_cast<int32_t>(w / E);
+  const uint32_t q = slots ? slots[w % E] : static_cast<uint32_t>(w % E);
   uint32_t* tbl = sp_tbl + wib * nch;
   for (int c = lane; c < nch; c += 32) tbl[c] = 0;
   __syncwarp();
@@ -2565,23 +2568,34 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   DevBuf& chan_key = c->buf("rca.chan_key");
   rs.ensure(static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum));
   chan_key.ensure(static_cast<size_t>(J) * std::max(R, 1) * nch * 8);
-  if (R > 0) {
+  // Sharded: only this shard's ranks are summarised; the other entries are
+  // zero so a sum all-reduce assembles the global tables.
+  const bool sharded = comm_active(c);
+  const int32_t r0 = sharded ? std::max(s->own_lo, 0) : 0;
+  const int32_t nr = sharded ? std::max(0, std::min(s->own_hi, R - 1) - r0 + 1) : R;
+  if (sharded) {
+    CSG_CUDA(cudaMemsetAsync(rs.p, 0, static_cast<size_t>(J) * std::max(R, 1) * sizeof(RankSum),
+                             st));
+    CSG_CUDA(cudaMemsetAsync(chan_key.p, 0,
+                             static_cast<size_t>(J) * std::max(R, 1) * nch * 8, st));
+  }
+  if (R > 0 && nr > 0) {
     int wpb = 32768 / (nch * 4);
     wpb = std::max(1, std::min(8, wpb));
-    const uint64_t warps = static_cast<uint64_t>(R) * J;
+    const uint64_t warps = static_cast<uint64_t>(nr) * J;
     static const bool no_fi = std::getenv("CSG_DISABLE_FLOW_INDEX") != nullptr;
     if (!no_fi && store_build_flow_index(s)) {
       ProfScope ps_(c->lc, "k_rank_summary_fi", st);
       k_rank_summary_fi<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
                           wpb * nch * 4, st>>>(sv, s->flow_view(), J, dt, cfg.delta_ms,
                                                rs.as<RankSum>(),
-                                               chan_key.as<unsigned long long>(), nch);
+                                               chan_key.as<unsigned long long>(), nch, r0, nr);
     } else {
       ProfScope ps_(c->lc, "k_rank_summary", st);
       k_rank_summary<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
                        wpb * nch * 4, st>>>(sv, J, dt, cfg.delta_ms,
                                             rs.as<RankSum>(),
-                                            chan_key.as<unsigned long long>(), nch);
+                                            chan_key.as<unsigned long long>(), nch, r0, nr);
     }
   }
   // sharded: every rank's summary lives on exactly one shard (zeros
@@ -2607,15 +2621,30 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   succ.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * sizeof(SuccProg));
   succ_key.ensure(static_cast<size_t>(J) * std::max<uint32_t>(M, 1) * nch * 8);
   if (!affected_only && M > 0) {
+    // sharded: the membership slots of owned ranks (contiguous in the
+    // model's rank -> slot CSR), zeros elsewhere
+    const uint32_t* slots = nullptr;
+    uint32_t E = M;
+    if (sharded) {
+      CSG_CUDA(cudaMemsetAsync(succ.p, 0, static_cast<size_t>(J) * M * sizeof(SuccProg), st));
+      CSG_CUDA(cudaMemsetAsync(succ_key.p, 0, static_cast<size_t>(J) * M * nch * 8, st));
+      const int32_t RS = m->rank_space;
+      const int32_t lo = std::min(r0, RS), hi = std::min(r0 + nr, RS);
+      const uint32_t e0 = m->h_rg_off[lo], e1 = m->h_rg_off[hi];
+      slots = m->rg_slot.as<uint32_t>() + e0;
+      E = e1 - e0;
+    }
     int wpb = 32768 / (nch * 4);
     wpb = std::max(1, std::min(8, wpb));
-    const uint64_t warps = static_cast<uint64_t>(M) * J;
-    ProfScope ps_(c->lc, "k_succ_prog", st);
-    k_succ_prog<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
-                  wpb * nch * 4, st>>>(sv, s->flow_view(), mv, J, M,
-                                       slot_group.as<uint32_t>(), rs.as<RankSum>(),
-                                       succ.as<SuccProg>(),
-                                       succ_key.as<unsigned long long>(), nch);
+    const uint64_t warps = static_cast<uint64_t>(E) * J;
+    if (warps) {
+      ProfScope ps_(c->lc, "k_succ_prog", st);
+      k_succ_prog<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
+                    wpb * nch * 4, st>>>(sv, s->flow_view(), mv, J, M,
+                                         slot_group.as<uint32_t>(), rs.as<RankSum>(),
+                                         succ.as<SuccProg>(),
+                                         succ_key.as<unsigned long long>(), nch, slots, E);
+    }
   }
   if (!affected_only && M > 0) {
     comm_group_start(c);

@@ -1054,6 +1054,8 @@ void store_build_index(csg_store* s) {
     throw Error(CSG_ERR_RUNTIME, "engine: store exceeds 2^32 records");
   const double mx = ng ? dkey_inv(h.ts_max_key) : 0.0;
   s->last_ts = (ng && mx > 0.0) ? mx : 0.0;
+  s->own_lo = n ? h.lmin_rank : 0;
+  s->own_hi = n ? h.lmax_rank : -1;
   s->min_rank = ng ? h.min_rank : 0;
   s->max_rank = ng ? h.max_rank : -1;
   s->min_chan = ng ? h.min_chan : 0;
