@@ -31,6 +31,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kDecideThreads = 256;
+constexpr int kSfBlocks = 148 * 4;  // persistent k_self_faulted grid
 constexpr int kChTbl = 4096;  // max channel id + 1 (store.cu enforces)
 
 __device__ inline double as_double(uint64_t u) {
@@ -821,7 +822,22 @@ __global__ void k_flow(StoreView s, ModelView m, int32_t Js,
 // ---------------------------------------------------------------------------
 // K6: per-trip decision (one block per trip).
 // ---------------------------------------------------------------------------
+// Straggler trip state carried from candidate generation (k_decide phase
+// 1) through the parallel self-evidence filter (k_self_faulted) to the
+// report (k_decide phase 2).
+struct StragState {
+  int32_t C;  // candidates (0: decided in phase 1, -1: aborted)
+  int32_t any_history;
+  uint32_t cev_used, pad;
+  unsigned long long cand_base, cev_base, sus_base, exo_base, ev_base, cap_cand, cap_cev;
+};
+
 struct DecideArgs {
+  int debug;
+  int phase;             // 1: candidates, 2: filter + report
+  StragState* state;     // [J]
+  uint32_t* sf_scratch;  // per k_self_faulted block
+  uint32_t sf_words;
   StoreView s;
   ModelView m;
   int32_t J;
@@ -1364,6 +1380,7 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
   const int32_t R = a.s.R;
   const double t = a.trip_t[j];
   const int32_t js = a.js_of[j];
+  const long long clk_g0 = clock64();
   const int32_t k = a.k;
   const int32_t opn = a.m.opn;
   int tot = 0;
@@ -1518,18 +1535,53 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
                any_history ? CSG_VERDICT_NO_STRAGGLER
                            : CSG_VERDICT_INSUFFICIENT_HISTORY,
                naff, 2 * a.N, sh);
+    if (threadIdx.x == 0) a.state[j].C = 0;
     return;
   }
-  // self-evidence filter (rca.cpp:795-869)
+  // the self-evidence filter (rca.cpp:795-869) runs in k_self_faulted, one
+  // block per candidate over every straggler trip
+  if (threadIdx.x == 0) {
+    StragState& S = a.state[j];
+    S.C = C;
+    S.any_history = any_history ? 1 : 0;
+    S.cev_used = sh.cev_used;
+    S.cand_base = sh.cand_base;
+    S.cev_base = sh.cev_base;
+    S.sus_base = sh.sus_base;
+    S.exo_base = sh.exo_base;
+    S.ev_base = sh.ev_base;
+    S.cap_cand = sh.cap_cand;
+    S.cap_cev = sh.cap_cev;
+  }
+}
+
+__device__ void decide_straggler_finish(const DecideArgs& a, int32_t j, BlockShared& sh,
+                                        uint32_t* scratch) {
+  const StragState S = a.state[j];
+  if (S.C <= 0) return;  // decided in phase 1 (or aborted)
+  const int32_t naff = a.n_aff[j];
+  const int C = S.C;
+  if (threadIdx.x == 0) {
+    sh.ncand = C;
+    sh.cev_used = S.cev_used;
+    sh.cand_base = S.cand_base;
+    sh.cev_base = S.cev_base;
+    sh.sus_base = S.sus_base;
+    sh.exo_base = S.exo_base;
+    sh.ev_base = S.ev_base;
+    sh.cap_cand = S.cap_cand;
+    sh.cap_cev = S.cap_cev;
+  }
+  __syncthreads();
+  const long long clk_g0 = clock64(), clk_g1 = clk_g0;
+  const uint32_t mwords = static_cast<uint32_t>((a.s.R + 31) / 32 + 1);
+  const uint32_t P = (a.scratch_per_trip - mwords) / 2;
+  uint32_t* A = scratch + mwords;
+  uint32_t* B = A + P;
   Cand* cands = a.pools.cand + sh.cand_base;
   int any_self = 0;
-  for (int x = 0; x < C; ++x) {
-    const Cand c = cands[x];
-    const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, j, c, sh, A);
-    if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
-    any_self |= sf ? 1 : 0;
-    __syncthreads();
-  }
+  for (int x = threadIdx.x; x < C; x += blockDim.x) any_self |= cands[x].pad ? 1 : 0;
+  any_self = __syncthreads_or(any_self);
   uint32_t* idx = A;
   uint32_t* ord = B;
   uint8_t* keep = reinterpret_cast<uint8_t*>(B + C);
@@ -1543,9 +1595,14 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
   for (int x = threadIdx.x; x < C; x += blockDim.x)
     keep[x] = (!any_self || cands[ord[x]].pad) ? 1 : 0;
   __syncthreads();
+  const long long clk_g2 = clock64();
   emit_reports(a, sh, ord, keep, C, tail);
   write_trip(a, j, sh.nsus ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_NO_STRAGGLER,
              naff, 3 * a.N, sh);
+  if (a.debug && threadIdx.x == 0)
+    printf("decide trip %d naff %d C %d any_self %d cycles: cands %lld self %lld emit %lld\n",
+           j, naff, C, any_self, clk_g1 - clk_g0, clk_g2 - clk_g1,
+           (long long)clock64() - clk_g2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2462,7 +2519,46 @@ __global__ void __launch_bounds__(kDecideThreads)
     return;
   }
   if (a.trip_kind[j] == CSG_TRIGGER_FAILURE) return;  // k_exonerate
-  decide_straggler(a, j, sh, scratch);
+  if (a.phase == 1) decide_straggler(a, j, sh, scratch);
+  else decide_straggler_finish(a, j, sh, scratch);
+}
+
+// Self-evidence filter for every straggler candidate of the batch: a block
+// per candidate (grid-stride over the candidates of all straggler trips,
+// flattened from the per-trip counts left by k_decide phase 1). Marks
+// cands[x].pad = self_faulted (rca.cpp:821-848); candidates without an
+// iteration window (flow findings) are self-faulted by definition.
+__global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
+  __shared__ unsigned long long s_total;
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int32_t j = 0; j < a.J; ++j)
+      if (a.trip_kind[j] != CSG_TRIGGER_FAILURE && a.state[j].C > 0) tot += a.state[j].C;
+    s_total = tot;
+  }
+  __syncthreads();
+  const unsigned long long total = s_total;
+  uint32_t* lst = a.sf_scratch + static_cast<uint64_t>(blockIdx.x) * a.sf_words;
+  int32_t jcur = 0;
+  unsigned long long jbase = 0;  // flattened index of trip jcur's first candidate
+  for (unsigned long long w = blockIdx.x; w < total; w += gridDim.x) {
+    // advance to the trip holding item w (w increases monotonically)
+    while (true) {
+      const bool strag = a.trip_kind[jcur] != CSG_TRIGGER_FAILURE && a.state[jcur].C > 0;
+      const unsigned long long cj = strag ? static_cast<unsigned long long>(a.state[jcur].C) : 0;
+      if (w < jbase + cj) break;
+      jbase += cj;
+      ++jcur;
+    }
+    const int32_t x = static_cast<int32_t>(w - jbase);
+    Cand* cands = a.pools.cand + a.state[jcur].cand_base;
+    const Cand c = cands[x];
+    const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, jcur, c, sh, lst);
+    if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -2912,6 +3008,17 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   a.n_opidx = s->op_indexed ? s->n_opidx : 0;
   a.min_op = s->min_op;
   a.scratch_per_trip = static_cast<uint32_t>(spt);
+  DevBuf& d_state = c->buf("rca.strag_state");
+  d_state.ensure(static_cast<size_t>(J) * sizeof(StragState) + 16);
+  CSG_CUDA(cudaMemsetAsync(d_state.p, 0, static_cast<size_t>(J) * sizeof(StragState), st));
+  a.state = d_state.as<StragState>();
+  a.sf_words = static_cast<uint32_t>(
+      std::max<uint64_t>(16, (spt - ((static_cast<uint64_t>(R) + 31) / 32 + 1)) / 2));
+  DevBuf& d_sf = c->buf("rca.sf_scratch");
+  if (Js > 0) d_sf.ensure(static_cast<size_t>(kSfBlocks) * a.sf_words * 4);
+  a.sf_scratch = d_sf.as<uint32_t>();
+  a.phase = 1;
+  a.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
   a.out = d_out.as<TripOut>();
   a.err = err.as<uint32_t>();
   const size_t shm = sizeof(BlockShared);
@@ -2978,6 +3085,18 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
     {
       ProfScope ps_(c->lc, "k_decide", st);
+      a.phase = 1;
+      k_decide<<<J, kDecideThreads, shm, st>>>(a);
+    }
+    if (Js > 0) {
+      // straggler self-evidence over every candidate in parallel, then the
+      // per-trip filter + report
+      {
+        ProfScope ps_(c->lc, "k_self_faulted", st);
+        k_self_faulted<<<kSfBlocks, kDecideThreads, shm, st>>>(a);
+      }
+      ProfScope ps_(c->lc, "k_decide", st);
+      a.phase = 2;
       k_decide<<<J, kDecideThreads, shm, st>>>(a);
     }
     // pack straight into mapped host memory; the results, the trip table,
