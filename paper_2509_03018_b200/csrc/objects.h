@@ -33,6 +33,8 @@ struct csg_ctx {
   csg::DevBuf& buf(const char* name) { return arena[name]; }
   std::map<std::string, csg::HostBuf> host_arena;  // mapped pinned buffers
   uint64_t slot_group_uid = 0;
+  uint64_t rca_bits_cap = 0;   // op-DAG scratch words that sufficed last time
+  uint64_t rca_pool_mult = 1;  // straggler pool growth that sufficed last time
   // low-latency host wait (ctx_sync): a mapped pinned word the stream's
   // last kernel sets; the host polls it instead of sleeping in the driver
   csg::HostBuf sig;

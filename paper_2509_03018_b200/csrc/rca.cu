@@ -1196,28 +1196,79 @@ __device__ void emit_reports(const DecideArgs& a, BlockShared& sh,
 
 // ---- straggler -------------------------------------------------------------
 
-// op-index segment [lo_key, hi_key] (keys = op - min_op), block-uniform
+// op-index segment [lo_key, hi_key] (keys = op - min_op), block-uniform;
+// warp 0 searches with 32-ary probes (a handful of dependent rounds over the
+// ~1e8-entry index instead of ~27 by one thread)
 __device__ void op_segment(const DecideArgs& a, uint64_t k0, uint64_t k1,
                            bool empty, BlockShared& sh, uint64_t& sb,
                            uint64_t& se) {
-  if (threadIdx.x == 0) {
-    uint64_t l = 0, h = a.n_opidx;
-    while (l < h) {
-      const uint64_t md = (l + h) >> 1;
-      if (a.opk[md] < k0) l = md + 1; else h = md;
+  if (threadIdx.x < 32) {
+    auto first = [&](uint64_t lo, uint64_t hi, auto pred) {
+      const int lane = threadIdx.x;
+      while (hi - lo > 32) {
+        const uint64_t len = hi - lo, step = (len + 31) / 32;
+        uint64_t off = (lane + 1) * step;
+        if (off > len) off = len;
+        const unsigned mm = __ballot_sync(FULL, pred(lo + off - 1));
+        if (!mm) return hi;
+        const int f = __ffs(mm) - 1;
+        uint64_t offf = (f + 1) * step;
+        if (offf > len) offf = len;
+        const uint64_t qf = lo + offf - 1;
+        if (f) {
+          uint64_t offp = f * step;
+          if (offp > len) offp = len;
+          lo = lo + offp;
+        }
+        hi = qf;
+      }
+      const uint64_t q = lo + lane;
+      const unsigned mm = __ballot_sync(FULL, q < hi && pred(q));
+      return mm ? lo + __ffs(mm) - 1 : hi;
+    };
+    const uint64_t l = first(0, a.n_opidx, [&](uint64_t i) { return a.opk[i] >= k0; });
+    const uint64_t h = empty ? l : first(l, a.n_opidx, [&](uint64_t i) { return a.opk[i] > k1; });
+    if (threadIdx.x == 0) {
+      sh.u64a = l;
+      sh.u64b = h;
     }
-    sh.u64a = l;
-    h = a.n_opidx;
-    while (l < h) {
-      const uint64_t md = (l + h) >> 1;
-      if (a.opk[md] <= k1) l = md + 1; else h = md;
-    }
-    sh.u64b = empty ? sh.u64a : l;
   }
   __syncthreads();
   sb = sh.u64a;
   se = sh.u64b;
   __syncthreads();
+}
+
+// Lower median (index kth of the qualifying keys) of a small candidate set:
+// keys staged in shared memory, then one rank count per key (O(n^2 / T));
+// larger sets go through the radix select.
+template <typename G>
+__device__ double small_select(uint64_t n, uint64_t kth, G get, BlockShared& sh) {
+  constexpr uint32_t kCap = kChTbl / 2;  // u64 keys in sh.chtbl
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(sh.chtbl);
+  if (n > kCap) return block_select(n, kth, get, sh);
+  __shared__ uint32_t s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t key;
+    if (get(i, &key)) keys[atomicAdd(&s_n, 1u)] = key;
+  }
+  __syncthreads();
+  const uint32_t m = s_n;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const unsigned long long v = keys[i];
+    uint32_t less = 0, leq = 0;
+    for (uint32_t q = 0; q < m; ++q) {
+      less += keys[q] < v;
+      leq += keys[q] <= v;
+    }
+    if (less <= kth && kth < leq) sh.u64c = v;
+  }
+  __syncthreads();
+  const double r = dkey_inv(sh.u64c);
+  __syncthreads();
+  return r;
 }
 
 // op range holding exactly the ops with static_cast<long>(op / opn) == it
@@ -1276,11 +1327,21 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
     const uint32_t p = static_cast<uint32_t>(mb) + lst[x];
     return a.s.ts[p] - as_double(a.s.pa[p]);
   };
-  for (int x = 0; x < n; ++x) {
+  // first occurrence of every op among mine (one parallel pass instead of
+  // a block barrier per element); the walk below visits only those
+  uint32_t* firstm = lst + n;  // bitmap behind the list
+  for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) firstm[w] = 0;
+  __syncthreads();
+  for (int x = threadIdx.x; x < n; x += blockDim.x) {
     const int64_t o = mine_op(x);
     bool dup = false;
-    for (int y = threadIdx.x; y < x; y += blockDim.x) dup |= mine_op(y) == o;
-    if (__syncthreads_or(dup)) continue;
+    for (int y = 0; y < x && !dup; ++y) dup = mine_op(y) == o;
+    if (!dup) atomicOr(&firstm[x >> 5], 1u << (x & 31));
+  }
+  __syncthreads();
+  for (int x = 0; x < n; ++x) {
+    if (!((firstm[x >> 5] >> (x & 31)) & 1u)) continue;
+    const int64_t o = mine_op(x);
     // max of my durations for op o
     double mine = -INFINITY;
     for (int y = x + threadIdx.x; y < n; y += blockDim.x)
@@ -1310,7 +1371,7 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
     nsib = block_sum_i(nsib, sh);
     double med;
     if (nsib > 0) {
-      med = block_select(se - sb, static_cast<uint64_t>((nsib - 1) / 2),
+      med = small_select(se - sb, static_cast<uint64_t>((nsib - 1) / 2),
                          [&](uint64_t i, uint64_t* key) {
                            const uint64_t y = sb + i;
                            if (a.oprank[y] == r || a.op_ts[y] > t) return false;
@@ -1334,7 +1395,7 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
         nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
       nco = block_sum_i(nco, sh);
       if (nco < 2) continue;
-      med = block_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
+      med = small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
                          [&](uint64_t i, uint64_t* key) {
                            const uint64_t y = cb + i;
                            if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
@@ -2946,11 +3007,14 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   // ---- output pools: failure regions first, straggler bump allocations after
   const uint64_t C2 = 2 * tot_max + 8;
   const uint64_t per_ev = std::max<uint64_t>(2 * nch + 1, k + 1);
-  uint64_t cand_cap = Js ? 2 * tot_all + 16 : 16;
-  uint64_t cev_cap = Js ? tot_all * per_ev + 16 : 16;
-  uint64_t sus_cap = sus_fail + (Js ? 6 * tot_all : 0) + 16;
-  uint64_t ev_cap = ev_fail + (Js ? tot_all * per_ev : 0) + 16;
-  uint64_t bits_cap = 1ull << 22;
+  const uint64_t pm = std::max<uint64_t>(1, c->rca_pool_mult);  // grown last time
+  uint64_t cand_cap = Js ? (2 * tot_all + 16) * pm : 16;
+  uint64_t cev_cap = Js ? (tot_all * per_ev + 16) * pm : 16;
+  uint64_t sus_cap = sus_fail + (Js ? 6 * tot_all * pm : 0) + 16;
+  uint64_t ev_cap = ev_fail + (Js ? tot_all * per_ev * pm : 0) + 16;
+  // grow-only across calls: a replay of the same store does not pay the
+  // DAG-scratch retry again
+  uint64_t bits_cap = std::max<uint64_t>(1ull << 22, c->rca_bits_cap);
   const uint64_t mwords = (static_cast<uint64_t>(R) + 31) / 32 + 1;
   uint64_t spt = 16;
   if (Js) {
@@ -3012,8 +3076,11 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   d_state.ensure(static_cast<size_t>(J) * sizeof(StragState) + 16);
   CSG_CUDA(cudaMemsetAsync(d_state.p, 0, static_cast<size_t>(J) * sizeof(StragState), st));
   a.state = d_state.as<StragState>();
-  a.sf_words = static_cast<uint32_t>(
-      std::max<uint64_t>(16, (spt - ((static_cast<uint64_t>(R) + 31) / 32 + 1)) / 2));
+  {  // self_faulted's list + first-occurrence bitmap behind it
+    const uint64_t base =
+        std::max<uint64_t>(16, (spt - ((static_cast<uint64_t>(R) + 31) / 32 + 1)) / 2);
+    a.sf_words = static_cast<uint32_t>(base + base / 32 + 2);
+  }
   DevBuf& d_sf = c->buf("rca.sf_scratch");
   if (Js > 0) d_sf.ensure(static_cast<size_t>(kSfBlocks) * a.sf_words * 4);
   a.sf_scratch = d_sf.as<uint32_t>();
@@ -3142,9 +3209,15 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (!(h_err & (DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH))) break;
     if (attempt >= 6)
       throw Error(CSG_ERR_RUNTIME, "engine: RCA output pools exhausted");
-    if (h_err & DEV_ERR_DAG_SCRATCH)
+    if (a.debug)
+      fprintf(stderr, "rca retry: %s%s\n", (h_err & DEV_ERR_POOL) ? "pools " : "",
+              (h_err & DEV_ERR_DAG_SCRATCH) ? "dag-scratch" : "");
+    if (h_err & DEV_ERR_DAG_SCRATCH) {
       bits_cap = std::max<uint64_t>(bits_cap * 4, used[P_BITS] * 2);
+      c->rca_bits_cap = bits_cap;
+    }
     if (h_err & DEV_ERR_POOL) {
+      c->rca_pool_mult = pm * 4;
       cand_cap *= 4;
       cev_cap *= 4;
       sus_cap = sus_fail + (sus_cap - sus_fail) * 4;
