@@ -879,6 +879,12 @@ enum { P_CAND = 0, P_CEV = 1, P_SUS = 2, P_EV = 3, P_BITS = 4 };
 
 struct BlockShared {
   int abort;
+  uint32_t dbg_n, dbg_d;  // self_faulted sizes (CSG_DEBUG_EXO)
+  // per-block cache of cohort medians (trip, iteration, op name) -> median
+  // (rca.cpp:833-840: the cohort does not depend on the candidate)
+  int32_t coh_n;
+  unsigned long long coh_key[32];
+  double coh_val[32];
   int32_t ncand;
   uint32_t cev_used;
   int32_t nret;
@@ -1244,7 +1250,7 @@ __device__ void op_segment(const DecideArgs& a, uint64_t k0, uint64_t k1,
 // larger sets go through the radix select.
 template <typename G>
 __device__ double small_select(uint64_t n, uint64_t kth, G get, BlockShared& sh) {
-  constexpr uint32_t kCap = kChTbl / 2;  // u64 keys in sh.chtbl
+  constexpr uint32_t kCap = 512;  // O(n^2 / T) beats the radix passes below this
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(sh.chtbl);
   if (n > kCap) return block_select(n, kth, get, sh);
   __shared__ uint32_t s_n;
@@ -1327,21 +1333,19 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
     const uint32_t p = static_cast<uint32_t>(mb) + lst[x];
     return a.s.ts[p] - as_double(a.s.pa[p]);
   };
-  // first occurrence of every op among mine (one parallel pass instead of
-  // a block barrier per element); the walk below visits only those
-  uint32_t* firstm = lst + n;  // bitmap behind the list
-  for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) firstm[w] = 0;
-  __syncthreads();
-  for (int x = threadIdx.x; x < n; x += blockDim.x) {
-    const int64_t o = mine_op(x);
-    bool dup = false;
-    for (int y = 0; y < x && !dup; ++y) dup = mine_op(y) == o;
-    if (!dup) atomicOr(&firstm[x >> 5], 1u << (x & 31));
+  if (threadIdx.x == 0) {
+    sh.dbg_n = n;
+    sh.dbg_d = 0;
   }
-  __syncthreads();
   for (int x = 0; x < n; ++x) {
-    if (!((firstm[x >> 5] >> (x & 31)) & 1u)) continue;
     const int64_t o = mine_op(x);
+    // per-channel completions of one op sit next to each other: the common
+    // duplicate is decided without a block-wide pass
+    if (x > 0 && mine_op(x - 1) == o) continue;
+    bool dup = false;
+    for (int y = threadIdx.x; y < x; y += blockDim.x) dup |= mine_op(y) == o;
+    if (__syncthreads_or(dup)) continue;
+    if (threadIdx.x == 0) ++sh.dbg_d;
     // max of my durations for op o
     double mine = -INFINITY;
     for (int y = x + threadIdx.x; y < n; y += blockDim.x)
@@ -1383,6 +1387,29 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
       // cohort of (program op name, iteration) (rca.cpp:833-840)
       const int64_t it = iter_of(o, opn);
       const uint8_t nm = a.m.op_name[static_cast<uint64_t>(o % opn)];
+      const unsigned long long ckey =
+          (static_cast<unsigned long long>(j) << 44) ^
+          (static_cast<unsigned long long>(nm) << 36) ^
+          (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
+      __shared__ int s_hit;
+      __shared__ double s_med;
+      if (threadIdx.x == 0) {
+        s_hit = 0;
+        for (int q = 0; q < sh.coh_n && q < 32; ++q)
+          if (sh.coh_key[q] == ckey) {
+            s_hit = 1;
+            s_med = sh.coh_val[q];
+          }
+      }
+      __syncthreads();
+      if (s_hit) {
+        med = s_med;
+        __syncthreads();
+        if (med <= 0) continue;
+        if (mine > __dmul_rn(a.skew, med)) return true;
+        continue;
+      }
+      __syncthreads();
       int64_t olo, ohi;
       iter_ops(it, opn, olo, ohi);
       const bool empty = ohi < a.min_op;
@@ -1394,15 +1421,25 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
       for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
         nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
       nco = block_sum_i(nco, sh);
+      if (nco < 2) {
+        med = 0;  // "skip": cached as a non-positive median
+      } else {
+        med = small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
+                           [&](uint64_t i, uint64_t* key) {
+                             const uint64_t y = cb + i;
+                             if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
+                             *key = dkey(a.op_dur[y]);
+                             return true;
+                           },
+                           sh);
+      }
+      if (threadIdx.x == 0) {
+        const int q = sh.coh_n < 32 ? sh.coh_n++ : static_cast<int>(ckey % 32);
+        sh.coh_key[q] = ckey;
+        sh.coh_val[q] = med;
+      }
+      __syncthreads();
       if (nco < 2) continue;
-      med = small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
-                         [&](uint64_t i, uint64_t* key) {
-                           const uint64_t y = cb + i;
-                           if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
-                           *key = dkey(a.op_dur[y]);
-                           return true;
-                         },
-                         sh);
     }
     if (med <= 0) continue;
     if (mine > __dmul_rn(a.skew, med)) return true;
@@ -2594,6 +2631,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
   BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
   __shared__ unsigned long long s_total;
   if (threadIdx.x == 0) {
+    sh.coh_n = 0;
     unsigned long long tot = 0;
     for (int32_t j = 0; j < a.J; ++j)
       if (a.trip_kind[j] != CSG_TRIGGER_FAILURE && a.state[j].C > 0) tot += a.state[j].C;
@@ -2616,8 +2654,13 @@ __global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
     const int32_t x = static_cast<int32_t>(w - jbase);
     Cand* cands = a.pools.cand + a.state[jcur].cand_base;
     const Cand c = cands[x];
+    const long long c0 = clock64();
     const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, jcur, c, sh, lst);
     if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
+    if (a.debug && threadIdx.x == 0 && w < 4)
+      printf("self_faulted item %llu trip %d cand %d rank %d it [%lld,%lld] sf %d: %lld cycles, "
+             "n_mine %u distinct %u\n", w, jcur, x, c.rank, (long long)c.it_lo,
+             (long long)c.it_hi, sf ? 1 : 0, (long long)clock64() - c0, sh.dbg_n, sh.dbg_d);
     __syncthreads();
   }
 }
