@@ -838,6 +838,11 @@ struct DecideArgs {
   StragState* state;     // [J]
   uint32_t* sf_scratch;  // per k_self_faulted block
   uint32_t sf_words;
+  // batch-wide cohort-median table (open addressing, power-of-two capacity)
+  unsigned long long* coh_key;  // ~0 = empty
+  double* coh_val;
+  unsigned* coh_state;          // 2 = value published
+  uint32_t coh_cap;
   StoreView s;
   ModelView m;
   int32_t J;
@@ -1391,19 +1396,47 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
           (static_cast<unsigned long long>(j) << 44) ^
           (static_cast<unsigned long long>(nm) << 36) ^
           (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
-      __shared__ int s_hit;
+      // Block cache first, then the batch-wide table: the first block to need
+      // a cohort claims its slot and computes it, later ones wait for the
+      // published value (the claimer is running, so the wait terminates).
+      __shared__ int s_hit, s_slot;
       __shared__ double s_med;
       if (threadIdx.x == 0) {
         s_hit = 0;
+        s_slot = -1;
         for (int q = 0; q < sh.coh_n && q < 32; ++q)
           if (sh.coh_key[q] == ckey) {
             s_hit = 1;
             s_med = sh.coh_val[q];
           }
+        if (!s_hit && a.coh_cap) {
+          const uint32_t mask = a.coh_cap - 1;
+          uint32_t h = static_cast<uint32_t>((ckey * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+          for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h = (h + 1) & mask) {
+            const unsigned long long k = atomicCAS(a.coh_key + h, ~0ull, ckey);
+            if (k == ~0ull) {  // claimed: this block computes it
+              s_slot = static_cast<int>(h);
+              break;
+            }
+            if (k == ckey) {  // someone else's: wait for the value
+              volatile unsigned* stv = a.coh_state + h;
+              while (*stv != 2u) {
+              }
+              __threadfence();
+              s_med = *reinterpret_cast<volatile double*>(a.coh_val + h);
+              s_hit = 1;
+              break;
+            }
+          }
+        }
       }
       __syncthreads();
       if (s_hit) {
         med = s_med;
+        if (threadIdx.x == 0 && sh.coh_n < 32) {
+          sh.coh_key[sh.coh_n] = ckey;
+          sh.coh_val[sh.coh_n++] = med;
+        }
         __syncthreads();
         if (med <= 0) continue;
         if (mine > __dmul_rn(a.skew, med)) return true;
@@ -1437,6 +1470,11 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
         const int q = sh.coh_n < 32 ? sh.coh_n++ : static_cast<int>(ckey % 32);
         sh.coh_key[q] = ckey;
         sh.coh_val[q] = med;
+        if (s_slot >= 0) {  // publish
+          a.coh_val[s_slot] = med;
+          __threadfence();
+          atomicExch(a.coh_state + s_slot, 2u);
+        }
       }
       __syncthreads();
       if (nco < 2) continue;
@@ -3127,6 +3165,14 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   DevBuf& d_sf = c->buf("rca.sf_scratch");
   if (Js > 0) d_sf.ensure(static_cast<size_t>(kSfBlocks) * a.sf_words * 4);
   a.sf_scratch = d_sf.as<uint32_t>();
+  DevBuf& d_coh = c->buf("rca.cohort");
+  a.coh_cap = Js > 0 ? 4096 : 0;
+  if (Js > 0) {
+    d_coh.ensure(static_cast<size_t>(a.coh_cap) * 20 + 64);
+    a.coh_key = d_coh.as<unsigned long long>();
+    a.coh_val = reinterpret_cast<double*>(a.coh_key + a.coh_cap);
+    a.coh_state = reinterpret_cast<unsigned*>(a.coh_val + a.coh_cap);
+  }
   a.phase = 1;
   a.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
   a.out = d_out.as<TripOut>();
@@ -3201,6 +3247,8 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (Js > 0) {
       // straggler self-evidence over every candidate in parallel, then the
       // per-trip filter + report
+      CSG_CUDA(cudaMemsetAsync(a.coh_key, 0xff, static_cast<size_t>(a.coh_cap) * 8, st));
+      CSG_CUDA(cudaMemsetAsync(a.coh_state, 0, static_cast<size_t>(a.coh_cap) * 4, st));
       {
         ProfScope ps_(c->lc, "k_self_faulted", st);
         k_self_faulted<<<kSfBlocks, kDecideThreads, shm, st>>>(a);
