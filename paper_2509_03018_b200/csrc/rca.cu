@@ -1289,6 +1289,33 @@ __device__ inline void iter_ops(int64_t it, int32_t opn, int64_t& lo, int64_t& h
   hi = it >= 0 ? it * opn + (opn - 1) : it * opn;
 }
 
+// Lower median of the (program op name nm, iteration it) cohort of non-Recv
+// completions with ts <= t (rca.cpp:833-840); 0 when fewer than two (the
+// caller skips the op). Block-collective.
+__device__ double cohort_median(const DecideArgs& a, int64_t it, uint8_t nm, double t,
+                                BlockShared& sh) {
+  int64_t olo, ohi;
+  iter_ops(it, a.m.opn, olo, ohi);
+  const bool empty = ohi < a.min_op;
+  const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
+  const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
+  uint64_t cb, ce;
+  op_segment(a, k0, k1, empty, sh, cb, ce);
+  int nco = 0;
+  for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
+    nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
+  nco = block_sum_i(nco, sh);
+  if (nco < 2) return 0;
+  return small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
+                      [&](uint64_t i, uint64_t* key) {
+                        const uint64_t y = cb + i;
+                        if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
+                        *key = dkey(a.op_dur[y]);
+                        return true;
+                      },
+                      sh);
+}
+
 // self_faulted (rca.cpp:821-848) for one lateness candidate. "mine" are the
 // candidate rank's completions (ts <= t, not Recv) in its iteration window:
 // from its rank-major segment on a single GPU, from the (gathered) op index
@@ -1443,29 +1470,9 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
         continue;
       }
       __syncthreads();
-      int64_t olo, ohi;
-      iter_ops(it, opn, olo, ohi);
-      const bool empty = ohi < a.min_op;
-      const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
-      const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
-      uint64_t cb, ce;
-      op_segment(a, k0, k1, empty, sh, cb, ce);
-      int nco = 0;
-      for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
-        nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
-      nco = block_sum_i(nco, sh);
-      if (nco < 2) {
-        med = 0;  // "skip": cached as a non-positive median
-      } else {
-        med = small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
-                           [&](uint64_t i, uint64_t* key) {
-                             const uint64_t y = cb + i;
-                             if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
-                             *key = dkey(a.op_dur[y]);
-                             return true;
-                           },
-                           sh);
-      }
+      const double cm = cohort_median(a, it, nm, t, sh);
+      const int nco = cm > 0 ? 2 : 0;  // non-positive: skip the op
+      med = cm;
       if (threadIdx.x == 0) {
         const int q = sh.coh_n < 32 ? sh.coh_n++ : static_cast<int>(ckey % 32);
         sh.coh_key[q] = ckey;
@@ -2659,6 +2666,77 @@ __global__ void __launch_bounds__(kDecideThreads)
   else decide_straggler_finish(a, j, sh, scratch);
 }
 
+// Cohort medians ahead of the self-evidence filter: block (j, q, nm)
+// computes the cohort (op name nm, iteration it_lo(j) + q) of straggler
+// trip j, where [it_lo(j), it_hi(j)] spans the iteration windows of the
+// trip's candidates, and publishes it in the batch-wide table — every cohort
+// a candidate can ask for is computed once, all in parallel, instead of by
+// the first candidate block that needs it while others wait.
+constexpr int kCohortNames = 4;  // AllGather, ReduceScatter, AllReduce, Send
+__global__ void __launch_bounds__(kDecideThreads) k_cohorts(DecideArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
+  const int32_t j = blockIdx.x;
+  const int32_t q = blockIdx.y;
+  const uint8_t nm = static_cast<uint8_t>(blockIdx.z);
+  if (a.trip_kind[j] == CSG_TRIGGER_FAILURE) return;
+  const StragState S = a.state[j];
+  if (S.C <= 0) return;
+  const Cand* cands = a.pools.cand + S.cand_base;
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int x = threadIdx.x; x < S.C; x += blockDim.x) {
+    const Cand& c = cands[x];
+    if (c.it_hi < c.it_lo) continue;
+    lo = min(lo, static_cast<long long>(c.it_lo));
+    hi = max(hi, static_cast<long long>(c.it_hi));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh.red_l[threadIdx.x >> 5] = lo;
+    sh.red_l[16 + (threadIdx.x >> 5)] = hi;
+  }
+  __syncthreads();
+  lo = LLONG_MAX;
+  hi = LLONG_MIN;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+    lo = min(lo, sh.red_l[w]);
+    hi = max(hi, sh.red_l[16 + w]);
+  }
+  __syncthreads();
+  const long long it = lo + q;
+  if (lo > hi || it > hi) return;
+  const unsigned long long ckey =
+      (static_cast<unsigned long long>(j) << 44) ^
+      (static_cast<unsigned long long>(nm) << 36) ^
+      (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
+  __shared__ int s_slot;
+  if (threadIdx.x == 0) {
+    s_slot = -1;
+    const uint32_t mask = a.coh_cap - 1;
+    uint32_t h = static_cast<uint32_t>((ckey * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+    for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h = (h + 1) & mask) {
+      const unsigned long long k = atomicCAS(a.coh_key + h, ~0ull, ckey);
+      if (k == ~0ull) {
+        s_slot = static_cast<int>(h);
+        break;
+      }
+      if (k == ckey) break;  // already there
+    }
+  }
+  __syncthreads();
+  if (s_slot < 0) return;
+  const double med = cohort_median(a, it, nm, a.trip_t[j], sh);
+  if (threadIdx.x == 0) {
+    a.coh_val[s_slot] = med;
+    __threadfence();
+    atomicExch(a.coh_state + s_slot, 2u);
+  }
+}
+
 // Self-evidence filter for every straggler candidate of the batch: a block
 // per candidate (grid-stride over the candidates of all straggler trips,
 // flattened from the per-trip counts left by k_decide phase 1). Marks
@@ -2695,7 +2773,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
     const long long c0 = clock64();
     const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, jcur, c, sh, lst);
     if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
-    if (a.debug && threadIdx.x == 0 && w < 4)
+    if (a.debug && threadIdx.x == 0 && (w < 4 || (w >= 20000 && w < 20006)))
       printf("self_faulted item %llu trip %d cand %d rank %d it [%lld,%lld] sf %d: %lld cycles, "
              "n_mine %u distinct %u\n", w, jcur, x, c.rank, (long long)c.it_lo,
              (long long)c.it_hi, sf ? 1 : 0, (long long)clock64() - c0, sh.dbg_n, sh.dbg_d);
@@ -3249,6 +3327,11 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       // per-trip filter + report
       CSG_CUDA(cudaMemsetAsync(a.coh_key, 0xff, static_cast<size_t>(a.coh_cap) * 8, st));
       CSG_CUDA(cudaMemsetAsync(a.coh_state, 0, static_cast<size_t>(a.coh_cap) * 4, st));
+      {
+        ProfScope ps_(c->lc, "k_cohorts", st);
+        k_cohorts<<<dim3(J, static_cast<unsigned>(std::max(k, 1) + 1), kCohortNames),
+                    kDecideThreads, shm, st>>>(a);
+      }
       {
         ProfScope ps_(c->lc, "k_self_faulted", st);
         k_self_faulted<<<kSfBlocks, kDecideThreads, shm, st>>>(a);
