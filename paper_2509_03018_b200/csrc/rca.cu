@@ -1250,6 +1250,60 @@ __device__ void op_segment(const DecideArgs& a, uint64_t k0, uint64_t k1,
   __syncthreads();
 }
 
+// Lower median of the qualifying keys of a range in one pass: keys staged
+// in shared memory (up to 2048), bitonic-sorted there, element (m-1)/2
+// returned with the count m. Ranges with more qualifying keys fall back to
+// the radix select (count in *m; caller handles m == 0). Block-collective.
+template <typename G>
+__device__ double staged_lower_median(uint64_t n, G get, BlockShared& sh, int* m_out) {
+  constexpr uint32_t kCap = kChTbl / 2;  // u64 keys in sh.chtbl
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(sh.chtbl);
+  __shared__ uint32_t s_n;
+  __shared__ int s_over;
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    s_over = 0;
+  }
+  __syncthreads();
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t key;
+    if (get(i, &key)) {
+      const uint32_t at = atomicAdd(&s_n, 1u);
+      if (at < kCap) keys[at] = key; else s_over = 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t m = s_n;
+  *m_out = static_cast<int>(m);
+  if (m == 0) return 0;
+  if (s_over) {
+    __syncthreads();
+    return block_select(n, static_cast<uint64_t>((m - 1) / 2), get, sh);
+  }
+  uint32_t P = 1;
+  while (P < m) P <<= 1;
+  for (uint32_t i = m + threadIdx.x; i < P; i += blockDim.x) keys[i] = ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const unsigned long long x = keys[i], y = keys[l];
+          if ((x > y) == ((i & k) == 0)) {
+            keys[i] = y;
+            keys[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const double r = dkey_inv(keys[(m - 1) / 2]);
+  __syncthreads();
+  return r;
+}
+
 // Lower median (index kth of the qualifying keys) of a small candidate set:
 // keys staged in shared memory, then one rank count per key (O(n^2 / T));
 // larger sets go through the radix select.
@@ -1302,18 +1356,15 @@ __device__ double cohort_median(const DecideArgs& a, int64_t it, uint8_t nm, dou
   uint64_t cb, ce;
   op_segment(a, k0, k1, empty, sh, cb, ce);
   int nco = 0;
-  for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
-    nco += (a.op_nm[y] == nm && a.op_ts[y] <= t);
-  nco = block_sum_i(nco, sh);
-  if (nco < 2) return 0;
-  return small_select(ce - cb, static_cast<uint64_t>((nco - 1) / 2),
-                      [&](uint64_t i, uint64_t* key) {
-                        const uint64_t y = cb + i;
-                        if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
-                        *key = dkey(a.op_dur[y]);
-                        return true;
-                      },
-                      sh);
+  const double med = staged_lower_median(ce - cb,
+                                         [&](uint64_t i, uint64_t* key) {
+                                           const uint64_t y = cb + i;
+                                           if (a.op_nm[y] != nm || a.op_ts[y] > t) return false;
+                                           *key = dkey(a.op_dur[y]);
+                                           return true;
+                                         },
+                                         sh, &nco);
+  return nco < 2 ? 0 : med;
 }
 
 // self_faulted (rca.cpp:821-848) for one lateness candidate. "mine" are the
@@ -1402,19 +1453,15 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
       op_segment(a, key, key, false, sh, sb, se);
     }
     int nsib = 0;
-    for (uint64_t y = sb + threadIdx.x; y < se; y += blockDim.x)
-      nsib += (a.oprank[y] != r && a.op_ts[y] <= t);
-    nsib = block_sum_i(nsib, sh);
-    double med;
+    double med = staged_lower_median(se - sb,
+                                     [&](uint64_t i, uint64_t* key) {
+                                       const uint64_t y = sb + i;
+                                       if (a.oprank[y] == r || a.op_ts[y] > t) return false;
+                                       *key = dkey(a.op_dur[y]);
+                                       return true;
+                                     },
+                                     sh, &nsib);
     if (nsib > 0) {
-      med = small_select(se - sb, static_cast<uint64_t>((nsib - 1) / 2),
-                         [&](uint64_t i, uint64_t* key) {
-                           const uint64_t y = sb + i;
-                           if (a.oprank[y] == r || a.op_ts[y] > t) return false;
-                           *key = dkey(a.op_dur[y]);
-                           return true;
-                         },
-                         sh);
     } else {
       // cohort of (program op name, iteration) (rca.cpp:833-840)
       const int64_t it = iter_of(o, opn);
