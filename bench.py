@@ -88,6 +88,10 @@ def scaled_config(ngpus: int) -> str:
     same single injected hang (BASELINE C4: one fault in the whole job)."""
     cfg = json.load(open(CONFIG))
     cfg["layout"]["dp"] = cfg["layout"]["dp"] * ngpus
+    if CONFIG.endswith("c2_hang_1024.json"):
+        # one simulated time span for every N (the hang at 22 s, logs to 26 s):
+        # ~1e7 records per 1024 ranks, the same tripped ticks at every scale
+        cfg["sim"]["max_sim_ms"] = 26000.0
     return json.dumps(cfg)
 
 
@@ -98,12 +102,14 @@ def load_workload(ngpus: int = 1, shard: int = 0):
     scen = E.Scenario.parse(scaled_config(ngpus))
     world = 1024 * ngpus
     lo, hi = D.shard_bounds(world, ngpus)[shard]
-    cache = f"/tmp/collsight_{os.path.basename(CONFIG)}_{TARGET_RECORDS}_n{ngpus}_s{shard}.rec"
+    cache = f"/tmp/collsight_v2_{os.path.basename(CONFIG)}_{TARGET_RECORDS}_n{ngpus}_s{shard}.rec"
     if os.path.exists(cache):
         recs = np.fromfile(cache, dtype=np.uint8).view(RECORD_DTYPE)
     else:
         t = time.time()
-        target = TARGET_RECORDS if ngpus == 1 else 0
+        # C2: the simulated time span bounds the trace (scaled_config); the
+        # record target only bounds workloads without one
+        target = 0 if CONFIG.endswith("c2_hang_1024.json") else TARGET_RECORDS
         recs = E.synthesize(scen, target, (lo, hi) if ngpus > 1 else None)
         recs.view(np.uint8).tofile(cache + ".tmp")
         os.replace(cache + ".tmp", cache)
