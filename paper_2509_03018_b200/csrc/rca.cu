@@ -597,28 +597,35 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
   __syncthreads();
   const bool strag = trip_kind[j] == CSG_TRIGGER_STRAGGLER;
   const int32_t js = js_of[j];
+  // pass 1, a warp per group: any member stuck (lanes over the members), or
+  // late for straggler trips; reachable = same connected component
+  uint8_t* af = aff_flag + static_cast<uint64_t>(j) * m.n_groups;
+  for (int32_t g = warp; g < m.n_groups; g += nwarps) {
+    bool reach = false;
+    const int32_t cg = m.comp[g];
+    for (int32_t i = 0; i < ncomp; ++i) reach |= comps[i] == cg;
+    bool flag = false;
+    if (reach) {
+      const uint32_t q0 = m.member_off[g], q1 = m.member_off[g + 1];
+      for (uint32_t qb = q0; qb < q1 && !flag; qb += 32) {
+        const uint32_t q = qb + lane;
+        bool st = false;
+        if (q < q1) {
+          const int32_t r = m.members[q];
+          st = r >= 0 && r < s.R && (rs[static_cast<uint64_t>(j) * s.R + r].flags & RS_STUCK);
+        }
+        flag = __any_sync(FULL, st);
+      }
+      if (!flag && strag && js >= 0 && gi[static_cast<uint64_t>(js) * m.n_groups + g].late)
+        flag = true;
+    }
+    if (lane == 0) af[g] = flag ? 1 : 0;
+  }
+  __syncthreads();
+  // pass 2: ordered compaction of the flagged groups
   for (int32_t g0 = 0; g0 < m.n_groups; g0 += blockDim.x) {
     const int32_t g = g0 + tid;
-    int hit = 0;
-    if (g < m.n_groups) {
-      bool reach = false;
-      const int32_t cg = m.comp[g];
-      for (int32_t i = 0; i < ncomp; ++i) reach |= comps[i] == cg;
-      if (reach) {
-        bool flag = false;
-        for (uint32_t q = m.member_off[g]; q < m.member_off[g + 1] && !flag; ++q) {
-          const int32_t r = m.members[q];
-          if (r >= 0 && r < s.R &&
-              (rs[static_cast<uint64_t>(j) * s.R + r].flags & RS_STUCK))
-            flag = true;
-        }
-        if (!flag && strag && js >= 0 &&
-            gi[static_cast<uint64_t>(js) * m.n_groups + g].late)
-          flag = true;
-        hit = flag ? 1 : 0;
-      }
-      aff_flag[static_cast<uint64_t>(j) * m.n_groups + g] = static_cast<uint8_t>(hit);
-    }
+    const int hit = g < m.n_groups ? af[g] : 0;
     int x = hit;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -2107,7 +2114,7 @@ constexpr size_t kExoSmemMax = 192 * 1024;
 // Trips with at most kExoStage candidates keep the exoneration keys, the
 // (op, rank) order and the retained list in shared memory: the greedy sweep
 // is O(C x retained) dependent lookups, latency-bound from global memory.
-constexpr uint32_t kExoStage = 1024;
+constexpr uint32_t kExoStage = 2048;
 struct ExoKey {
   int64_t op;
   int32_t rank;
@@ -3072,7 +3079,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   n_aff.ensure(static_cast<size_t>(J) * 4);
   {
     ProfScope ps_(c->lc, "k_affected", st);
-    k_affected<<<J, 256, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
+    k_affected<<<J, 1024, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
                                   gi.as<GroupIter>(), aff.as<int32_t>(),
                                   aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
   }
