@@ -93,6 +93,9 @@ std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target,
                                           int32_t rank_hi = 0x7fffffff);
 
 // Trace codec.
+// Multithreaded parse of a valid trace; false when the exact parser must
+// decide (fast_jsonl.cpp).
+bool fast_parse_trace(std::string_view text, std::vector<csg_packed_record>& out);
 std::vector<csg_packed_record> parse_trace_text(std::string_view text);
 std::vector<csg_packed_record> load_trace_file(const std::string& path);
 

@@ -7,6 +7,7 @@
 // (validate_record, trace.cpp:39-57) and reported as a TraceParseError.
 // Fields the analyzer never reads (node, stuck_ms, total_chunks) are checked
 // and then dropped; state counters must fit the packed u32 lanes.
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -121,6 +122,12 @@ csg_packed_record parse_line(std::string_view text, int line) {
 
 std::vector<csg_packed_record> parse_trace_text(std::string_view text) {
   std::vector<csg_packed_record> out;
+  // multithreaded fast path for valid traces (fast_jsonl.cpp); anything it
+  // does not fully vouch for is parsed again below with the exact grammar
+  // and error reporting
+  static const bool exact_only = std::getenv("CSG_JSONL_EXACT") != nullptr;
+  if (!exact_only && fast_parse_trace(text, out)) return out;
+  out.clear();
   int line = 0;
   size_t pos = 0;
   while (pos < text.size()) {
