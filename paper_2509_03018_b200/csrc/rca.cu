@@ -1831,10 +1831,18 @@ __global__ void k_fail_count(StoreView s, ModelView m,
                              const FailItem* __restrict__ items, int32_t n_items,
                              const RankSum* __restrict__ rs,
                              GroupPick* __restrict__ pick,
-                             uint32_t* __restrict__ cnt) {
+                             uint32_t* __restrict__ cnt,
+                             const unsigned* __restrict__ n_dev) {
+  // n_items: grid bound (and scan length - 1); n_dev: the planned count when
+  // the items were planned on the device (the tail up to n_items scans as 0)
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= n_items) return;
+  if (w == 0 && lane == 0) cnt[n_items] = 0;  // closes the offset scan
+  const int64_t ni = n_dev ? static_cast<int64_t>(*n_dev) : n_items;
+  if (w >= ni) {
+    if (lane == 0 && w < n_items) cnt[w] = 0;
+    return;
+  }
   const FailItem it = items[w];
   const RankSum* rsj = rs + static_cast<uint64_t>(it.j) * s.R;
   const uint32_t mo = m.member_off[it.g];
@@ -1942,13 +1950,14 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
                              const uint32_t* __restrict__ off,
                              Cand* __restrict__ cand,
                              csg_evidence* __restrict__ cev,
-                             uint32_t* __restrict__ err) {
+                             uint32_t* __restrict__ err,
+                             const unsigned* __restrict__ n_dev) {
   constexpr int kWarps = 4;
   constexpr int kStage = 256;  // members staged in shared memory
   __shared__ int32_t srank[kWarps][kStage];     // suspect ranks, else INT_MAX
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= n_items) return;
+  if (w >= (n_dev ? static_cast<int64_t>(*n_dev) : n_items)) return;
   const FailItem it = items[w];
   const GroupPick pk = pick[w];
   if (pk.mode == 0) return;
@@ -2046,6 +2055,93 @@ struct ExoTrip {
   uint32_t sus_off, ev_off;  // output regions (upper bounds from the host)
 };
 
+// Failure planning on the device (no host round trip after k_affected):
+// per trip its candidate bound C = members of its affected groups, then in
+// trip order the items, exoneration trips and output regions the host would
+// otherwise lay out (same formulas as the host path in rca_batch).
+struct FailPlan {
+  unsigned n_items, pad;
+  unsigned long long cand_ub, sus_fail, ev_fail, scratch_bytes;
+};
+
+__host__ __device__ inline uint64_t exo_scratch_need(uint64_t C, uint64_t Rs) {
+  uint64_t P = 1;
+  while (P < C) P <<= 1;
+  const uint64_t need = ((P * 4 + 15) & ~15ull) + ((C * 8 + 15) & ~15ull) +
+                        ((C * 4 + 15) & ~15ull) + ((C + 15) & ~15ull) +
+                        4 * ((Rs + 3) & ~3ull) + 8 * (((Rs + 31) / 32 + 3) & ~3ull) +
+                        32 * C + 64;
+  return (need + 255) & ~255ull;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_fail_plan(int32_t J, int32_t G, const int32_t* __restrict__ kind,
+                const int32_t* __restrict__ naff, const int32_t* __restrict__ aff,
+                ModelView m, int32_t R, int EV, FailItem* __restrict__ items,
+                ExoTrip* __restrict__ exo, FailPlan* __restrict__ plan,
+                unsigned long long* __restrict__ used) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int32_t j = warp; j < J; j += nw) {
+    const int32_t na = naff[j];
+    const bool ok = kind[j] == CSG_TRIGGER_FAILURE && na > 0 && m.opn > 0;
+    unsigned long long C = 0;
+    if (ok)
+      for (int32_t i = lane; i < na; i += 32) {
+        const int32_t g = aff[static_cast<uint64_t>(j) * G + i];
+        C += m.member_off[g + 1] - m.member_off[g];
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) C += __shfl_xor_sync(FULL, C, o);
+    if (lane == 0) {
+      ExoTrip e;
+      memset(&e, 0, sizeof(e));
+      e.j = ok ? j : -1;
+      e.naff = na;
+      e.n_cand = static_cast<uint32_t>(C);  // bound for the layout pass
+      exo[j] = e;
+    }
+  }
+  __syncthreads();
+  __shared__ unsigned s_ni;
+  if (threadIdx.x == 0) {
+    unsigned ni = 0;
+    unsigned long long sb = 0, sus = 0, ev = 0, cub = 0;
+    const uint64_t Rs = R > 0 ? R : 1;
+    for (int32_t j = 0; j < J; ++j) {
+      ExoTrip& e = exo[j];
+      if (e.j < 0) continue;
+      const unsigned long long C = e.n_cand;
+      e.n_cand = 0;
+      e.first_item = ni;
+      e.n_items = static_cast<uint32_t>(e.naff);
+      e.scratch_off = sb;
+      e.sus_off = static_cast<uint32_t>(sus);
+      e.ev_off = static_cast<uint32_t>(ev);
+      ni += e.naff;
+      sb += exo_scratch_need(C, Rs);
+      sus += 2 * C;
+      ev += C * EV;
+      cub += C;
+    }
+    plan->n_items = ni;
+    plan->cand_ub = cub;
+    plan->sus_fail = sus;
+    plan->ev_fail = ev;
+    plan->scratch_bytes = sb;
+    for (int q = 0; q < 8; ++q) used[q] = 0;
+    used[2] = sus;  // P_SUS: straggler bump allocations start after these
+    used[3] = ev;   // P_EV
+    s_ni = ni;
+  }
+  __syncthreads();
+  for (int32_t j = warp; j < J; j += nw) {
+    const ExoTrip e = exo[j];
+    if (e.j < 0) continue;
+    for (int32_t i = lane; i < e.naff; i += 32)
+      items[e.first_item + i] = FailItem{j, aff[static_cast<uint64_t>(j) * G + i]};
+  }
+}
+
 struct ExoArgs {
   int debug;
   StoreView s;
@@ -2132,6 +2228,7 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   __shared__ int32_t s_rsum[kExoStage];
   __shared__ uint8_t s_keep[kExoStage];
   ExoTrip& tp = a.trips[blockIdx.x];
+  if (tp.j < 0) return;  // not a failure trip with affected groups (device plan)
   const int tid = threadIdx.x;
   const uint32_t cbase = a.off[tp.first_item];
   const uint32_t C = a.off[tp.first_item + tp.n_items] - cbase;
@@ -3087,7 +3184,25 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   h_affb.ensure(static_cast<size_t>(J) * (static_cast<size_t>(G) + 1) * 4 + 16);
   int32_t* h_na = h_affb.as<int32_t>();
   int32_t* h_ag = h_na + J;
-  {
+  // Failure-only batches are planned on the device (k_fail_plan) when the
+  // upper-bound layout (every failure trip affecting every group) is small:
+  // no host round trip between k_affected and the candidate kernels; the
+  // affected groups come back with the final results.
+  const int EV = kEvSlots(nch);
+  int32_t Jf = 0;
+  for (int32_t j = 0; j < J; ++j) Jf += h_kind[j] == CSG_TRIGGER_FAILURE ? 1 : 0;
+  const uint64_t ub_items = static_cast<uint64_t>(Jf) * G;
+  const uint64_t ub_cand = static_cast<uint64_t>(Jf) * M;
+  const uint64_t ub_scratch =
+      static_cast<uint64_t>(Jf) * exo_scratch_need(M, static_cast<uint64_t>(std::max(R, 1)));
+  const uint64_t ub_bytes = ub_cand * (sizeof(Cand) + 2 * EV * sizeof(csg_evidence) +
+                                       2 * sizeof(csg_suspect)) +
+                            ub_scratch + ub_items * (sizeof(FailItem) + sizeof(GroupPick) + 4);
+  static const bool no_dev_plan = std::getenv("CSG_HOST_FAIL_PLAN") != nullptr;
+  const bool dev_plan = !no_dev_plan && !affected_only && Js == 0 && Jf > 0 && opn > 0 &&
+                        M > 0 && ub_bytes <= (512ull << 20) && ub_items < (1ull << 30) &&
+                        2 * ub_cand < 0xF0000000ull && ub_cand * EV < 0xF0000000ull;
+  if (!dev_plan) {
     FetchArgs fa{};
     fa.add(n_aff.p, h_na, static_cast<size_t>(J) * 4);
     // only each trip's affected groups cross PCIe, not the J x G matrix
@@ -3095,7 +3210,8 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     ctx_sync(c, &fa);
   }
   tl_mark("affected sync returned");
-  std::vector<int32_t> h_naff(h_na, h_na + J);
+  std::vector<int32_t> h_naff(J, 0);
+  if (!dev_plan) h_naff.assign(h_na, h_na + J);
   out.aff = h_ag;
   CSG_CUDA(cudaGetLastError());
   c->d2h_bytes += static_cast<uint64_t>(J) * 4 + static_cast<uint64_t>(J) * G * 4;
@@ -3122,7 +3238,6 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   }
 
   // ---- failure trips: per-group candidates + per-trip exoneration ----
-  const int EV = kEvSlots(nch);
   std::vector<FailItem> items;
   std::vector<ExoTrip> exo;
   std::vector<uint64_t> item_m;  // members per item (upper bound of its cands)
@@ -3131,7 +3246,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   int32_t m_max = 1;
   for (int32_t g = 0; g < G; ++g)
     m_max = std::max<int32_t>(m_max, m->h_member_off[g + 1] - m->h_member_off[g]);
-  for (int32_t j = 0; j < J; ++j) {
+  for (int32_t j = 0; j < J && !dev_plan; ++j) {
     uint64_t tot = 0;
     for (int32_t i = 0; i < h_naff[j]; ++i) {
       const int32_t g = out.aff[static_cast<size_t>(j) * G + i];
@@ -3176,6 +3291,54 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   ExoTrip* d_exo_ptr = nullptr;
   DevBuf& d_exs = c->buf("rca.exo_scratch");
   tl_mark("fail items planned");
+  DevBuf& d_plan = c->buf("rca.fail_plan");
+  d_plan.ensure(sizeof(FailPlan) + 16);
+  int32_t n_exo_grid = static_cast<int32_t>(exo.size());
+  if (dev_plan) {
+    d_items.ensure(ub_items * sizeof(FailItem) + 16);
+    d_exo_ptr = reinterpret_cast<ExoTrip*>(c->buf("rca.exo_dev").p);
+    {
+      DevBuf& dx = c->buf("rca.exo_dev");
+      dx.ensure(static_cast<size_t>(J) * sizeof(ExoTrip) + 16);
+      d_exo_ptr = dx.as<ExoTrip>();
+    }
+    d_pick.ensure(ub_items * sizeof(GroupPick) + 16);
+    d_off.ensure((ub_items + 1) * 4);
+    d_cand.ensure(ub_cand * sizeof(Cand) + sizeof(Cand));
+    d_cev.ensure(ub_cand * EV * sizeof(csg_evidence) + sizeof(csg_evidence));
+    d_exs.ensure(ub_scratch + 256);
+    DevBuf& p_used0 = c->buf("rca.p_used");
+    p_used0.ensure(8 * 8);
+    {
+      ProfScope ps_(c->lc, "k_fail_plan", st);
+      k_fail_plan<<<1, 1024, 0, st>>>(J, G, dkind, n_aff.as<int32_t>(), aff.as<int32_t>(), mv,
+                                      R, EV, d_items.as<FailItem>(), d_exo_ptr,
+                                      d_plan.as<FailPlan>(),
+                                      p_used0.as<unsigned long long>());
+    }
+    const unsigned* n_dev = &d_plan.as<FailPlan>()->n_items;
+    {
+      ProfScope ps_(c->lc, "k_fail_count", st);
+      k_fail_count<<<static_cast<unsigned>((ub_items * 32 + 255) / 256), 256, 0, st>>>(
+          sv, mv, d_items.as<FailItem>(), static_cast<int32_t>(ub_items), rs.as<RankSum>(),
+          d_pick.as<GroupPick>(), d_off.as<uint32_t>(), n_dev);
+    }
+    exclusive_scan_u32(d_off.as<uint32_t>(), ub_items + 1, c->buf("rca.scan_tmp"), st, c->lc);
+    {
+      ProfScope ps_(c->lc, "k_fail_cands", st);
+      k_fail_cands<<<static_cast<unsigned>((ub_items * 32 + 127) / 128), 128, 0, st>>>(
+          sv, mv, d_items.as<FailItem>(), static_cast<int32_t>(ub_items), rs.as<RankSum>(),
+          chan_key.as<unsigned long long>(), succ.as<SuccProg>(),
+          succ_key.as<unsigned long long>(), M, nch, d_pick.as<GroupPick>(),
+          d_off.as<uint32_t>(), d_cand.as<Cand>(), d_cev.as<csg_evidence>(),
+          err.as<uint32_t>(), n_dev);
+    }
+    // pool regions sized by the bounds; the exact values come back with the
+    // results (needed only if a retry re-initialises the pools)
+    sus_fail = 2 * ub_cand;
+    ev_fail = ub_cand * EV;
+    n_exo_grid = J;
+  }
   if (n_items > 0) {
     // items, exoneration trips and the zero closing the offset scan: one
     // pinned upload
@@ -3188,9 +3351,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     std::memset(d_items.stage.as<unsigned char>() + zo, 0, 4);
     CSG_CUDA(cudaMemcpyAsync(d_items.p, d_items.stage.p, zo + 4, cudaMemcpyHostToDevice, st));
     d_pick.ensure(static_cast<size_t>(n_items) * sizeof(GroupPick));
-    d_off.ensure(static_cast<size_t>(n_items + 1) * 4);
-    CSG_CUDA(cudaMemcpyAsync(d_off.as<uint32_t>() + n_items, d_items.as<unsigned char>() + zo, 4,
-                             cudaMemcpyDeviceToDevice, st));
+    d_off.ensure(static_cast<size_t>(n_items + 1) * 4);  // [n_items] zeroed by k_fail_count
     d_cand.ensure(cand_ub * sizeof(Cand) + sizeof(Cand));
     d_cev.ensure(cand_ub * EV * sizeof(csg_evidence) + sizeof(csg_evidence));
     d_exo_ptr = reinterpret_cast<ExoTrip*>(d_items.as<unsigned char>() + xo);
@@ -3200,7 +3361,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       k_fail_count<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 255) / 256),
                      256, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
                                    rs.as<RankSum>(), d_pick.as<GroupPick>(),
-                                   d_off.as<uint32_t>());
+                                   d_off.as<uint32_t>(), nullptr);
     }
     exclusive_scan_u32(d_off.as<uint32_t>(), static_cast<uint64_t>(n_items) + 1,
                        c->buf("rca.scan_tmp"), st, c->lc);
@@ -3213,7 +3374,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                                    M, nch,
                                    d_pick.as<GroupPick>(), d_off.as<uint32_t>(),
                                    d_cand.as<Cand>(), d_cev.as<csg_evidence>(),
-                                   err.as<uint32_t>());
+                                   err.as<uint32_t>(), nullptr);
     }
   }
 
@@ -3343,9 +3504,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     a.pools.u32 = p_u32.as<uint32_t>();
     a.pools.u32_cap = static_cast<unsigned long long>(J) * spt;
     a.pools.used = p_used.as<unsigned long long>();
-    unsigned long long init_used[8] = {0, 0, sus_fail, ev_fail, 0, 0, 0, 0};
-    CSG_CUDA(cudaMemcpyAsync(p_used.p, init_used, 8 * 8, cudaMemcpyHostToDevice, st));
-    if (!exo.empty()) {
+    // device-planned batches: k_fail_plan initialised the pool usage on the
+    // first attempt; a retry uses the exact region sizes it reported
+    if (!dev_plan || attempt > 0) {
+      unsigned long long init_used[8] = {0, 0, sus_fail, ev_fail, 0, 0, 0, 0};
+      CSG_CUDA(cudaMemcpyAsync(p_used.p, init_used, 8 * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (n_exo_grid > 0) {
       ExoArgs ea;
       ea.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
       ea.s = sv;
@@ -3355,7 +3520,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ea.EV = EV;
       ea.off = d_off.as<uint32_t>();
       ea.trips = d_exo_ptr;
-      ea.n_trips = static_cast<int32_t>(exo.size());
+      ea.n_trips = n_exo_grid;
       ea.scratch = d_exs.as<unsigned char>();
       ea.bits = p_bits.as<unsigned long long>();
       ea.bits_cap = bits_cap;
@@ -3369,7 +3534,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kExoSmemMax)));
       ProfScope ps_(c->lc, "k_exonerate", st);
-      k_exonerate<<<static_cast<unsigned>(exo.size()), kExoThreads, kExoSmemMax, st>>>(ea);
+      k_exonerate<<<static_cast<unsigned>(n_exo_grid), kExoThreads, kExoSmemMax, st>>>(ea);
     }
     {
       ProfScope ps_(c->lc, "k_decide", st);
@@ -3420,7 +3585,18 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       fa.add(p_used.p, hrp + 16, 8 * 8);
       fa.add(d_ptot.p, hrp + 80, 16);
       fa.add(d_out.p, hrp + 96, static_cast<size_t>(J) * sizeof(TripOut));
+      if (dev_plan) {  // the affected groups and the plan ride on this trip
+        fa.add(n_aff.p, h_na, static_cast<size_t>(J) * 4);
+        if (G) fa.add_rows(aff.p, h_ag, static_cast<size_t>(G) * 4, n_aff.as<int32_t>(), J);
+        fa.add(d_plan.p, d_plan.stage.p ? d_plan.stage.p : (d_plan.stage.ensure(64), d_plan.stage.p),
+               sizeof(FailPlan));
+      }
       ctx_sync(c, &fa);
+    }
+    if (dev_plan) {
+      const FailPlan* fp = d_plan.stage.as<FailPlan>();
+      sus_fail = fp->sus_fail;
+      ev_fail = fp->ev_fail;
     }
     std::memcpy(&h_err, hrp, 4);
     std::memcpy(used, hrp + 16, 8 * 8);
