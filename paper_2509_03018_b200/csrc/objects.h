@@ -237,17 +237,19 @@ struct FetchSeg {
   const int32_t* row_len;
   uint32_t nrows;
 };
-constexpr int kFetchSegs = 6;
+constexpr int kFetchSegs = 8;
 struct FetchArgs {
   FetchSeg seg[kFetchSegs];
   int n;
   void add(const void* src, void* dst, size_t bytes) {
+    if (n >= kFetchSegs) throw csg::Error(CSG_ERR_RUNTIME, "fetch: too many segments");
     seg[n++] = FetchSeg{static_cast<const unsigned char*>(src),
                         static_cast<unsigned char*>(dst), static_cast<uint32_t>(bytes),
                         nullptr, 0};
   }
   void add_rows(const void* src, void* dst, size_t stride, const int32_t* lens,
                 uint32_t nrows) {
+    if (n >= kFetchSegs) throw csg::Error(CSG_ERR_RUNTIME, "fetch: too many segments");
     seg[n++] = FetchSeg{static_cast<const unsigned char*>(src),
                         static_cast<unsigned char*>(dst), static_cast<uint32_t>(stride),
                         lens, nrows};
