@@ -2228,7 +2228,19 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   __shared__ int32_t s_rsum[kExoStage];
   __shared__ uint8_t s_keep[kExoStage];
   ExoTrip& tp = a.trips[blockIdx.x];
-  if (tp.j < 0) return;  // not a failure trip with affected groups (device plan)
+  if (tp.j < 0) {
+    // device plan (one entry per trip, failure-only batch): no affected group
+    // or no program -> FalseTrigger, as k_decide would write it
+    if (threadIdx.x == 0) {
+      TripOut o;
+      memset(&o, 0, sizeof(o));
+      o.verdict = CSG_VERDICT_FALSE_TRIGGER;
+      o.n_aff = tp.naff;
+      o.scanned = a.N;
+      a.out[blockIdx.x] = o;
+    }
+    return;
+  }
   const int tid = threadIdx.x;
   const uint32_t cbase = a.off[tp.first_item];
   const uint32_t C = a.off[tp.first_item + tp.n_items] - cbase;
@@ -2750,44 +2762,29 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   }
 }
 
-// Dense packing of every trip's suspects, exonerated and evidence, planned
-// and copied on the device straight into mapped pinned host memory: the
-// host learns sizes and receives the data in the same round trip.
-// out[j] offsets are rewritten to the packed positions; tot = {sus, ev}.
-__global__ void k_pack_plan(TripOut* __restrict__ out, int32_t J,
-                            uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                            unsigned long long* __restrict__ tot) {
-  if (threadIdx.x || blockIdx.x) return;
-  uint64_t ns = 0, ne = 0;
-  for (int32_t j = 0; j < J; ++j) {
-    TripOut& t = out[j];
-    src[3 * j + 0] = t.sus_off;
-    dst[3 * j + 0] = static_cast<uint32_t>(ns);
-    t.sus_off = static_cast<uint32_t>(ns);
-    ns += t.n_sus;
-    src[3 * j + 1] = t.exo_off;
-    dst[3 * j + 1] = static_cast<uint32_t>(ns);
-    t.exo_off = static_cast<uint32_t>(ns);
-    ns += t.n_exo;
-    src[3 * j + 2] = t.ev_off;
-    dst[3 * j + 2] = static_cast<uint32_t>(ne);
-    t.ev_off = static_cast<uint32_t>(ne);
-    ne += t.n_ev;
-  }
-  tot[0] = ns;
-  tot[1] = ne;
-}
-
-__global__ void k_pack(const TripOut* __restrict__ out, const uint32_t* __restrict__ src,
-                       const uint32_t* __restrict__ dst,
+// Dense packing of every trip's suspects, exonerated and evidence, copied
+// on the device straight into mapped pinned host memory.
+__global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
                        const csg_suspect* __restrict__ sus,
                        const csg_evidence* __restrict__ ev,
                        csg_suspect* __restrict__ osus,
                        csg_evidence* __restrict__ oev) {
+  // block (j, kind): its packed offset is the sum of the earlier regions'
+  // counts in (trip, suspects / exonerated / evidence) order; the host
+  // derives the same offsets from the fetched trip table
   const int32_t j = blockIdx.x / 3, kind = blockIdx.x % 3;
+  __shared__ uint32_t s_dst;
+  if (threadIdx.x == 0) {
+    uint32_t d = 0;
+    for (int32_t q = 0; q < j; ++q) d += kind < 2 ? out[q].n_sus + out[q].n_exo : out[q].n_ev;
+    if (kind == 1) d += out[j].n_sus;
+    s_dst = d;
+  }
+  __syncthreads();
   const TripOut& t = out[j];
   const uint32_t n = kind == 0 ? t.n_sus : kind == 1 ? t.n_exo : t.n_ev;
-  const uint32_t s0 = src[blockIdx.x], d0 = dst[blockIdx.x];
+  const uint32_t s0 = kind == 0 ? t.sus_off : kind == 1 ? t.exo_off : t.ev_off;
+  const uint32_t d0 = s_dst;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     if (kind < 2) osus[d0 + i] = sus[s0 + i];
     else oev[d0 + i] = ev[s0 + i];
@@ -3476,13 +3473,6 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   uint32_t h_err = 0;
   unsigned long long used[8];
   std::vector<TripOut> to(J);
-  unsigned long long ptot[2] = {0, 0};
-  DevBuf& d_psrc = c->buf("rca.pack_src");
-  DevBuf& d_pdst = c->buf("rca.pack_dst");
-  DevBuf& d_ptot = c->buf("rca.pack_tot");
-  d_psrc.ensure(static_cast<size_t>(J) * 12 + 4);
-  d_pdst.ensure(static_cast<size_t>(J) * 12 + 4);
-  d_ptot.ensure(16);
   HostBuf& h_sus = c->hbuf("rca.packed_sus");
   HostBuf& h_ev = c->hbuf("rca.packed_ev");
   for (int attempt = 0;; ++attempt) {
@@ -3536,7 +3526,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ProfScope ps_(c->lc, "k_exonerate", st);
       k_exonerate<<<static_cast<unsigned>(n_exo_grid), kExoThreads, kExoSmemMax, st>>>(ea);
     }
-    {
+    if (!dev_plan) {  // device-planned batches are failure-only: k_exonerate wrote every trip
       ProfScope ps_(c->lc, "k_decide", st);
       a.phase = 1;
       k_decide<<<J, kDecideThreads, shm, st>>>(a);
@@ -3561,19 +3551,13 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
     // pack straight into mapped host memory; the results, the trip table,
     // the pool usage and the error word all come back in ONE round trip
-    {
-      ProfScope ps_(c->lc, "k_pack_plan", st);
-      k_pack_plan<<<1, 1, 0, st>>>(d_out.as<TripOut>(), J, d_psrc.as<uint32_t>(),
-                                   d_pdst.as<uint32_t>(), d_ptot.as<unsigned long long>());
-    }
     h_sus.ensure(sus_cap * sizeof(csg_suspect) + 64);
     h_ev.ensure(ev_cap * sizeof(csg_evidence) + 64);
     if (J > 0) {
       ProfScope ps_(c->lc, "k_pack", st);
       k_pack<<<static_cast<unsigned>(3 * J), 128, 0, st>>>(
-          d_out.as<TripOut>(), d_psrc.as<uint32_t>(), d_pdst.as<uint32_t>(),
-          p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(), h_sus.as<csg_suspect>(),
-          h_ev.as<csg_evidence>());
+          d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
+          h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>());
     }
     // pinned: [0] error word, [16] pool usage, [80] packed totals, [96..) trips
     HostBuf& hr = c->hbuf("rca.tail");
@@ -3583,7 +3567,6 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       FetchArgs fa{};
       fa.add(err.p, hrp, 4);
       fa.add(p_used.p, hrp + 16, 8 * 8);
-      fa.add(d_ptot.p, hrp + 80, 16);
       fa.add(d_out.p, hrp + 96, static_cast<size_t>(J) * sizeof(TripOut));
       if (dev_plan) {  // the affected groups and the plan ride on this trip
         fa.add(n_aff.p, h_na, static_cast<size_t>(J) * 4);
@@ -3600,7 +3583,6 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     }
     std::memcpy(&h_err, hrp, 4);
     std::memcpy(used, hrp + 16, 8 * 8);
-    std::memcpy(ptot, hrp + 80, 16);
     std::memcpy(to.data(), hrp + 96, J * sizeof(TripOut));
     CSG_CUDA(cudaGetLastError());
     if (h_err & DEV_ERR_RC_TABLE)
@@ -3630,7 +3612,17 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     h_err &= ~(DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH);
     CSG_CUDA(cudaMemcpyAsync(err.p, &h_err, 4, cudaMemcpyHostToDevice, st));
   }
-  const uint64_t ns_tot = ptot[0], ne_tot = ptot[1];
+  // packed offsets, in the order k_pack wrote them
+  uint64_t ns_tot = 0, ne_tot = 0;
+  for (int32_t j = 0; j < J; ++j) {
+    TripOut& t = to[j];
+    t.sus_off = static_cast<uint32_t>(ns_tot);
+    ns_tot += t.n_sus;
+    t.exo_off = static_cast<uint32_t>(ns_tot);
+    ns_tot += t.n_exo;
+    t.ev_off = static_cast<uint32_t>(ne_tot);
+    ne_tot += t.n_ev;
+  }
   out.sus.assign(h_sus.as<csg_suspect>(), h_sus.as<csg_suspect>() + ns_tot);
   out.ev.assign(h_ev.as<csg_evidence>(), h_ev.as<csg_evidence>() + ne_tot);
   c->d2h_bytes += J * sizeof(TripOut) + ns_tot * sizeof(csg_suspect) +

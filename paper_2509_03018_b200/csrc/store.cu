@@ -261,19 +261,6 @@ __global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir) {
   }
 }
 
-// rank_off over absolute ranks [0, R] from the scanned tile offsets.
-__global__ void k_rank_off_hist(const uint32_t* __restrict__ goff, uint32_t T,
-                                int32_t min_rank, int32_t max_rank, int32_t R,
-                                uint64_t n, uint32_t* __restrict__ off) {
-  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r > R) return;
-  uint32_t v;
-  if (r < min_rank) v = 0;
-  else if (r > max_rank) v = static_cast<uint32_t>(n);
-  else v = goff[static_cast<uint64_t>(r - min_rank) * T];
-  off[r] = v;
-}
-
 struct ScatterOut {
   ulonglong2* tso;  // {ts, op_seq}
   int2* cc;         // {comm, channel}
@@ -327,7 +314,8 @@ template <int ITEMS, int NBUF, int DPT>
 __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
-              int32_t D, ScatterOut o, int mode) {
+              int32_t D, ScatterOut o, int mode, int32_t max_rank, int32_t R,
+              uint32_t* __restrict__ rank_off) {
   constexpr int kW = kTileThreads / 32;
   constexpr int TR = kTileThreads * ITEMS;
   constexpr int SUB = kTile / TR;
@@ -340,6 +328,12 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
   __shared__ uint32_t wsum[32];
   __shared__ __align__(8) unsigned long long mbar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // segment offsets over absolute ranks [0, R] from the scanned tile
+  // offsets (folded in here: one launch less)
+  for (int32_t r = blockIdx.x * kTileThreads + tid; r <= R; r += gridDim.x * kTileThreads)
+    rank_off[r] = r < min_rank ? 0u
+                  : r > max_rank ? static_cast<uint32_t>(n)
+                                 : goff[static_cast<uint64_t>(r - min_rank) * T];
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -1127,18 +1121,16 @@ void store_build_index(csg_store* s) {
       ProfScope ps_(c->lc, "k_scatter", st);
       if (dbl)
         k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode);
+                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             s->rank_off.as<uint32_t>());
       else if (D <= 1024)
         k_scatter<4, 1, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode);
+                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             s->rank_off.as<uint32_t>());
       else
         k_scatter<4, 1, 8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode);
-    }
-    {
-      ProfScope ps_(c->lc, "k_rank_off", st);
-      k_rank_off_hist<<<(R + 1 + 255) / 256, 256, 0, st>>>(
-          goff.as<uint32_t>(), ntiles, lmin, h.lmax_rank, R, n, s->rank_off.as<uint32_t>());
+                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             s->rank_off.as<uint32_t>());
     }
   } else {
     // general path: (rank, store index) pairs, LSD radix sort, gather
