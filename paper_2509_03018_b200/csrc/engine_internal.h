@@ -108,6 +108,22 @@ struct ColView {
   }
 };
 
+// Payload words read straight from the packed store record of a rank-major
+// position (perm): the index does not copy the 16-byte payload, which only
+// the window sums, progress lookups and straggler durations touch. Word 1 of
+// a state record is rdma_done alone (the reserved lane masked off).
+template <int W>
+struct PayView {
+  const unsigned char* recs = nullptr;  // packed records (48 B each)
+  const uint32_t* perm = nullptr;
+  __device__ __forceinline__ uint64_t operator[](uint64_t p) const {
+    const unsigned char* r = recs + static_cast<uint64_t>(perm[p]) * 48;
+    const uint64_t v = *reinterpret_cast<const unsigned long long*>(r + 32 + 8 * W);
+    if (W == 1 && (r[28] & 1)) return v & 0xffffffffull;  // CSG_KIND_STATE
+    return v;
+  }
+};
+
 struct StoreView {
   uint64_t n = 0;          // records
   int32_t R = 0;           // rank space [0, R)
@@ -121,8 +137,8 @@ struct StoreView {
   ColView<int32_t, 2, 0> comm;         // {comm, channel} pairs
   ColView<int32_t, 2, 1> chan;
   const uint8_t* ko = nullptr;         // kind | op_name << 1
-  ColView<uint64_t, 2, 0> pa;          // payload pairs: start_ms bits | ready | tx << 32
-  ColView<uint64_t, 2, 1> pb;          //                msg_bytes | done
+  PayView<0> pa;                       // payload: start_ms bits | ready | tx << 32
+  PayView<1> pb;                       //          msg_bytes | done
 };
 
 constexpr uint32_t kCmChunk = 128;  // records per cmax chunk

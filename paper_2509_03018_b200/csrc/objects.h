@@ -90,7 +90,6 @@ struct csg_store {
   csg::DevBuf runmax;  // chunked prefix max of ts (StoreView::cmax)
   csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
   csg::DevBuf cc;   // {comm, channel} (8 B)
-  csg::DevBuf pay;  // {start_ms | ready,tx ; msg_bytes | done} (16 B)
   csg::SortScratch sort;
   // op-ordered completion index for the straggler self-evidence pass
   bool op_indexed = false;
@@ -126,8 +125,10 @@ struct csg_store {
     v.comm.p = cc.as<int32_t>();
     v.chan.p = cc.as<int32_t>();
     v.ko = ko.as<uint8_t>();
-    v.pa.p = pay.as<uint64_t>();
-    v.pb.p = pay.as<uint64_t>();
+    v.pa.recs = recs.as<unsigned char>();
+    v.pa.perm = perm.as<uint32_t>();
+    v.pb.recs = recs.as<unsigned char>();
+    v.pb.perm = perm.as<uint32_t>();
     return v;
   }
   csg::FlowView flow_view() const {

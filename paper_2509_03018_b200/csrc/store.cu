@@ -265,8 +265,7 @@ struct ScatterOut {
   ulonglong2* tso;  // {ts, op_seq}
   int2* cc;         // {comm, channel}
   uint8_t* ko;      // kind | op_name << 1
-  ulonglong2* pay;  // payload pair
-  uint32_t* perm;   // store index per rank-major position
+  uint32_t* perm;   // store index per rank-major position (payload via perm)
 };
 
 // --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
@@ -314,7 +313,7 @@ template <int ITEMS, int NBUF, int DPT>
 __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
-              int32_t D, ScatterOut o, int mode, int32_t max_rank, int32_t R,
+              int32_t D, ScatterOut o, int32_t max_rank, int32_t R,
               uint32_t* __restrict__ rank_off) {
   constexpr int kW = kTileThreads / 32;
   constexpr int TR = kTileThreads * ITEMS;
@@ -477,10 +476,9 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     // of one digit run. Four records per thread in flight (independent
     // shared-memory chains; 8 warps per SM leave little else to hide them).
     constexpr int kB = 4;
-    if (mode != 2)
     for (uint32_t p0 = tid; p0 < cnt; p0 += kB * kTileThreads) {
       uint32_t li[kB], q[kB];
-      ulonglong2 h0[kB], hm[kB], h1[kB];
+      ulonglong2 h0[kB], hm[kB];
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
         const uint32_t p = p0 + k * kTileThreads;
@@ -491,7 +489,6 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
         const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(sb + li[k] * 48);
         h0[k] = rec[0];
         hm[k] = rec[1];
-        h1[k] = rec[2];
       }
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
@@ -504,17 +501,12 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
         const uint32_t p = p0 + k * kTileThreads;
         if (p >= cnt) break;
         const uint32_t qq = q[k];
-        if (mode == 1) {
-          if (qq == 0xFFFFFFFFu) o.ko[0] = static_cast<uint8_t>(h0[k].x + hm[k].y + h1[k].x);
-          continue;
-        }
         o.tso[qq] = h0[k];
         o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
                              static_cast<int32_t>(hm[k].y & 0xffffffffu));
         const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
         const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
         o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
-        o.pay[qq] = make_ulonglong2(h1[k].x, (kind & 1) ? (h1[k].y & 0xffffffffull) : h1[k].y);
         o.perm[qq] = static_cast<uint32_t>(first + li[k]);
       }
     }
@@ -638,14 +630,13 @@ __global__ void k_gather(const csg_packed_record* __restrict__ r,
     // 48-byte records are 16-byte aligned: three 16-byte vector loads.
     const ulonglong2* rec =
         reinterpret_cast<const ulonglong2*>(r + perm[p]);
-    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1), h1 = __ldg(rec + 2);
+    const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1);
     o.tso[p] = h0;
     o.cc[p] = make_int2(static_cast<int32_t>(hm.x >> 32),
                         static_cast<int32_t>(hm.y & 0xffffffffu));
     const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
     const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
     o.ko[p] = static_cast<uint8_t>((kind & 1) | (name << 1));
-    o.pay[p] = make_ulonglong2(h1.x, (kind & 1) ? (h1.y & 0xffffffffull) : h1.y);
   }
 }
 
@@ -1065,7 +1056,6 @@ void store_build_index(csg_store* s) {
   s->runmax.ensure((n / kCmChunk + static_cast<size_t>(R) + 2) * 8);
   s->cc.ensure(n * 8 + 8);
   s->ko.ensure(n + 8);
-  s->pay.ensure(n * 16 + 16);
   static const bool force_general = std::getenv("CSG_INDEX_RADIX") != nullptr;
   const bool fused = n && !force_general &&
                      static_cast<int64_t>(h.lmax_rank) - h.lmin_rank < kHistDigits;
@@ -1089,7 +1079,7 @@ void store_build_index(csg_store* s) {
                                                  sums.as<unsigned long long>(), nt);
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                 s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
+                 s->perm.as<uint32_t>()};
     // Rank spans <= 1024: 2048-record sub-tiles double-buffered in one CTA
     // per SM. Wider spans (or CSG_SCATTER_CFG=2): 1024-record sub-tiles, one
     // bulk-copy buffer per CTA, several CTAs per SM.
@@ -1116,20 +1106,19 @@ void store_build_index(csg_store* s) {
       CSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, D <= 1024 ? k_scatter<4, 1, 4> : k_scatter<4, 1, 8>, kTileThreads, smem));
     const unsigned grid = std::min<unsigned>(ntiles, 148u * std::max(per_sm, 1));
-    static const int smode = std::getenv("CSG_SCATTER_MODE") ? std::atoi(std::getenv("CSG_SCATTER_MODE")) : 0;
     {
       ProfScope ps_(c->lc, "k_scatter", st);
       if (dbl)
         k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             ntiles, lmin, D, o, h.lmax_rank, R,
                                                              s->rank_off.as<uint32_t>());
       else if (D <= 1024)
         k_scatter<4, 1, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             ntiles, lmin, D, o, h.lmax_rank, R,
                                                              s->rank_off.as<uint32_t>());
       else
         k_scatter<4, 1, 8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, smode, h.lmax_rank, R,
+                                                             ntiles, lmin, D, o, h.lmax_rank, R,
                                                              s->rank_off.as<uint32_t>());
     }
   } else {
@@ -1150,7 +1139,7 @@ void store_build_index(csg_store* s) {
       {
         ProfScope ps_(c->lc, "k_gather", st);
         ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                     s->pay.as<ulonglong2>(), s->perm.as<uint32_t>()};
+                     s->perm.as<uint32_t>()};
         k_gather<<<grid_for(n), 256, 0, st>>>(recs, s->perm.as<uint32_t>(), n, o);
       }
     }

@@ -568,9 +568,9 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     WinSum* asum = acc.as<WinSum>();
     WinMax* amax = reinterpret_cast<WinMax*>(acc.as<unsigned char>() + sb);
     unsigned* done = reinterpret_cast<unsigned*>(acc.as<unsigned char>() + sb + mb);
-    // about 2k records per block of a sampled rank's (average) segment
+    // about 512 records per block of a sampled rank's (average) segment
     const uint64_t avg = s->R > 0 ? s->n / static_cast<uint64_t>(s->R) : 0;
-    const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, avg / 2048)));
+    const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, avg / 512)));
     static bool attr = false;
     if (!attr) {
       CSG_CUDA(cudaFuncSetAttribute(k_trigger, cudaFuncAttributeMaxDynamicSharedMemorySize,
