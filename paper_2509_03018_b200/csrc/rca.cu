@@ -2210,7 +2210,7 @@ constexpr size_t kExoSmemMax = 192 * 1024;
 // Trips with at most kExoStage candidates keep the exoneration keys, the
 // (op, rank) order and the retained list in shared memory: the greedy sweep
 // is O(C x retained) dependent lookups, latency-bound from global memory.
-constexpr uint32_t kExoStage = 2048;
+constexpr uint32_t kExoStage = 4096;
 struct ExoKey {
   int64_t op;
   int32_t rank;
