@@ -531,12 +531,13 @@ __global__ void __launch_bounds__(1024)
     k_chunkmax_blk(const ulonglong2* __restrict__ tso,
                    const uint32_t* __restrict__ off, double* __restrict__ cm,
                    uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
-                   unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg) {
+                   unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg,
+                   int32_t r0) {
   __shared__ double pmax[32];
   __shared__ int desc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int32_t r = blockIdx.x;
+  const int32_t r = r0 + blockIdx.x;  // the store's own rank range only
   const uint32_t b = off[r], e = off[r + 1];
   const uint32_t L = e - b;
   if (threadIdx.x == 0) {
@@ -1156,14 +1157,17 @@ void store_build_index(csg_store* s) {
   flist.ensure(static_cast<size_t>(R) * 4 + 4);
   fcnt.ensure(8);
   CSG_CUDA(cudaMemsetAsync(fcnt.p, 0, 8, st));
+  if (R) CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4, st));
   if (n && R) {
+    // ranks outside [lmin, lmax] (a shard's foreign ranks) have no records:
+    // their chunk maxima are never read and their flags stay 0
+    const int32_t r0 = std::max(h.lmin_rank, 0), r1 = std::min(h.lmax_rank, R - 1);
     ProfScope ps_(c->lc, "k_chunkmax", st);
-    k_chunkmax_blk<<<R, 1024, 0, st>>>(s->tso.as<ulonglong2>(), s->rank_off.as<uint32_t>(),
-                                       s->runmax.as<double>(), s->fl_unsorted.as<uint32_t>(),
-                                       flist.as<uint32_t>(), fcnt.as<unsigned>(),
-                                       &s->stats_dev.as<StoreStats>()->max_seg);
-  } else if (R) {
-    CSG_CUDA(cudaMemsetAsync(s->fl_unsorted.p, 0, static_cast<size_t>(R) * 4, st));
+    if (r1 >= r0)
+      k_chunkmax_blk<<<r1 - r0 + 1, 1024, 0, st>>>(
+          s->tso.as<ulonglong2>(), s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
+          s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(), fcnt.as<unsigned>(),
+          &s->stats_dev.as<StoreStats>()->max_seg, r0);
   }
   // the longest segment stays on the device until the next host round trip
   // (trigger_run picks it up with the trips); shards agree on it over NCCL
