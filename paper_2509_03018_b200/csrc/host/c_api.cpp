@@ -3,12 +3,16 @@
 // Conventions of the reference C API (proj/src/c_api.cpp:27-158): opaque
 // handles, thread-local last-error text, ConfigError -> 2, TraceParseError
 // -> 3, any other failure -> 4, NULL arguments -> 5 before any work.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime_api.h>
 
 #include "collsight.h"
 #include "collsight_b200.h"
@@ -99,20 +103,39 @@ collsight_result* analyze_records(const csh::Scenario& cfg,
     check(csg_model_create(ctx, &tables.topo, &tables.prog, &g_model));
     g_model_key = key;
   }
+  // CSG_E2E_PROF=1: wall time of each phase on stderr
+  static const bool prof = std::getenv("CSG_E2E_PROF") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   if (!g_store) check(csg_store_create(ctx, &g_store));
   check(csg_store_clear(g_store));
   check(csg_store_append(g_store, recs, n));
+  if (prof) cudaDeviceSynchronize();
+  const auto t1 = clk::now();
   Results e;
   check(csg_run_detection(g_store, g_model, &cfg.trigger, &cfg.analysis,
                           cfg.seed, &e.res, nullptr, 0, nullptr));
+  const auto t2 = clk::now();
   std::vector<csg_report_view> views(csg_results_count(e.res));
   for (size_t i = 0; i < views.size(); ++i) check(csg_results_get(e.res, i, &views[i]));
   auto out = std::make_unique<collsight_result>();
   out->reports_jsonl = csh::reports_to_jsonl(views, cfg);
+  const auto t3 = clk::now();
   out->text = csh::reports_to_text(views, cfg) + csh::analyze_summary_text();
   out->summary_json = csh::analyze_summary_json(views.size());
   out->triggers = views.size();
   if (report_out_path) csh::write_file(report_out_path, out->reports_jsonl);
+  const auto t4 = clk::now();
+  if (prof) {
+    auto ms = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr,
+                 "[e2e] append %.3f ms, run_detection %.3f ms, jsonl %.3f ms, text+file "
+                 "%.3f ms (%zu reports, %zu jsonl bytes)\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), views.size(),
+                 out->reports_jsonl.size());
+  }
   return out.release();
 }
 

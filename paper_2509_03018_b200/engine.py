@@ -376,9 +376,29 @@ def affected_groups(store: TraceStore, model: Model, cfg: AnalysisConfig,
     return out[: n.value].tolist(), sc.value
 
 
-def run_detection(store: TraceStore, model: Model, tcfg: TriggerConfig,
-                  acfg: AnalysisConfig, seed: int):
-    """-> (list of report dicts, sampled ranks)"""
+class Results:
+    """Host-resident csg_results of one detection replay; report dicts are
+    built on demand (the replay itself has finished when this exists)."""
+
+    def __init__(self, h: C.c_void_p):
+        self._h = h
+
+    def __len__(self) -> int:
+        return int(lib().csg_results_count(self._h)) if self._h else 0
+
+    def reports(self) -> List[dict]:
+        h, self._h = self._h, None
+        return _take_results(h) if h else []
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().csg_results_free(self._h)
+            self._h = None
+
+
+def run_detection_results(store: TraceStore, model: Model, tcfg: TriggerConfig,
+                          acfg: AnalysisConfig, seed: int):
+    """-> (Results, sampled ranks); the reports stay in host C structs."""
     tc, ac = tcfg.c(), acfg.c()
     h = C.c_void_p()
     sampled = np.zeros(len(model.topo.groups) + 1, dtype=np.int32)
@@ -386,7 +406,14 @@ def run_detection(store: TraceStore, model: Model, tcfg: TriggerConfig,
     _check(lib().csg_run_detection(store.h, model.h, C.byref(tc), C.byref(ac),
                                    C.c_uint64(seed), C.byref(h), _abi.ptr(sampled),
                                    C.c_size_t(len(sampled)), C.byref(ns)))
-    return _take_results(h), sampled[: ns.value].tolist()
+    return Results(h), sampled[: ns.value].tolist()
+
+
+def run_detection(store: TraceStore, model: Model, tcfg: TriggerConfig,
+                  acfg: AnalysisConfig, seed: int):
+    """-> (list of report dicts, sampled ranks)"""
+    res, sampled = run_detection_results(store, model, tcfg, acfg, seed)
+    return res.reports(), sampled
 
 
 def check_min_op(pairs):
