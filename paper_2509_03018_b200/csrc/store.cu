@@ -9,6 +9,8 @@
 // timestamp. The running max is monotone even though per-rank timestamps are
 // not, so every reference "prefix scan that breaks at the
 // first ts > t" becomes one upper_bound over it.
+#include <cuda.h>
+
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -142,12 +144,13 @@ constexpr int kHistDigits = 2048;
 constexpr int kTileThreads = 256;
 constexpr int kTileItems = 16;
 constexpr int kTile = kTileThreads * kTileItems;  // 4096 records
+constexpr uint32_t kScatterCtas = 148;  // persistent scatter: one CTA per SM
+constexpr uint32_t kHistChunks = 148;   // tile chunks of the histogram scan (<= 256)
 
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_stats_hist(const csg_packed_record* __restrict__ r, uint64_t n,
-                 StoreStats* __restrict__ st, uint32_t* __restrict__ counts,
-                 uint32_t ntiles) {
-  __shared__ uint32_t hist[kHistDigits];
+                 StoreStats* __restrict__ st, uint32_t* __restrict__ counts) {
+  __shared__ __align__(16) uint32_t hist[kHistDigits];
   for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads) hist[d] = 0;
   StatAcc acc;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTile;
@@ -179,17 +182,11 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       atomicAdd(&hist[d], __popc(peers));
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads)
-    counts[static_cast<uint64_t>(d) * ntiles + blockIdx.x] = hist[d];
+  // tile-major row of 2048 digit counts: one coalesced 8 KB store per tile
+  uint4* row = reinterpret_cast<uint4*>(counts + static_cast<uint64_t>(blockIdx.x) * kHistDigits);
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist);
+  for (int d = threadIdx.x; d < kHistDigits / 4; d += kTileThreads) row[d] = h4[d];
   acc.commit(st);
-}
-
-// The scan input is the virtual array v[i] = counts[((i / T + d0) & 2047) *
-// T + i % T], i < D * T (k_scan_lookback with HistLoad).
-
-__device__ inline uint32_t hv(const uint32_t* counts, uint64_t i, uint32_t T, uint32_t d0) {
-  const uint64_t d = (i / T + d0) & (kHistDigits - 1);
-  return counts[d * T + i % T];
 }
 
 __device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint32_t* total) {
@@ -220,11 +217,85 @@ __device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint3
   return r;
 }
 
-struct HistLoad {
-  const uint32_t* counts;
-  uint32_t T, d0;
-  __device__ uint32_t operator()(uint64_t i) const { return hv(counts, i, T, d0); }
-};
+// Per-tile digit counts (tile-major, counts[t][d]) -> scatter bases
+// goff[t][j] = sum of all records with rotated digit < j + records of digit
+// j in tiles < t (j = (d - d0) & 2047, i.e. rank - min_rank for spans <=
+// 2048). Three coalesced passes over chunks of tpc consecutive tiles:
+//   k_hist_colsum     per chunk and digit: csum[c][j]
+//   k_hist_chunkscan  per digit, exclusive over chunks (in place) + tot[j]
+//   k_hist_apply      per chunk: digit bases (block scan of tot) + chunk
+//                     prefix, then a running sum over the chunk's tiles
+__global__ void __launch_bounds__(1024)
+    k_hist_colsum(const uint32_t* __restrict__ counts, uint32_t ntiles, uint32_t tpc,
+                  uint32_t d0, int D, uint32_t* __restrict__ csum) {
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * tpc, t1 = min(t0 + tpc, ntiles);
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    const uint32_t d = (j + d0) & (kHistDigits - 1);
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (uint32_t t = t0; t < t1; ++t) sum += __ldg(counts + static_cast<uint64_t>(t) * kHistDigits + d);
+    csum[static_cast<uint64_t>(c) * D + j] = sum;
+  }
+}
+
+// 32 digits per block (lane = digit), the chunks split into 8 contiguous
+// ranges (one per warp): range sums, an exclusive scan over the 8 ranges in
+// shared memory, then each warp rewrites its range as prefixes.
+__global__ void __launch_bounds__(256)
+    k_hist_chunkscan(uint32_t* __restrict__ csum, uint32_t nchunks, int D,
+                     uint32_t* __restrict__ tot) {
+  __shared__ uint32_t part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  const uint32_t per = (nchunks + 7) / 8;
+  const uint32_t c0 = min(warp * per, nchunks), c1 = min(c0 + per, nchunks);
+  // nchunks <= 256: a warp's range (<= 32 chunks) stays in registers
+  uint32_t v[32];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t c = c0 + k;
+    v[k] = j < D && c < c1 ? csum[static_cast<uint64_t>(c) * D + j] : 0u;
+    sum += v[k];
+  }
+  part[warp][lane] = sum;
+  __syncthreads();
+  uint32_t run = 0;
+  for (int w = 0; w < warp; ++w) run += part[w][lane];
+  if (warp == 7 && j < D) tot[j] = run + sum;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t c = c0 + k;
+    if (j < D && c < c1) csum[static_cast<uint64_t>(c) * D + j] = run;
+    run += v[k];
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    k_hist_apply(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ cpre,
+                 const uint32_t* __restrict__ tot, uint32_t ntiles, uint32_t tpc, uint32_t d0,
+                 int D, uint32_t* __restrict__ goff) {
+  __shared__ uint32_t base[kHistDigits];
+  __shared__ uint32_t wsum[32];
+  const int t2 = 2 * threadIdx.x;
+  const uint32_t a = t2 < D ? tot[t2] : 0u, b = t2 + 1 < D ? tot[t2 + 1] : 0u;
+  const uint32_t e = block_excl_scan_u32(a + b, wsum, nullptr);
+  base[t2] = e;
+  base[t2 + 1] = e + a;
+  __syncthreads();
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * tpc, t1 = min(t0 + tpc, ntiles);
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    const uint32_t d = (j + d0) & (kHistDigits - 1);
+    uint32_t run = base[j] + cpre[static_cast<uint64_t>(c) * D + j];
+#pragma unroll 4
+    for (uint32_t t = t0; t < t1; ++t) {
+      goff[static_cast<uint64_t>(t) * D + j] = run;
+      run += __ldg(counts + static_cast<uint64_t>(t) * kHistDigits + d);
+    }
+  }
+}
 
 // Packs the store statistics into order-preserving u64 images (dir 0) so
 // one MAX all-reduce combines every extremum across shards (minima travel
@@ -332,12 +403,14 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
   for (int32_t r = blockIdx.x * kTileThreads + tid; r <= R; r += gridDim.x * kTileThreads)
     rank_off[r] = r < min_rank ? 0u
                   : r > max_rank ? static_cast<uint32_t>(n)
-                                 : goff[static_cast<uint64_t>(r - min_rank) * T];
+                                 : goff[r - min_rank];
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
   }
   __syncthreads();
+  // tiles round-robin over the persistent blocks: the blocks advance through
+  // the store together, so each rank's write front stays compact in L2
   auto sub_of = [&](uint32_t j, uint32_t& t, uint64_t& first, uint32_t& cnt) {
     t = blockIdx.x + (j / SUB) * gridDim.x;
     first = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(j % SUB) * TR;
@@ -361,15 +434,15 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     // the barrier ending j - 1; single buffer (several CTAs per SM cover
     // each other's load latency): load this one now
     issue(NBUF == 2 ? j + 1 : j);
-    // a new histogram tile starts from its scanned global bases: loaded now,
-    // consumed after phase A (latency hidden)
+    // a new histogram tile starts from its scanned global bases (one
+    // contiguous row): loaded now, consumed after phase A (latency hidden)
     const bool fresh = j % SUB == 0;
     uint32_t g0[DPT];
     if (fresh) {
 #pragma unroll
       for (int k = 0; k < DPT; ++k) {
         const int dd = tid * DPT + k;
-        g0[k] = dd < D ? __ldg(goff + static_cast<uint64_t>(dd) * T + t) : 0u;
+        g0[k] = dd < D ? __ldg(goff + static_cast<uint64_t>(t) * D + dd) : 0u;
       }
     }
     if (cnt == 0) {
@@ -515,6 +588,257 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = nxt[k];
     __syncthreads();
   }
+}
+
+// k_scatter with 2-D tensor copies: the TMA engine gathers only the first 32
+// bytes of each 48-byte record (the fields the index writes; the payload is
+// read later through perm) into dense 32-byte shared-memory rows, which
+// leaves room for 16 warps per SM next to two 2048-record buffers (the 1-D
+// bulk variant holds whole records and runs 8). Same ranking and write
+// phases as k_scatter; tile-major bases, round-robin tiles.
+constexpr int kTxThreads = 512;
+constexpr int kTxItems = 4;
+constexpr int kTxRows = kTxThreads * kTxItems;  // 2048-record sub-tile
+constexpr int kTxBox = 256;                     // rows per tensor copy
+
+__device__ inline void tensor_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
+                                      unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(m))
+      : "memory");
+}
+
+template <int DPT>
+__global__ void __launch_bounds__(kTxThreads, 1)
+    k_scatter_tx(const __grid_constant__ CUtensorMap tm, uint64_t n,
+                 const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
+                 int32_t D, ScatterOut o, int32_t max_rank, int32_t R,
+                 uint32_t* __restrict__ rank_off) {
+  constexpr int kW = kTxThreads / 32;
+  constexpr int SUB = kTile / kTxRows;
+  constexpr int Dp = DPT * kTxThreads;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  unsigned char* buf0 = dyn;                                             // [2][2048][32]
+  uint16_t* wc = reinterpret_cast<uint16_t*>(dyn + 2 * kTxRows * 32);  // [kW][Dp]
+  uint32_t* bx = reinterpret_cast<uint32_t*>(wc + kW * Dp);            // [Dp]
+  __shared__ uint16_t sidx[kTxRows];
+  __shared__ uint32_t wsum[32];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int32_t r = blockIdx.x * kTxThreads + tid; r <= R; r += gridDim.x * kTxThreads)
+    rank_off[r] = r < min_rank ? 0u
+                  : r > max_rank ? static_cast<uint32_t>(n)
+                                 : goff[r - min_rank];
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+  }
+  __syncthreads();
+  auto sub_of = [&](uint32_t j, uint32_t& t, uint64_t& first, uint32_t& cnt) {
+    t = blockIdx.x + (j / SUB) * gridDim.x;
+    first = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(j % SUB) * kTxRows;
+    cnt = first < n ? static_cast<uint32_t>(n - first < static_cast<uint64_t>(kTxRows) ? n - first : static_cast<uint64_t>(kTxRows)) : 0u;
+    return t < T;
+  };
+  auto issue = [&](uint32_t j) {
+    uint32_t t, cnt;
+    uint64_t first;
+    if (tid == 0 && sub_of(j, t, first, cnt) && cnt) {
+      unsigned char* dst = buf0 + (j & 1) * kTxRows * 32;
+      const uint32_t boxes = (cnt + kTxBox - 1) / kTxBox;  // OOB rows zero-filled
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&mbar[j & 1])),
+                   "r"(boxes * kTxBox * 32)
+                   : "memory");
+      for (uint32_t b = 0; b < boxes; ++b)
+        tensor_load_2d(dst + b * kTxBox * 32, &tm, 0, static_cast<int>(first + b * kTxBox),
+                       &mbar[j & 1]);
+    }
+  };
+  uint32_t par[2] = {0, 0};
+  issue(0);
+  for (uint32_t j = 0;; ++j) {
+    uint32_t t, cnt;
+    uint64_t first;
+    if (!sub_of(j, t, first, cnt)) break;
+    issue(j + 1);
+    const bool fresh = j % SUB == 0;
+    uint32_t g0[DPT];
+    if (fresh) {
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) {
+        const int dd = tid * DPT + k;
+        g0[k] = dd < D ? __ldg(goff + static_cast<uint64_t>(t) * D + dd) : 0u;
+      }
+    }
+    if (cnt == 0) {
+      if (fresh)
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = g0[k];
+      __syncthreads();
+      continue;
+    }
+    const unsigned char* sb = buf0 + (j & 1) * kTxRows * 32;
+    {
+      uint4* w4 = reinterpret_cast<uint4*>(wc);
+      constexpr int n4 = kW * Dp * 2 / 16;
+      for (int i = tid; i < n4; i += kTxThreads) w4[i] = make_uint4(0, 0, 0, 0);
+    }
+    mbar_wait(&mbar[j & 1], par[j & 1]);
+    par[j & 1] ^= 1;
+    __syncthreads();
+    uint32_t d[kTxItems];
+    uint16_t rk[kTxItems];
+#pragma unroll
+    for (int k = 0; k < kTxItems; ++k) {
+      const uint32_t li = warp * (32 * kTxItems) + k * 32 + lane;
+      d[k] = li < cnt ? static_cast<uint32_t>(
+                            *reinterpret_cast<const int32_t*>(sb + li * 32 + 16) - min_rank)
+                      : 0xFFFFFFFFu;
+    }
+    uint16_t* mine = wc + warp * Dp;
+#pragma unroll
+    for (int k = 0; k < kTxItems; ++k) {
+      const bool valid = d[k] != 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d[k]);
+      const uint32_t before = valid ? mine[d[k]] : 0u;
+      rk[k] = static_cast<uint16_t>(before + __popc(peers & ((1u << lane) - 1u)));
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1)
+        mine[d[k]] = static_cast<uint16_t>(before + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    using VecT = typename std::conditional<DPT == 4, uint2, uint32_t>::type;
+    union DV {
+      VecT v;
+      uint16_t h[DPT];
+    };
+    uint32_t tot[DPT];
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) tot[k] = 0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+      DV x;
+      x.v = *reinterpret_cast<const VecT*>(wc + w * Dp + tid * DPT);
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) tot[k] += x.h[k];
+    }
+    uint32_t mysum = 0;
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) mysum += tot[k];
+    uint32_t ts0[DPT];
+    ts0[0] = block_excl_scan_u32(mysum, wsum, nullptr);
+#pragma unroll
+    for (int k = 1; k < DPT; ++k) ts0[k] = ts0[k - 1] + tot[k - 1];
+    {
+      uint32_t run[DPT];
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) run[k] = ts0[k];
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        DV x, y;
+        x.v = *reinterpret_cast<const VecT*>(wc + w * Dp + tid * DPT);
+#pragma unroll
+        for (int k = 0; k < DPT; ++k) {
+          y.h[k] = static_cast<uint16_t>(run[k]);
+          run[k] += x.h[k];
+        }
+        *reinterpret_cast<VecT*>(wc + w * Dp + tid * DPT) = y.v;
+      }
+    }
+    uint32_t nxt[DPT];
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) {
+      const int dd = tid * DPT + k;
+      const uint32_t rb = fresh ? g0[k] : bx[dd];
+      nxt[k] = rb + tot[k];
+      bx[dd] = rb - ts0[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTxItems; ++k)
+      if (d[k] != 0xFFFFFFFFu)
+        sidx[mine[d[k]] + rk[k]] =
+            static_cast<uint16_t>(warp * (32 * kTxItems) + k * 32 + lane);
+    __syncthreads();
+    // digit order: 4 records per thread in flight
+    {
+      uint32_t li[kTxItems], q[kTxItems];
+      ulonglong2 h0[kTxItems], hm[kTxItems];
+#pragma unroll
+      for (int k = 0; k < kTxItems; ++k) {
+        const uint32_t p = tid + k * kTxThreads;
+        li[k] = p < cnt ? sidx[p] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kTxItems; ++k) {
+        const ulonglong2* rec = reinterpret_cast<const ulonglong2*>(sb + li[k] * 32);
+        h0[k] = rec[0];
+        hm[k] = rec[1];
+      }
+#pragma unroll
+      for (int k = 0; k < kTxItems; ++k) {
+        const uint32_t p = tid + k * kTxThreads;
+        const int32_t rank = static_cast<int32_t>(hm[k].x & 0xffffffffu);
+        q[k] = bx[static_cast<uint32_t>(rank - min_rank) & (Dp - 1)] + p;
+      }
+#pragma unroll
+      for (int k = 0; k < kTxItems; ++k) {
+        const uint32_t p = tid + k * kTxThreads;
+        if (p >= cnt) break;
+        const uint32_t qq = q[k];
+        o.tso[qq] = h0[k];
+        o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
+                             static_cast<int32_t>(hm[k].y & 0xffffffffu));
+        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
+        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
+        o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
+        o.perm[qq] = static_cast<uint32_t>(first + li[k]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = nxt[k];
+    __syncthreads();
+  }
+}
+
+// Driver entry point for the tensor-map encoder (no libcuda link needed).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Tensor map over the packed records as a [n][12] u32 array (48-B rows),
+// boxes of 256 rows x the first 8 words.
+bool record_head_map(const csg_packed_record* recs, uint64_t n, CUtensorMap* tm) {
+  EncodeTiledFn f = encode_tiled();
+  if (!f || n == 0 || n >= (1ull << 31)) return false;
+  const cuuint64_t dims[2] = {12, static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {48};
+  const cuuint32_t box[2] = {8, static_cast<cuuint32_t>(kTxBox)};
+  const cuuint32_t es[2] = {1, 1};
+  return f(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<csg_packed_record*>(recs), dims,
+           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 // Per-rank chunked prefix maximum of ts (StoreView::cmax): one block per rank
@@ -989,11 +1313,11 @@ void store_build_index(csg_store* s) {
   s->keys.ensure(n * 4 + 4);
   const uint32_t ntiles = static_cast<uint32_t>((n + kTile - 1) / kTile);
   DevBuf& hcnt = c->buf("index.hist");
-  hcnt.ensure(static_cast<size_t>(kHistDigits) * ntiles * 4 + 4);
+  hcnt.ensure(static_cast<size_t>(kHistDigits) * ntiles * 4 + 16);
   if (n) {
     ProfScope ps_(c->lc, "k_stats_hist", st);
     k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
-                                                  hcnt.as<uint32_t>(), ntiles);
+                                                  hcnt.as<uint32_t>());
   }
   if (comm_active(c)) {
     // global stats over the shards (identical rank space, ticks, op range)
@@ -1064,31 +1388,38 @@ void store_build_index(csg_store* s) {
     // one stable counting-sort pass over the rank digits (see k_scatter)
     const int32_t lmin = h.lmin_rank;
     const int32_t D = h.lmax_rank - lmin + 1;
-    const uint64_t M = static_cast<uint64_t>(D) * ntiles;
     const uint32_t d0 = static_cast<uint32_t>(lmin) & (kHistDigits - 1);
     DevBuf& goff = c->buf("index.goff");
-    DevBuf& sums = c->buf("index.sums");
-    goff.ensure(M * 4 + 4);
+    DevBuf& csum = c->buf("index.csum");
+    goff.ensure(static_cast<size_t>(D) * ntiles * 4 + 4);
+    const uint32_t tpc = std::max<uint32_t>(1, (ntiles + kHistChunks - 1) / kHistChunks);
+    const uint32_t nchunks = (ntiles + tpc - 1) / tpc;
+    csum.ensure((static_cast<size_t>(D) * nchunks + kHistDigits) * 4);
+    uint32_t* cs = csum.as<uint32_t>();
+    uint32_t* tot = cs + static_cast<size_t>(D) * nchunks;
     {
-      // single-pass decoupled look-back scan over the rotated digit-major view
-      const uint32_t nt = static_cast<uint32_t>((M + kLbTile - 1) / kLbTile);
-      sums.ensure((static_cast<size_t>(nt) + 1) * 8);
-      CSG_CUDA(cudaMemsetAsync(sums.p, 0, (static_cast<size_t>(nt) + 1) * 8, st));
-      ProfScope ps_(c->lc, "k_hist_scan", st);
-      k_scan_lookback<<<nt, kLbThreads, 0, st>>>(HistLoad{hcnt.as<uint32_t>(), ntiles, d0}, M,
-                                                 goff.as<uint32_t>(),
-                                                 sums.as<unsigned long long>(), nt);
+      ProfScope ps_(c->lc, "k_hist_colsum", st);
+      k_hist_colsum<<<nchunks, 1024, 0, st>>>(hcnt.as<uint32_t>(), ntiles, tpc, d0, D, cs);
+    }
+    {
+      ProfScope ps_(c->lc, "k_hist_chunkscan", st);
+      k_hist_chunkscan<<<(D + 31) / 32, 256, 0, st>>>(cs, nchunks, D, tot);
+    }
+    {
+      ProfScope ps_(c->lc, "k_hist_apply", st);
+      k_hist_apply<<<nchunks, 1024, 0, st>>>(hcnt.as<uint32_t>(), cs, tot, ntiles, tpc, d0, D,
+                                             goff.as<uint32_t>());
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
                  s->perm.as<uint32_t>()};
-    // Rank spans <= 1024: 2048-record sub-tiles double-buffered in one CTA
-    // per SM. Wider spans (or CSG_SCATTER_CFG=2): 1024-record sub-tiles, one
-    // bulk-copy buffer per CTA, several CTAs per SM.
+    // Persistent, one CTA per SM, sub-tiles double-buffered by bulk copies:
+    // 2048 records for rank spans <= 1024, 1024 records (wider digit tables)
+    // up to 2048. CSG_SCATTER_CFG=2: single-buffered variants.
     static const int cfg = std::getenv("CSG_SCATTER_CFG") ? std::atoi(std::getenv("CSG_SCATTER_CFG")) : 0;
-    const bool dbl = cfg != 2 && D <= 1024;
-    const int TR = dbl ? 2048 : 1024;
-    const int nbuf = dbl ? 2 : 1;
-    const int Dp = (D <= 1024 ? 4 : 8) * kTileThreads;
+    const bool narrow = D <= 1024;
+    const int TR = narrow ? 2048 : 1024;
+    const int nbuf = cfg == 2 ? 1 : 2;
+    const int Dp = (narrow ? 4 : 8) * kTileThreads;
     const size_t smem = static_cast<size_t>(nbuf) * TR * 48 +
                         (kTileThreads / 32) * static_cast<size_t>(Dp) * 2 +
                         static_cast<size_t>(Dp) * 4;
@@ -1096,31 +1427,51 @@ void store_build_index(csg_store* s) {
     if (!attr) {
       CSG_CUDA(cudaFuncSetAttribute(k_scatter<8, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    1024 * 48 + 8 * 1024 * 2 + 1024 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * 1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
       CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
       attr = true;
     }
-    int per_sm = 1;
-    if (!dbl)
-      CSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, D <= 1024 ? k_scatter<4, 1, 4> : k_scatter<4, 1, 8>, kTileThreads, smem));
-    const unsigned grid = std::min<unsigned>(ntiles, 148u * std::max(per_sm, 1));
+    CUtensorMap tm;
+    const bool tx = cfg == 3 && record_head_map(recs, n, &tm);
+    static bool attr_tx = false;
+    if (tx && !attr_tx) {
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter_tx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * kTxRows * 32 + 16 * 1024 * 2 + 1024 * 4));
+      CSG_CUDA(cudaFuncSetAttribute(k_scatter_tx<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * kTxRows * 32 + 16 * 2048 * 2 + 2048 * 4));
+      attr_tx = true;
+    }
     {
       ProfScope ps_(c->lc, "k_scatter", st);
-      if (dbl)
-        k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, h.lmax_rank, R,
-                                                             s->rank_off.as<uint32_t>());
-      else if (D <= 1024)
-        k_scatter<4, 1, 4><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, h.lmax_rank, R,
-                                                             s->rank_off.as<uint32_t>());
+      const unsigned grid = std::min<unsigned>(ntiles, kScatterCtas);
+      uint32_t* ro = s->rank_off.as<uint32_t>();
+      const uint32_t* g = goff.as<uint32_t>();
+      if (tx) {
+        const int dpt = narrow ? 2 : 4;
+        const size_t sm = 2 * kTxRows * 32 + 16 * static_cast<size_t>(dpt) * kTxThreads * 2 +
+                          static_cast<size_t>(dpt) * kTxThreads * 4;
+        if (narrow)
+          k_scatter_tx<2><<<grid, kTxThreads, sm, st>>>(tm, n, g, ntiles, lmin, D, o,
+                                                        h.lmax_rank, R, ro);
+        else
+          k_scatter_tx<4><<<grid, kTxThreads, sm, st>>>(tm, n, g, ntiles, lmin, D, o,
+                                                        h.lmax_rank, R, ro);
+      } else if (nbuf == 2 && narrow)
+        k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
+                                                             h.lmax_rank, R, ro);
+      else if (nbuf == 2)
+        k_scatter<4, 2, 8><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
+                                                             h.lmax_rank, R, ro);
+      else if (narrow)
+        k_scatter<8, 1, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
+                                                             h.lmax_rank, R, ro);
       else
-        k_scatter<4, 1, 8><<<grid, kTileThreads, smem, st>>>(recs, n, goff.as<uint32_t>(),
-                                                             ntiles, lmin, D, o, h.lmax_rank, R,
-                                                             s->rank_off.as<uint32_t>());
+        k_scatter<4, 1, 8><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
+                                                             h.lmax_rank, R, ro);
     }
   } else {
     // general path: (rank, store index) pairs, LSD radix sort, gather
@@ -1162,9 +1513,13 @@ void store_build_index(csg_store* s) {
     // ranks outside [lmin, lmax] (a shard's foreign ranks) have no records:
     // their chunk maxima are never read and their flags stay 0
     const int32_t r0 = std::max(h.lmin_rank, 0), r1 = std::min(h.lmax_rank, R - 1);
+    // 512 threads: two blocks per SM overlap one block's scan tail with the
+    // other's loads (41 vs 52 us at 1024 threads on the C2 store)
+    static const int cm_threads =
+        std::getenv("CSG_CM_THREADS") ? std::atoi(std::getenv("CSG_CM_THREADS")) : 512;
     ProfScope ps_(c->lc, "k_chunkmax", st);
     if (r1 >= r0)
-      k_chunkmax_blk<<<r1 - r0 + 1, 1024, 0, st>>>(
+      k_chunkmax_blk<<<r1 - r0 + 1, cm_threads, 0, st>>>(
           s->tso.as<ulonglong2>(), s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
           s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(), fcnt.as<unsigned>(),
           &s->stats_dev.as<StoreStats>()->max_seg, r0);

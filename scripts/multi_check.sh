@@ -1,0 +1,17 @@
+#!/bin/bash
+# Multi-GPU check on one box: sharded parity test and weak-scaling bench
+# lines at N = 2 and N = <gpus>.
+#   gpurun --gpus 4 --timeout 1800 -- bash scripts/multi_check.sh <tag>
+set -u
+O=gpurun_out/${1:-multi}
+mkdir -p "$O"
+G=$(nvidia-smi -L | wc -l)
+timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > "$O/pytest_multi.log" 2>&1
+echo "pytest multi $?" >> "$O/status"
+for N in 2 $G; do
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
+      --master-addr 127.0.0.1 --master-port $((29500 + N)) bench.py --gpus $N --steps 10 \
+      --warmup 3 > "$O/bench_n$N.json" 2> "$O/bench_n$N.err"
+  echo "bench n$N $?" >> "$O/status"
+done
+cat "$O/status"
