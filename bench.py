@@ -345,7 +345,7 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if ws > 1:
         dist.destroy_process_group()
 
@@ -480,7 +480,7 @@ def run_reference(args):
                             "sample": sample},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def first_trip_tick(recs, scen):
@@ -495,7 +495,23 @@ def first_trip_tick(recs, scen):
     return t
 
 
+_RESULT_FD = None
+
+
+def emit(out: dict) -> None:
+    """The one JSON result line, on the real stdout."""
+    fd = _RESULT_FD if _RESULT_FD is not None else sys.stdout.fileno()
+    os.write(fd, (json.dumps(out) + "\n").encode())
+
+
 def main():
+    global _RESULT_FD
+    # everything else native code prints on stdout (e.g. the NCCL version
+    # banner at communicator init) goes to stderr: stdout carries only the
+    # result line
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -2292,13 +2292,74 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   };
   long long clk0 = clock64(), clk1 = 0, clk2 = 0, clk3 = 0, clk4 = 0, clk5 = 0;
   long long cy_y = 0, cy_dd = 0, cy_walk = 0;
-  // 1. stable (op, rank) order
-  block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
-    const ExoKey kx = key(x), ky = key(y);
-    if (kx.op != ky.op) return kx.op < ky.op;
-    if (kx.rank != ky.rank) return kx.rank < ky.rank;
-    return x < y;
-  });
+  // 1. stable (op, rank) order. When (op - min op, rank, index) packs into
+  // 64 bits and P keys fit the free shared memory past the staged keys, the
+  // bitonic network sorts the packed keys directly (no indirection through
+  // the 40-byte key records per compare-exchange).
+  bool packed = false;
+  if (staged && P <= (kExoSmemMax - kExoStageBytes) / 8) {
+    __shared__ long long s_opmin, s_opmax;
+    __shared__ int s_rmax;
+    if (tid == 0) {
+      s_opmin = LLONG_MAX;
+      s_opmax = LLONG_MIN;
+      s_rmax = 0;
+    }
+    __syncthreads();
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    int rm = 0;
+    for (uint32_t i = tid; i < C; i += blockDim.x) {
+      mn = min(mn, static_cast<long long>(sk[i].op));
+      mx = max(mx, static_cast<long long>(sk[i].op));
+      rm = max(rm, sk[i].rank);
+    }
+    atomicMin(&s_opmin, mn);
+    atomicMax(&s_opmax, mx);
+    atomicMax(&s_rmax, rm);
+    __syncthreads();
+    const unsigned long long span =
+        static_cast<unsigned long long>(s_opmax) - static_cast<unsigned long long>(s_opmin);
+    const int ib = 32 - __clz(static_cast<int>(P - 1) | 1);
+    const int rb = 32 - __clz(s_rmax | 1);
+    const int ob = 64 - __clzll(static_cast<long long>(span | 1));
+    if (s_rmax >= 0 && ob + rb + ib <= 64 && (span >> 62) == 0) {
+      packed = true;
+      unsigned long long* pk =
+          reinterpret_cast<unsigned long long*>(dynb + kExoStageBytes);
+      const long long omin = s_opmin;
+      for (uint32_t i = tid; i < P; i += blockDim.x)
+        pk[i] = i < C ? ((static_cast<unsigned long long>(sk[i].op - omin) << (rb + ib)) |
+                         (static_cast<unsigned long long>(sk[i].rank) << ib) | i)
+                      : ~0ull;
+      __syncthreads();
+      for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t i = tid; i < P; i += blockDim.x) {
+            const uint32_t l = i ^ jj;
+            if (l > i) {
+              const unsigned long long x = pk[i], y = pk[l];
+              if (((i & k) == 0) == (x > y)) {
+                pk[i] = y;
+                pk[l] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      const unsigned long long im = (1ull << ib) - 1;
+      for (uint32_t i = tid; i < P; i += blockDim.x)
+        ord[i] = i < C ? static_cast<uint32_t>(pk[i] & im) : 0xFFFFFFFFu;
+      __syncthreads();
+    }
+  }
+  if (!packed)
+    block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
+      const ExoKey kx = key(x), ky = key(y);
+      if (kx.op != ky.op) return kx.op < ky.op;
+      if (kx.rank != ky.rank) return kx.rank < ky.rank;
+      return x < y;
+    });
   clk1 = clock64();
   // 2. distinct valid (>= 0) candidate ops, ascending (ordered compaction)
   {
