@@ -1529,13 +1529,10 @@ void store_build_index(csg_store* s) {
   s->max_seg = 0;
   s->max_seg_pending = n && R;
   if (comm_active(c)) {
-    unsigned long long* d = &s->stats_dev.as<StoreStats>()->max_seg;
-    comm_allreduce(c, d, 1, ncclUint64, ncclMax);
-    unsigned long long v = 0;
-    CSG_CUDA(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, st));
-    CSG_CUDA(cudaStreamSynchronize(st));
-    s->max_seg = v;
-    s->max_seg_pending = false;
+    // reduced in stream order; every shard reads the global value at its
+    // next round trip (also shards without records)
+    comm_allreduce(c, &s->stats_dev.as<StoreStats>()->max_seg, 1, ncclUint64, ncclMax);
+    s->max_seg_pending = true;
   }
   CSG_CUDA(cudaGetLastError());
   s->indexed = true;
