@@ -235,6 +235,29 @@ void ctx_sync(csg_ctx* c, const FetchArgs* fetch) {
   if (e != cudaSuccess && e != cudaErrorNotReady) CSG_CUDA(e);
   if (e == cudaErrorNotReady) CSG_CUDA(cudaStreamSynchronize(c->stream));
 }
+FetchTicket ctx_fetch_issue(csg_ctx* c, const FetchArgs& fetch) {
+  c->sig.ensure(64);
+  const unsigned long long v = ++c->sig_seq;
+  k_fetch<<<1, 256, 0, c->stream>>>(fetch, c->sig.as<unsigned long long>(), v);
+  CSG_CUDA(cudaGetLastError());
+  ++c->lc.launches;
+  if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
+  CSG_CUDA(cudaEventRecord(c->ev_fetch, c->stream));
+  return FetchTicket{v};
+}
+
+void ctx_fetch_wait(csg_ctx* c, const FetchTicket& t) {
+  volatile unsigned long long* f = c->sig.as<volatile unsigned long long>();
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*f < t.seq) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(500)) {
+      CSG_CUDA(cudaEventSynchronize(c->ev_fetch));
+      break;
+    }
+  }
+  const cudaError_t e = cudaEventQuery(c->ev_fetch);
+  if (e != cudaSuccess && e != cudaErrorNotReady) CSG_CUDA(e);
+}
 }  // namespace csg
 
 extern "C" {
@@ -289,6 +312,7 @@ void csg_ctx_free(csg_ctx* c) {
   c->scratch_b.release();
   c->scratch_c.release();
   cudaEventDestroy(c->ev_start);
+  if (c->ev_fetch) cudaEventDestroy(c->ev_fetch);
   cudaEventDestroy(c->ev_stop);
   cudaStreamDestroy(c->stream);
   delete c;

@@ -13,6 +13,7 @@ struct csg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  cudaEvent_t ev_fetch = nullptr;  // recorded after an issued fetch (ctx_fetch_issue)
   double device_ms = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
   // sharded mode (csg_ctx_comm_init): NCCL communicator over nranks GPUs
@@ -86,6 +87,11 @@ struct csg_store {
   int32_t R = 0, nch = 0;
   uint64_t max_seg = 0;  // longest rank segment
   bool max_seg_pending = false;  // still on the device (stats_dev->max_seg)
+  bool max_seg_unreduced = false;  // sharded: not yet MAX-reduced over the shards
+  // layout of the last fused index build: the next build launches its
+  // scatter on it before the statistics reach the host (store_build_index)
+  bool spec_ok = false;
+  int32_t sp_lmin = 0, sp_lmax = -1, sp_R = 0;
   csg::DevBuf rank_off, perm, keys, ko;
   csg::DevBuf runmax;  // chunked prefix max of ts (StoreView::cmax)
   csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
@@ -257,8 +263,18 @@ struct FetchArgs {
   }
 };
 void ctx_sync(csg_ctx* c, const FetchArgs* fetch = nullptr);
+// Split round trip: enqueue the fetch now, keep enqueueing work, wait for the
+// fetched bytes later (without draining the work queued after the fetch).
+struct FetchTicket {
+  uint64_t seq = 0;
+};
+FetchTicket ctx_fetch_issue(csg_ctx* c, const FetchArgs& fetch);
+void ctx_fetch_wait(csg_ctx* c, const FetchTicket& t);
 // Brings stats_dev->max_seg to the host if still pending (one round trip).
 void store_resolve_max_seg(csg_store* s);
+// Sharded stores: enqueue the MAX all-reduce of the longest segment if it is
+// still local (callers may be inside an NCCL group).
+void store_reduce_max_seg(csg_store* s);
 
 // Per-thread error text for csg_last_error.
 void set_error(const std::string& msg);

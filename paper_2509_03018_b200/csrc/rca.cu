@@ -561,10 +561,13 @@ __global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
 }
 
 // ---------------------------------------------------------------------------
-// K4: affected_groups (rca.cpp:400-461), one block per trip. Reachability
-// from the trigger rank's groups is the static group graph's connected
-// component (computed once per model on the host).
+// K4: affected_groups (rca.cpp:400-461), grid (trip, slice): each block
+// flags one slice of the groups (latency-bound member lookups spread over
+// the GPU), the last block of a trip to finish compacts the flags in group
+// order. Reachability from the trigger rank's groups is the static group
+// graph's connected component (computed once per model on the host).
 // ---------------------------------------------------------------------------
+constexpr int kAffSlices = 16;
 __global__ void k_affected(StoreView s, ModelView m, int32_t J,
                            const int32_t* __restrict__ trip_kind,
                            const int32_t* __restrict__ trip_rank,
@@ -573,11 +576,13 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
                            const GroupIter* __restrict__ gi,
                            int32_t* __restrict__ aff,
                            uint8_t* __restrict__ aff_flag,
-                           int32_t* __restrict__ n_aff) {
+                           int32_t* __restrict__ n_aff,
+                           unsigned* __restrict__ slices_done) {
   __shared__ int32_t comps[64];
   __shared__ int32_t ncomp;
   __shared__ int32_t wsum[32];
   __shared__ int32_t base;
+  __shared__ bool last;
   const int32_t j = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -600,7 +605,7 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
   // pass 1, a warp per group: any member stuck (lanes over the members), or
   // late for straggler trips; reachable = same connected component
   uint8_t* af = aff_flag + static_cast<uint64_t>(j) * m.n_groups;
-  for (int32_t g = warp; g < m.n_groups; g += nwarps) {
+  for (int32_t g = blockIdx.y * nwarps + warp; g < m.n_groups; g += gridDim.y * nwarps) {
     bool reach = false;
     const int32_t cg = m.comp[g];
     for (int32_t i = 0; i < ncomp; ++i) reach |= comps[i] == cg;
@@ -621,11 +626,21 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
     }
     if (lane == 0) af[g] = flag ? 1 : 0;
   }
+  // the last slice of trip j to finish compacts (its flag reads bypass L1)
+  __threadfence();
   __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(slices_done + j, 1u);
+    last = prev == gridDim.y - 1;
+    if (last) slices_done[j] = 0;  // ready for the next launch
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   // pass 2: ordered compaction of the flagged groups
   for (int32_t g0 = 0; g0 < m.n_groups; g0 += blockDim.x) {
     const int32_t g = g0 + tid;
-    const int hit = g < m.n_groups ? af[g] : 0;
+    const int hit = g < m.n_groups ? __ldcg(af + g) : 0;
     int x = hit;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -3233,10 +3248,16 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   aff_flag.ensure(static_cast<size_t>(J) * std::max(G, 1));
   n_aff.ensure(static_cast<size_t>(J) * 4);
   {
+    // per-trip slice counters: zeroed once, reset by the last slice
+    DevBuf& sdone = c->buf("rca.aff_slices");
+    if (sdone.bytes < static_cast<size_t>(J) * 4) {
+      sdone.ensure(static_cast<size_t>(J) * 4);
+      CSG_CUDA(cudaMemsetAsync(sdone.p, 0, sdone.bytes, st));
+    }
     ProfScope ps_(c->lc, "k_affected", st);
-    k_affected<<<J, 1024, 0, st>>>(sv, mv, J, dkind, drank, djs, rs.as<RankSum>(),
-                                  gi.as<GroupIter>(), aff.as<int32_t>(),
-                                  aff_flag.as<uint8_t>(), n_aff.as<int32_t>());
+    k_affected<<<dim3(J, kAffSlices), 1024, 0, st>>>(
+        sv, mv, J, dkind, drank, djs, rs.as<RankSum>(), gi.as<GroupIter>(), aff.as<int32_t>(),
+        aff_flag.as<uint8_t>(), n_aff.as<int32_t>(), sdone.as<unsigned>());
   }
   HostBuf& h_affb = c->hbuf("rca.aff");
   h_affb.ensure(static_cast<size_t>(J) * (static_cast<size_t>(G) + 1) * 4 + 16);

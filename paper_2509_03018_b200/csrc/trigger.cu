@@ -591,6 +591,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
       comm_group_start(c);
       comm_allreduce(c, asum, sb / 8, ncclUint64, ncclSum);
       comm_allreduce(c, amax, mb / 8, ncclUint64, ncclMax);
+      store_reduce_max_seg(s);
       comm_group_end(c);
       ProfScope ps_(c->lc, "k_trigger_ema", c->stream);
       k_trigger_ema<<<S, 512, tsmem, c->stream>>>(
@@ -599,8 +600,11 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     }
   } else {
   trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
+  comm_group_start(c);
   comm_allreduce(c, ws.p, static_cast<size_t>(T) * S * sizeof(WinStat) / 8, ncclUint64,
                  ncclSum);
+  store_reduce_max_seg(s);
+  comm_group_end(c);
   {
     ProfScope ps_(c->lc, "k_ema_ticks", c->stream);
     k_ema_ticks<<<(S + 127) / 128, 128, 0, c->stream>>>(ws.as<WinStat>(), T, S, p,

@@ -59,3 +59,57 @@ def test_fused_index_matches_radix_index(dp, lo, hi, cut):
     assert a["q"] == b["q"]
     assert a["ll"] == b["ll"]
     assert a["reports"] == b["reports"]
+
+
+SPEC_CHILD = r"""
+import json, os, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+from paper_2509_03018_b200 import engine as E
+cfg = json.load(open(os.path.join(%(root)r, 'configs', 'c2_mini_128.json')))
+cfg['layout']['dp'] = 64
+cfg['sim']['max_sim_ms'] = 2600.0
+cfg['faults'][0]['onset_ms'] = 1504.0
+scen = E.Scenario.parse(json.dumps(cfg))
+full = E.synthesize(scen, 0, (0, 1 << 30))
+topo, prog = scen.layout()
+tc, ac, seed = scen.configs()
+model = E.Model(topo, prog)
+store = E.TraceStore()
+part = full[(full['rank'] >= 100) & (full['rank'] < 900)]
+bad = full[:5000].copy()
+bad['rank'][77] = -3
+steps = [full, full, part, part[: len(part) * 2 // 3], full, bad, full, full]
+out = []
+for recs in steps:
+    store.clear()
+    store.append(recs)
+    try:
+        got, sampled = E.run_detection(store, model, tc, ac, seed)
+        ranks = sorted(set(np.unique(recs['rank']).tolist()))
+        q = [store.query(ranks[i::7], 300.0 * i, 300.0 * i + 900.0) for i in range(7)]
+        out.append({'n': len(recs), 'reports': got, 'q': q})
+    except Exception as e:
+        out.append({'error': type(e).__name__})
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.gpu
+def test_speculative_index_layout_matches_fresh_builds():
+    """Rebuilding one store over the same rank layout launches the index on
+    the last layout before the statistics reach the host (store_build_index);
+    hits (same span, any n), misses (other span) and invalid input must give
+    exactly what builds without speculation give."""
+    def go(env_extra):
+        env = dict(os.environ, **env_extra)
+        r = subprocess.run([sys.executable, "-c", SPEC_CHILD % dict(root=ROOT)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    a = go({})
+    b = go({"CSG_INDEX_NOSPEC": "1"})
+    assert len(a) == len(b) == 8
+    assert a[5] == b[5] == {"error": a[5].get("error")} and "error" in a[5]
+    for x, y in zip(a, b):
+        assert x == y
