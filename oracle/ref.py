@@ -81,6 +81,21 @@ def simulate(cfg_json: str, with_jsonl: bool = False):
     return (arr, _take(jl)) if with_jsonl else arr
 
 
+def simulate_prog(cfg_json: str, prog: OpProgram, msg_bytes: int) -> np.ndarray:
+    """Reference run_simulation with a custom program (SURVEY.md §8(d) C1);
+    layout, sim config and faults from the scenario JSON."""
+    out = C.c_void_p()
+    n = C.c_size_t()
+    pd, keep = prog.desc()
+    _check(lib().ref_simulate_prog(cfg_json.encode(), C.byref(pd),
+                                   C.c_uint64(msg_bytes), C.byref(out), C.byref(n)))
+    arr = np.frombuffer(C.string_at(out.value, n.value * 48),
+                        dtype=_abi.RECORD_DTYPE).copy() if n.value else \
+        np.zeros(0, dtype=_abi.RECORD_DTYPE)
+    lib().ref_free(out)
+    return arr
+
+
 def run_detection_cfg(cfg_json: str, recs: np.ndarray):
     """-> (reports_to_jsonl text, full reports list, sampled, seconds)"""
     recs, p, n = _recs(recs)

@@ -25,6 +25,7 @@
 #include "collsight/rca.hpp"
 #include "collsight/runner.hpp"
 #include "collsight/scenario.hpp"
+#include "collsight/sim.hpp"
 #include "collsight/trace.hpp"
 #include "collsight/trigger.hpp"
 #include "csg_engine.h"
@@ -262,6 +263,30 @@ int ref_simulate(const char* cfg_json, csg_packed_record** out, size_t* n,
     for (std::size_t i = 0; i < run.records.size(); ++i)
       (*out)[i] = pack(run.records[i]);
     if (jsonl) *jsonl = dup(serialize_records(run.records));
+    return 0;
+  });
+}
+
+// Program-driven simulate (a custom one-op AllReduce
+// program is expressible only through the C++ API): layout, sim config and
+// faults come from the scenario JSON, the program from `pd` with every op's
+// msg_bytes set to `msg_bytes`. run_simulation: proj/include/collsight/
+// sim.hpp:90.
+int ref_simulate_prog(const char* cfg_json, const csg_program_desc* pd,
+                      uint64_t msg_bytes, csg_packed_record** out, size_t* n) {
+  return guard([&] {
+    const ScenarioConfig cfg = parse_scenario(cfg_json);
+    const Topology topo = cfg.build_topology();
+    OpProgram program = make_program(pd);
+    for (auto& op : program.ops) op.msg_bytes = msg_bytes;
+    validate_program(program, topo);
+    std::vector<TraceRecord> records;
+    run_simulation(topo, program, cfg.faults, cfg.sim,
+                   [&](const TraceRecord& r) { records.push_back(r); });
+    *n = records.size();
+    *out = static_cast<csg_packed_record*>(
+        std::malloc(sizeof(csg_packed_record) * (records.size() + 1)));
+    for (std::size_t i = 0; i < records.size(); ++i) (*out)[i] = pack(records[i]);
     return 0;
   });
 }
