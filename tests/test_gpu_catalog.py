@@ -15,7 +15,8 @@ from tests.conftest import GOLDEN
 from tests.golden import codec
 
 CATALOG = ["clean"] + [f"scenario{i}" for i in range(1, 8)] + \
-    ["synth_hang_128", "synth_strag_128"]
+    ["synth_hang_128", "synth_strag_128"] + \
+    ["sweep_gpu_down", "sweep_nic_flap", "sweep_slow_pcie", "sweep_opseq_lag"]
 MANIFEST = json.load(open(os.path.join(GOLDEN, "manifest.json")))
 
 
