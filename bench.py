@@ -320,6 +320,12 @@ def run_ours(args):
                        "sharded index + trigger + RCA with NCCL, D2H of reports; max "
                        "over ranks"}
     if rank == 0 and ws == 1:
+        if WORKLOAD in FIXED_JOB:
+            # the C-API call below owns its own context and store: release the
+            # timed store first (C4 on one GPU does not fit twice in HBM)
+            import gc
+            del store, model
+            gc.collect()
         pinned = torch.empty(n * 48, dtype=torch.uint8, pin_memory=True)
         host = pinned.numpy().view(recs.dtype)
         host[:] = recs
