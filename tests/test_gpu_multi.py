@@ -49,6 +49,17 @@ def _worker(rank, world, port, q):
             store = E.TraceStore(ctx, shard)
             got, _ = E.run_detection(store, E.Model(topo, prog, ctx), tc, ac, seed)
             res[name] = got == full
+        # C1: the 32-rank ring AllReduce program (tests/test_c1.py)
+        from tests.test_c1 import VARIANTS, golden as c1_golden, layout as c1_layout
+        topo, prog, _ = c1_layout()
+        for name in VARIANTS:
+            recs, full = c1_golden(name)
+            cfg = open(os.path.join(GOLDEN, "configs", name + ".json")).read()
+            tc, ac, seed = E.Scenario.parse(cfg).configs()
+            shard = D.shard_records(recs, topo.world_size, world, rank)
+            store = E.TraceStore(ctx, shard)
+            got, _ = E.run_detection(store, E.Model(topo, prog, ctx), tc, ac, seed)
+            res[name] = got == full
         q.put((rank, res, ctx.comm_info()))
     finally:
         dist.destroy_process_group()
