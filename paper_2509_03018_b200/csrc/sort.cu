@@ -26,17 +26,21 @@ __global__ void __launch_bounds__(kThreads)
   hist[tid] = 0;
   __syncthreads();
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTile;
+  // every key of the tile loaded before the first match (kItems loads in
+  // flight per thread; the guarded load-match-atomic chain serialised them)
+  uint32_t d[kItems];
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const uint64_t idx = base + static_cast<uint64_t>(i) * kThreads + tid;
-    if (idx < n) {
-      const uint32_t d = static_cast<uint32_t>((keys[idx] >> shift) & 255u);
-      // Warp-aggregated increment: one shared atomic per distinct digit.
-      const unsigned act = __activemask();
-      const unsigned peers = __match_any_sync(act, d);
-      if ((threadIdx.x & 31) == __ffs(peers) - 1)
-        atomicAdd(&hist[d], __popc(peers));
-    }
+    d[i] = idx < n ? static_cast<uint32_t>((keys[idx] >> shift) & 255u) : kRadix;
+  }
+  // Warp-aggregated increment: one shared atomic per distinct digit (the
+  // out-of-range sentinel kRadix is skipped).
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const unsigned peers = __match_any_sync(0xffffffffu, d[i]);
+    if (d[i] < kRadix && (threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(&hist[d[i]], __popc(peers));
   }
   __syncthreads();
   counts[static_cast<uint64_t>(tid) * ntiles + blockIdx.x] = hist[tid];
