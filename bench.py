@@ -306,8 +306,10 @@ def run_ours(args):
             t0 = time.perf_counter()
             store.clear()
             store.append(host)              # H2D of this shard's records
-            rep_e2e, _ = E.run_detection(store, model, tcfg, acfg, seed)  # + D2H
+            res_e2e, _ = E.run_detection_results(store, model, tcfg, acfg, seed)  # + D2H
+            jsonl = res_e2e.jsonl(scen)     # the drop-in's report bytes (C++)
             times.append(time.perf_counter() - t0)
+        rep_e2e = res_e2e
         _, h2d, d2h = ctx.kernel_stats()
         k = len(times)
         tt = torch.tensor([float(np.mean(times))], device="cuda")
@@ -317,8 +319,8 @@ def run_ours(args):
                "d2h_bytes_per_step": int(d2h // k) * ws,
                "ms_per_step": float(tt.item()) * 1e3, "triggers": len(rep_e2e),
                "note": "engine API per shard: H2D of the shard from pinned memory, "
-                       "sharded index + trigger + RCA with NCCL, D2H of reports; max "
-                       "over ranks"}
+                       "sharded index + trigger + RCA with NCCL, D2H of reports, JSONL "
+                       "rendering; max over ranks"}
     if rank == 0 and ws == 1:
         if WORKLOAD in FIXED_JOB:
             # the C-API call below owns its own context and store: release the

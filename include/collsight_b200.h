@@ -29,6 +29,14 @@ collsight_status collsight_b200_run_analyze_packed(
     const collsight_scenario* scenario, const csg_packed_record* records,
     size_t n, const char* report_out_path, collsight_result** out);
 
+/* reports_to_jsonl (reference proj/src/runner.cpp:103-169) of engine results
+ * from csg_run_detection under the scenario's config: the report bytes a
+ * sharded (multi-GPU) caller writes, identical to collsight_run_analyze's.
+ * Caller frees with collsight_b200_free. */
+collsight_status collsight_b200_results_jsonl(const collsight_scenario* scenario,
+                                              const csg_results* results,
+                                              char** jsonl_out);
+
 /* Engine tables of a parsed scenario. The returned JSON text describes the
  * layout and program as {"world_size","groups":[{"kind","members"}],
  * "ops":[{"name","group","src","dst","deps"}]}; caller frees with

@@ -258,6 +258,17 @@ collsight_status collsight_b200_scenario_configs(const collsight_scenario* s,
   return COLLSIGHT_OK;
 }
 
+collsight_status collsight_b200_results_jsonl(const collsight_scenario* s,
+                                              const csg_results* res, char** jsonl_out) {
+  if (!s || !res || !jsonl_out) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    std::vector<csg_report_view> views(csg_results_count(res));
+    for (size_t i = 0; i < views.size(); ++i) check(csg_results_get(res, i, &views[i]));
+    *jsonl_out = dup(csh::reports_to_jsonl(views, s->cfg));
+    return COLLSIGHT_OK;
+  });
+}
+
 collsight_status collsight_b200_layout_json(int tp, int pp, int dp, int rpn,
                                             int cpp, int nics,
                                             uint64_t msg_bytes,

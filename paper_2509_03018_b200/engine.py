@@ -390,6 +390,18 @@ class Results:
         h, self._h = self._h, None
         return _take_results(h) if h else []
 
+    def jsonl(self, scenario: "Scenario") -> str:
+        """reports_to_jsonl bytes under the scenario's config, rendered in C++
+        (collsight_b200_results_jsonl); the results stay usable."""
+        if not self._h:
+            raise EngineError(5, "results already consumed")
+        js = C.c_void_p()
+        _ccheck(lib().collsight_b200_results_jsonl(scenario.h, self._h, C.byref(js)))
+        try:
+            return C.string_at(js.value).decode()
+        finally:
+            lib().collsight_b200_free(js)
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib().csg_results_free(self._h)

@@ -211,3 +211,17 @@ def test_random_windows_match_reference(eng, oracle, name, shuffle):
         got = eng.analyze(store, model, acfg, trig)
         want = oracle.analyze(topo, prog, acfg, recs, trig)
         assert got == want, (k, trig)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["scenario1", "scenario7", "sweep_opseq_lag"])
+def test_results_jsonl_bytes(eng, name):
+    """collsight_b200_results_jsonl over engine-API results (the sharded
+    callers' renderer) gives the reference reports_to_jsonl bytes."""
+    recs, reports, _ = golden(name)
+    scen = eng.Scenario.load(os.path.join(GOLDEN, "configs", name + ".json"))
+    topo, prog = scen.layout()
+    tcfg, acfg, seed = scen.configs()
+    res, _ = eng.run_detection_results(eng.TraceStore(records=recs), eng.Model(topo, prog),
+                                       tcfg, acfg, seed)
+    assert res.jsonl(scen) == reports
