@@ -7,7 +7,9 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <unordered_map>
 #include <string>
@@ -110,6 +112,8 @@ std::vector<int32_t> sample_ranks_host(const csg_model* m, int32_t cap_i,
   return out;
 }
 
+void store_append_jsonl_mem(csg_store* s, const char* text, uint64_t len, int* accepted);
+void store_append_jsonl_file(csg_store* s, const char* path, int* accepted);
 void store_query(csg_store* s, const int32_t* ranks, size_t nr, double t0,
                  double t1, std::vector<uint64_t>& out);
 void store_last_log(csg_store* s, const int32_t* members, size_t nm, double t,
@@ -212,6 +216,19 @@ __global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long lon
   }
 }
 }  // namespace
+
+void smem_optin_raw(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  CSG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& g = granted[{dev, func}];
+  if (g >= bytes) return;
+  CSG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes)));
+  g = bytes;
+}
 
 void ctx_sync(csg_ctx* c, const FetchArgs* fetch) {
   c->sig.ensure(64);
@@ -440,6 +457,27 @@ csg_status csg_store_append(csg_store* s, const csg_packed_record* host,
 csg_status csg_store_append_device(csg_store* s, const csg_packed_record* dev,
                                    size_t n) {
   return append_impl(s, dev, n, cudaMemcpyDeviceToDevice);
+}
+
+csg_status csg_store_append_jsonl(csg_store* s, const char* text, size_t len,
+                                  int* accepted) {
+  if (!s || (!text && len) || !accepted) return fail(CSG_ERR_ARG, "null argument");
+  return guarded([&] {
+    CSG_CUDA(cudaSetDevice(s->ctx->device));
+    csg_ctx::Timed tm(s->ctx);
+    store_append_jsonl_mem(s, text, len, accepted);
+    return CSG_OK;
+  });
+}
+
+csg_status csg_store_append_jsonl_file(csg_store* s, const char* path, int* accepted) {
+  if (!s || !path || !accepted) return fail(CSG_ERR_ARG, "null argument");
+  return guarded([&] {
+    CSG_CUDA(cudaSetDevice(s->ctx->device));
+    csg_ctx::Timed tm(s->ctx);
+    store_append_jsonl_file(s, path, accepted);
+    return CSG_OK;
+  });
 }
 
 csg_status csg_store_clear(csg_store* s) {
@@ -743,7 +781,7 @@ csg_status csg_affected_groups(csg_store* store, const csg_model* model,
     const int32_t n = r.trips[0].n_aff;
     *n_out = n;
     for (int32_t i = 0; i < n && static_cast<size_t>(i) < cap; ++i) out[i] = r.aff[i];
-    if (scanned) *scanned += store->n;
+    if (scanned) *scanned += store->n_global;  // records over all shards
     return CSG_OK;
   });
 }

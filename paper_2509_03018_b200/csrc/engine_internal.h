@@ -27,7 +27,15 @@ struct Error : std::runtime_error {
                              " at " __FILE__ ":" + std::to_string(__LINE__)); \
   } while (0)
 
-// Growable device buffer (bytes).
+// Dynamic shared-memory opt-in for a kernel on the CURRENT device.
+// cudaFuncSetAttribute is per device, so the "already set" cache is keyed by
+// (device, kernel) and holds the largest size granted; thread-safe.
+void smem_optin_raw(const void* func, size_t bytes);
+template <typename F>
+inline void smem_optin(F* func, size_t bytes) {
+  smem_optin_raw(reinterpret_cast<const void*>(func), bytes);
+}
+
 // Grow-only pinned host buffer mapped into the device address space
 // (kernels write results straight into it; no separate copy-back).
 struct HostBuf {

@@ -69,6 +69,8 @@ struct StoreStats {
   unsigned long long n_total;  // records over all shards
   int lmin_rank, lmax_rank;    // this shard's own rank range (not reduced)
   unsigned long long max_seg;  // longest rank segment (k_runmax_blk)
+  unsigned int overlap;        // sharded: two shards' own rank ranges overlap
+  unsigned int pad_;
 };
 
 struct csg_store {

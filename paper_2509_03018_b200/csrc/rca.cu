@@ -3550,8 +3550,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   a.out = d_out.as<TripOut>();
   a.err = err.as<uint32_t>();
   const size_t shm = sizeof(BlockShared);
-  CSG_CUDA(cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(shm)));
+  smem_optin(k_decide, shm);
   uint32_t h_err = 0;
   unsigned long long used[8];
   std::vector<TripOut> to(J);
@@ -3602,9 +3601,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ea.out = d_out.as<TripOut>();
       ea.N = s->n_global;
       ea.err = err.as<uint32_t>();
-      CSG_CUDA(cudaFuncSetAttribute(k_exonerate,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kExoSmemMax)));
+      smem_optin(k_exonerate, kExoSmemMax);
       ProfScope ps_(c->lc, "k_exonerate", st);
       k_exonerate<<<static_cast<unsigned>(n_exo_grid), kExoThreads, kExoSmemMax, st>>>(ea);
     }

@@ -310,8 +310,14 @@ __device__ inline unsigned long long i64_key(long long v) {
 __device__ inline long long key_i64(unsigned long long k) {
   return static_cast<long long>(k ^ 0x8000000000000000ull);
 }
-__global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir) {
+// Sharded statistics as u64 images: pk[0, 7 + 2P) combine by MAX (minima as
+// complements; slots 7 + 2i, 8 + 2i carry shard i's own rank range, zero
+// elsewhere, so the MAX is an all-gather of the ranges), pk[7 + 2P, 9 + 2P)
+// by SUM.
+__global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir, int P,
+                             int me) {
   if (threadIdx.x || blockIdx.x) return;
+  unsigned long long* sum = pk + 7 + 2 * P;
   if (dir == 0) {
     pk[0] = st->ts_max_key;
     pk[1] = ~i64_key(st->min_rank);
@@ -320,8 +326,13 @@ __global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir) {
     pk[4] = i64_key(st->max_chan);
     pk[5] = ~i64_key(st->min_op);
     pk[6] = i64_key(st->max_op);
-    pk[8] = st->n_nan;
-    pk[9] = st->n_total;
+    for (int i = 0; i < P; ++i) {
+      const bool own = i == me && st->lmin_rank <= st->lmax_rank;  // empty shard: none
+      pk[7 + 2 * i] = own ? i64_key(st->lmin_rank) : 0ull;
+      pk[8 + 2 * i] = own ? i64_key(st->lmax_rank) : 0ull;
+    }
+    sum[0] = st->n_nan;
+    sum[1] = st->n_total;
   } else {
     st->ts_max_key = pk[0];
     st->min_rank = static_cast<int>(key_i64(~pk[1]));
@@ -330,8 +341,20 @@ __global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir) {
     st->max_chan = static_cast<int>(key_i64(pk[4]));
     st->min_op = key_i64(~pk[5]);
     st->max_op = key_i64(pk[6]);
-    st->n_nan = pk[8];
-    st->n_total = pk[9];
+    st->n_nan = sum[0];
+    st->n_total = sum[1];
+    // a rank split across shards would make the RCA's sum all-reduces of
+    // per-rank tables add two shards' timestamps: shards must own disjoint
+    // rank ranges
+    unsigned ov = 0;
+    for (int i = 0; i < P; ++i)
+      for (int j = i + 1; j < P; ++j) {
+        if (!pk[7 + 2 * i] || !pk[7 + 2 * j]) continue;
+        const long long lo_i = key_i64(pk[7 + 2 * i]), hi_i = key_i64(pk[8 + 2 * i]);
+        const long long lo_j = key_i64(pk[7 + 2 * j]), hi_j = key_i64(pk[8 + 2 * j]);
+        if (lo_i <= hi_j && lo_j <= hi_i) ov = 1;
+      }
+    st->overlap = ov;
   }
 }
 
@@ -1343,20 +1366,21 @@ void store_build_index(csg_store* s) {
     // one MAX all-reduce over order-preserving u64 images (minima as
     // complements) and one SUM all-reduce for the counts
     DevBuf& pk = c->buf("store.stats_pack");
-    pk.ensure(16 * 8);
+    const int P = c->nranks;
+    pk.ensure((9 + 2 * static_cast<size_t>(P)) * 8);
     {
       ProfScope ps_(c->lc, "k_stats_pack", st);
       k_stats_pack<<<1, 32, 0, st>>>(s->stats_dev.as<StoreStats>(),
-                                     pk.as<unsigned long long>(), 0);
+                                     pk.as<unsigned long long>(), 0, P, c->rank);
     }
     comm_group_start(c);
-    comm_allreduce(c, pk.p, 7, ncclUint64, ncclMax);
-    comm_allreduce(c, pk.as<unsigned long long>() + 8, 2, ncclUint64, ncclSum);
+    comm_allreduce(c, pk.p, 7 + 2 * static_cast<size_t>(P), ncclUint64, ncclMax);
+    comm_allreduce(c, pk.as<unsigned long long>() + 7 + 2 * P, 2, ncclUint64, ncclSum);
     comm_group_end(c);
     {
       ProfScope ps_(c->lc, "k_stats_pack", st);
       k_stats_pack<<<1, 32, 0, st>>>(s->stats_dev.as<StoreStats>(),
-                                     pk.as<unsigned long long>(), 1);
+                                     pk.as<unsigned long long>(), 1, P, c->rank);
     }
   }
   HostBuf& hs = c->hbuf("store.stats");
@@ -1415,27 +1439,15 @@ void store_build_index(csg_store* s) {
     const size_t smem = static_cast<size_t>(nbuf) * TR * 48 +
                         (kTileThreads / 32) * static_cast<size_t>(Dp) * 2 +
                         static_cast<size_t>(Dp) * 4;
-    static bool attr = false;
-    if (!attr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * 1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<8, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2048 * 48 + 8 * 1024 * 2 + 1024 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter<4, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    1024 * 48 + 8 * 2048 * 2 + 2048 * 4));
-      attr = true;
-    }
+    smem_optin(k_scatter<8, 2, 4>, 2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4);
+    smem_optin(k_scatter<4, 2, 8>, 2 * 1024 * 48 + 8 * 2048 * 2 + 2048 * 4);
+    smem_optin(k_scatter<8, 1, 4>, 2048 * 48 + 8 * 1024 * 2 + 1024 * 4);
+    smem_optin(k_scatter<4, 1, 8>, 1024 * 48 + 8 * 2048 * 2 + 2048 * 4);
     CUtensorMap tm;
     const bool tx = cfg == 3 && record_head_map(recs, n, &tm);
-    static bool attr_tx = false;
-    if (tx && !attr_tx) {
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter_tx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kTxRows * 32 + 16 * 1024 * 2 + 1024 * 4));
-      CSG_CUDA(cudaFuncSetAttribute(k_scatter_tx<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kTxRows * 32 + 16 * 2048 * 2 + 2048 * 4));
-      attr_tx = true;
+    if (tx) {
+      smem_optin(k_scatter_tx<2>, 2 * kTxRows * 32 + 16 * 1024 * 2 + 1024 * 4);
+      smem_optin(k_scatter_tx<4>, 2 * kTxRows * 32 + 16 * 2048 * 2 + 2048 * 4);
     }
     {
       ProfScope ps_(c->lc, "k_scatter", st);
@@ -1537,6 +1549,10 @@ void store_build_index(csg_store* s) {
   s->spec_ok = false;
   const uint64_t ng = h.n_total;
   s->n_global = ng;
+  if (h.overlap)
+    throw Error(CSG_ERR_RUNTIME,
+                "engine: sharded store: shards' rank ranges overlap (records of "
+                "one rank must live on one shard; shard by rank range)");
   if (ng && h.min_rank < 0)
     throw Error(CSG_ERR_RUNTIME,
                 "engine: negative rank in trace record (ranks must be >= 0)");
@@ -1760,12 +1776,7 @@ bool store_build_flow_index(csg_store* s) {
     int32_t P = 64;
     while (static_cast<uint64_t>(P) < s->max_seg && P < cap) P <<= 1;
     const size_t smem = static_cast<size_t>(P) * 8;
-    static bool attr = false;
-    if (!attr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_flow_fix, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kFlowSmemMax * 8));
-      attr = true;
-    }
+    smem_optin(k_flow_fix, kFlowSmemMax * 8);
     {
       ProfScope ps_(c->lc, "k_flow_fix", st);
       k_flow_fix<<<static_cast<unsigned>(std::min<int32_t>(R, 148)), 1024, smem, st>>>(

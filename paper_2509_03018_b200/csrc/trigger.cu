@@ -13,6 +13,7 @@
 // Floating point: the EMA and threshold products use explicit _rn intrinsics
 // (and the file is built with -fmad=false) so no FMA contraction happens,
 // matching the reference's SSE2 build.
+#include <algorithm>
 #include <cstring>
 
 #include "comm.cuh"
@@ -22,66 +23,23 @@
 namespace csg {
 namespace {
 
-__global__ void k_window_stats(StoreView s, const double* __restrict__ ticks,
-                               int32_t T, const int32_t* __restrict__ sampled,
-                               int32_t S, double delta,
-                               WinStat* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= static_cast<int64_t>(T) * S) return;
-  const int32_t k = static_cast<int32_t>(w / S), si = static_cast<int32_t>(w % S);
-  const double t = ticks[k];
-  const double t0 = t - delta;  // store.query({r}, t - cfg.delta_ms, t)
-  const int32_t r = sampled[si];
-  uint32_t nrec = 0, ncomp = 0, hstate = 0;
-  unsigned long long bytes = 0;
-  double mn = INFINITY, mx = -INFINITY;
-  if (r >= 0 && r < s.R) {
-    const uint32_t e = s.rank_off[r + 1];
-    for (uint32_t p = s.rank_off[r] + lane; p < e; p += 32) {
-      const double x = s.ts[p];
-      if (x < t0 || x > t) continue;
-      ++nrec;
-      if (ko_kind(s.ko[p]) == CSG_KIND_COMPLETION) {
-        ++ncomp;
-        bytes += s.pb[p];
-        mn = fmin(mn, x);
-        mx = fmax(mx, x);
-      } else {
-        hstate = 1;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    nrec += __shfl_xor_sync(0xffffffffu, nrec, o);
-    ncomp += __shfl_xor_sync(0xffffffffu, ncomp, o);
-    hstate |= __shfl_xor_sync(0xffffffffu, hstate, o);
-    bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if (lane == 0) {
-    WinStat ws;
-    ws.n_rec = nrec;
-    ws.n_comp = ncomp;
-    ws.has_state = hstate;
-    ws.pad = 0;
-    ws.bytes = bytes;
-    ws.min_end = ncomp ? mn : 0.0;
-    ws.max_end = ncomp ? mx : 0.0;
-    out[w] = ws;
-  }
-}
-
-// The same window statistics with one pass over each sampled rank's
-// records: a block per sampled rank bins every record into the (few) tick
-// windows that contain it, accumulating in shared memory. Window k holds x
-// iff !(x < t_k - delta) && !(x > t_k) (trace.cpp:107 with t0 = t_k - delta).
-__global__ void k_window_bins(StoreView s, const double* __restrict__ ticks,
-                              int32_t T, const int32_t* __restrict__ sampled,
+// Window statistics (TraceStore::query per sampled rank and tick,
+// trace.cpp:101-119, reduced as evaluate does, trigger.cpp:62-104) with one
+// pass over each sampled rank's records per tile of ticks: block (si, tile)
+// bins every record into the (few) windows of its tile that contain it,
+// accumulating in shared memory. Window k holds x iff !(x < t_k - delta) &&
+// !(x > t_k) (trace.cpp:107 with t0 = t_k - delta). Tiles of TT ticks keep
+// the bins in shared memory for any tick count: a segment is read once per
+// tile, not once per tick.
+__global__ void k_window_bins(StoreView s, const double* __restrict__ ticks_all,
+                              int32_t T_all, int32_t TT,
+                              const int32_t* __restrict__ sampled,
                               int32_t S, double delta,
-                              WinStat* __restrict__ out) {
+                              WinStat* __restrict__ out_all) {
+  const int32_t k0 = blockIdx.y * TT;
+  const int32_t T = min(TT, T_all - k0);
+  const double* ticks = ticks_all + k0;
+  WinStat* out = out_all + static_cast<int64_t>(k0) * S;
   extern __shared__ __align__(16) unsigned char wb_dyn[];
   double* st = reinterpret_cast<double*>(wb_dyn);                       // [T]
   unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
@@ -499,24 +457,13 @@ void trigger_window_stats(csg_store* s, const double* d_ticks, int32_t T,
                           WinStat* d_out) {
   if (T <= 0 || S <= 0) return;
   csg_ctx* c = s->ctx;
-  const size_t smem = static_cast<size_t>(T) * 44;
-  if (smem <= 200 * 1024) {
-    CSG_CUDA(cudaFuncSetAttribute(k_window_bins,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(200 * 1024)));
-    ProfScope ps_(c->lc, "k_window_bins", c->stream);
-    k_window_bins<<<S, 512, smem, c->stream>>>(s->view(), d_ticks, T, d_sampled, S,
-                                               delta, d_out);
-    CSG_CUDA(cudaGetLastError());
-    return;
-  }
-  const uint64_t warps = static_cast<uint64_t>(T) * S;
-  {
-    ProfScope ps_(c->lc, "k_window_stats", c->stream);
-    k_window_stats<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
-                     c->stream>>>(s->view(), d_ticks, T, d_sampled, S, delta,
-                                  d_out);
-  }
+  constexpr int32_t kTileTicks = 4096;  // 44 B of bins per tick: 176 KB
+  const int32_t TT = std::min(T, kTileTicks);
+  const size_t smem = static_cast<size_t>(TT) * 44;
+  smem_optin(k_window_bins, smem);
+  ProfScope ps_(c->lc, "k_window_bins", c->stream);
+  k_window_bins<<<dim3(S, (T + TT - 1) / TT), 512, smem, c->stream>>>(
+      s->view(), d_ticks, T, TT, d_sampled, S, delta, d_out);
   CSG_CUDA(cudaGetLastError());
 }
 
@@ -571,14 +518,8 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     // about 512 records per block of a sampled rank's (average) segment
     const uint64_t avg = s->R > 0 ? s->n / static_cast<uint64_t>(s->R) : 0;
     const int32_t B = static_cast<int32_t>(std::min<uint64_t>(64, std::max<uint64_t>(1, avg / 512)));
-    static bool attr = false;
-    if (!attr) {
-      CSG_CUDA(cudaFuncSetAttribute(k_trigger, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      CSG_CUDA(cudaFuncSetAttribute(k_trigger_ema, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      attr = true;
-    }
+    smem_optin(k_trigger, 200 * 1024);
+    smem_optin(k_trigger_ema, 200 * 1024);
     const bool sharded = comm_active(c);
     {
       ProfScope ps_(c->lc, "k_trigger", c->stream);
@@ -655,28 +596,47 @@ void trigger_evaluate_single(csg_store* s, const int32_t* sampled, int32_t S,
     mx = std::max(mx, sampled[i]);
   }
   state->ensure(mx + 1);
-  DevBuf d_s, d_t, ws, ev, tr;
-  d_s.ensure(S * 4);
-  d_t.ensure(8);
-  ws.ensure(S * sizeof(WinStat));
-  ev.ensure(sizeof(csg_trigger_event));
-  tr.ensure(4);
-  CSG_CUDA(cudaMemcpyAsync(d_s.p, sampled, S * 4, cudaMemcpyHostToDevice, c->stream));
-  CSG_CUDA(cudaMemcpyAsync(d_t.p, &t, 8, cudaMemcpyHostToDevice, c->stream));
-  trigger_window_stats(s, d_t.as<double>(), 1, d_s.as<int32_t>(), S, p.delta,
-                       ws.as<WinStat>());
+  // scratch reused across ticks (csg_evaluate is the per-tick API): the
+  // sampled list and tick time travel in one upload, the trip flag and the
+  // event come back in one mapped-memory round trip
+  DevBuf& in = c->buf("eval.in");
+  DevBuf& ws = c->buf("eval.ws");
+  DevBuf& out = c->buf("eval.out");
+  const size_t in_bytes = 8 + static_cast<size_t>(S) * 4;
+  in.ensure(in_bytes);
+  HostBuf& hin = c->hbuf("eval.in");
+  hin.ensure(in_bytes);
+  std::memcpy(hin.p, &t, 8);
+  std::memcpy(hin.as<unsigned char>() + 8, sampled, static_cast<size_t>(S) * 4);
+  CSG_CUDA(cudaMemcpyAsync(in.p, hin.p, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  ws.ensure(static_cast<size_t>(S) * sizeof(WinStat));
+  out.ensure(16 + sizeof(csg_trigger_event));
+  const double* d_t = in.as<double>();
+  const int32_t* d_s = reinterpret_cast<const int32_t*>(in.as<unsigned char>() + 8);
+  int32_t* d_tr = out.as<int32_t>();
+  csg_trigger_event* d_ev = reinterpret_cast<csg_trigger_event*>(out.as<unsigned char>() + 16);
+  trigger_window_stats(s, d_t, 1, d_s, S, p.delta, ws.as<WinStat>());
+  if (comm_active(c)) {
+    // a sampled rank lives on one shard; the others contribute empty
+    // (all-zero) windows, so a SUM all-reduce yields the owner's window and
+    // every rank evaluates (and persists) the same baselines
+    comm_group_start(c);
+    comm_allreduce(c, ws.p, static_cast<size_t>(S) * sizeof(WinStat) / 8, ncclUint64,
+                   ncclSum);
+    comm_group_end(c);
+  }
   {
     ProfScope ps_(c->lc, "k_ema_single", c->stream);
-    k_ema_single<<<1, 32, 0, c->stream>>>(ws.as<WinStat>(), d_s.as<int32_t>(), S, p,
-                                          t, state->slots.as<TrigSlot>(),
-                                          ev.as<csg_trigger_event>(),
-                                          tr.as<int32_t>());
+    k_ema_single<<<1, 32, 0, c->stream>>>(ws.as<WinStat>(), d_s, S, p, t,
+                                          state->slots.as<TrigSlot>(), d_ev, d_tr);
   }
-  CSG_CUDA(cudaMemcpyAsync(tripped, tr.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  CSG_CUDA(cudaMemcpyAsync(event, ev.p, sizeof(*event), cudaMemcpyDeviceToHost,
-                           c->stream));
-  ctx_sync(c);
-  CSG_CUDA(cudaGetLastError());
+  HostBuf& hb = c->hbuf("eval.out");
+  hb.ensure(16 + sizeof(csg_trigger_event));
+  FetchArgs fa{};
+  fa.add(out.p, hb.p, 16 + sizeof(csg_trigger_event));
+  ctx_sync(c, &fa);
+  std::memcpy(tripped, hb.p, 4);
+  std::memcpy(event, hb.as<unsigned char>() + 16, sizeof(*event));
 }
 
 }  // namespace csg

@@ -225,3 +225,29 @@ def test_results_jsonl_bytes(eng, name):
     res, _ = eng.run_detection_results(eng.TraceStore(records=recs), eng.Model(topo, prog),
                                        tcfg, acfg, seed)
     assert res.jsonl(scen) == reports
+
+
+LONG_TICKS = json.load(open(os.path.join(GOLDEN, "long_ticks.json"))) \
+    if os.path.exists(os.path.join(GOLDEN, "long_ticks.json")) else {}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(LONG_TICKS))
+def test_long_tick_runs_match_reference(eng, case):
+    """More ticks than the one-launch trigger holds (> 4266): the tiled
+    window-statistics path (tests/golden/make_long_ticks.py)."""
+    from tests.golden.make_golden import fnv1a64
+    from tests.golden.make_long_ticks import config, full_hash
+    want = LONG_TICKS[case]
+    recs = codec.load_file(os.path.join(GOLDEN, f"catalog_{want['trace']}.rec.xz"))
+    scen = eng.Scenario.parse(config(want["trace"], want["detect_interval_ms"]))
+    topo, prog = scen.layout()
+    tcfg, acfg, seed = scen.configs()
+    got, sampled = eng.run_detection(eng.TraceStore(records=recs), eng.Model(topo, prog),
+                                     tcfg, acfg, seed)
+    assert sampled == want["sampled"]
+    trig = [[r["kind"], r["suspect_rank"], r["time_ms"]] for r in got]
+    assert trig == want["triggers"], first_diff(trig, want["triggers"])
+    assert full_hash(got) == want["full_fnv1a64"]
+    res = eng.run_analyze_packed(scen, recs)
+    assert fnv1a64(res.reports_jsonl.encode()) == want["reports_fnv1a64"]
