@@ -347,6 +347,8 @@ def run_ours(args):
                "triggers": int(res.trigger_count),
                "note": "collsight_b200_run_analyze_packed: H2D of the packed store, "
                        "device index + trigger + RCA, D2H of reports, JSONL rendering"}
+        if WORKLOAD not in FIXED_JOB and not args.no_jsonl:
+            e2e["jsonl"] = jsonl_e2e(E, scen, recs, res.reports_jsonl, args.steps)
 
     cpu = None
     # C4: no CPU reference is feasible (80 GB of AoS records)
@@ -388,6 +390,47 @@ def run_ours(args):
         emit(out)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def jsonl_e2e(E, scen, recs, want_reports, steps):
+    """The reference's own entry point on a trace FILE: collsight_run_analyze
+    (scenario, path) — the JSONL text streamed to HBM and parsed on the device
+    (csrc/jsonl.cu), then the same detection replay and report rendering.
+    The file is the packed store serialized in the reference's format
+    (page-cache warm: the first call reads it untimed). The host-parser arm
+    (CSG_JSONL_HOST=1: multithreaded CPU parse + packed H2D) is timed once for
+    comparison."""
+    rpn = json.load(open(CONFIG))["layout"]["ranks_per_node"]
+    path = f"/tmp/collsight_{WORKLOAD}_{len(recs)}.jsonl"
+    if not os.path.exists(path):
+        E.write_trace(recs, path + ".tmp", rpn)
+        os.replace(path + ".tmp", path)
+    size = os.path.getsize(path)
+    res = E.run_analyze(scen, path)  # warm: page cache, staging, allocations
+    assert res.reports_jsonl == want_reports, "JSONL replay differs from the packed replay"
+    times = []
+    for _ in range(max(1, min(steps, 5))):
+        t0 = time.perf_counter()
+        res = E.run_analyze(scen, path)
+        times.append(time.perf_counter() - t0)
+    os.environ["CSG_JSONL_HOST"] = "1"
+    try:
+        t0 = time.perf_counter()
+        res_h = E.run_analyze(scen, path)
+        host_s = time.perf_counter() - t0
+    finally:
+        del os.environ["CSG_JSONL_HOST"]
+    assert res_h.reports_jsonl == want_reports
+    t = float(np.mean(times))
+    return {"value": len(recs) / t, "unit": UNIT, "ms_per_step": t * 1e3,
+            "file_bytes": size, "h2d_bytes_per_step": size,
+            "text_GBps": size / t / 1e9,
+            "host_parser_value": len(recs) / host_s, "host_parser_ms": host_s * 1e3,
+            "host_cores": os.cpu_count(),
+            "note": "collsight_run_analyze(scenario, trace.jsonl): file -> pinned "
+                    "staging -> HBM, device JSONL parse (k_jsonl_count/scan/parse), "
+                    "detection + RCA, JSONL reports; host_parser_* = the same call "
+                    "with the multithreaded CPU parser (CSG_JSONL_HOST=1)"}
 
 
 def _capped_windows(store, cfg_text, ticks, cap_s):
@@ -559,6 +602,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-jsonl", action="store_true",
+                    help="skip the JSONL-file e2e measurement")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     select_workload(args.workload)

@@ -61,6 +61,17 @@ collsight_status collsight_b200_layout_json(int tp, int pp, int dp,
 collsight_status collsight_b200_parse_trace(const char* text, size_t len,
                                             csg_packed_record** out,
                                             size_t* n);
+/* packed records -> JSONL in the reference's serialize_records format
+ * (proj/src/trace.cpp:189-322), multithreaded; the dropped fields are written
+ * as node = rank / ranks_per_node, stuck_ms = 0, total_chunks = gpu_ready, so
+ * the text parses back to the same records. Caller frees *text with
+ * collsight_b200_free; *len excludes the terminating NUL. */
+collsight_status collsight_b200_serialize_trace(const csg_packed_record* records,
+                                                size_t n, int32_t ranks_per_node,
+                                                char** text, size_t* len);
+/* The same text written to a file (a JSONL trace for collsight_run_analyze). */
+collsight_status collsight_b200_write_trace(const csg_packed_record* records, size_t n,
+                                            int32_t ranks_per_node, const char* path);
 void collsight_b200_free(void* p);
 
 /* The engine context the collsight_* calls run on (created on first use on

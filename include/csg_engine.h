@@ -251,6 +251,27 @@ csg_status csg_store_append(csg_store* store, const csg_packed_record* host,
                             size_t n);
 csg_status csg_store_append_device(csg_store* store,
                                    const csg_packed_record* device, size_t n);
+/* JSONL trace text -> records, parsed on the device (the reference's
+ * load_trace_file / parse_trace_text, proj/src/trace.cpp:241-346: one record
+ * per non-empty line, in line order). The text streams through pinned
+ * staging into HBM and is parsed there. *accepted = 1: the records were
+ * appended. *accepted = 0 (status still CSG_OK): some line is outside what
+ * the device parser vouches for — invalid input, JSON escapes, unknown or
+ * duplicate fields, more than 19 significant digits (see csrc/jsonl.cuh) —
+ * or the file cannot be read; the store is unchanged and the caller parses
+ * the text with the exact host parser, which raises the reference's error
+ * (TraceParseError with its line number) or accepts the trace. */
+csg_status csg_store_append_jsonl(csg_store* store, const char* text, size_t len,
+                                  int* accepted);
+csg_status csg_store_append_jsonl_file(csg_store* store, const char* path,
+                                       int* accepted);
+/* Known-answer hooks: the host instantiation of the device line parser and
+ * of its decimal -> binary64 conversion (1 = accepted, 0 = left to the exact
+ * parser). */
+int csg_jsonl_parse_line(const char* line, size_t len, csg_packed_record* out);
+int csg_jsonl_parse_double(const char* tok, size_t len, double* out);
+/* Copies the store's first n packed records back to host memory. */
+csg_status csg_store_records(const csg_store* store, csg_packed_record* host, size_t n);
 csg_status csg_store_clear(csg_store* store);
 size_t csg_store_size(const csg_store* store);
 /* Builds the device indices now (otherwise built lazily on first use). */

@@ -480,6 +480,19 @@ csg_status csg_store_append_jsonl_file(csg_store* s, const char* path, int* acce
   });
 }
 
+csg_status csg_store_records(const csg_store* s, csg_packed_record* host, size_t n) {
+  if (!s || (!host && n)) return fail(CSG_ERR_ARG, "null argument");
+  return guarded([&] {
+    if (n > s->n) throw Error(CSG_ERR_ARG, "csg_store_records: n exceeds the store size");
+    CSG_CUDA(cudaSetDevice(s->ctx->device));
+    if (n)
+      CSG_CUDA(cudaMemcpyAsync(host, s->recs.p, n * sizeof(csg_packed_record),
+                               cudaMemcpyDeviceToHost, s->ctx->stream));
+    CSG_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    return CSG_OK;
+  });
+}
+
 csg_status csg_store_clear(csg_store* s) {
   if (!s) return fail(CSG_ERR_ARG, "null argument");
   s->n = 0;

@@ -23,10 +23,26 @@ struct collsight_scenario {
 };
 
 struct collsight_result {
-  std::string text;
   std::string summary_json;
   std::string reports_jsonl;
   uint64_t triggers = 0;
+  // reports_to_text (+ the run summary) is rendered on the first
+  // collsight_result_text call, from the reports kept here: the same bytes
+  // as the reference's eager rendering, not paid by callers that only read
+  // the JSONL reports
+  csh::Scenario cfg;
+  csg_results* res = nullptr;
+  std::once_flag text_once;
+  std::string text;
+  ~collsight_result() { csg_results_free(res); }
+  const std::string& text_view() {
+    std::call_once(text_once, [&] {
+      std::vector<csg_report_view> views(res ? csg_results_count(res) : 0);
+      for (size_t i = 0; i < views.size(); ++i) csg_results_get(res, i, &views[i]);
+      text = csh::reports_to_text(views, cfg) + csh::analyze_summary_text();
+    });
+    return text;
+  }
 };
 
 namespace {
@@ -83,11 +99,50 @@ struct Results {
   ~Results() { csg_results_free(res); }
 };
 
-collsight_result* analyze_records(const csh::Scenario& cfg,
-                                  const csg_packed_record* recs, size_t n,
+// Fills the (cleared) device store: packed records, or a JSONL trace file
+// parsed on the device (falling back to the exact host parser, which raises
+// the reference's TraceParseError, when the device parser defers).
+struct StoreInput {
+  const csg_packed_record* recs = nullptr;
+  size_t n = 0;
+  const char* jsonl_path = nullptr;
+};
+
+void fill_store(csg_store* store, const StoreInput& in) {
+  if (!in.jsonl_path) {
+    check(csg_store_append(store, in.recs, in.n));
+    return;
+  }
+  const bool host_only = std::getenv("CSG_JSONL_HOST") != nullptr;  // A/B switch
+  int accepted = 0;
+  if (!host_only) check(csg_store_append_jsonl_file(store, in.jsonl_path, &accepted));
+  if (accepted) return;
+  const std::vector<csg_packed_record> recs = csh::load_trace_file(in.jsonl_path);
+  check(csg_store_clear(store));
+  check(csg_store_append(store, recs.data(), recs.size()));
+}
+
+collsight_result* analyze_records(const csh::Scenario& cfg, const StoreInput& in,
                                   const char* report_out_path) {
   std::lock_guard<std::mutex> lk(g_mu);
-  csg_ctx* ctx = engine();
+  csg_ctx* ctx = nullptr;
+  try {
+    ctx = engine();
+  } catch (...) {
+    // no usable device: a bad trace is still reported first, as the
+    // reference's load_trace_file would
+    if (in.jsonl_path) (void)csh::load_trace_file(in.jsonl_path);
+    throw;
+  }
+  // CSG_E2E_PROF=1: wall time of each phase on stderr
+  static const bool prof = std::getenv("CSG_E2E_PROF") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  // the trace first (load_trace_file precedes the layout in the reference's
+  // run_analyze path, so a bad trace is reported before a bad layout)
+  if (!g_store) check(csg_store_create(ctx, &g_store));
+  check(csg_store_clear(g_store));
+  fill_store(g_store, in);
   const std::string key = std::to_string(cfg.tp) + "," + std::to_string(cfg.pp) +
                           "," + std::to_string(cfg.dp) + "," +
                           std::to_string(cfg.ranks_per_node) + "," +
@@ -103,13 +158,6 @@ collsight_result* analyze_records(const csh::Scenario& cfg,
     check(csg_model_create(ctx, &tables.topo, &tables.prog, &g_model));
     g_model_key = key;
   }
-  // CSG_E2E_PROF=1: wall time of each phase on stderr
-  static const bool prof = std::getenv("CSG_E2E_PROF") != nullptr;
-  using clk = std::chrono::steady_clock;
-  const auto t0 = clk::now();
-  if (!g_store) check(csg_store_create(ctx, &g_store));
-  check(csg_store_clear(g_store));
-  check(csg_store_append(g_store, recs, n));
   if (prof) cudaDeviceSynchronize();
   const auto t1 = clk::now();
   Results e;
@@ -121,7 +169,9 @@ collsight_result* analyze_records(const csh::Scenario& cfg,
   auto out = std::make_unique<collsight_result>();
   out->reports_jsonl = csh::reports_to_jsonl(views, cfg);
   const auto t3 = clk::now();
-  out->text = csh::reports_to_text(views, cfg) + csh::analyze_summary_text();
+  out->cfg = cfg;
+  out->res = e.res;  // the result handle owns the reports from here on
+  e.res = nullptr;
   out->summary_json = csh::analyze_summary_json(views.size());
   out->triggers = views.size();
   if (report_out_path) csh::write_file(report_out_path, out->reports_jsonl);
@@ -131,7 +181,7 @@ collsight_result* analyze_records(const csh::Scenario& cfg,
       return std::chrono::duration<double, std::milli>(b - a).count();
     };
     std::fprintf(stderr,
-                 "[e2e] append %.3f ms, run_detection %.3f ms, jsonl %.3f ms, text+file "
+                 "[e2e] append %.3f ms, run_detection %.3f ms, jsonl %.3f ms, summary+file "
                  "%.3f ms (%zu reports, %zu jsonl bytes)\n",
                  ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), views.size(),
                  out->reports_jsonl.size());
@@ -207,14 +257,15 @@ collsight_status collsight_run_analyze(const collsight_scenario* s,
   if (!s || !trace_in_path || !out)
     return fail(COLLSIGHT_ERR_ARG, "null argument");
   return guarded([&] {
-    const std::vector<csg_packed_record> recs = csh::load_trace_file(trace_in_path);
-    *out = analyze_records(s->cfg, recs.data(), recs.size(), report_out_path);
+    StoreInput in;
+    in.jsonl_path = trace_in_path;
+    *out = analyze_records(s->cfg, in, report_out_path);
     return COLLSIGHT_OK;
   });
 }
 
 const char* collsight_result_text(const collsight_result* r) {
-  return r ? r->text.c_str() : "";
+  return r ? const_cast<collsight_result*>(r)->text_view().c_str() : "";
 }
 const char* collsight_result_summary_json(const collsight_result* r) {
   return r ? r->summary_json.c_str() : "";
@@ -232,7 +283,10 @@ collsight_status collsight_b200_run_analyze_packed(
     const char* report_out_path, collsight_result** out) {
   if (!s || (!records && n) || !out) return fail(COLLSIGHT_ERR_ARG, "null argument");
   return guarded([&] {
-    *out = analyze_records(s->cfg, records, n, report_out_path);
+    StoreInput in;
+    in.recs = records;
+    in.n = n;
+    *out = analyze_records(s->cfg, in, report_out_path);
     return COLLSIGHT_OK;
   });
 }
@@ -291,6 +345,27 @@ collsight_status collsight_b200_parse_trace(const char* text, size_t len,
     *out = static_cast<csg_packed_record*>(
         std::malloc(sizeof(csg_packed_record) * (v.size() + 1)));
     if (!v.empty()) std::memcpy(*out, v.data(), v.size() * sizeof(csg_packed_record));
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_serialize_trace(const csg_packed_record* records,
+                                                size_t n, int32_t ranks_per_node,
+                                                char** text, size_t* len) {
+  if ((!records && n) || !text || !len) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const std::string s = csh::serialize_packed(records, n, ranks_per_node);
+    *text = dup(s);
+    *len = s.size();
+    return COLLSIGHT_OK;
+  });
+}
+
+collsight_status collsight_b200_write_trace(const csg_packed_record* records, size_t n,
+                                            int32_t ranks_per_node, const char* path) {
+  if ((!records && n) || !path) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    csh::write_file(path, csh::serialize_packed(records, n, ranks_per_node));
     return COLLSIGHT_OK;
   });
 }

@@ -98,6 +98,8 @@ std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target,
 bool fast_parse_trace(std::string_view text, std::vector<csg_packed_record>& out);
 std::vector<csg_packed_record> parse_trace_text(std::string_view text);
 std::vector<csg_packed_record> load_trace_file(const std::string& path);
+// packed records -> reference-format JSONL (serialize.cpp)
+std::string serialize_packed(const csg_packed_record* recs, size_t n, int32_t ranks_per_node);
 
 // Report rendering over engine results.
 struct Outcome {

@@ -178,6 +178,28 @@ class TraceStore:
         r = np.ascontiguousarray(np.atleast_1d(records), dtype=_abi.RECORD_DTYPE)
         _check(lib().csg_store_append(self.h, _abi.ptr(r), C.c_size_t(len(r))))
 
+    def append_jsonl(self, text) -> bool:
+        """JSONL trace text parsed on the device (csg_store_append_jsonl).
+        False: the device parser deferred (store unchanged) — parse with
+        parse_trace() (the exact host parser) instead."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        acc = C.c_int()
+        _check(lib().csg_store_append_jsonl(self.h, b, C.c_size_t(len(b)), C.byref(acc)))
+        return bool(acc.value)
+
+    def append_jsonl_file(self, path: str) -> bool:
+        acc = C.c_int()
+        _check(lib().csg_store_append_jsonl_file(self.h, path.encode(), C.byref(acc)))
+        return bool(acc.value)
+
+    def records(self) -> np.ndarray:
+        """The store's packed records in store order (device -> host copy)."""
+        n = self.size()
+        out = np.zeros(n, dtype=_abi.RECORD_DTYPE)
+        if n:
+            _check(lib().csg_store_records(self.h, _abi.ptr(out), C.c_size_t(n)))
+        return out
+
     def append_device(self, ptr: int, n: int):
         _check(lib().csg_store_append_device(self.h, C.c_void_p(ptr), C.c_size_t(n)))
 
@@ -551,6 +573,43 @@ def run_analyze_packed(scenario: Scenario, records: np.ndarray,
         scenario.h, _abi.ptr(r), C.c_size_t(len(r)),
         report_path.encode() if report_path else None, C.byref(h)))
     return _take_run(h)
+
+
+def jsonl_parse_line(line) -> Optional[np.ndarray]:
+    """Host instantiation of the device line parser: the record, or None
+    when it defers to the exact parser."""
+    b = line.encode() if isinstance(line, str) else bytes(line)
+    out = np.zeros(1, dtype=_abi.RECORD_DTYPE)
+    ok = lib().csg_jsonl_parse_line(b, C.c_size_t(len(b)), _abi.ptr(out))
+    return out if ok else None
+
+
+def jsonl_parse_double(tok) -> Optional[float]:
+    b = tok.encode() if isinstance(tok, str) else bytes(tok)
+    d = C.c_double()
+    ok = lib().csg_jsonl_parse_double(b, C.c_size_t(len(b)), C.byref(d))
+    return d.value if ok else None
+
+
+def serialize_records(records: np.ndarray, ranks_per_node: int = 8) -> str:
+    """Packed records -> reference-format JSONL (collsight_b200_serialize_trace)."""
+    r = np.ascontiguousarray(records, dtype=_abi.RECORD_DTYPE)
+    out = C.c_void_p()
+    n = C.c_size_t()
+    _ccheck(lib().collsight_b200_serialize_trace(_abi.ptr(r), C.c_size_t(len(r)),
+                                                 C.c_int32(ranks_per_node), C.byref(out),
+                                                 C.byref(n)))
+    try:
+        return C.string_at(out.value, n.value).decode()
+    finally:
+        lib().collsight_b200_free(out)
+
+
+def write_trace(records: np.ndarray, path: str, ranks_per_node: int = 8) -> None:
+    """Packed records -> a reference-format JSONL trace file."""
+    r = np.ascontiguousarray(records, dtype=_abi.RECORD_DTYPE)
+    _ccheck(lib().collsight_b200_write_trace(_abi.ptr(r), C.c_size_t(len(r)),
+                                             C.c_int32(ranks_per_node), path.encode()))
 
 
 def parse_trace(text: str) -> np.ndarray:
