@@ -93,6 +93,7 @@ struct csg_store {
   // layout of the last fused index build: the next build launches its
   // scatter on it before the statistics reach the host (store_build_index)
   bool spec_ok = false;
+  bool spec_general = false;  // last build took the general path (stats + keys first)
   int32_t sp_lmin = 0, sp_lmax = -1, sp_R = 0;
   csg::DevBuf rank_off, perm, keys, ko;
   csg::DevBuf runmax;  // chunked prefix max of ts (StoreView::cmax)

@@ -499,6 +499,78 @@ __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
   }
 }
 
+// Incremental form for trips in time order: the prefix of straggler trip js
+// (records before the first ts > t_js) contains the prefix of trip js - 1,
+// so each record is folded into the table of the first trip whose prefix
+// holds it (one pass over the store instead of one per trip), and
+// k_iter_prefix then combines the tables over the trips (running min/max
+// per (slot, iteration) cell).
+__global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
+                                  const int32_t* __restrict__ strag_trip,
+                                  const RankSum* __restrict__ rs, int64_t it_min,
+                                  int32_t n_it, uint32_t M,
+                                  unsigned long long* __restrict__ tbl_s,
+                                  unsigned long long* __restrict__ tbl_e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= s.R || w >= m.rank_space) return;
+  const int32_t r = static_cast<int32_t>(w);
+  const uint32_t g0 = m.rg_off[r], g1 = m.rg_off[r + 1];
+  if (g0 == g1) return;
+  const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  // the rank's (group, slot) pairs in registers (a rank sits in <= 3 groups)
+  int32_t gq[4];
+  uint32_t sq[4];
+  const int ng = min(static_cast<int>(g1 - g0), 4);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    gq[q] = q < ng ? m.rg_group[g0 + q] : INT_MIN;
+    sq[q] = q < ng ? m.rg_slot[g0 + q] : kNoPos;
+  }
+  const bool many = g1 - g0 > 4;
+  uint32_t done = b;
+  for (int32_t js = 0; js < Js && done < e; ++js) {
+    const int32_t j = strag_trip[js];
+    const uint32_t cend = min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, e);
+    for (uint32_t p = done + lane; p < cend; p += 32) {
+      if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
+      const int32_t cm = s.comm[p];
+      uint32_t slot = kNoPos;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (slot == kNoPos && gq[q] == cm) slot = sq[q];
+      if (slot == kNoPos && many)
+        for (uint32_t q = g0 + 4; q < g1; ++q)
+          if (m.rg_group[q] == cm) {
+            slot = m.rg_slot[q];
+            break;
+          }
+      if (slot == kNoPos) continue;
+      const int64_t it = iter_of(s.op[p], m.opn) - it_min;
+      const uint64_t idx = (static_cast<uint64_t>(js) * M + slot) * n_it + it;
+      atomicMin(&tbl_s[idx], static_cast<unsigned long long>(dkey(as_double(s.pa[p]))));
+      atomicMax(&tbl_e[idx], static_cast<unsigned long long>(dkey(s.ts[p])));
+    }
+    done = max(done, cend);
+  }
+}
+
+__global__ void k_iter_prefix(int32_t Js, uint64_t cells,
+                              unsigned long long* __restrict__ tbl_s,
+                              unsigned long long* __restrict__ tbl_e) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cells;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long a = tbl_s[c], z = tbl_e[c];
+    for (int32_t js = 1; js < Js; ++js) {
+      const uint64_t i = static_cast<uint64_t>(js) * cells + c;
+      a = min(a, tbl_s[i]);
+      z = max(z, tbl_e[i]);
+      tbl_s[i] = a;
+      tbl_e[i] = z;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3: complete_iterations (rca.cpp:352-372) + group_has_late_member
 // (rca.cpp:374-396), one warp per (straggler trip, group).
@@ -674,21 +746,19 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
 // an affected group with enough history): the first op (ascending) with a
 // skewed window flow, and the first op with an incomplete window flow.
 // ---------------------------------------------------------------------------
-__global__ void k_flow(StoreView s, ModelView m, int32_t Js,
-                       const int32_t* __restrict__ strag_trip,
-                       const double* __restrict__ trip_t, double delta_a,
-                       double skew, int32_t k, uint32_t M,
-                       const uint32_t* __restrict__ slot_group,
-                       const RankSum* __restrict__ rs,
-                       const GroupIter* __restrict__ gi,
-                       const uint8_t* __restrict__ aff_flag,
-                       FlowSum* __restrict__ fs, uint32_t* __restrict__ err) {
-  constexpr int kWarps = 4;
-  __shared__ uint32_t buf[kWarps][kFlowBuf];
-  __shared__ uint32_t sbits[kWarps][kChTbl / 32];
-  __shared__ uint32_t cbits[kWarps][kChTbl / 32];
+constexpr int kFlowWarps = 4;
+__device__ void flow_scan_one(int64_t w, StoreView s, ModelView m, int32_t Js,
+                              const int32_t* __restrict__ strag_trip,
+                              const double* __restrict__ trip_t, double delta_a,
+                              double skew, int32_t k, uint32_t M,
+                              const uint32_t* __restrict__ slot_group,
+                              const RankSum* __restrict__ rs,
+                              const GroupIter* __restrict__ gi,
+                              const uint8_t* __restrict__ aff_flag,
+                              FlowSum* __restrict__ fs, uint32_t* __restrict__ err,
+                              uint32_t (*buf)[kFlowBuf], uint32_t (*sbits)[kChTbl / 32],
+                              uint32_t (*cbits)[kChTbl / 32]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= static_cast<int64_t>(M) * Js) return;
   const int32_t js = static_cast<int32_t>(w / M);
   const uint32_t slot = static_cast<uint32_t>(w % M);
@@ -841,6 +911,239 @@ __global__ void k_flow(StoreView s, ModelView m, int32_t Js,
   if (lane == 0) fs[static_cast<uint64_t>(js) * M + slot] = out;
 }
 
+// k_flow: one warp per (straggler trip, membership slot), or per listed
+// (trip, slot) item (the members k_flow_fi could not stage)
+__global__ void __launch_bounds__(kFlowWarps * 32)
+    k_flow(StoreView s, ModelView m, int32_t Js, const int32_t* __restrict__ strag_trip,
+           const double* __restrict__ trip_t, double delta_a, double skew, int32_t k,
+           uint32_t M, const uint32_t* __restrict__ slot_group,
+           const RankSum* __restrict__ rs, const GroupIter* __restrict__ gi,
+           const uint8_t* __restrict__ aff_flag, FlowSum* __restrict__ fs,
+           uint32_t* __restrict__ err, const uint32_t* __restrict__ only,
+           const unsigned* __restrict__ n_only) {
+  __shared__ uint32_t buf[kFlowWarps][kFlowBuf];
+  __shared__ uint32_t sbits[kFlowWarps][kChTbl / 32];
+  __shared__ uint32_t cbits[kFlowWarps][kChTbl / 32];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (!only) {
+    flow_scan_one(gw, s, m, Js, strag_trip, trip_t, delta_a, skew, k, M, slot_group, rs, gi,
+                  aff_flag, fs, err, buf, sbits, cbits);
+    return;
+  }
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = gw; i < static_cast<int64_t>(*n_only); i += nw)
+    flow_scan_one(only[i], s, m, Js, strag_trip, trip_t, delta_a, skew, k, M, slot_group, rs,
+                  gi, aff_flag, fs, err, buf, sbits, cbits);
+}
+
+// k_flow over the flow index: the member's window records of the group are
+// staged once in shared memory in (op, store order) order — the segment's
+// own order when its op_seq never descends, else the flow index's — and
+// both rules walk the staged op runs: (a) per op the lower median of the
+// window completions' durations and the first (store order) one above
+// skew x median; (b) per window state op the state channels and, by a range
+// lookup in the flow index, the op's prefix completions of the group
+// ("completed_channels" covers the whole prefix, not just the window). A
+// member whose window exceeds the staging area takes k_flow's scans.
+constexpr int kFlowStage = 256;
+constexpr int kFlow2Warps = 4;
+__global__ void __launch_bounds__(kFlow2Warps * 32)
+    k_flow_fi(StoreView s, FlowView fv, ModelView m, int32_t Js,
+              const int32_t* __restrict__ strag_trip, const double* __restrict__ trip_t,
+              double delta_a, double skew, int32_t k, uint32_t M,
+              const uint32_t* __restrict__ slot_group, const RankSum* __restrict__ rs,
+              const GroupIter* __restrict__ gi, const uint8_t* __restrict__ aff_flag,
+              FlowSum* __restrict__ fs, uint32_t* __restrict__ err,
+              uint32_t* __restrict__ spill, unsigned* __restrict__ n_spill) {
+  __shared__ uint32_t sp[kFlow2Warps][kFlowStage];   // staged rank-major positions
+  __shared__ uint32_t sbits[kFlow2Warps][kChTbl / 32];
+  __shared__ uint32_t cbits[kFlow2Warps][kChTbl / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(M) * Js) return;
+  const int32_t js = static_cast<int32_t>(w / M);
+  const uint32_t slot = static_cast<uint32_t>(w % M);
+  const int32_t g = static_cast<int32_t>(slot_group[slot]);
+  const int32_t j = strag_trip[js];
+  FlowSum out;
+  memset(&out, 0, sizeof(out));
+  const uint64_t gidx = static_cast<uint64_t>(js) * m.n_groups + g;
+  const bool run = aff_flag[static_cast<uint64_t>(j) * m.n_groups + g] &&
+                   m.member_off[g + 1] - m.member_off[g] >= 2 &&
+                   gi[gidx].n_common >= k && m.member_slot[slot] == slot;
+  const int32_t r = m.members[slot];
+  if (!run || r < 0 || r >= s.R) {
+    if (lane == 0) fs[static_cast<uint64_t>(js) * M + slot] = out;
+    return;
+  }
+  const double t = trip_t[j];
+  const double ws = t - delta_a;
+  const uint32_t b = s.rank_off[r], se = s.rank_off[r + 1];
+  const uint32_t e = min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, se);
+  const uint32_t p0 = min(seg_first(s, r, ws, false), e);
+  const bool uns = fv.unsorted[r] != 0;
+  auto win_rec = [&](uint32_t p) -> int {  // 1 completion, 2 state, 0 neither
+    if (s.comm[p] != g || s.ts[p] < ws) return 0;
+    const uint8_t ko = s.ko[p];
+    if (ko_kind(ko) == CSG_KIND_COMPLETION) return ko_opname(ko) != CSG_OP_RECV ? 1 : 0;
+    const uint64_t pi = static_cast<uint64_t>(s.op[p]) % static_cast<uint64_t>(m.opn);
+    return m.op_name[pi] != CSG_OP_RECV ? 2 : 0;
+  };
+  // stage the window records in (op, store order) order
+  int n = 0;
+  if (!uns) {
+    for (uint32_t base = p0; base < e; base += 32) {
+      const uint32_t p = base + lane;
+      const bool ok = p < e && win_rec(p) != 0;
+      const unsigned mm = __ballot_sync(FULL, ok);
+      const int at = n + __popc(mm & ((1u << lane) - 1u));
+      if (ok && at < kFlowStage) sp[wib][at] = p;
+      n += __popc(mm);
+    }
+  } else {
+    // unsorted segment: the window's op range in flow order, filtered to
+    // prefix positions at or after p0 (positions before p0 are all < ws)
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (uint32_t p = p0 + lane; p < e; p += 32)
+      if (win_rec(p)) {
+        lo = min(lo, static_cast<long long>(s.op[p]));
+        hi = max(hi, static_cast<long long>(s.op[p]));
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+      hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if (lo <= hi) {
+      const uint32_t fo = warp_partition_point(b, se, [&](uint32_t i) {
+        return s.op[fv.at(true, i)] >= lo;
+      });
+      const uint32_t fe = warp_partition_point(fo, se, [&](uint32_t i) {
+        return s.op[fv.at(true, i)] > hi;
+      });
+      for (uint32_t base = fo; base < fe; base += 32) {
+        const uint32_t i = base + lane;
+        uint32_t p = 0;
+        bool ok = false;
+        if (i < fe) {
+          p = fv.at(true, i);
+          ok = p >= p0 && p < e && win_rec(p) != 0;
+        }
+        const unsigned mm = __ballot_sync(FULL, ok);
+        const int at = n + __popc(mm & ((1u << lane) - 1u));
+        if (ok && at < kFlowStage) sp[wib][at] = p;
+        n += __popc(mm);
+      }
+    }
+  }
+  __syncwarp();
+  if (n > kFlowStage) {  // the scan kernel's path for this member
+    if (lane == 0) {
+      const unsigned at = atomicAdd(n_spill, 1u);
+      spill[at] = static_cast<uint32_t>(w);
+    }
+    return;
+  }
+  const uint32_t* st = sp[wib];
+  auto dur = [&](uint32_t p) { return s.ts[p] - as_double(s.pa[p]); };
+  // (a) FlowSkewed: first op (ascending) with a skewed window flow
+  for (int q0 = 0; q0 < n;) {
+    const int64_t op = s.op[st[q0]];
+    int q1 = q0 + 1;
+    while (q1 < n && s.op[st[q1]] == op) ++q1;
+    // completions of this op, store order
+    int nc = 0;
+    for (int q = q0; q < q1; ++q) nc += s.ko[st[q]] & 1 ? 0 : 1;  // CSG_KIND_COMPLETION == 0
+    if (nc >= 2) {
+      auto cv = [&](int i) {  // i-th completion of the run
+        int c = -1;
+        for (int q = q0; q < q1; ++q)
+          if (!(s.ko[st[q]] & 1) && ++c == i) return dur(st[q]);
+        return 0.0;
+      };
+      const double med = warp_lower_median(nc, cv);
+      int hit = -1;
+      if (med > 0) {
+        const double lim = __dmul_rn(skew, med);
+        for (int base = 0; base < nc && hit < 0; base += 32) {
+          const int i = base + lane;
+          const unsigned mm = __ballot_sync(FULL, i < nc && cv(i) > lim);
+          if (mm) hit = base + __ffs(mm) - 1;
+        }
+      }
+      if (hit >= 0) {
+        int c = -1;
+        uint32_t p = 0;
+        for (int q = q0; q < q1; ++q)
+          if (!(s.ko[st[q]] & 1) && ++c == hit) p = st[q];
+        out.flags |= 1;
+        out.skew_op = op;
+        out.skew_chan = s.chan[p];
+        out.skew_start = as_double(s.pa[p]);
+        out.skew_end = s.ts[p];
+        break;
+      }
+    }
+    q0 = q1;
+  }
+  // (b) FlowIncomplete: first window state op (ascending) with a state
+  // channel left incomplete while another completed
+  const int words = (s.nch + 31) / 32;
+  for (int q0 = 0; q0 < n;) {
+    const int64_t op = s.op[st[q0]];
+    int q1 = q0 + 1;
+    while (q1 < n && s.op[st[q1]] == op) ++q1;
+    bool has_state = false;
+    for (int q = q0; q < q1 && !has_state; ++q) has_state = s.ko[st[q]] & 1;
+    if (has_state) {
+      for (int q = lane; q < words; q += 32) {
+        sbits[wib][q] = 0;
+        cbits[wib][q] = 0;
+      }
+      __syncwarp();
+      for (int q = q0 + lane; q < q1; q += 32)
+        if (s.ko[st[q]] & 1) {
+          const int32_t ch = s.chan[st[q]];
+          atomicOr(&sbits[wib][ch >> 5], 1u << (ch & 31));
+        }
+      // prefix completions of (r, op) in the group: the op's flow-index range
+      const uint32_t fo = warp_partition_point(b, se, [&](uint32_t i) {
+        return s.op[fv.at(uns, i)] >= op;
+      });
+      const uint32_t fe = warp_partition_point(fo, se, [&](uint32_t i) {
+        return s.op[fv.at(uns, i)] > op;
+      });
+      for (uint32_t i = fo + lane; i < fe; i += 32) {
+        const uint32_t p = fv.at(uns, i);
+        const uint8_t ko = s.ko[p];
+        if (p < e && ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV &&
+            s.comm[p] == g) {
+          const int32_t ch = s.chan[p];
+          atomicOr(&cbits[wib][ch >> 5], 1u << (ch & 31));
+        }
+      }
+      __syncwarp();
+      bool any = false;
+      int first = -1;
+      for (int q = 0; q < words; ++q) {
+        const uint32_t sb = sbits[wib][q], cb = cbits[wib][q];
+        any |= (sb & cb) != 0;
+        if (first < 0 && (sb & ~cb)) first = q * 32 + __ffs(sb & ~cb) - 1;
+      }
+      __syncwarp();
+      if (any && first >= 0) {
+        out.flags |= 2;
+        out.inc_op = op;
+        out.inc_chan = first;
+        break;
+      }
+    }
+    q0 = q1;
+  }
+  (void)err;
+  if (lane == 0) fs[static_cast<uint64_t>(js) * M + slot] = out;
+}
+
 // ---------------------------------------------------------------------------
 // K6: per-trip decision (one block per trip).
 // ---------------------------------------------------------------------------
@@ -864,6 +1167,7 @@ struct DecideArgs {
   unsigned long long* coh_key;  // ~0 = empty
   double* coh_val;
   unsigned* coh_state;          // 2 = value published
+  longlong2* coh_meta;          // claimed slot: {iteration, trip << 8 | op name}
   uint32_t coh_cap;
   StoreView s;
   ModelView m;
@@ -895,7 +1199,28 @@ struct DecideArgs {
   const uint8_t* op_nm;
   uint64_t n_opidx;
   int sharded;
-  int64_t min_op;
+  int64_t min_op, max_op;
+  // sorted self-evidence path (k_sf_prep / k_opsort / k_sf_fast): per op
+  // key (op - min_op) the op index segment [opoff[k], opoff[k+1]), its
+  // durations sorted ascending as ordered keys (sdur, same positions) and
+  // the segment's latest timestamp (opmax; NaN = not sorted)
+  FlowView f;
+  const uint32_t* opoff;
+  unsigned long long* sdur;
+  double* sts;     // timestamps of the sorted entries
+  int32_t* srank;  // ranks of the sorted entries
+  double* opmax;
+  struct SfPlan* plan;
+  int sf_fast;  // k_self_faulted takes only the candidates k_sf_fast deferred
+  // parallel straggler candidates (k_sl_*): per (straggler trip, membership
+  // slot) lateness | flow-candidate bits, per (straggler trip, affected
+  // group index) candidate / evidence counts, then offsets
+  uint32_t* emit_rank;  // per trip: per-rank first position, rank bitmap, offsets
+  uint64_t emit_stride;
+  int sl_par;
+  const int32_t* strag_trip;
+  uint8_t* sl_late;
+  uint2* sl_cnt;
   uint32_t scratch_per_trip;  // u32 words
   Pools pools;
   TripOut* out;
@@ -1767,6 +2092,187 @@ __device__ void decide_straggler(const DecideArgs& a, int32_t j,
   }
 }
 
+// Candidate order for the report (rca.cpp:850-853: stable sort by
+// (stuck_op, rank)) as a bitonic sort of packed (op - min op, rank, index)
+// keys in the trip's scratch; the O(C^2) rank-count sort when the packing
+// does not fit.
+__device__ void strag_order(const DecideArgs& a, const Cand* cands, int C, uint32_t* A,
+                            uint32_t P, uint32_t* ord, BlockShared& sh) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  int rmax = 0;
+  for (int x = threadIdx.x; x < C; x += blockDim.x) {
+    mn = min(mn, static_cast<long long>(cands[x].op));
+    mx = max(mx, static_cast<long long>(cands[x].op));
+    rmax = max(rmax, cands[x].rank);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+    mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+    rmax = max(rmax, __shfl_xor_sync(FULL, rmax, o));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sh.red_l[warp] = mn;
+    sh.red_u[0][warp] = static_cast<unsigned long long>(mx);
+    sh.red_i[warp] = rmax;
+  }
+  __syncthreads();
+  mn = LLONG_MAX;
+  mx = LLONG_MIN;
+  rmax = 0;
+  for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+    mn = min(mn, sh.red_l[q]);
+    mx = max(mx, static_cast<long long>(sh.red_u[0][q]));
+    rmax = max(rmax, sh.red_i[q]);
+  }
+  __syncthreads();
+  int ib = 1, rb = 1;
+  while ((1ll << ib) < C) ++ib;
+  while ((1ll << rb) <= rmax) ++rb;
+  const int ob = 64 - ib - rb;
+  uint32_t Pw = 1;
+  while (Pw < static_cast<uint32_t>(C)) Pw <<= 1;
+  unsigned long long* K = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(A) + 7) & ~static_cast<uintptr_t>(7));
+  const bool fits = rmax >= 0 && ob > 0 && ob < 63 && mx - mn < (1ll << ob) &&
+                    2ull * Pw + 2 <= P;
+  if (!fits) {
+    for (int i = threadIdx.x; i < C; i += blockDim.x) A[i] = i;
+    __syncthreads();
+    block_stable_sort(C, A, ord, [&](uint32_t x, uint32_t y) {
+      if (cands[x].op != cands[y].op) return cands[x].op < cands[y].op;
+      return cands[x].rank < cands[y].rank;
+    });
+    return;
+  }
+  for (uint32_t x = threadIdx.x; x < Pw; x += blockDim.x)
+    K[x] = x < static_cast<uint32_t>(C)
+               ? (static_cast<unsigned long long>(cands[x].op - mn) << (rb + ib)) |
+                     (static_cast<unsigned long long>(cands[x].rank) << ib) | x
+               : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= Pw; k <<= 1) {
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = threadIdx.x; i < Pw; i += blockDim.x) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const unsigned long long x = K[i], y = K[l];
+          if ((x > y) == ((i & k) == 0)) {
+            K[i] = y;
+            K[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const unsigned long long im = (1ull << ib) - 1;
+  for (int x = threadIdx.x; x < C; x += blockDim.x) ord[x] = static_cast<uint32_t>(K[x] & im);
+  __syncthreads();
+}
+
+// Report assembly (rca.cpp:854-866) in parallel: exonerated in sorted order;
+// suspects = the first retained entry per rank (a per-rank minimum of the
+// sorted position), their evidence in sorted order; suspects then ordered by
+// rank (ranks are unique among them: a prefix popcount over a rank bitmap).
+__device__ void emit_reports_par(const DecideArgs& a, BlockShared& sh, int32_t j,
+                                 const uint32_t* ord, const uint8_t* keep, int C) {
+  const Cand* cands = a.pools.cand + sh.cand_base;
+  const int32_t RS = a.m.rank_space;
+  const uint32_t rw = static_cast<uint32_t>(RS + 31) / 32;
+  uint32_t* minpos = a.emit_rank + static_cast<uint64_t>(j) * a.emit_stride;
+  uint32_t* rbits = minpos + RS;
+  uint32_t* woff = rbits + rw;
+  for (int32_t r = threadIdx.x; r < RS; r += blockDim.x) minpos[r] = 0xFFFFFFFFu;
+  for (uint32_t w = threadIdx.x; w < rw; w += blockDim.x) rbits[w] = 0;
+  __syncthreads();
+  for (int x = threadIdx.x; x < C; x += blockDim.x)
+    if (keep[x]) {
+      const int32_t r = cands[ord[x]].rank;
+      if (r >= 0 && r < RS) atomicMin(&minpos[r], static_cast<uint32_t>(x));
+    }
+  __syncthreads();
+  csg_suspect* sus = a.pools.sus + sh.sus_base;
+  csg_suspect* exo = a.pools.sus + sh.exo_base;
+  csg_evidence* evo = a.pools.ev + sh.ev_base;
+  const csg_evidence* cev = a.pools.cev + sh.cev_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;
+  __shared__ uint32_t scan3[32][3];
+  uint32_t run_e = 0, run_s = 0, run_v = 0;
+  for (int base = 0; base < C; base += blockDim.x) {
+    const int x = base + threadIdx.x;
+    const bool valid = x < C;
+    Cand c;
+    if (valid) c = cands[ord[x]];
+    const bool isexo = valid && !keep[x];
+    const bool isfirst = valid && keep[x] && c.rank >= 0 && c.rank < RS &&
+                         minpos[c.rank] == static_cast<uint32_t>(x);
+    const uint32_t evn = isfirst ? c.ev_n : 0;
+    uint32_t e = isexo, f = isfirst, v = evn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t e2 = __shfl_up_sync(FULL, e, o), f2 = __shfl_up_sync(FULL, f, o),
+                     v2 = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) {
+        e += e2;
+        f += f2;
+        v += v2;
+      }
+    }
+    if (lane == 31) {
+      scan3[warp][0] = e;
+      scan3[warp][1] = f;
+      scan3[warp][2] = v;
+    }
+    __syncthreads();
+    uint32_t be = 0, bf = 0, bv = 0, te = 0, tf = 0, tv = 0;
+    for (int q = 0; q < nwb; ++q) {
+      if (q < warp) {
+        be += scan3[q][0];
+        bf += scan3[q][1];
+        bv += scan3[q][2];
+      }
+      te += scan3[q][0];
+      tf += scan3[q][1];
+      tv += scan3[q][2];
+    }
+    if (isexo) exo[run_e + be + e - 1] = to_suspect(c);
+    if (isfirst) {
+      sus[run_s + bf + f - 1] = to_suspect(c);
+      atomicOr(&rbits[c.rank >> 5], 1u << (c.rank & 31));
+      const uint32_t v0 = run_v + bv + v - evn;
+      for (uint32_t q = 0; q < evn; ++q) evo[v0 + q] = cev[c.ev_off + q];
+    }
+    run_e += te;
+    run_s += tf;
+    run_v += tv;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (uint32_t w = 0; w < rw; ++w) {
+      woff[w] = acc;
+      acc += __popc(rbits[w]);
+    }
+    sh.nsus = static_cast<int32_t>(run_s);
+    sh.nexo = static_cast<int32_t>(run_e);
+    sh.nev = run_v;
+  }
+  __syncthreads();
+  csg_suspect* tmp = exo + run_e;  // spare room behind the exonerated
+  for (uint32_t i = threadIdx.x; i < run_s; i += blockDim.x) {
+    const int32_t r = sus[i].rank;
+    const uint32_t pos = woff[r >> 5] + __popc(rbits[r >> 5] & ((1u << (r & 31)) - 1u));
+    tmp[pos] = sus[i];
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < run_s; i += blockDim.x) sus[i] = tmp[i];
+  __syncthreads();
+}
+
 __device__ void decide_straggler_finish(const DecideArgs& a, int32_t j, BlockShared& sh,
                                         uint32_t* scratch) {
   const StragState S = a.state[j];
@@ -1785,7 +2291,7 @@ __device__ void decide_straggler_finish(const DecideArgs& a, int32_t j, BlockSha
     sh.cap_cev = S.cap_cev;
   }
   __syncthreads();
-  const long long clk_g0 = clock64(), clk_g1 = clk_g0;
+  const long long clk_g0 = clock64();
   const uint32_t mwords = static_cast<uint32_t>((a.s.R + 31) / 32 + 1);
   const uint32_t P = (a.scratch_per_trip - mwords) / 2;
   uint32_t* A = scratch + mwords;
@@ -1794,27 +2300,21 @@ __device__ void decide_straggler_finish(const DecideArgs& a, int32_t j, BlockSha
   int any_self = 0;
   for (int x = threadIdx.x; x < C; x += blockDim.x) any_self |= cands[x].pad ? 1 : 0;
   any_self = __syncthreads_or(any_self);
-  uint32_t* idx = A;
   uint32_t* ord = B;
   uint8_t* keep = reinterpret_cast<uint8_t*>(B + C);
   uint32_t* tail = reinterpret_cast<uint32_t*>(keep + ((C + 3) & ~3));
-  for (int i = threadIdx.x; i < C; i += blockDim.x) idx[i] = i;
-  __syncthreads();
-  block_stable_sort(C, idx, ord, [&](uint32_t x, uint32_t y) {
-    if (cands[x].op != cands[y].op) return cands[x].op < cands[y].op;
-    return cands[x].rank < cands[y].rank;
-  });
+  strag_order(a, cands, C, A, P, ord, sh);
   for (int x = threadIdx.x; x < C; x += blockDim.x)
     keep[x] = (!any_self || cands[ord[x]].pad) ? 1 : 0;
   __syncthreads();
   const long long clk_g2 = clock64();
-  emit_reports(a, sh, ord, keep, C, tail);
+  if (a.emit_rank) emit_reports_par(a, sh, j, ord, keep, C);
+  else emit_reports(a, sh, ord, keep, C, tail);
   write_trip(a, j, sh.nsus ? CSG_VERDICT_SUSPECTS : CSG_VERDICT_NO_STRAGGLER,
              naff, 3 * a.N, sh);
   if (a.debug && threadIdx.x == 0)
-    printf("decide trip %d naff %d C %d any_self %d cycles: cands %lld self %lld emit %lld\n",
-           j, naff, C, any_self, clk_g1 - clk_g0, clk_g2 - clk_g1,
-           (long long)clock64() - clk_g2);
+    printf("decide trip %d naff %d C %d any_self %d cycles: order %lld emit %lld\n",
+           j, naff, C, any_self, clk_g2 - clk_g0, (long long)clock64() - clk_g2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2886,6 +3386,7 @@ __global__ void __launch_bounds__(kDecideThreads)
     return;
   }
   if (a.trip_kind[j] == CSG_TRIGGER_FAILURE) return;  // k_exonerate
+  if (a.phase == 1 && a.sl_par) return;  // k_sl_late .. k_sl_emit
   if (a.phase == 1) decide_straggler(a, j, sh, scratch);
   else decide_straggler_finish(a, j, sh, scratch);
 }
@@ -2931,33 +3432,55 @@ __global__ void __launch_bounds__(kDecideThreads) k_cohorts(DecideArgs a) {
     hi = max(hi, sh.red_l[16 + w]);
   }
   __syncthreads();
-  const long long it = lo + q;
-  if (lo > hi || it > hi) return;
-  const unsigned long long ckey =
-      (static_cast<unsigned long long>(j) << 44) ^
-      (static_cast<unsigned long long>(nm) << 36) ^
-      (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
-  __shared__ int s_slot;
-  if (threadIdx.x == 0) {
-    s_slot = -1;
-    const uint32_t mask = a.coh_cap - 1;
-    uint32_t h = static_cast<uint32_t>((ckey * 0x9E3779B97F4A7C15ull) >> 40) & mask;
-    for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h = (h + 1) & mask) {
-      const unsigned long long k = atomicCAS(a.coh_key + h, ~0ull, ckey);
-      if (k == ~0ull) {
-        s_slot = static_cast<int>(h);
-        break;
+  // every iteration of the trip's candidate windows (grid.y strides them)
+  for (long long it = lo + q; lo <= hi && it <= hi; it += gridDim.y) {
+    const unsigned long long ckey =
+        (static_cast<unsigned long long>(j) << 44) ^
+        (static_cast<unsigned long long>(nm) << 36) ^
+        (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
+    __shared__ int s_slot;
+    if (threadIdx.x == 0) {
+      s_slot = -1;
+      const uint32_t mask = a.coh_cap - 1;
+      uint32_t h = static_cast<uint32_t>((ckey * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+      for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h = (h + 1) & mask) {
+        const unsigned long long k = atomicCAS(a.coh_key + h, ~0ull, ckey);
+        if (k == ~0ull) {
+          s_slot = static_cast<int>(h);
+          break;
+        }
+        if (k == ckey) break;  // already there
       }
-      if (k == ckey) break;  // already there
     }
+    __syncthreads();
+    if (s_slot >= 0) {
+      const double med = cohort_median(a, it, nm, a.trip_t[j], sh);
+      if (threadIdx.x == 0) {
+        a.coh_val[s_slot] = med;
+        __threadfence();
+        atomicExch(a.coh_state + s_slot, 2u);
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (s_slot < 0) return;
-  const double med = cohort_median(a, it, nm, a.trip_t[j], sh);
-  if (threadIdx.x == 0) {
-    a.coh_val[s_slot] = med;
-    __threadfence();
-    atomicExch(a.coh_state + s_slot, 2u);
+}
+
+// The cohorts k_sf_fast claimed (state 0): one block per claimed slot.
+__global__ void __launch_bounds__(kDecideThreads) k_cohorts_lazy(DecideArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
+  for (uint32_t h = blockIdx.x; h < a.coh_cap; h += gridDim.x) {
+    if (a.coh_key[h] == ~0ull || a.coh_state[h] == 2u) continue;
+    const longlong2 mt = a.coh_meta[h];
+    const int32_t j = static_cast<int32_t>(mt.y >> 8);
+    const uint8_t nm = static_cast<uint8_t>(mt.y & 0xff);
+    const double med = cohort_median(a, mt.x, nm, a.trip_t[j], sh);
+    if (threadIdx.x == 0) {
+      a.coh_val[h] = med;
+      __threadfence();
+      atomicExch(a.coh_state + h, 2u);
+    }
+    __syncthreads();
   }
 }
 
@@ -2994,6 +3517,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
     const int32_t x = static_cast<int32_t>(w - jbase);
     Cand* cands = a.pools.cand + a.state[jcur].cand_base;
     const Cand c = cands[x];
+    if (a.sf_fast && c.pad != 2) continue;  // decided by k_sf_fast
     const long long c0 = clock64();
     const bool sf = c.it_hi < c.it_lo ? true : self_faulted(a, jcur, c, sh, lst);
     if (threadIdx.x == 0) cands[x].pad = sf ? 1 : 0;
@@ -3002,6 +3526,795 @@ __global__ void __launch_bounds__(kDecideThreads) k_self_faulted(DecideArgs a) {
              "n_mine %u distinct %u\n", w, jcur, x, c.rank, (long long)c.it_lo,
              (long long)c.it_hi, sf ? 1 : 0, (long long)clock64() - c0, sh.dbg_n, sh.dbg_d);
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Straggler candidates (analyze_straggler, rca.cpp:654-789) for all trips and
+// groups in parallel. The reference walks the affected groups in ascending
+// order and, per group, appends (1) its late members in member order, (2)
+// FlowSkewed findings of not-yet-candidate members in rank order, (3)
+// FlowIncomplete findings likewise. "Not yet candidate" only depends on
+// earlier groups: a rank is marked before group g's flow passes iff it is
+// late in g, or late or flow-flagged in an earlier affected group with
+// history (the first such group gives it a candidate either way). So every
+// (trip, group) decides its candidates on its own:
+//   k_sl_late   warp per (trip, affected group): window medians, late bits
+//   k_sl_count  warp per (trip, affected group): flow-candidate types from
+//               the member's earlier groups, candidate / evidence counts
+//   k_sl_scan   block per trip: offsets in group order, pool allocation
+//   k_sl_emit   warp per (trip, affected group): candidates + evidence
+// ---------------------------------------------------------------------------
+// Warp-collective ascending bitonic sort of n (<= cap, power-of-two P)
+// ordered keys in shared memory.
+__device__ void warp_bitonic_u64(unsigned long long* v, uint32_t P) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = lane; i < P; i += 32) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const unsigned long long x = v[i], y = v[l];
+          if ((x > y) == ((i & k) == 0)) {
+            v[i] = y;
+            v[l] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+constexpr int kSlWarps = 4;
+constexpr int kSlCap = 1024;  // members whose keys a warp sorts in shared memory
+constexpr uint8_t kSlHist = 0x80;   // slot of an affected group with history
+constexpr uint8_t kSlSkew = 0x10;   // FlowSkewed candidate
+constexpr uint8_t kSlInc = 0x20;    // FlowIncomplete candidate
+
+// lower median (element (m-1)/2) of m keys, warp-collective
+template <typename V>
+__device__ double warp_lower_median_sorted(int m, V val, unsigned long long* buf) {
+  const int lane = threadIdx.x & 31;
+  if (m > kSlCap) return warp_lower_median(m, [&](int i) { return dkey_inv(val(i)); });
+  uint32_t P = 32;
+  while (P < static_cast<uint32_t>(m)) P <<= 1;
+  for (uint32_t i = lane; i < P; i += 32) buf[i] = i < static_cast<uint32_t>(m) ? val(i) : ~0ull;
+  __syncwarp();
+  warp_bitonic_u64(buf, P);
+  const double r = dkey_inv(buf[(m - 1) / 2]);
+  __syncwarp();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSlWarps * 32) k_sl_late(DecideArgs a, int32_t Js) {
+  __shared__ unsigned long long buf[kSlWarps][kSlCap];
+  __shared__ double smed[kSlWarps][2][kMaxK];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int32_t G = a.m.n_groups;
+  const uint64_t w = blockIdx.x * (uint64_t)kSlWarps + wib;
+  if (w >= static_cast<uint64_t>(Js) * G) return;
+  const int32_t js = static_cast<int32_t>(w / G), i = static_cast<int32_t>(w % G);
+  const int32_t j = a.strag_trip[js];
+  if (i >= a.n_aff[j] || a.m.opn == 0) return;
+  const int32_t g = a.aff[static_cast<uint64_t>(j) * G + i];
+  const uint32_t mo = a.m.member_off[g];
+  const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
+  if (m < 2) return;
+  const uint64_t gidx = static_cast<uint64_t>(js) * G + g;
+  if (a.gi[gidx].n_common < a.k) return;
+  const uint64_t rowbase = static_cast<uint64_t>(js) * a.M;
+  const int32_t k = a.k;
+  // lower medians of the members' starts / ends per window iteration
+  // (rca.cpp:670-681)
+  for (int q = 0; q < k; ++q) {
+    const int64_t it = a.gi_last[gidx * k + q] - a.it_min;
+    const double ms = warp_lower_median_sorted(
+        m, [&](int x) { return a.tbl_s[(rowbase + a.m.member_slot[mo + x]) * a.n_it + it]; },
+        buf[wib]);
+    const double me = warp_lower_median_sorted(
+        m, [&](int x) { return a.tbl_e[(rowbase + a.m.member_slot[mo + x]) * a.n_it + it]; },
+        buf[wib]);
+    if (lane == 0) {
+      smed[wib][0][q] = ms;
+      smed[wib][1][q] = me;
+    }
+  }
+  __syncwarp();
+  for (int x = lane; x < m; x += 32) {
+    uint32_t bits = 3;
+    const uint64_t cell = (rowbase + a.m.member_slot[mo + x]) * a.n_it;
+    for (int q = 0; q < k; ++q) {
+      const int64_t it = a.gi_last[gidx * k + q] - a.it_min;
+      if (dkey_inv(a.tbl_s[cell + it]) - smed[wib][0][q] < a.thr) bits &= ~1u;
+      if (dkey_inv(a.tbl_e[cell + it]) - smed[wib][1][q] < a.thr) bits &= ~2u;
+    }
+    a.sl_late[rowbase + mo + x] = static_cast<uint8_t>(kSlHist | bits);
+  }
+}
+
+__global__ void __launch_bounds__(kSlWarps * 32) k_sl_count(DecideArgs a, int32_t Js) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int32_t G = a.m.n_groups;
+  const uint64_t w = blockIdx.x * (uint64_t)kSlWarps + wib;
+  if (w >= static_cast<uint64_t>(Js) * G) return;
+  const int32_t js = static_cast<int32_t>(w / G), i = static_cast<int32_t>(w % G);
+  const int32_t j = a.strag_trip[js];
+  uint2 cnt = make_uint2(0, 0);
+  if (i < a.n_aff[j] && a.m.opn != 0) {
+    const int32_t g = a.aff[static_cast<uint64_t>(j) * G + i];
+    const uint32_t mo = a.m.member_off[g];
+    const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
+    const uint64_t rowbase = static_cast<uint64_t>(js) * a.M;
+    if (m >= 2 && (a.sl_late[rowbase + mo] & kSlHist)) {
+      uint32_t nl = 0, nf = 0;
+      for (int x = lane; x < m; x += 32) {
+        const uint32_t slot = mo + x;
+        uint8_t v = a.sl_late[rowbase + slot];
+        const bool lt = (v & 3) != 0;
+        const int32_t ff = a.fs[rowbase + slot].flags;
+        uint8_t type = 0;
+        if (!lt && (ff & 3)) {
+          // marked by an earlier affected group with history?
+          const int32_t r = a.m.members[slot];
+          bool marked = false;
+          if (r >= 0 && r < a.m.rank_space)
+            for (uint32_t q = a.m.rg_off[r]; q < a.m.rg_off[r + 1] && !marked; ++q) {
+              const int32_t g2 = a.m.rg_group[q];
+              if (g2 >= g) continue;
+              const uint32_t s2 = a.m.rg_slot[q];
+              const uint8_t v2 = a.sl_late[rowbase + s2];
+              if (!(v2 & kSlHist)) continue;
+              marked = (v2 & 3) || (a.fs[rowbase + s2].flags & 3);
+            }
+          if (!marked) type = (ff & 1) ? kSlSkew : kSlInc;
+        }
+        if (type) a.sl_late[rowbase + slot] = static_cast<uint8_t>(v | type);
+        nl += lt ? 1u : 0u;
+        nf += type ? 1u : 0u;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        nl += __shfl_xor_sync(FULL, nl, o);
+        nf += __shfl_xor_sync(FULL, nf, o);
+      }
+      cnt = make_uint2(nl + nf, nl * static_cast<uint32_t>(a.k) + nf);
+    }
+  }
+  if (lane == 0) a.sl_cnt[static_cast<uint64_t>(js) * G + i] = cnt;
+}
+
+// Per straggler trip: exclusive scan of the groups' (candidates, evidence)
+// counts in affected-group order (in place), pool allocation, trip state.
+__global__ void __launch_bounds__(1024) k_sl_scan(DecideArgs a) {
+  __shared__ uint32_t wc[32], we[32];
+  __shared__ uint32_t run_c, run_e;
+  __shared__ int s_hist;
+  const int32_t js = blockIdx.x;
+  const int32_t j = a.strag_trip[js];
+  const int32_t G = a.m.n_groups;
+  const int32_t naff = a.n_aff[j];
+  if (naff == 0 || a.m.opn == 0) return;  // false trigger: k_decide
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    run_c = 0;
+    run_e = 0;
+    s_hist = 0;
+  }
+  __syncthreads();
+  uint2* cnt = a.sl_cnt + static_cast<uint64_t>(js) * G;
+  const uint64_t rowbase = static_cast<uint64_t>(js) * a.M;
+  int hist = 0;
+  for (int32_t b0 = 0; b0 < naff; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    uint2 v = i < naff ? cnt[i] : make_uint2(0, 0);
+    if (i < naff) {
+      const int32_t g = a.aff[static_cast<uint64_t>(j) * G + i];
+      if (a.m.member_off[g + 1] - a.m.member_off[g] >= 2 &&
+          (a.sl_late[rowbase + a.m.member_off[g]] & kSlHist))
+        hist = 1;
+    }
+    uint32_t c = v.x, e = v.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t c2 = __shfl_up_sync(FULL, c, o), e2 = __shfl_up_sync(FULL, e, o);
+      if (lane >= o) {
+        c += c2;
+        e += e2;
+      }
+    }
+    if (lane == 31) {
+      wc[warp] = c;
+      we[warp] = e;
+    }
+    __syncthreads();
+    uint32_t bc = run_c, be = run_e, tc = 0, te = 0;
+    for (int q = 0; q < nw; ++q) {
+      if (q < warp) {
+        bc += wc[q];
+        be += we[q];
+      }
+      tc += wc[q];
+      te += we[q];
+    }
+    if (i < naff) cnt[i] = make_uint2(bc + c - v.x, be + e - v.y);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      run_c += tc;
+      run_e += te;
+    }
+    __syncthreads();
+  }
+  if (hist) s_hist = 1;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint32_t C = run_c, CE = run_e;
+  StragState S;
+  memset(&S, 0, sizeof(S));
+  S.any_history = s_hist;
+  TripOut o;
+  memset(&o, 0, sizeof(o));
+  o.n_aff = naff;
+  if (C == 0) {
+    o.verdict = s_hist ? CSG_VERDICT_NO_STRAGGLER : CSG_VERDICT_INSUFFICIENT_HISTORY;
+    o.scanned = 2 * a.N;
+    a.out[j] = o;
+    a.state[j] = S;
+    return;
+  }
+  bool ok1, ok2, ok3, ok4;
+  S.cap_cand = C;
+  S.cap_cev = CE;
+  S.cand_base = pool_alloc(a.pools.used, P_CAND, C, a.pools.cand_cap, a.err, DEV_ERR_POOL, &ok1);
+  S.cev_base = pool_alloc(a.pools.used, P_CEV, CE, a.pools.cev_cap, a.err, DEV_ERR_POOL, &ok2);
+  S.sus_base = pool_alloc(a.pools.used, P_SUS, 3ull * C, a.pools.sus_cap, a.err, DEV_ERR_POOL,
+                          &ok3);
+  S.exo_base = S.sus_base + C;
+  S.ev_base = pool_alloc(a.pools.used, P_EV, CE, a.pools.ev_cap, a.err, DEV_ERR_POOL, &ok4);
+  if (!(ok1 && ok2 && ok3 && ok4)) {
+    S.C = 0;  // the host retries with larger pools (DEV_ERR_POOL)
+    a.state[j] = S;
+    return;
+  }
+  S.C = static_cast<int32_t>(C);
+  S.cev_used = CE;
+  a.state[j] = S;
+}
+
+__device__ inline void sl_cev(const DecideArgs& a, const StragState& S, uint32_t at,
+                              int32_t rank, int32_t ch, double tms, int64_t op) {
+  csg_evidence e;
+  e.rank = rank;
+  e.channel = ch;
+  e.time_ms = tms;
+  e.op_seq = op;
+  a.pools.cev[S.cev_base + at] = e;
+}
+
+__global__ void __launch_bounds__(kSlWarps * 32) k_sl_emit(DecideArgs a, int32_t Js) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int32_t G = a.m.n_groups;
+  const uint64_t w = blockIdx.x * (uint64_t)kSlWarps + wib;
+  if (w >= static_cast<uint64_t>(Js) * G) return;
+  const int32_t js = static_cast<int32_t>(w / G), i = static_cast<int32_t>(w % G);
+  const int32_t j = a.strag_trip[js];
+  if (i >= a.n_aff[j] || a.m.opn == 0) return;
+  const StragState S = a.state[j];
+  if (S.C <= 0) return;
+  const int32_t g = a.aff[static_cast<uint64_t>(j) * G + i];
+  const uint32_t mo = a.m.member_off[g];
+  const int32_t m = static_cast<int32_t>(a.m.member_off[g + 1] - mo);
+  const uint64_t rowbase = static_cast<uint64_t>(js) * a.M;
+  if (m < 2 || !(a.sl_late[rowbase + mo] & kSlHist)) return;
+  const uint2 off = a.sl_cnt[static_cast<uint64_t>(js) * G + i];
+  const uint64_t gidx = static_cast<uint64_t>(js) * G + g;
+  const int32_t k = a.k, opn = a.m.opn;
+  const int64_t gfo = a.m.group_first_op[g];
+  const int64_t wlo = a.gi_last[gidx * k], whi = a.gi_last[gidx * k + k - 1];
+  Cand* cands = a.pools.cand + S.cand_base;
+  // (1) late members in member order
+  uint32_t nl = 0;
+  for (int b0 = 0; b0 < m; b0 += 32) {
+    const int x = b0 + lane;
+    const uint8_t v = x < m ? a.sl_late[rowbase + mo + x] : 0;
+    const bool lt = (v & 3) != 0;
+    const unsigned mm = __ballot_sync(FULL, lt);
+    if (lt) {
+      const uint32_t pos = nl + __popc(mm & ((1u << lane) - 1u));
+      const int32_t r = a.m.members[mo + x];
+      const uint64_t cell = (rowbase + a.m.member_slot[mo + x]) * a.n_it;
+      Cand c;
+      memset(&c, 0, sizeof(c));
+      c.rank = r;
+      c.cat = (v & 1) ? CSG_RC_STRAGGLER_LATE_START : CSG_RC_STRAGGLER_LATE_END;
+      c.side = CSG_SIDE_LOCAL;
+      c.group = g;
+      c.op = whi * opn + gfo;
+      c.onset = dkey_inv(a.tbl_s[cell + (wlo - a.it_min)]);
+      c.it_lo = wlo;
+      c.it_hi = whi;
+      c.ev_off = off.y + pos * k;
+      c.ev_n = k;
+      for (int q = 0; q < k; ++q) {
+        const int64_t it = a.gi_last[gidx * k + q];
+        sl_cev(a, S, c.ev_off + q, r, -1, dkey_inv(a.tbl_s[cell + (it - a.it_min)]),
+               it * opn + gfo);
+      }
+      cands[off.x + pos] = c;
+    }
+    nl += __popc(mm);
+  }
+  // (2) FlowSkewed then (3) FlowIncomplete, each in ascending rank order
+  uint32_t base_c = off.x + nl, base_e = off.y + nl * static_cast<uint32_t>(k);
+  for (int pass = 0; pass < 2; ++pass) {
+    const uint8_t want = pass == 0 ? kSlSkew : kSlInc;
+    uint32_t nt = 0;
+    for (int b0 = 0; b0 < m; b0 += 32) {
+      const int x = b0 + lane;
+      const bool is = x < m && (a.sl_late[rowbase + mo + x] & want);
+      if (is) {
+        const int32_t r = a.m.members[mo + x];
+        uint32_t pos = 0;  // rank-order position among this pass's findings
+        for (int y = 0; y < m; ++y)
+          if ((a.sl_late[rowbase + mo + y] & want) && a.m.members[mo + y] < r) ++pos;
+        const FlowSum f = a.fs[rowbase + mo + x];
+        Cand c;
+        memset(&c, 0, sizeof(c));
+        c.rank = r;
+        c.side = CSG_SIDE_LOCAL;
+        c.group = g;
+        c.it_lo = 0;
+        c.it_hi = -1;
+        c.ev_off = base_e + pos;
+        c.ev_n = 1;
+        if (pass == 0) {
+          c.cat = CSG_RC_FLOW_SKEWED;
+          c.op = f.skew_op;
+          c.onset = f.skew_start;
+          sl_cev(a, S, c.ev_off, r, f.skew_chan, f.skew_end, f.skew_op);
+        } else {
+          c.cat = CSG_RC_FLOW_INCOMPLETE;
+          c.op = f.inc_op;
+          c.onset = a.trip_t[j];
+          sl_cev(a, S, c.ev_off, r, f.inc_chan, a.trip_t[j], f.inc_op);
+        }
+        cands[base_c + pos] = c;
+      }
+      nt += __popc(__ballot_sync(FULL, is));
+    }
+    base_c += nt;
+    base_e += nt;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sorted self-evidence path. self_faulted (rca.cpp:821-848) asks, for a
+// candidate rank r and each op o of its iteration window that r completed,
+// whether r's longest duration of o exceeds skew x the lower median of every
+// other rank's durations of o (ts <= t). The sibling multiset is the op's
+// whole op-index segment minus r's own entries, so with the segment sorted
+// once (k_opsort) the median is a lookup: element q = (m - k_r - 1) / 2 of
+// the segment with r's k_r values skipped lies in [q, q + k_r] and follows
+// from one window load and a merge against r's sorted values. A warp per
+// candidate (k_sf_fast) does that for every op of the window; candidates it
+// cannot decide this way (sharded store, a segment with entries after t or
+// too long to sort, more than 32 completions of one op, a cohort the table
+// does not hold) are left to k_self_faulted (Cand::pad = 2).
+// ---------------------------------------------------------------------------
+struct SfPlan {
+  unsigned long long k0, k1;  // op keys covered by the candidates' windows
+  unsigned long long total;   // straggler candidates in the batch
+  int32_t any;
+  int32_t pad;
+  unsigned long long cstart[1];  // [J + 1] flattened candidate offsets
+};
+
+constexpr int kOpSortWarpCap = 512;    // entries a warp sorts in shared memory
+constexpr int kOpSortBlockCap = 8192;  // entries a block sorts (64 KB)
+constexpr int kSfWarps = 4;
+
+__global__ void __launch_bounds__(1024) k_sf_prep(DecideArgs a) {
+  SfPlan* pl = a.plan;
+  __shared__ long long s_lo[32], s_hi[32];
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int32_t j = 0; j < a.J; ++j) {
+    if (a.trip_kind[j] == CSG_TRIGGER_FAILURE) continue;
+    const StragState S = a.state[j];
+    if (S.C <= 0) continue;
+    const Cand* cands = a.pools.cand + S.cand_base;
+    for (int x = threadIdx.x; x < S.C; x += blockDim.x) {
+      const Cand& c = cands[x];
+      if (c.it_hi < c.it_lo) continue;
+      lo = min(lo, static_cast<long long>(c.it_lo));
+      hi = max(hi, static_cast<long long>(c.it_hi));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[threadIdx.x >> 5] = lo;
+    s_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      lo = min(lo, s_lo[w]);
+      hi = max(hi, s_hi[w]);
+    }
+    unsigned long long tot = 0;
+    for (int32_t j = 0; j < a.J; ++j) {
+      pl->cstart[j] = tot;
+      if (a.trip_kind[j] != CSG_TRIGGER_FAILURE && a.state[j].C > 0) tot += a.state[j].C;
+    }
+    pl->cstart[a.J] = tot;
+    pl->total = tot;
+    pl->any = 0;
+    if (lo <= hi && a.m.opn > 0) {
+      int64_t olo, ohi, x0, x1;
+      iter_ops(lo, a.m.opn, olo, x1);
+      iter_ops(hi, a.m.opn, x0, ohi);
+      // keys of ops inside the store's op range
+      const long long mo = a.min_op;
+      const long long k0 = max(0ll, static_cast<long long>(olo) - mo);
+      const long long k1 = min(static_cast<long long>(ohi), static_cast<long long>(a.max_op)) - mo;
+      if (k1 >= k0) {
+        pl->k0 = static_cast<unsigned long long>(k0);
+        pl->k1 = static_cast<unsigned long long>(k1);
+        pl->any = 1;
+      }
+    }
+  }
+}
+
+// Per op key in the plan's range: sort the op-index segment's entries by
+// duration (warp per op up to kOpSortWarpCap entries; longer segments go to
+// k_opsort_large) into sdur / sts / srank, and record the segment's latest
+// timestamp.
+__device__ void warp_bitonic_kv(unsigned long long* v, uint16_t* ix, uint32_t P) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = lane; i < P; i += 32) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const unsigned long long x = v[i], y = v[l];
+          if ((x > y) == ((i & k) == 0)) {
+            v[i] = y;
+            v[l] = x;
+            const uint16_t t = ix[i];
+            ix[i] = ix[l];
+            ix[l] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_opsort(DecideArgs a, unsigned* __restrict__ large,
+                                                unsigned* __restrict__ n_large,
+                                                uint32_t large_cap) {
+  __shared__ unsigned long long buf[8][kOpSortWarpCap];
+  __shared__ uint16_t ibuf[8][kOpSortWarpCap];
+  const SfPlan* pl = a.plan;
+  if (!pl->any) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned long long* v = buf[wib];
+  uint16_t* ix = ibuf[wib];
+  const unsigned long long k0 = pl->k0, k1 = pl->k1;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t kk = k0 + (blockIdx.x * (uint64_t)(blockDim.x >> 5) + wib); kk <= k1; kk += nw) {
+    const uint32_t sb = a.opoff[kk], se = a.opoff[kk + 1];
+    const uint32_t m = se - sb;
+    if (m == 0) continue;
+    if (m > kOpSortWarpCap) {
+      if (lane == 0) {
+        const unsigned at = atomicAdd(n_large, 1u);
+        if (at < large_cap) large[at] = static_cast<unsigned>(kk - k0);
+        else a.opmax[kk] = __longlong_as_double(0x7FF8000000000000ll);  // unsorted
+      }
+      continue;
+    }
+    uint32_t P = 32;
+    while (P < m) P <<= 1;
+    double mx = -INFINITY;
+    for (uint32_t i = lane; i < P; i += 32) {
+      if (i < m) {
+        v[i] = dkey(a.op_dur[sb + i]);
+        mx = fmax(mx, a.op_ts[sb + i]);
+      } else {
+        v[i] = ~0ull;
+      }
+      ix[i] = static_cast<uint16_t>(i);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    warp_bitonic_kv(v, ix, P);
+    for (uint32_t i = lane; i < m; i += 32) {
+      a.sdur[sb + i] = v[i];
+      a.sts[sb + i] = a.op_ts[sb + ix[i]];
+      a.srank[sb + i] = a.oprank[sb + ix[i]];
+    }
+    if (lane == 0) a.opmax[kk] = mx;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_opsort_large(DecideArgs a,
+                                                       const unsigned* __restrict__ large,
+                                                       const unsigned* __restrict__ n_large,
+                                                       uint32_t large_cap) {
+  extern __shared__ __align__(16) unsigned long long sv[];  // [kOpSortBlockCap] + u16 idx
+  uint16_t* si = reinterpret_cast<uint16_t*>(sv + kOpSortBlockCap);
+  __shared__ double s_mx[32];
+  const SfPlan* pl = a.plan;
+  if (!pl->any) return;
+  const uint32_t nl = min(*n_large, large_cap);
+  for (uint32_t w = blockIdx.x; w < nl; w += gridDim.x) {
+    const unsigned long long kk = pl->k0 + large[w];
+    const uint32_t sb = a.opoff[kk], se = a.opoff[kk + 1];
+    const uint32_t m = se - sb;
+    if (m > kOpSortBlockCap) {
+      if (threadIdx.x == 0) a.opmax[kk] = __longlong_as_double(0x7FF8000000000000ll);
+      continue;
+    }
+    uint32_t P = 32;
+    while (P < m) P <<= 1;
+    double mx = -INFINITY;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+      if (i < m) {
+        sv[i] = dkey(a.op_dur[sb + i]);
+        mx = fmax(mx, a.op_ts[sb + i]);
+      } else {
+        sv[i] = ~0ull;
+      }
+      si[i] = static_cast<uint16_t>(i);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+          const uint32_t l = i ^ jj;
+          if (l > i) {
+            const unsigned long long x = sv[i], y = sv[l];
+            if ((x > y) == ((i & k) == 0)) {
+              sv[i] = y;
+              sv[l] = x;
+              const uint16_t t = si[i];
+              si[i] = si[l];
+              si[l] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      a.sdur[sb + i] = sv[i];
+      a.sts[sb + i] = a.op_ts[sb + si[i]];
+      a.srank[sb + i] = a.oprank[sb + si[i]];
+    }
+    if (threadIdx.x == 0) {
+      double t = -INFINITY;
+      for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) t = fmax(t, s_mx[q]);
+      a.opmax[kk] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// Warp-collective ascending sort of one u64 key per lane.
+__device__ inline unsigned long long warp_sort32(unsigned long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(FULL, v, jj);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & jj) == 0;
+      v = (lower == up) ? min(v, o) : max(v, o);
+    }
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kSfWarps * 32) k_sf_fast(DecideArgs a,
+                                                           unsigned* __restrict__ why,
+                                                           int pass) {
+  const SfPlan* pl = a.plan;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned long long total = pl->total;
+  const uint64_t nw = (uint64_t)gridDim.x * kSfWarps;
+  const int32_t opn = a.m.opn;
+  for (unsigned long long w = blockIdx.x * (uint64_t)kSfWarps + wib; w < total; w += nw) {
+    // trip of flattened candidate w
+    int32_t lo = 0, hi = a.J;  // cstart[lo] <= w < cstart[hi]
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pl->cstart[mid] <= w) lo = mid; else hi = mid;
+    }
+    const int32_t j = lo;
+    Cand* cands = a.pools.cand + a.state[j].cand_base;
+    const uint32_t x = static_cast<uint32_t>(w - pl->cstart[j]);
+    const Cand c = cands[x];
+    if (pass == 1 && c.pad != 3) continue;  // second pass: waited for cohorts only
+    // 0 not self-faulted, 1 self-faulted, 2 deferred to k_self_faulted,
+    // 3 needs a cohort median (claimed for k_cohorts_lazy; second pass)
+    int verdict = 0;
+    int reason = 0;
+    const int32_t r = c.rank;
+    const double t = a.trip_t[j];
+    if (c.it_hi < c.it_lo) {
+      verdict = 1;
+    } else if (a.sharded || a.f.n == 0 || opn <= 0) {
+      verdict = 2;
+      reason = 1;
+    } else if (r >= 0 && r < a.s.R) {
+      const uint32_t b = a.s.rank_off[r], e = a.s.rank_off[r + 1];
+      const bool uns = a.f.unsorted[r] != 0;
+      auto opat = [&](uint32_t i) { return a.s.op[a.f.at(uns, i)]; };
+      int64_t olo, ohi, x0, x1;
+      iter_ops(c.it_lo, opn, olo, x1);
+      iter_ops(c.it_hi, opn, x0, ohi);
+      const uint32_t fo = warp_partition_point(b, e, [&](uint32_t i) { return opat(i) >= olo; });
+      const uint32_t fe = warp_partition_point(fo, e, [&](uint32_t i) { return opat(i) > ohi; });
+      // the window's ops in ascending order: each op's run of the flow
+      // order, found by a partition point from the run start
+      bool pending = false;
+      for (uint32_t p0 = fo; p0 < fe && verdict == 0;) {
+        const int64_t o = opat(p0);
+        const uint32_t p1 = warp_partition_point(p0, fe, [&](uint32_t i) { return opat(i) > o; });
+        // r's completions of o (non-Recv, ts <= t): value k of the run on lane k
+        int kr = 0;
+        unsigned long long mv = 0;
+        for (uint32_t base = p0; base < p1 && kr <= 32; base += 32) {
+          const uint32_t i = base + lane;
+          bool ok = false;
+          unsigned long long dk = 0;
+          if (i < p1) {
+            const uint32_t p = a.f.at(uns, i);
+            const uint8_t ko = a.s.ko[p];
+            ok = ko_kind(ko) == CSG_KIND_COMPLETION && ko_opname(ko) != CSG_OP_RECV &&
+                 a.s.ts[p] <= t;
+            if (ok) dk = dkey(a.s.ts[p] - as_double(a.s.pa[p]));
+          }
+          const unsigned mm = __ballot_sync(FULL, ok);
+          for (unsigned q = mm; q; q &= q - 1) {
+            const int src = __ffs(q) - 1;
+            const unsigned long long v = __shfl_sync(FULL, dk, src);
+            if (lane == kr + __popc(mm & ((1u << src) - 1u))) mv = v;
+          }
+          kr += __popc(mm);
+        }
+        p0 = p1;
+        if (kr == 0) continue;
+        if (kr > 32) {
+          verdict = 2;
+          reason = 2;
+          break;
+        }
+        unsigned long long mine = lane < kr ? mv : 0ull;
+#pragma unroll
+        for (int s2 = 16; s2; s2 >>= 1) mine = max(mine, __shfl_xor_sync(FULL, mine, s2));
+        const uint64_t key = static_cast<uint64_t>(o - a.min_op);
+        const uint32_t sb = a.opoff[key], se = a.opoff[key + 1];
+        const uint32_t m = se - sb;
+        const double omx = a.opmax[key];
+        if (omx != omx || m < static_cast<uint32_t>(kr)) {
+          verdict = 2;
+          reason = 3;
+          break;
+        }
+        // entries after t: siblings = the sorted entries with ts <= t of
+        // other ranks; order statistic by two counting passes
+        const bool filtered = !(omx <= t);
+        uint32_t nsib = m - kr;
+        if (filtered) {
+          uint32_t cnt = 0;
+          for (uint32_t base = 0; base < m; base += 32) {
+            const uint32_t i = base + lane;
+            const bool keep = i < m && a.sts[sb + i] <= t && a.srank[sb + i] != r;
+            cnt += __popc(__ballot_sync(FULL, keep));
+          }
+          nsib = cnt;
+        }
+        double med;
+        if (nsib == 0) {
+          // no siblings: the (op name, iteration) cohort of k_cohorts
+          const int64_t it = iter_of(o, opn);
+          const uint8_t nm = a.m.op_name[static_cast<uint64_t>(o % opn)];
+          const unsigned long long ckey =
+              (static_cast<unsigned long long>(j) << 44) ^
+              (static_cast<unsigned long long>(nm) << 36) ^
+              (static_cast<unsigned long long>(it) & ((1ull << 36) - 1));
+          // 1 published, 2 claimed / pending (first pass only: the second
+          // pass and k_self_faulted must not leave claims nobody computes)
+          int found = 0;
+          double cv = 0;
+          if (lane == 0 && a.coh_cap) {
+            const uint32_t mask = a.coh_cap - 1;
+            uint32_t h = static_cast<uint32_t>((ckey * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+            for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h = (h + 1) & mask) {
+              const unsigned long long kk2 =
+                  pass == 0 ? atomicCAS(a.coh_key + h, ~0ull, ckey) : a.coh_key[h];
+              if (kk2 == ~0ull) {
+                if (pass == 0) {  // claimed: k_cohorts_lazy computes it
+                  a.coh_meta[h] = make_longlong2(it, (static_cast<long long>(j) << 8) | nm);
+                  found = 2;
+                }
+                break;
+              }
+              if (kk2 == ckey) {
+                if (*reinterpret_cast<volatile unsigned*>(a.coh_state + h) == 2u) {
+                  found = 1;
+                  cv = a.coh_val[h];
+                } else {
+                  found = 2;
+                }
+                break;
+              }
+            }
+          }
+          found = __shfl_sync(FULL, found, 0);
+          if (found == 2 && pass == 0) {  // decide the other ops, then wait for it
+            pending = true;
+            continue;
+          }
+          if (found != 1) {
+            verdict = 2;
+            reason = 5;
+            break;
+          }
+          med = __shfl_sync(FULL, cv, 0);
+        } else if (filtered) {
+          const uint32_t q = (nsib - 1) / 2;
+          uint32_t cnt = 0, at = 0;
+          for (uint32_t base = 0; base < m; base += 32) {
+            const uint32_t i = base + lane;
+            const bool keep = i < m && a.sts[sb + i] <= t && a.srank[sb + i] != r;
+            const unsigned mm = __ballot_sync(FULL, keep);
+            const uint32_t c2 = __popc(mm);
+            if (cnt + c2 > q) {  // the q-th kept entry is in this chunk
+              unsigned x2 = mm;
+              for (uint32_t z = cnt; z < q; ++z) x2 &= x2 - 1;
+              at = base + __ffs(x2) - 1;
+              break;
+            }
+            cnt += c2;
+          }
+          med = dkey_inv(a.sdur[sb + at]);
+        } else {
+          // element q of the sorted segment with r's kr values skipped
+          const uint32_t qm = (m - kr - 1) / 2;
+          const unsigned long long sorted_mine = warp_sort32(lane < kr ? mv : ~0ull);
+          const unsigned long long win = lane <= kr ? a.sdur[sb + qm + lane] : ~0ull;
+          int pos = 0;
+          for (int i = 0; i < kr; ++i) {
+            const unsigned long long vi = __shfl_sync(FULL, sorted_mine, i);
+            const unsigned long long lp = __shfl_sync(FULL, win, pos);
+            if (vi <= lp) ++pos; else break;
+          }
+          med = dkey_inv(__shfl_sync(FULL, win, pos));
+        }
+        if (med > 0 && dkey_inv(mine) > __dmul_rn(a.skew, med)) verdict = 1;
+      }
+      if (verdict == 0 && pending) verdict = 3;
+    }
+    if (lane == 0) {
+      cands[x].pad = static_cast<uint8_t>(verdict);
+      if (why) atomicAdd(why + reason, 1u);
+    }
+    __syncwarp();
   }
 }
 
@@ -3220,7 +4533,28 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       tbl_e.ensure(cells * 8);
       CSG_CUDA(cudaMemsetAsync(tbl_s.p, 0xff, cells * 8, st));
       CSG_CUDA(cudaMemsetAsync(tbl_e.p, 0, cells * 8, st));
-      if (R > 0) {
+      // straggler trips in time order (every run_detection batch): one pass
+      // over the store, then a running min/max over the trips' tables
+      bool ordered = true;
+      for (int32_t x = 1; x < Js; ++x)
+        ordered = ordered && h_t[h_strag[x]] >= h_t[h_strag[x - 1]];
+      static const bool inc_off = std::getenv("CSG_ITER_PER_TRIP") != nullptr;
+      if (R > 0 && ordered && !inc_off) {
+        {
+          const uint64_t warps = static_cast<uint64_t>(R);
+          ProfScope ps_(c->lc, "k_iter_tables", st);
+          k_iter_tables_inc<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
+              sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it, M,
+              tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>());
+        }
+        if (Js > 1) {
+          const uint64_t per = static_cast<uint64_t>(M) * n_it;
+          ProfScope ps_(c->lc, "k_iter_prefix", st);
+          k_iter_prefix<<<static_cast<unsigned>(std::min<uint64_t>((per + 255) / 256, 148 * 16)),
+                          256, 0, st>>>(Js, per, tbl_s.as<unsigned long long>(),
+                                        tbl_e.as<unsigned long long>());
+        }
+      } else if (R > 0) {
         const uint64_t warps = static_cast<uint64_t>(R) * Js;
         ProfScope ps_(c->lc, "k_iter_tables", st);
         k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
@@ -3307,11 +4641,34 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   if (Js > 0 && opn > 0 && M > 0) {
     store_build_op_index(s, opn);
     const uint64_t warps = static_cast<uint64_t>(M) * Js;
-    ProfScope ps_(c->lc, "k_flow", st);
-    k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
-        sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
-        slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
-        aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>());
+    static const bool flow_scan = std::getenv("CSG_FLOW_SCAN") != nullptr;
+    if (!flow_scan && s->flow_indexed) {
+      DevBuf& spill = c->buf("rca.flow_spill");
+      spill.ensure(warps * 4 + 16);
+      unsigned* nsp = spill.as<unsigned>();
+      CSG_CUDA(cudaMemsetAsync(nsp, 0, 16, st));
+      {
+        ProfScope ps_(c->lc, "k_flow_fi", st);
+        k_flow_fi<<<static_cast<unsigned>((warps * 32 + kFlow2Warps * 32 - 1) / (kFlow2Warps * 32)),
+                    kFlow2Warps * 32, 0, st>>>(
+            sv, s->flow_view(), mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+            slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+            aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>(),
+            spill.as<uint32_t>() + 4, nsp);
+      }
+      ProfScope ps_(c->lc, "k_flow", st);
+      k_flow<<<148 * 2, kFlowWarps * 32, 0, st>>>(
+          sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+          slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+          aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>(),
+          spill.as<uint32_t>() + 4, nsp);
+    } else {
+      ProfScope ps_(c->lc, "k_flow", st);
+      k_flow<<<static_cast<unsigned>((warps * 32 + 127) / 128), 128, 0, st>>>(
+          sv, mv, Js, dstrag, dt, cfg.delta_ms, cfg.flow_skew_factor, k, M,
+          slot_group.as<uint32_t>(), rs.as<RankSum>(), gi.as<GroupIter>(),
+          aff_flag.as<uint8_t>(), fs.as<FlowSum>(), err.as<uint32_t>(), nullptr, nullptr);
+    }
     comm_allreduce(c, fs.p, static_cast<size_t>(Js) * M * sizeof(FlowSum) / 8,
                    ncclUint64, ncclSum);
   }
@@ -3524,6 +4881,62 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   a.sharded = comm_active(c) ? 1 : 0;
   a.n_opidx = s->op_indexed ? s->n_opidx : 0;
   a.min_op = s->min_op;
+  a.max_op = s->max_op;
+  a.sf_fast = 0;
+  a.f = FlowView();
+  a.opoff = nullptr;
+  a.sdur = nullptr;
+  a.sts = nullptr;
+  a.srank = nullptr;
+  a.opmax = nullptr;
+  a.plan = nullptr;
+  static const bool sf_slow = std::getenv("CSG_SF_SLOW") != nullptr;
+  DevBuf& d_sfl = c->buf("rca.sf_large");
+  constexpr uint32_t kLargeCap = 1u << 16;
+  if (Js > 0 && !a.sharded && !sf_slow && s->op_indexed && s->flow_indexed) {
+    a.sf_fast = 1;
+    a.f = s->flow_view();
+    a.opoff = s->op_seg_off.as<uint32_t>();
+    DevBuf& d_sdur = c->buf("rca.sdur");
+    d_sdur.ensure(s->n_opidx * 8 + 16);
+    a.sdur = d_sdur.as<unsigned long long>();
+    DevBuf& d_sts = c->buf("rca.sts");
+    d_sts.ensure(s->n_opidx * 8 + 16);
+    a.sts = d_sts.as<double>();
+    DevBuf& d_srk = c->buf("rca.srank");
+    d_srk.ensure(s->n_opidx * 4 + 16);
+    a.srank = d_srk.as<int32_t>();
+    DevBuf& d_opmax = c->buf("rca.opmax");
+    const uint64_t range = s->max_op >= s->min_op ? static_cast<uint64_t>(s->max_op - s->min_op) : 0;
+    d_opmax.ensure((range + 2) * 8 + 16);
+    a.opmax = d_opmax.as<double>();
+    DevBuf& d_plan2 = c->buf("rca.sf_plan");
+    d_plan2.ensure(sizeof(SfPlan) + static_cast<size_t>(J + 1) * 8 + 16);
+    a.plan = d_plan2.as<SfPlan>();
+    d_sfl.ensure(static_cast<size_t>(kLargeCap) * 4 + 64);
+  }
+  static const bool sl_serial = std::getenv("CSG_SL_SERIAL") != nullptr;
+  a.sl_par = (Js > 0 && !sl_serial && M > 0 && opn > 0) ? 1 : 0;
+  a.strag_trip = dstrag;
+  DevBuf& d_sll = c->buf("rca.sl_late");
+  DevBuf& d_slc = c->buf("rca.sl_cnt");
+  if (a.sl_par) {
+    d_sll.ensure(static_cast<size_t>(Js) * M + 16);
+    d_slc.ensure(static_cast<size_t>(Js) * std::max(G, 1) * sizeof(uint2) + 16);
+    CSG_CUDA(cudaMemsetAsync(d_sll.p, 0, static_cast<size_t>(Js) * M, st));
+  }
+  a.sl_late = d_sll.as<uint8_t>();
+  a.emit_rank = nullptr;
+  a.emit_stride = 0;
+  static const bool emit_serial = std::getenv("CSG_SL_SERIAL") != nullptr;
+  if (Js > 0 && !emit_serial) {
+    const uint64_t RS = static_cast<uint64_t>(std::max(m->view().rank_space, 1));
+    a.emit_stride = RS + 2 * ((RS + 31) / 32) + 8;
+    DevBuf& d_er = c->buf("rca.emit_rank");
+    d_er.ensure(static_cast<size_t>(J) * a.emit_stride * 4 + 16);
+    a.emit_rank = d_er.as<uint32_t>();
+  }
+  a.sl_cnt = d_slc.as<uint2>();
   a.scratch_per_trip = static_cast<uint32_t>(spt);
   DevBuf& d_state = c->buf("rca.strag_state");
   d_state.ensure(static_cast<size_t>(J) * sizeof(StragState) + 16);
@@ -3538,12 +4951,18 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   if (Js > 0) d_sf.ensure(static_cast<size_t>(kSfBlocks) * a.sf_words * 4);
   a.sf_scratch = d_sf.as<uint32_t>();
   DevBuf& d_coh = c->buf("rca.cohort");
-  a.coh_cap = Js > 0 ? 4096 : 0;
+  a.coh_cap = 0;
+  if (Js > 0) {  // (trip, op name, iteration) cohorts: room for 32 iterations per trip
+    uint32_t cap = 4096;
+    while (cap < static_cast<uint64_t>(J) * kCohortNames * 64) cap <<= 1;
+    a.coh_cap = cap;
+  }
   if (Js > 0) {
-    d_coh.ensure(static_cast<size_t>(a.coh_cap) * 20 + 64);
+    d_coh.ensure(static_cast<size_t>(a.coh_cap) * 36 + 64);
     a.coh_key = d_coh.as<unsigned long long>();
     a.coh_val = reinterpret_cast<double*>(a.coh_key + a.coh_cap);
-    a.coh_state = reinterpret_cast<unsigned*>(a.coh_val + a.coh_cap);
+    a.coh_meta = reinterpret_cast<longlong2*>(a.coh_val + a.coh_cap);
+    a.coh_state = reinterpret_cast<unsigned*>(a.coh_meta + a.coh_cap);
   }
   a.phase = 1;
   a.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
@@ -3605,6 +5024,26 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ProfScope ps_(c->lc, "k_exonerate", st);
       k_exonerate<<<static_cast<unsigned>(n_exo_grid), kExoThreads, kExoSmemMax, st>>>(ea);
     }
+    if (a.sl_par) {  // straggler candidates, every (trip, group) in parallel
+      const uint64_t wg = static_cast<uint64_t>(Js) * G;
+      const unsigned gb = static_cast<unsigned>((wg + kSlWarps - 1) / kSlWarps);
+      {  // every attempt: k_sl_scan turns the counts into offsets in place
+        ProfScope ps_(c->lc, "k_sl_late", st);
+        k_sl_late<<<gb, kSlWarps * 32, 0, st>>>(a, Js);
+      }
+      {
+        ProfScope ps_(c->lc, "k_sl_count", st);
+        k_sl_count<<<gb, kSlWarps * 32, 0, st>>>(a, Js);
+      }
+      {
+        ProfScope ps_(c->lc, "k_sl_scan", st);
+        k_sl_scan<<<Js, 1024, 0, st>>>(a);
+      }
+      {
+        ProfScope ps_(c->lc, "k_sl_emit", st);
+        k_sl_emit<<<gb, kSlWarps * 32, 0, st>>>(a, Js);
+      }
+    }
     if (!dev_plan) {  // device-planned batches are failure-only: k_exonerate wrote every trip
       ProfScope ps_(c->lc, "k_decide", st);
       a.phase = 1;
@@ -3615,10 +5054,52 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       // per-trip filter + report
       CSG_CUDA(cudaMemsetAsync(a.coh_key, 0xff, static_cast<size_t>(a.coh_cap) * 8, st));
       CSG_CUDA(cudaMemsetAsync(a.coh_state, 0, static_cast<size_t>(a.coh_cap) * 4, st));
-      {
+      if (!a.sf_fast) {  // every cohort of the candidates' windows, up front
         ProfScope ps_(c->lc, "k_cohorts", st);
         k_cohorts<<<dim3(J, static_cast<unsigned>(std::max(k, 1) + 1), kCohortNames),
                     kDecideThreads, shm, st>>>(a);
+      }
+      if (a.sf_fast) {
+        unsigned* nl = d_sfl.as<unsigned>();
+        unsigned* large = nl + 16;
+        CSG_CUDA(cudaMemsetAsync(nl, 0, 16, st));
+        {
+          ProfScope ps_(c->lc, "k_sf_prep", st);
+          k_sf_prep<<<1, 1024, 0, st>>>(a);
+        }
+        {
+          ProfScope ps_(c->lc, "k_opsort", st);
+          k_opsort<<<148 * 4, 256, 0, st>>>(a, large, nl, kLargeCap);
+        }
+        {
+          const size_t lsm = static_cast<size_t>(kOpSortBlockCap) * 10;
+          smem_optin(k_opsort_large, lsm);
+          ProfScope ps_(c->lc, "k_opsort_large", st);
+          k_opsort_large<<<148, 1024, lsm, st>>>(a, large, nl, kLargeCap);
+        }
+        static const bool dbg_sf = std::getenv("CSG_DEBUG_SF") != nullptr;
+        unsigned* why = dbg_sf ? nl + 8 : nullptr;
+        if (why) CSG_CUDA(cudaMemsetAsync(why, 0, 8 * 4, st));
+        {
+          ProfScope ps_(c->lc, "k_sf_fast", st);
+          k_sf_fast<<<148 * 16, kSfWarps * 32, 0, st>>>(a, why, 0);
+        }
+        {  // the cohorts the first pass asked for, then their candidates again
+          ProfScope ps_(c->lc, "k_cohorts", st);
+          k_cohorts_lazy<<<148 * 2, kDecideThreads, shm, st>>>(a);
+        }
+        {
+          ProfScope ps_(c->lc, "k_sf_fast", st);
+          k_sf_fast<<<148 * 16, kSfWarps * 32, 0, st>>>(a, nullptr, 1);
+        }
+        if (why) {
+          unsigned hw[8];
+          CSG_CUDA(cudaMemcpyAsync(hw, why, sizeof(hw), cudaMemcpyDeviceToHost, st));
+          CSG_CUDA(cudaStreamSynchronize(st));
+          fprintf(stderr, "k_sf_fast: decided %u, deferred: no index %u, >32 completions %u, "
+                  "unsorted segment %u, -- %u, cohort missing %u\n",
+                  hw[0], hw[1], hw[2], hw[3], hw[4], hw[5]);
+        }
       }
       {
         ProfScope ps_(c->lc, "k_self_faulted", st);
@@ -3674,9 +5155,15 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (!(h_err & (DEV_ERR_POOL | DEV_ERR_DAG_SCRATCH))) break;
     if (attempt >= 6)
       throw Error(CSG_ERR_RUNTIME, "engine: RCA output pools exhausted");
-    if (a.debug)
-      fprintf(stderr, "rca retry: %s%s\n", (h_err & DEV_ERR_POOL) ? "pools " : "",
-              (h_err & DEV_ERR_DAG_SCRATCH) ? "dag-scratch" : "");
+    static const bool dbg_retry = std::getenv("CSG_DEBUG_RETRY") != nullptr;
+    if (a.debug || dbg_retry)
+      fprintf(stderr, "rca retry %d: %s%s used cand %llu/%llu cev %llu/%llu sus %llu/%llu ev %llu/%llu\n",
+              attempt, (h_err & DEV_ERR_POOL) ? "pools " : "",
+              (h_err & DEV_ERR_DAG_SCRATCH) ? "dag-scratch" : "",
+              (unsigned long long)used[P_CAND], (unsigned long long)cand_cap,
+              (unsigned long long)used[P_CEV], (unsigned long long)cev_cap,
+              (unsigned long long)used[P_SUS], (unsigned long long)sus_cap,
+              (unsigned long long)used[P_EV], (unsigned long long)ev_cap);
     if (h_err & DEV_ERR_DAG_SCRATCH) {
       bits_cap = std::max<uint64_t>(bits_cap * 4, used[P_BITS] * 2);
       c->rca_bits_cap = bits_cap;

@@ -363,6 +363,7 @@ struct ScatterOut {
   int2* cc;         // {comm, channel}
   uint8_t* ko;      // kind | op_name << 1
   uint32_t* perm;   // store index per rank-major position (payload via perm)
+  uint4* aos;       // experiment (CSG_SCATTER_CFG=9): one 32-byte record per position
 };
 
 // --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
@@ -406,7 +407,7 @@ __device__ inline void mbar_wait(unsigned long long* m, uint32_t parity) {
 // is written once into the rank-major SoA columns in contiguous digit runs.
 // bx[d] carries the running global base of digit d through the sub-tiles of
 // one histogram tile.
-template <int ITEMS, int NBUF, int DPT>
+template <int ITEMS, int NBUF, int DPT, bool AOS = false>
 __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
@@ -601,11 +602,21 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
         const uint32_t p = p0 + k * kTileThreads;
         if (p >= cnt) break;
         const uint32_t qq = q[k];
+        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
+        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
+        if (AOS) {
+          const uint32_t ko = (kind & 1) | (name << 1);
+          uint4* d = o.aos + 2ull * qq;
+          d[0] = make_uint4(static_cast<uint32_t>(h0[k].x), static_cast<uint32_t>(h0[k].x >> 32),
+                            static_cast<uint32_t>(h0[k].y), static_cast<uint32_t>(h0[k].y >> 32));
+          d[1] = make_uint4(static_cast<uint32_t>(hm[k].x >> 32),
+                            static_cast<uint32_t>(hm[k].y & 0xffffu) | (ko << 16),
+                            static_cast<uint32_t>(first + li[k]), 0u);
+          continue;
+        }
         o.tso[qq] = h0[k];
         o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
                              static_cast<int32_t>(hm[k].y & 0xffffffffu));
-        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
-        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
         o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
         o.perm[qq] = static_cast<uint32_t>(first + li[k]);
       }
@@ -1308,6 +1319,21 @@ __global__ void k_opidx_scatter(StoreView s, const uint32_t* __restrict__ offs,
   }
 }
 
+// Dense op-segment offsets of the op index: off[k] = first entry with key
+// >= k, k in [0, range + 1] (keys = op - min_op, sorted ascending).
+__global__ void k_opidx_off(const uint64_t* __restrict__ keys, uint64_t n, uint64_t range,
+                            uint32_t* __restrict__ off) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= range + 1;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    off[k] = static_cast<uint32_t>(lo);
+  }
+}
+
 unsigned grid_for(uint64_t n, int threads = 256) {
   uint64_t g = (n + threads - 1) / threads;
   if (g > 148ull * 64) g = 148ull * 64;
@@ -1356,11 +1382,30 @@ void store_build_index(csg_store* s) {
   const uint32_t ntiles = static_cast<uint32_t>((n + kTile - 1) / kTile);
   DevBuf& hcnt = c->buf("index.hist");
   hcnt.ensure(static_cast<size_t>(kHistDigits) * ntiles * 4 + 16);
-  if (n) {
+  // CSG_SCATTER_CFG: 0 = block-ranked persistent scatter (k_scatter),
+  // 2 = its single-buffered variants, 3 = 2-D tensor-copy scatter
+  static const int cfg = std::getenv("CSG_SCATTER_CFG") ? std::atoi(std::getenv("CSG_SCATTER_CFG")) : 0;
+  // A store whose last build took the general (wide rank span) path is
+  // rebuilt the same way: its first pass writes the statistics together
+  // with the (rank, store index) sort pairs, instead of a digit histogram
+  // the general path never reads (one pass over the records less). If the
+  // statistics then call for the fused path, its histogram pass runs after.
+  static const bool spec_on0 = std::getenv("CSG_INDEX_NOSPEC") == nullptr;
+  const bool keys_first = spec_on0 && s->spec_general && n > 0 && n <= 0xFFFFFFF0ull;
+  auto stats_keys = [&](StoreStats* sdst) {
+    ProfScope ps_(c->lc, "k_stats_keys", st);
+    const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, 148ull * 8));
+    k_stats_keys<<<g, 256, 0, st>>>(recs, n, sdst, s->keys.as<uint32_t>(),
+                                    s->perm.as<uint32_t>());
+  };
+  auto stats_hist = [&](StoreStats* sdst) {
     ProfScope ps_(c->lc, "k_stats_hist", st);
-    k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, s->stats_dev.as<StoreStats>(),
-                                                  hcnt.as<uint32_t>());
-  }
+    k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, sdst, hcnt.as<uint32_t>());
+  };
+  DevBuf& st2 = c->buf("index.stats2");  // statistics of a second pass (discarded)
+  st2.ensure(sizeof(StoreStats));
+  if (keys_first) stats_keys(s->stats_dev.as<StoreStats>());
+  else if (n) stats_hist(s->stats_dev.as<StoreStats>());
   if (comm_active(c)) {
     // global stats over the shards (identical rank space, ticks, op range)
     // one MAX all-reduce over order-preserving u64 images (minima as
@@ -1401,6 +1446,10 @@ void store_build_index(csg_store* s) {
   const bool fused = n && !force_general &&
                      static_cast<int64_t>(lmax_) - lmin_ < kHistDigits;
   if (fused) {
+    if (keys_first) {  // speculated the general path: the histogram is missing
+      CSG_CUDA(cudaMemcpyAsync(st2.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+      stats_hist(st2.as<StoreStats>());
+    }
     // one stable counting-sort pass over the rank digits (see k_scatter)
     const int32_t lmin = lmin_;
     const int32_t D = lmax_ - lmin + 1;
@@ -1427,11 +1476,10 @@ void store_build_index(csg_store* s) {
                                              goff.as<uint32_t>(), go);
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                 s->perm.as<uint32_t>()};
+                 s->perm.as<uint32_t>(), nullptr};
     // Persistent, one CTA per SM, sub-tiles double-buffered by bulk copies:
     // 2048 records for rank spans <= 1024, 1024 records (wider digit tables)
     // up to 2048. CSG_SCATTER_CFG=2: single-buffered variants.
-    static const int cfg = std::getenv("CSG_SCATTER_CFG") ? std::atoi(std::getenv("CSG_SCATTER_CFG")) : 0;
     const bool narrow = D <= 1024;
     const int TR = narrow ? 2048 : 1024;
     const int nbuf = cfg == 2 ? 1 : 2;
@@ -1464,9 +1512,20 @@ void store_build_index(csg_store* s) {
         else
           k_scatter_tx<4><<<grid, kTxThreads, sm, st>>>(tm, n, g, ntiles, lmin, D, o,
                                                         lmax_, R, ro, go);
-      } else if (nbuf == 2 && narrow)
+      } else if (nbuf == 2 && narrow) {
+        if (cfg == 9) {  // experiment: the same scatter into one 32-byte AoS record
+          DevBuf& aos = c->buf("index.aos_experiment");
+          aos.ensure(n * 32 + 64);
+          ScatterOut oa = o;
+          oa.aos = aos.as<uint4>();
+          smem_optin(k_scatter<8, 2, 4, true>, 2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4);
+          ProfScope pa_(c->lc, "k_scatter_aos", st);
+          k_scatter<8, 2, 4, true><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D,
+                                                                    oa, lmax_, R, ro, go);
+        }
         k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
+      }
       else if (nbuf == 2)
         k_scatter<4, 2, 8><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
@@ -1479,14 +1538,9 @@ void store_build_index(csg_store* s) {
     }
   } else {
     // general path: (rank, store index) pairs, LSD radix sort, gather
-    if (n) {
-      DevBuf& st2 = c->buf("index.stats2");
-      st2.ensure(sizeof(StoreStats));
+    if (n && !keys_first) {
       CSG_CUDA(cudaMemcpyAsync(st2.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-      ProfScope ps_(c->lc, "k_stats_keys", st);
-      const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, 148ull * 8));
-      k_stats_keys<<<g, 256, 0, st>>>(recs, n, st2.as<StoreStats>(), s->keys.as<uint32_t>(),
-                                      s->perm.as<uint32_t>());
+      stats_keys(st2.as<StoreStats>());
     }
     if (n) {
       radix_sort_u32(s->keys.as<uint32_t>(), s->perm.as<uint32_t>(), n,
@@ -1495,7 +1549,7 @@ void store_build_index(csg_store* s) {
       {
         ProfScope ps_(c->lc, "k_gather", st);
         ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                     s->perm.as<uint32_t>()};
+                     s->perm.as<uint32_t>(), nullptr};
         k_gather<<<grid_for(n), 256, 0, st>>>(recs, s->perm.as<uint32_t>(), n, o);
       }
     }
@@ -1587,6 +1641,8 @@ void store_build_index(csg_store* s) {
   s->sp_lmin = h.lmin_rank;
   s->sp_lmax = h.lmax_rank;
   s->sp_R = R;
+  s->spec_general = n && (force_general ||
+                          static_cast<int64_t>(h.lmax_rank) - h.lmin_rank >= kHistDigits);
   // the longest segment stays on the device until the next host round trip
   // (trigger_run picks it up with the trips); shards agree on it over NCCL
   s->max_seg = 0;
@@ -1721,6 +1777,13 @@ void store_build_op_index(csg_store* s, int32_t opn) {
           s->opidx_dur.as<double>(), s->opidx_nm.as<uint8_t>());
     }
     s->n_opidx = total;  // padding sorted to the end
+  }
+  {  // dense per-op segment offsets (the straggler self-evidence lookups)
+    const uint64_t range = s->max_op >= s->min_op ? static_cast<uint64_t>(s->max_op - s->min_op) : 0;
+    s->op_seg_off.ensure((range + 2) * 4 + 16);
+    ProfScope ps_(c->lc, "k_opidx_off", st);
+    k_opidx_off<<<grid_for(range + 2), 256, 0, st>>>(s->opidx_keys.as<uint64_t>(), s->n_opidx,
+                                                     range, s->op_seg_off.as<uint32_t>());
   }
   CSG_CUDA(cudaGetLastError());
   s->op_indexed = true;

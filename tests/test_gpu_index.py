@@ -67,7 +67,7 @@ import numpy as np
 sys.path.insert(0, %(root)r)
 from paper_2509_03018_b200 import engine as E
 cfg = json.load(open(os.path.join(%(root)r, 'configs', 'c2_mini_128.json')))
-cfg['layout']['dp'] = 64
+cfg['layout']['dp'] = %(dp)d
 cfg['sim']['max_sim_ms'] = 2600.0
 cfg['faults'][0]['onset_ms'] = 1504.0
 scen = E.Scenario.parse(json.dumps(cfg))
@@ -96,14 +96,17 @@ print(json.dumps(out))
 
 
 @pytest.mark.gpu
-def test_speculative_index_layout_matches_fresh_builds():
+@pytest.mark.parametrize("dp", [64, 160])
+def test_speculative_index_layout_matches_fresh_builds(dp):
     """Rebuilding one store over the same rank layout launches the index on
     the last layout before the statistics reach the host (store_build_index);
     hits (same span, any n), misses (other span) and invalid input must give
-    exactly what builds without speculation give."""
+    exactly what builds without speculation give. dp=160 (2560 ranks) takes
+    the general path, whose rebuilds write the sort pairs in the statistics
+    pass (and miss to the fused path for the narrow slices)."""
     def go(env_extra):
         env = dict(os.environ, **env_extra)
-        r = subprocess.run([sys.executable, "-c", SPEC_CHILD % dict(root=ROOT)], env=env,
+        r = subprocess.run([sys.executable, "-c", SPEC_CHILD % dict(root=ROOT, dp=dp)], env=env,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         return json.loads(r.stdout.strip().splitlines()[-1])
