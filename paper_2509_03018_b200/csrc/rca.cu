@@ -379,7 +379,7 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
                             SuccProg* __restrict__ out,
                             unsigned long long* __restrict__ sp_key,
                             int32_t nch, const uint32_t* __restrict__ slots,
-                            uint32_t nslots) {
+                            uint32_t nslots, const int32_t* __restrict__ trip_kind) {
   extern __shared__ uint32_t sp_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -388,6 +388,8 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
   const uint32_t E = slots ? nslots : M;
   if (w >= static_cast<int64_t>(E) * J) return;
   const int32_t j = static_cast<int32_t>(w / E);
+  // only failure analysis reads the successor's progress (k_fail_cands)
+  if (trip_kind[j] != CSG_TRIGGER_FAILURE) return;
   const uint32_t q = slots ? slots[w % E] : static_cast<uint32_t>(w % E);
   uint32_t* tbl = sp_tbl + wib * nch;
   for (int c = lane; c < nch; c += 32) tbl[c] = 0;
@@ -1168,6 +1170,11 @@ struct DecideArgs {
   double* coh_val;
   unsigned* coh_state;          // 2 = value published
   longlong2* coh_meta;          // claimed slot: {iteration, trip << 8 | op name}
+  // per (op name, iteration) over all entries: median, latest timestamp
+  unsigned long long* coh2_key;
+  double* coh2_val;
+  double* coh2_mx;
+  unsigned* coh2_state;
   uint32_t coh_cap;
   StoreView s;
   ModelView m;
@@ -1380,11 +1387,17 @@ __device__ double block_select(uint64_t n, uint64_t kth, G get,
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.hist[i] = 0;
     __syncthreads();
     const uint64_t mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    // warp-aggregated digit counts: skewed key sets (durations share their
+    // top bytes) would serialise on one shared-memory counter otherwise
+    for (uint64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+      const uint64_t i = b0 + threadIdx.x;
+      uint32_t d = 256;
       uint64_t key;
-      if (!get(i, &key)) continue;
-      if ((key & mask) != (prefix & mask)) continue;
-      atomicAdd(&sh.hist[(key >> shift) & 255], 1u);
+      if (i < n && get(i, &key) && (key & mask) == (prefix & mask))
+        d = static_cast<uint32_t>((key >> shift) & 255);
+      const unsigned peers = __match_any_sync(FULL, d);
+      if (d < 256 && (threadIdx.x & 31) == __ffs(peers) - 1)
+        atomicAdd(&sh.hist[d], static_cast<uint32_t>(__popc(peers)));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1612,10 +1625,15 @@ __device__ double staged_lower_median(uint64_t n, G get, BlockShared& sh, int* m
     s_over = 0;
   }
   __syncthreads();
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    uint64_t key;
-    if (get(i, &key)) {
-      const uint32_t at = atomicAdd(&s_n, 1u);
+  for (uint64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+    const uint64_t i = b0 + threadIdx.x;
+    uint64_t key = 0;
+    const bool ok = i < n && get(i, &key);
+    const unsigned mm = __ballot_sync(FULL, ok);  // one counter update per warp
+    uint32_t at = 0;
+    if ((threadIdx.x & 31) == 0 && mm) at = atomicAdd(&s_n, static_cast<uint32_t>(__popc(mm)));
+    at = __shfl_sync(FULL, at, 0) + __popc(mm & ((1u << (threadIdx.x & 31)) - 1u));
+    if (ok) {
       if (at < kCap) keys[at] = key; else s_over = 1;
     }
   }
@@ -1662,9 +1680,15 @@ __device__ double small_select(uint64_t n, uint64_t kth, G get, BlockShared& sh)
   __shared__ uint32_t s_n;
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    uint64_t key;
-    if (get(i, &key)) keys[atomicAdd(&s_n, 1u)] = key;
+  for (uint64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+    const uint64_t i = b0 + threadIdx.x;
+    uint64_t key = 0;
+    const bool ok = i < n && get(i, &key);
+    const unsigned mm = __ballot_sync(FULL, ok);
+    uint32_t at = 0;
+    if ((threadIdx.x & 31) == 0 && mm) at = atomicAdd(&s_n, static_cast<uint32_t>(__popc(mm)));
+    at = __shfl_sync(FULL, at, 0) + __popc(mm & ((1u << (threadIdx.x & 31)) - 1u));
+    if (ok) keys[at] = key;
   }
   __syncthreads();
   const uint32_t m = s_n;
@@ -3469,12 +3493,77 @@ __global__ void __launch_bounds__(kDecideThreads) k_cohorts(DecideArgs a) {
 __global__ void __launch_bounds__(kDecideThreads) k_cohorts_lazy(DecideArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   BlockShared& sh = *reinterpret_cast<BlockShared*>(dyn);
+  __shared__ int s_mine, s_slot2;
   for (uint32_t h = blockIdx.x; h < a.coh_cap; h += gridDim.x) {
     if (a.coh_key[h] == ~0ull || a.coh_state[h] == 2u) continue;
     const longlong2 mt = a.coh_meta[h];
     const int32_t j = static_cast<int32_t>(mt.y >> 8);
     const uint8_t nm = static_cast<uint8_t>(mt.y & 0xff);
-    const double med = cohort_median(a, mt.x, nm, a.trip_t[j], sh);
+    const double t = a.trip_t[j];
+    // The (op name, iteration) cohort over all of its entries, once per
+    // batch: trips whose time follows every entry use it as is (the ts <= t
+    // filter keeps everything); the claimer computes, the others wait.
+    const unsigned long long key2 =
+        (static_cast<unsigned long long>(nm) << 48) ^
+        (static_cast<unsigned long long>(mt.x) & ((1ull << 48) - 1));
+    if (threadIdx.x == 0) {
+      s_mine = 0;
+      s_slot2 = -1;
+      const uint32_t mask = a.coh_cap - 1;
+      uint32_t h2 = static_cast<uint32_t>((key2 * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+      for (uint32_t probe = 0; probe < a.coh_cap; ++probe, h2 = (h2 + 1) & mask) {
+        const unsigned long long k2 = atomicCAS(a.coh2_key + h2, ~0ull, key2);
+        if (k2 == ~0ull || k2 == key2) {
+          s_mine = k2 == ~0ull;
+          s_slot2 = static_cast<int>(h2);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    double med = 0;
+    bool done = false;
+    if (s_slot2 >= 0) {
+      const int h2 = s_slot2;
+      if (s_mine) {
+        const double mall = cohort_median(a, mt.x, nm, INFINITY, sh);
+        // latest timestamp of the cohort's entries
+        int64_t olo, ohi;
+        iter_ops(mt.x, a.m.opn, olo, ohi);
+        const bool empty = ohi < a.min_op;
+        const uint64_t k0 = olo < a.min_op ? 0 : static_cast<uint64_t>(olo - a.min_op);
+        const uint64_t k1 = empty ? 0 : static_cast<uint64_t>(ohi - a.min_op);
+        uint64_t cb, ce;
+        op_segment(a, k0, k1, empty, sh, cb, ce);
+        double mx = -INFINITY;
+        for (uint64_t y = cb + threadIdx.x; y < ce; y += blockDim.x)
+          if (a.op_nm[y] == nm) mx = fmax(mx, a.op_ts[y]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        if ((threadIdx.x & 31) == 0) sh.red_u[0][threadIdx.x >> 5] = dkey(mx);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned long long m2 = 0;
+          for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) m2 = max(m2, sh.red_u[0][q]);
+          a.coh2_val[h2] = mall;
+          a.coh2_mx[h2] = dkey_inv(m2);
+          __threadfence();
+          atomicExch(a.coh2_state + h2, 2u);
+        }
+        __syncthreads();
+      } else if (threadIdx.x == 0) {
+        while (*reinterpret_cast<volatile unsigned*>(a.coh2_state + h2) != 2u) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      const double mx = *reinterpret_cast<volatile double*>(a.coh2_mx + h2);
+      if (mx <= t) {
+        med = *reinterpret_cast<volatile double*>(a.coh2_val + h2);
+        done = true;
+      }
+    }
+    if (!done) med = cohort_median(a, mt.x, nm, t, sh);
     if (threadIdx.x == 0) {
       a.coh_val[h] = med;
       __threadfence();
@@ -4496,7 +4585,8 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                     wpb * nch * 4, st>>>(sv, s->flow_view(), mv, J, M,
                                          slot_group.as<uint32_t>(), rs.as<RankSum>(),
                                          succ.as<SuccProg>(),
-                                         succ_key.as<unsigned long long>(), nch, slots, E);
+                                         succ_key.as<unsigned long long>(), nch, slots, E,
+                                         dkind);
     }
   }
   if (!affected_only && M > 0) {
@@ -4958,11 +5048,15 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     a.coh_cap = cap;
   }
   if (Js > 0) {
-    d_coh.ensure(static_cast<size_t>(a.coh_cap) * 36 + 64);
+    d_coh.ensure(static_cast<size_t>(a.coh_cap) * 64 + 64);
     a.coh_key = d_coh.as<unsigned long long>();
     a.coh_val = reinterpret_cast<double*>(a.coh_key + a.coh_cap);
     a.coh_meta = reinterpret_cast<longlong2*>(a.coh_val + a.coh_cap);
-    a.coh_state = reinterpret_cast<unsigned*>(a.coh_meta + a.coh_cap);
+    a.coh2_key = reinterpret_cast<unsigned long long*>(a.coh_meta + a.coh_cap);
+    a.coh2_val = reinterpret_cast<double*>(a.coh2_key + a.coh_cap);
+    a.coh2_mx = a.coh2_val + a.coh_cap;
+    a.coh_state = reinterpret_cast<unsigned*>(a.coh2_mx + a.coh_cap);
+    a.coh2_state = a.coh_state + a.coh_cap;
   }
   a.phase = 1;
   a.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
@@ -5053,7 +5147,8 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       // straggler self-evidence over every candidate in parallel, then the
       // per-trip filter + report
       CSG_CUDA(cudaMemsetAsync(a.coh_key, 0xff, static_cast<size_t>(a.coh_cap) * 8, st));
-      CSG_CUDA(cudaMemsetAsync(a.coh_state, 0, static_cast<size_t>(a.coh_cap) * 4, st));
+      CSG_CUDA(cudaMemsetAsync(a.coh_state, 0, static_cast<size_t>(a.coh_cap) * 8, st));
+      CSG_CUDA(cudaMemsetAsync(a.coh2_key, 0xff, static_cast<size_t>(a.coh_cap) * 8, st));
       if (!a.sf_fast) {  // every cohort of the candidates' windows, up front
         ProfScope ps_(c->lc, "k_cohorts", st);
         k_cohorts<<<dim3(J, static_cast<unsigned>(std::max(k, 1) + 1), kCohortNames),

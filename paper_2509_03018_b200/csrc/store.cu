@@ -363,7 +363,6 @@ struct ScatterOut {
   int2* cc;         // {comm, channel}
   uint8_t* ko;      // kind | op_name << 1
   uint32_t* perm;   // store index per rank-major position (payload via perm)
-  uint4* aos;       // experiment (CSG_SCATTER_CFG=9): one 32-byte record per position
 };
 
 // --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
@@ -407,7 +406,7 @@ __device__ inline void mbar_wait(unsigned long long* m, uint32_t parity) {
 // is written once into the rank-major SoA columns in contiguous digit runs.
 // bx[d] carries the running global base of digit d through the sub-tiles of
 // one histogram tile.
-template <int ITEMS, int NBUF, int DPT, bool AOS = false>
+template <int ITEMS, int NBUF, int DPT>
 __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
     k_scatter(const csg_packed_record* __restrict__ r, uint64_t n,
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
@@ -602,21 +601,11 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
         const uint32_t p = p0 + k * kTileThreads;
         if (p >= cnt) break;
         const uint32_t qq = q[k];
-        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
-        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
-        if (AOS) {
-          const uint32_t ko = (kind & 1) | (name << 1);
-          uint4* d = o.aos + 2ull * qq;
-          d[0] = make_uint4(static_cast<uint32_t>(h0[k].x), static_cast<uint32_t>(h0[k].x >> 32),
-                            static_cast<uint32_t>(h0[k].y), static_cast<uint32_t>(h0[k].y >> 32));
-          d[1] = make_uint4(static_cast<uint32_t>(hm[k].x >> 32),
-                            static_cast<uint32_t>(hm[k].y & 0xffffu) | (ko << 16),
-                            static_cast<uint32_t>(first + li[k]), 0u);
-          continue;
-        }
         o.tso[qq] = h0[k];
         o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
                              static_cast<int32_t>(hm[k].y & 0xffffffffu));
+        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
+        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
         o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
         o.perm[qq] = static_cast<uint32_t>(first + li[k]);
       }
@@ -1476,7 +1465,7 @@ void store_build_index(csg_store* s) {
                                              goff.as<uint32_t>(), go);
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                 s->perm.as<uint32_t>(), nullptr};
+                 s->perm.as<uint32_t>()};
     // Persistent, one CTA per SM, sub-tiles double-buffered by bulk copies:
     // 2048 records for rank spans <= 1024, 1024 records (wider digit tables)
     // up to 2048. CSG_SCATTER_CFG=2: single-buffered variants.
@@ -1512,20 +1501,9 @@ void store_build_index(csg_store* s) {
         else
           k_scatter_tx<4><<<grid, kTxThreads, sm, st>>>(tm, n, g, ntiles, lmin, D, o,
                                                         lmax_, R, ro, go);
-      } else if (nbuf == 2 && narrow) {
-        if (cfg == 9) {  // experiment: the same scatter into one 32-byte AoS record
-          DevBuf& aos = c->buf("index.aos_experiment");
-          aos.ensure(n * 32 + 64);
-          ScatterOut oa = o;
-          oa.aos = aos.as<uint4>();
-          smem_optin(k_scatter<8, 2, 4, true>, 2 * 2048 * 48 + 8 * 1024 * 2 + 1024 * 4);
-          ProfScope pa_(c->lc, "k_scatter_aos", st);
-          k_scatter<8, 2, 4, true><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D,
-                                                                    oa, lmax_, R, ro, go);
-        }
+      } else if (nbuf == 2 && narrow)
         k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
-      }
       else if (nbuf == 2)
         k_scatter<4, 2, 8><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
@@ -1549,7 +1527,7 @@ void store_build_index(csg_store* s) {
       {
         ProfScope ps_(c->lc, "k_gather", st);
         ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                     s->perm.as<uint32_t>(), nullptr};
+                     s->perm.as<uint32_t>()};
         k_gather<<<grid_for(n), 256, 0, st>>>(recs, s->perm.as<uint32_t>(), n, o);
       }
     }
