@@ -70,15 +70,16 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # Algorithmic bytes per record for the roofline, per launch
 # = bytes/record x records in the store:
 #  k_scatter:     read the 48 B packed record once (bulk copy into shared
-#                 memory), write ts 8 + op 8 + comm 4 + chan 4 + kind|op_name 1
-#                 + store index 4 = 29 B of rank-major columns (the payload
-#                 stays in the packed record, read through the store index)
+#                 memory), write the 16 B {ts, op_seq} and the 16 B {comm,
+#                 chan, store index, kind|op_name} rank-major records = 32 B
+#                 (the payload stays in the packed record, read through the
+#                 store index)
 #  k_stats_hist:  read the record's first 32 B (ts, op_seq, rank, comm,
 #                 channel, kind)
 #  k_chunkmax:    read the {ts, op_seq} pair 16 B (chunk maxima: 1/128 of that)
 #  k_gather/k_downsweep/k_upsweep: general (rank span > 2048) index path
-ALGO_BYTES = {"k_scatter": 77.0, "k_stats_hist": 32.0, "k_chunkmax": 16.0,
-              "k_gather": 77.0, "k_downsweep": 16.0, "k_upsweep": 4.0}
+ALGO_BYTES = {"k_scatter": 80.0, "k_stats_hist": 32.0, "k_chunkmax": 16.0,
+              "k_gather": 80.0, "k_downsweep": 16.0, "k_upsweep": 4.0}
 
 
 def log(*a):

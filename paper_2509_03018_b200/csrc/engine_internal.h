@@ -105,9 +105,10 @@ constexpr uint32_t kNoPos = 0xFFFFFFFFu;
 
 // Rank-major, structure-of-arrays view of the store built by the index.
 // Interleaved column: element i is field OFF of a STRIDE-wide rank-major
-// record. The index builder writes {ts, op_seq}, {comm, channel} and the
-// 16-byte payload with one wide store each (fewer, fuller sectors on the
-// scattered write side); readers index columns as before.
+// record. The index builder writes {ts, op_seq} and {comm, channel, store
+// index, kind | op_name} with one 16-byte store each (full sectors on the
+// scattered write side when a digit run holds two records); readers index
+// columns as before.
 template <typename T, int STRIDE, int OFF>
 struct ColView {
   const T* p = nullptr;
@@ -123,7 +124,7 @@ struct ColView {
 template <int W>
 struct PayView {
   const unsigned char* recs = nullptr;  // packed records (48 B each)
-  const uint32_t* perm = nullptr;
+  ColView<uint32_t, 4, 2> perm;         // store index (meta word 2)
   __device__ __forceinline__ uint64_t operator[](uint64_t p) const {
     const unsigned char* r = recs + static_cast<uint64_t>(perm[p]) * 48;
     const uint64_t v = *reinterpret_cast<const unsigned long long*>(r + 32 + 8 * W);
@@ -137,14 +138,16 @@ struct StoreView {
   int32_t R = 0;           // rank space [0, R)
   int32_t nch = 0;         // channel space [0, nch)
   const uint32_t* rank_off = nullptr;  // [R+1]
-  const uint32_t* perm = nullptr;      // rank-major pos -> store index
+  ColView<uint32_t, 4, 2> perm;        // rank-major pos -> store index (meta word 2)
   const double* cmax = nullptr;        // per-rank chunked prefix max of ts
                                        // (chunk c of rank r at r + off[r]/128 + c)
   ColView<double, 2, 0> ts;            // {ts, op_seq} pairs
   ColView<int64_t, 2, 1> op;
-  ColView<int32_t, 2, 0> comm;         // {comm, channel} pairs
-  ColView<int32_t, 2, 1> chan;
-  const uint8_t* ko = nullptr;         // kind | op_name << 1
+  // 16-byte meta record per position: {comm, channel, store index, kind |
+  // op_name << 1} — written by the index with one 16-byte store
+  ColView<int32_t, 4, 0> comm;
+  ColView<int32_t, 4, 1> chan;
+  ColView<uint8_t, 16, 12> ko;         // kind | op_name << 1
   PayView<0> pa;                       // payload: start_ms bits | ready | tx << 32
   PayView<1> pb;                       //          msg_bytes | done
 };

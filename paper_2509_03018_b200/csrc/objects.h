@@ -95,10 +95,10 @@ struct csg_store {
   bool spec_ok = false;
   bool spec_general = false;  // last build took the general path (stats + keys first)
   int32_t sp_lmin = 0, sp_lmax = -1, sp_R = 0;
-  csg::DevBuf rank_off, perm, keys, ko;
+  csg::DevBuf rank_off, perm, keys;  // perm, keys: general-path sort pairs
   csg::DevBuf runmax;  // chunked prefix max of ts (StoreView::cmax)
   csg::DevBuf tso;  // {ts, op_seq} per rank-major position (16 B)
-  csg::DevBuf cc;   // {comm, channel} (8 B)
+  csg::DevBuf meta;  // {comm, channel, store index, kind | op_name << 1} (16 B)
   csg::SortScratch sort;
   // op-ordered completion index for the straggler self-evidence pass
   bool op_indexed = false;
@@ -127,17 +127,17 @@ struct csg_store {
     v.R = R;
     v.nch = nch;
     v.rank_off = rank_off.as<uint32_t>();
-    v.perm = perm.as<uint32_t>();
+    v.perm.p = meta.as<uint32_t>();
     v.cmax = runmax.as<double>();
     v.ts.p = tso.as<double>();
     v.op.p = tso.as<int64_t>();
-    v.comm.p = cc.as<int32_t>();
-    v.chan.p = cc.as<int32_t>();
-    v.ko = ko.as<uint8_t>();
+    v.comm.p = meta.as<int32_t>();
+    v.chan.p = meta.as<int32_t>();
+    v.ko.p = meta.as<uint8_t>();
     v.pa.recs = recs.as<unsigned char>();
-    v.pa.perm = perm.as<uint32_t>();
+    v.pa.perm.p = meta.as<uint32_t>();
     v.pb.recs = recs.as<unsigned char>();
-    v.pb.perm = perm.as<uint32_t>();
+    v.pb.perm.p = meta.as<uint32_t>();
     return v;
   }
   csg::FlowView flow_view() const {

@@ -1218,6 +1218,8 @@ struct DecideArgs {
   int32_t* srank;  // ranks of the sorted entries
   double* opmax;
   struct SfPlan* plan;
+  int64_t* pend_ops;  // [candidate][kSfPend] ops waiting for a cohort (k_sf_fast)
+  uint8_t* pend_n;
   int sf_fast;  // k_self_faulted takes only the candidates k_sf_fast deferred
   // parallel straggler candidates (k_sl_*): per (straggler trip, membership
   // slot) lateness | flow-candidate bits, per (straggler trip, affected
@@ -1865,11 +1867,13 @@ __device__ bool self_faulted(const DecideArgs& a, int32_t j, const Cand& c,
             }
             if (k == ckey) {  // someone else's: wait for the value
               volatile unsigned* stv = a.coh_state + h;
-              while (*stv != 2u) {
+              while (*stv < 2u) {
               }
               __threadfence();
-              s_med = *reinterpret_cast<volatile double*>(a.coh_val + h);
-              s_hit = 1;
+              if (*stv == 2u) {  // 3: abandoned (k_coh_collect overflow), compute here
+                s_med = *reinterpret_cast<volatile double*>(a.coh_val + h);
+                s_hit = 1;
+              }
               break;
             }
           }
@@ -2939,7 +2943,8 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
     lo = U[0];
     hi = U[K - 1];
     const unsigned long long V = static_cast<unsigned long long>(hi - lo + 1);
-    const unsigned long long want = V * words + (V + 1) / 2;
+    // + per candidate rank: the op groups whose only retained rank it is
+    const unsigned long long want = V * words + (V + 1) / 2 + static_cast<unsigned long long>(C) * words;
     if (tid == 0) {
       const unsigned long long b0 = atomicAdd(a.bits_used, want);
       sh_u[0] = b0;
@@ -3067,6 +3072,29 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   __shared__ unsigned long long NE[kMaskWords], MU[kMaskWords];
   // [K] retained-rank summary (K <= C)
   int32_t* rsum = staged ? s_rsum : reinterpret_cast<int32_t*>(ret_g);
+  // dependency drops by rank: RB[rid(r)] = the op groups whose retained set
+  // is exactly {r}; then c (rank r) is dropped iff its ancestors meet a
+  // multi-rank group or a single-rank group outside RB[rid(r)] — a word scan
+  // instead of one rsum lookup per retained ancestor group. rid: compact
+  // ids of the candidate ranks (the report's minpos array, reset there).
+  unsigned long long* RB = nullptr;
+  __shared__ unsigned s_nrid;
+  if (K >= 2 && words <= kMaskWords) {
+    const unsigned long long V = static_cast<unsigned long long>(hi - lo + 1);
+    RB = a.bits + sh_u[0] + V * words + (V + 1) / 2;
+    for (unsigned long long i = tid; i < static_cast<unsigned long long>(C) * words; i += blockDim.x)
+      RB[i] = 0;
+    for (uint32_t r = tid; r < Rs; r += blockDim.x) minpos[r] = 0xFFFFFFFFu;
+    if (tid == 0) s_nrid = 0;
+    __syncthreads();
+    for (uint32_t x2 = tid; x2 < C; x2 += blockDim.x) {
+      const int32_t r = key(x2).rank;
+      if (r >= 0 && static_cast<uint32_t>(r) < Rs &&
+          atomicCAS(&minpos[r], 0xFFFFFFFFu, 0xFFFFFFFEu) == 0xFFFFFFFFu)
+        minpos[r] = atomicAdd(&s_nrid, 1u);
+    }
+    __syncthreads();
+  }
   if (tid < 32) {
     const int lane = tid;
     const bool masks = words <= kMaskWords;
@@ -3112,8 +3140,27 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
         const uint32_t i = base + lane;
         bool dd = false;
         long long c1 = clock64();
-        if (i < y && dag) {
-          const int32_t r = key(ord[i]).rank;
+        const int32_t rr = i < y ? key(ord[i]).rank : -1;
+        const unsigned long long* rb =
+            RB && rr >= 0 && static_cast<uint32_t>(rr) < Rs ? RB + static_cast<uint64_t>(minpos[rr]) * words
+                                                            : nullptr;
+        if (i < y && dag && rb) {
+          // eight words of the ancestor row and of RB per round trip (the
+          // rows of wide op windows live in global memory)
+          for (int w0 = 0; w0 < words && !dd; w0 += 8) {
+            unsigned long long av[8], rv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              av[q] = w0 + q < words ? row[w0 + q] : 0ull;
+              rv[q] = w0 + q < words ? rb[w0 + q] : 0ull;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (w0 + q < words)
+                dd = dd || (av[q] & MU[w0 + q]) || (av[q] & NE[w0 + q] & ~MU[w0 + q] & ~rv[q]);
+          }
+        } else if (i < y && dag) {
+          const int32_t r = rr;
           for (int w = 0; w < words && !dd; ++w) {
             unsigned long long av = row[w];
             if (masks) {
@@ -3251,6 +3298,8 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
           NE[g >> 6] |= 1ull << (g & 63);
           if (gs == -2) MU[g >> 6] |= 1ull << (g & 63);
         }
+        if (RB && gs >= 0 && static_cast<uint32_t>(gs) < Rs)
+          RB[static_cast<uint64_t>(minpos[gs]) * words + (g >> 6)] |= 1ull << (g & 63);
       }
       __syncwarp();
       x = y;
@@ -3570,6 +3619,179 @@ __global__ void __launch_bounds__(kDecideThreads) k_cohorts_lazy(DecideArgs a) {
       atomicExch(a.coh_state + h, 2u);
     }
     __syncthreads();
+  }
+}
+
+// The claimed cohorts as one multi-block radix select: every (trip, op name,
+// iteration) slot k_sf_fast claimed becomes an item over its iteration's
+// op-index range; a count pass and eight 8-bit digit passes run over all
+// items' entries at once (4096-entry units spread over the whole GPU, block
+// histograms merged into per-item global ones), a tiny pick kernel narrows
+// each item's prefix between passes. The lower median of an item is element
+// (m - 1) / 2 of its entries with op name nm and ts <= t; fewer than two
+// entries give 0 (rca.cpp:833-840: the op is then skipped).
+struct CohItem {
+  uint32_t slot;
+  uint32_t m;       // matching entries
+  uint64_t cb, ce;  // op-index range of the iteration
+  uint64_t unit0;   // first work unit
+  uint64_t prefix;  // selected key bits so far
+  uint64_t kth;     // rank still to find inside the prefix
+  double t;
+  int32_t nm;
+  int32_t pad;
+};
+struct CohPlan {
+  unsigned n_items;
+  unsigned pad;
+  unsigned long long units;
+};
+constexpr int kCohUnit = 4096;
+constexpr uint32_t kCohItemsCap = 8192;
+
+__global__ void __launch_bounds__(1024) k_coh_collect(DecideArgs a, CohItem* __restrict__ items,
+                                                      CohPlan* __restrict__ plan,
+                                                      uint32_t* __restrict__ hist) {
+  __shared__ unsigned s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b0 = 0; b0 < a.coh_cap; b0 += blockDim.x) {
+    const uint32_t h = b0 + threadIdx.x;
+    const bool want = h < a.coh_cap && a.coh_key[h] != ~0ull && a.coh_state[h] != 2u;
+    const unsigned mm = __ballot_sync(FULL, want);
+    unsigned at = 0;
+    if (lane == 0 && mm) at = atomicAdd(&s_n, static_cast<unsigned>(__popc(mm)));
+    at = __shfl_sync(FULL, at, 0) + __popc(mm & ((1u << lane) - 1u));
+    if (want && at >= kCohItemsCap) atomicExch(a.coh_state + h, 3u);  // abandoned
+    if (want && at < kCohItemsCap) {
+      const longlong2 mt = a.coh_meta[h];
+      const int32_t j = static_cast<int32_t>(mt.y >> 8);
+      CohItem it;
+      it.slot = h;
+      it.m = 0;
+      it.nm = static_cast<int32_t>(mt.y & 0xff);
+      it.t = a.trip_t[j];
+      int64_t olo, ohi;
+      iter_ops(mt.x, a.m.opn, olo, ohi);
+      olo = max(olo, a.min_op);
+      ohi = min(ohi, a.max_op);
+      if (olo <= ohi) {
+        it.cb = a.opoff[olo - a.min_op];
+        it.ce = a.opoff[ohi - a.min_op + 1];
+      } else {
+        it.cb = it.ce = 0;
+      }
+      it.prefix = 0;
+      it.kth = 0;
+      it.unit0 = 0;
+      it.pad = 0;
+      items[at] = it;
+    }
+  }
+  __syncthreads();
+  const unsigned n = min(s_n, kCohItemsCap);
+  for (uint64_t i = threadIdx.x; i < static_cast<uint64_t>(n) * 256; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) {
+    unsigned long long u = 0;
+    for (unsigned i = 0; i < n; ++i) {
+      items[i].unit0 = u;
+      u += (items[i].ce - items[i].cb + kCohUnit - 1) / kCohUnit;
+    }
+    plan->n_items = n;
+    plan->units = u;
+  }
+}
+
+// shift < 0: count pass; else the digit at `shift` of the keys matching the
+// item's prefix above it
+__global__ void __launch_bounds__(256) k_coh_pass(DecideArgs a, CohItem* __restrict__ items,
+                                                  const CohPlan* __restrict__ plan,
+                                                  uint32_t* __restrict__ hist, int shift) {
+  __shared__ uint32_t sh[256];
+  __shared__ uint32_t s_cnt;
+  const unsigned n = plan->n_items;
+  const unsigned long long U = plan->units;
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long u = blockIdx.x; u < U; u += gridDim.x) {
+    unsigned lo = 0, hi = n;  // items[lo].unit0 <= u < items[hi].unit0
+    while (hi - lo > 1) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (items[mid].unit0 <= u) lo = mid; else hi = mid;
+    }
+    const CohItem it = items[lo];
+    const uint64_t y0 = it.cb + (u - it.unit0) * kCohUnit;
+    const uint64_t y1 = min(it.ce, y0 + kCohUnit);
+    const uint64_t mask = shift >= 56 || shift < 0 ? 0ull : (~0ull << (shift + 8));
+    if (shift >= 0) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    } else if (threadIdx.x == 0) {
+      s_cnt = 0;
+    }
+    __syncthreads();
+    uint32_t cnt = 0;
+    for (uint64_t b0 = y0; b0 < y1; b0 += blockDim.x) {
+      const uint64_t y = b0 + threadIdx.x;
+      uint32_t d = 256;
+      if (y < y1 && a.op_nm[y] == it.nm && a.op_ts[y] <= it.t) {
+        if (shift < 0) {
+          ++cnt;
+        } else {
+          const uint64_t key = dkey(a.op_dur[y]);
+          if ((key & mask) == (it.prefix & mask)) d = static_cast<uint32_t>((key >> shift) & 255);
+        }
+      }
+      if (shift >= 0) {
+        const unsigned peers = __match_any_sync(FULL, d);
+        if (d < 256 && lane == __ffs(peers) - 1) atomicAdd(&sh[d], static_cast<uint32_t>(__popc(peers)));
+      }
+    }
+    if (shift < 0) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+      if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    }
+    __syncthreads();
+    if (shift < 0) {
+      if (threadIdx.x == 0 && s_cnt) atomicAdd(&items[lo].m, s_cnt);
+    } else {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[static_cast<uint64_t>(lo) * 256 + i], sh[i]);
+    }
+    __syncthreads();
+  }
+}
+
+// shift < 0: after the count pass (kth = (m - 1) / 2); else pick the digit
+// bucket holding the kth key; last pass (shift == 0) publishes the medians.
+__global__ void k_coh_pick(DecideArgs a, CohItem* __restrict__ items,
+                           const CohPlan* __restrict__ plan, uint32_t* __restrict__ hist,
+                           int shift) {
+  const unsigned n = plan->n_items;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    CohItem& it = items[i];
+    if (shift < 0) {
+      it.kth = it.m >= 1 ? (it.m - 1) / 2 : 0;
+      continue;
+    }
+    uint32_t* hh = hist + static_cast<uint64_t>(i) * 256;
+    uint64_t acc = 0;
+    int bsel = 255;
+    for (int b = 0; b < 256; ++b) {
+      if (acc + hh[b] > it.kth) {
+        bsel = b;
+        break;
+      }
+      acc += hh[b];
+    }
+    for (int b = 0; b < 256; ++b) hh[b] = 0;
+    it.prefix |= static_cast<uint64_t>(bsel) << shift;
+    it.kth -= acc;
+    if (shift == 0) {
+      a.coh_val[it.slot] = it.m < 2 ? 0.0 : dkey_inv(it.prefix);
+      __threadfence();
+      atomicExch(a.coh_state + it.slot, 2u);
+    }
   }
 }
 
@@ -4002,6 +4224,7 @@ struct SfPlan {
 constexpr int kOpSortWarpCap = 512;    // entries a warp sorts in shared memory
 constexpr int kOpSortBlockCap = 8192;  // entries a block sorts (64 KB)
 constexpr int kSfWarps = 4;
+constexpr int kSfPend = 8;
 
 __global__ void __launch_bounds__(1024) k_sf_prep(DecideArgs a) {
   SfPlan* pl = a.plan;
@@ -4201,6 +4424,25 @@ __global__ void __launch_bounds__(1024) k_opsort_large(DecideArgs a,
   }
 }
 
+// Sharded stores: every shard decided its own ranks' candidates (0 for the
+// others); the verdicts travel as one byte per flattened candidate through a
+// MAX all-reduce (dir 0: pack, dir 1: unpack).
+__global__ void k_sf_pads(DecideArgs a, uint8_t* __restrict__ flat, int dir) {
+  const SfPlan* pl = a.plan;
+  const unsigned long long total = pl->total;
+  for (unsigned long long w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    int32_t lo = 0, hi = a.J;
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pl->cstart[mid] <= w) lo = mid; else hi = mid;
+    }
+    Cand& c = a.pools.cand[a.state[lo].cand_base + (w - pl->cstart[lo])];
+    if (dir == 0) flat[w] = c.pad;
+    else c.pad = flat[w];
+  }
+}
+
 // Warp-collective ascending sort of one u64 key per lane.
 __device__ inline unsigned long long warp_sort32(unsigned long long v) {
   const int lane = threadIdx.x & 31;
@@ -4245,9 +4487,11 @@ __global__ void __launch_bounds__(kSfWarps * 32) k_sf_fast(DecideArgs a,
     const double t = a.trip_t[j];
     if (c.it_hi < c.it_lo) {
       verdict = 1;
-    } else if (a.sharded || a.f.n == 0 || opn <= 0) {
+    } else if (a.f.n == 0 || opn <= 0) {
       verdict = 2;
       reason = 1;
+    } else if (a.sharded && !(r >= 0 && r < a.s.R && a.s.rank_off[r + 1] > a.s.rank_off[r])) {
+      verdict = 0;  // another shard's rank: its owner decides (k_sf_pads MAX-combines)
     } else if (r >= 0 && r < a.s.R) {
       const uint32_t b = a.s.rank_off[r], e = a.s.rank_off[r + 1];
       const bool uns = a.f.unsorted[r] != 0;
@@ -4255,14 +4499,32 @@ __global__ void __launch_bounds__(kSfWarps * 32) k_sf_fast(DecideArgs a,
       int64_t olo, ohi, x0, x1;
       iter_ops(c.it_lo, opn, olo, x1);
       iter_ops(c.it_hi, opn, x0, ohi);
-      const uint32_t fo = warp_partition_point(b, e, [&](uint32_t i) { return opat(i) >= olo; });
-      const uint32_t fe = warp_partition_point(fo, e, [&](uint32_t i) { return opat(i) > ohi; });
       // the window's ops in ascending order: each op's run of the flow
-      // order, found by a partition point from the run start
+      // order, found by a partition point from the run start. The second
+      // pass revisits only the ops whose cohort the first pass waited for
+      // (up to kSfPend of them, listed by the first pass).
+      const uint32_t np = pass == 1 ? a.pend_n[w] : 0u;
+      const bool listed = pass == 1 && np <= static_cast<uint32_t>(kSfPend);
+      uint32_t fo = b, fe = e;
+      if (!listed) {
+        fo = warp_partition_point(b, e, [&](uint32_t i) { return opat(i) >= olo; });
+        fe = warp_partition_point(fo, e, [&](uint32_t i) { return opat(i) > ohi; });
+      }
       bool pending = false;
-      for (uint32_t p0 = fo; p0 < fe && verdict == 0;) {
-        const int64_t o = opat(p0);
-        const uint32_t p1 = warp_partition_point(p0, fe, [&](uint32_t i) { return opat(i) > o; });
+      uint32_t npend = 0, pi = 0;
+      for (uint32_t p0 = fo; verdict == 0;) {
+        int64_t o;
+        uint32_t p1;
+        if (listed) {
+          if (pi >= np) break;
+          o = a.pend_ops[w * kSfPend + pi++];
+          p0 = warp_partition_point(b, e, [&](uint32_t i) { return opat(i) >= o; });
+          p1 = warp_partition_point(p0, e, [&](uint32_t i) { return opat(i) > o; });
+        } else {
+          if (p0 >= fe) break;
+          o = opat(p0);
+          p1 = warp_partition_point(p0, fe, [&](uint32_t i) { return opat(i) > o; });
+        }
         // r's completions of o (non-Recv, ts <= t): value k of the run on lane k
         int kr = 0;
         unsigned long long mv = 0;
@@ -4357,6 +4619,9 @@ __global__ void __launch_bounds__(kSfWarps * 32) k_sf_fast(DecideArgs a,
           found = __shfl_sync(FULL, found, 0);
           if (found == 2 && pass == 0) {  // decide the other ops, then wait for it
             pending = true;
+            if (npend < static_cast<uint32_t>(kSfPend) && lane == 0)
+              a.pend_ops[w * kSfPend + npend] = o;
+            ++npend;
             continue;
           }
           if (found != 1) {
@@ -4397,7 +4662,10 @@ __global__ void __launch_bounds__(kSfWarps * 32) k_sf_fast(DecideArgs a,
         }
         if (med > 0 && dkey_inv(mine) > __dmul_rn(a.skew, med)) verdict = 1;
       }
-      if (verdict == 0 && pending) verdict = 3;
+      if (verdict == 0 && pending) {
+        verdict = 3;
+        if (lane == 0) a.pend_n[w] = static_cast<uint8_t>(min(npend, 255u));
+      }
     }
     if (lane == 0) {
       cands[x].pad = static_cast<uint8_t>(verdict);
@@ -4983,7 +5251,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
   static const bool sf_slow = std::getenv("CSG_SF_SLOW") != nullptr;
   DevBuf& d_sfl = c->buf("rca.sf_large");
   constexpr uint32_t kLargeCap = 1u << 16;
-  if (Js > 0 && !a.sharded && !sf_slow && s->op_indexed && s->flow_indexed) {
+  if (Js > 0 && !sf_slow && s->op_indexed && s->flow_indexed) {
     a.sf_fast = 1;
     a.f = s->flow_view();
     a.opoff = s->op_seg_off.as<uint32_t>();
@@ -5005,6 +5273,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     a.plan = d_plan2.as<SfPlan>();
     d_sfl.ensure(static_cast<size_t>(kLargeCap) * 4 + 64);
   }
+  DevBuf& d_pend = c->buf("rca.sf_pend");
+  a.pend_ops = nullptr;
+  a.pend_n = nullptr;
   static const bool sl_serial = std::getenv("CSG_SL_SERIAL") != nullptr;
   a.sl_par = (Js > 0 && !sl_serial && M > 0 && opn > 0) ? 1 : 0;
   a.strag_trip = dstrag;
@@ -5155,6 +5426,9 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                     kDecideThreads, shm, st>>>(a);
       }
       if (a.sf_fast) {
+        d_pend.ensure(cand_cap * (kSfPend * 8 + 1) + 64);
+        a.pend_ops = d_pend.as<int64_t>();
+        a.pend_n = reinterpret_cast<uint8_t*>(a.pend_ops + cand_cap * kSfPend);
         unsigned* nl = d_sfl.as<unsigned>();
         unsigned* large = nl + 16;
         CSG_CUDA(cudaMemsetAsync(nl, 0, 16, st));
@@ -5181,11 +5455,36 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
         }
         {  // the cohorts the first pass asked for, then their candidates again
           ProfScope ps_(c->lc, "k_cohorts", st);
-          k_cohorts_lazy<<<148 * 2, kDecideThreads, shm, st>>>(a);
+          static const bool coh_block = std::getenv("CSG_COHORT_BLOCK") != nullptr;
+          if (coh_block) {
+            k_cohorts_lazy<<<148 * 2, kDecideThreads, shm, st>>>(a);
+          } else {
+            DevBuf& d_ci = c->buf("rca.coh_items");
+            d_ci.ensure(sizeof(CohPlan) + static_cast<size_t>(kCohItemsCap) * sizeof(CohItem) +
+                        static_cast<size_t>(kCohItemsCap) * 256 * 4 + 64);
+            CohPlan* cplan = d_ci.as<CohPlan>();
+            CohItem* citems = reinterpret_cast<CohItem*>(d_ci.as<unsigned char>() + 64);
+            uint32_t* chist = reinterpret_cast<uint32_t*>(citems + kCohItemsCap);
+            k_coh_collect<<<1, 1024, 0, st>>>(a, citems, cplan, chist);
+            k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, -1);
+            k_coh_pick<<<8, 256, 0, st>>>(a, citems, cplan, chist, -1);
+            for (int sh2 = 56; sh2 >= 0; sh2 -= 8) {
+              k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
+              k_coh_pick<<<8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
+            }
+          }
         }
         {
-          ProfScope ps_(c->lc, "k_sf_fast", st);
+          ProfScope ps_(c->lc, "k_sf_fast_p2", st);
           k_sf_fast<<<148 * 16, kSfWarps * 32, 0, st>>>(a, nullptr, 1);
+        }
+        if (a.sharded) {  // owners' verdicts to every shard
+          DevBuf& d_fl = c->buf("rca.sf_flat");
+          d_fl.ensure(cand_cap + 16);
+          CSG_CUDA(cudaMemsetAsync(d_fl.p, 0, cand_cap, st));
+          k_sf_pads<<<148 * 4, 256, 0, st>>>(a, d_fl.as<uint8_t>(), 0);
+          comm_allreduce(c, d_fl.p, cand_cap, ncclUint8, ncclMax);
+          k_sf_pads<<<148 * 4, 256, 0, st>>>(a, d_fl.as<uint8_t>(), 1);
         }
         if (why) {
           unsigned hw[8];

@@ -358,12 +358,22 @@ __global__ void k_stats_pack(StoreStats* st, unsigned long long* pk, int dir, in
   }
 }
 
+__device__ int g_scatter_prof_on;
+__device__ unsigned long long g_scatter_cyc[6];
+
 struct ScatterOut {
   ulonglong2* tso;  // {ts, op_seq}
-  int2* cc;         // {comm, channel}
-  uint8_t* ko;      // kind | op_name << 1
-  uint32_t* perm;   // store index per rank-major position (payload via perm)
+  uint4* meta;      // {comm, channel, store index (payload via it), kind | op_name << 1}
 };
+
+// The rank-major meta word of a packed record's second 16 bytes (rank |
+// comm << 32, channel | kind << 32 | op_name << 40) and its store index.
+__device__ __forceinline__ uint4 meta_of(const ulonglong2& hm, uint32_t idx) {
+  const uint32_t kind = static_cast<uint32_t>((hm.y >> 32) & 0xff);
+  const uint32_t name = static_cast<uint32_t>((hm.y >> 40) & 0xff);
+  return make_uint4(static_cast<uint32_t>(hm.x >> 32), static_cast<uint32_t>(hm.y & 0xffffffffu),
+                    idx, (kind & 1) | (name << 1));
+}
 
 // --- 1D bulk async copies (TMA engine) into shared memory, mbarrier-tracked
 __device__ inline uint32_t smem_u32(const void* p) {
@@ -413,6 +423,9 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
               int32_t D, ScatterOut o, int32_t max_rank, int32_t R,
               uint32_t* __restrict__ rank_off, const int* go) {
   if (go && !*go) return;
+  // CSG_DEBUG_SCATTER: per-phase cycle totals (thread 0 of every block)
+  const bool prof = g_scatter_prof_on && threadIdx.x == 0;
+  long long pc[6] = {0, 0, 0, 0, 0, 0};
   constexpr int kW = kTileThreads / 32;
   constexpr int TR = kTileThreads * ITEMS;
   constexpr int SUB = kTile / TR;
@@ -485,6 +498,7 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
       constexpr int n4 = kW * Dp * 2 / 16;
       for (int i = tid; i < n4; i += kTileThreads) w4[i] = make_uint4(0, 0, 0, 0);
     }
+    long long pc0 = prof ? clock64() : 0;
     if (NBUF == 2 && (j & 1)) {
       mbar_wait(&mbar[1], par1);
       par1 ^= 1;
@@ -493,6 +507,11 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
       par0 ^= 1;
     }
     __syncthreads();
+    if (prof) {
+      const long long c = clock64();
+      pc[0] += c - pc0;
+      pc0 = c;
+    }
     // Phase A: warp w owns sub-tile records [32*ITEMS*w, 32*ITEMS*(w+1)),
     // item k of lane l is record 32*ITEMS*w + 32k + l (record order).
     uint32_t d[ITEMS];
@@ -517,6 +536,11 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
       __syncwarp();
     }
     __syncthreads();
+    if (prof) {
+      const long long c = clock64();
+      pc[1] += c - pc0;
+      pc0 = c;
+    }
     // per digit (thread t owns digits [DPT*t, DPT*t + DPT), one vector load
     // per warp row): cross-warp prefix + sub-tile start folded into the
     // warp counters; bx becomes (running base - sub-tile start) for phase B
@@ -567,11 +591,21 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
       bx[dd] = rb - ts0[k];
     }
     __syncthreads();
+    if (prof) {
+      const long long c = clock64();
+      pc[2] += c - pc0;
+      pc0 = c;
+    }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k)
       if (d[k] != 0xFFFFFFFFu)
         sidx[mine[d[k]] + rk[k]] = static_cast<uint16_t>(warp * (32 * ITEMS) + k * 32 + lane);
     __syncthreads();
+    if (prof) {
+      const long long c = clock64();
+      pc[3] += c - pc0;
+      pc0 = c;
+    }
     // Phase B: digit order; consecutive threads write consecutive positions
     // of one digit run. Four records per thread in flight (independent
     // shared-memory chains; 8 warps per SM leave little else to hide them).
@@ -602,19 +636,20 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
         if (p >= cnt) break;
         const uint32_t qq = q[k];
         o.tso[qq] = h0[k];
-        o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
-                             static_cast<int32_t>(hm[k].y & 0xffffffffu));
-        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
-        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
-        o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
-        o.perm[qq] = static_cast<uint32_t>(first + li[k]);
+        o.meta[qq] = meta_of(hm[k], static_cast<uint32_t>(first + li[k]));
       }
     }
     __syncthreads();
+    if (prof) {
+      pc[4] += clock64() - pc0;
+      pc[5] += 1;
+    }
 #pragma unroll
     for (int k = 0; k < DPT; ++k) bx[tid * DPT + k] = nxt[k];
     __syncthreads();
   }
+  if (prof)
+    for (int q = 0; q < 6; ++q) atomicAdd(&g_scatter_cyc[q], static_cast<unsigned long long>(pc[q]));
 }
 
 // k_scatter with 2-D tensor copies: the TMA engine gathers only the first 32
@@ -820,12 +855,7 @@ __global__ void __launch_bounds__(kTxThreads, 1)
         if (p >= cnt) break;
         const uint32_t qq = q[k];
         o.tso[qq] = h0[k];
-        o.cc[qq] = make_int2(static_cast<int32_t>(hm[k].x >> 32),
-                             static_cast<int32_t>(hm[k].y & 0xffffffffu));
-        const uint8_t kind = static_cast<uint8_t>((hm[k].y >> 32) & 0xff);
-        const uint8_t name = static_cast<uint8_t>((hm[k].y >> 40) & 0xff);
-        o.ko[qq] = static_cast<uint8_t>((kind & 1) | (name << 1));
-        o.perm[qq] = static_cast<uint32_t>(first + li[k]);
+        o.meta[qq] = meta_of(hm[k], static_cast<uint32_t>(first + li[k]));
       }
     }
     __syncthreads();
@@ -986,11 +1016,7 @@ __global__ void k_gather(const csg_packed_record* __restrict__ r,
         reinterpret_cast<const ulonglong2*>(r + perm[p]);
     const ulonglong2 h0 = __ldg(rec), hm = __ldg(rec + 1);
     o.tso[p] = h0;
-    o.cc[p] = make_int2(static_cast<int32_t>(hm.x >> 32),
-                        static_cast<int32_t>(hm.y & 0xffffffffu));
-    const uint8_t kind = static_cast<uint8_t>((hm.y >> 32) & 0xff);
-    const uint8_t name = static_cast<uint8_t>((hm.y >> 40) & 0xff);
-    o.ko[p] = static_cast<uint8_t>((kind & 1) | (name << 1));
+    o.meta[p] = meta_of(hm, perm[p]);
   }
 }
 
@@ -1430,8 +1456,7 @@ void store_build_index(csg_store* s) {
   s->rank_off.ensure((static_cast<size_t>(R) + 1) * 4);
   s->tso.ensure(n * 16 + 16);
   s->runmax.ensure((n / kCmChunk + static_cast<size_t>(R) + 2) * 8);
-  s->cc.ensure(n * 8 + 8);
-  s->ko.ensure(n + 8);
+  s->meta.ensure(n * 16 + 16);
   const bool fused = n && !force_general &&
                      static_cast<int64_t>(lmax_) - lmin_ < kHistDigits;
   if (fused) {
@@ -1464,8 +1489,7 @@ void store_build_index(csg_store* s) {
       k_hist_apply<<<nchunks, 1024, 0, st>>>(hcnt.as<uint32_t>(), cs, tot, ntiles, tpc, d0, D,
                                              goff.as<uint32_t>(), go);
     }
-    ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                 s->perm.as<uint32_t>()};
+    ScatterOut o{s->tso.as<ulonglong2>(), s->meta.as<uint4>()};
     // Persistent, one CTA per SM, sub-tiles double-buffered by bulk copies:
     // 2048 records for rank spans <= 1024, 1024 records (wider digit tables)
     // up to 2048. CSG_SCATTER_CFG=2: single-buffered variants.
@@ -1501,9 +1525,29 @@ void store_build_index(csg_store* s) {
         else
           k_scatter_tx<4><<<grid, kTxThreads, sm, st>>>(tm, n, g, ntiles, lmin, D, o,
                                                         lmax_, R, ro, go);
-      } else if (nbuf == 2 && narrow)
+      } else if (nbuf == 2 && narrow) {
+        static const bool dbg = std::getenv("CSG_DEBUG_SCATTER") != nullptr;
+        if (dbg) {
+          const int on = 1;
+          unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+          CSG_CUDA(cudaMemcpyToSymbolAsync(g_scatter_prof_on, &on, sizeof(on), 0,
+                                           cudaMemcpyHostToDevice, st));
+          CSG_CUDA(cudaMemcpyToSymbolAsync(g_scatter_cyc, z, sizeof(z), 0,
+                                           cudaMemcpyHostToDevice, st));
+        }
         k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
+        if (dbg) {
+          unsigned long long z[6];
+          CSG_CUDA(cudaMemcpyFromSymbolAsync(z, g_scatter_cyc, sizeof(z), 0,
+                                             cudaMemcpyDeviceToHost, st));
+          CSG_CUDA(cudaStreamSynchronize(st));
+          const double sub = z[5] ? static_cast<double>(z[5]) : 1.0;
+          fprintf(stderr, "k_scatter cycles per sub-tile (thread 0): wait %.0f rank %.0f scan "
+                  "%.0f stage %.0f write %.0f over %llu sub-tiles\n", z[0] / sub, z[1] / sub,
+                  z[2] / sub, z[3] / sub, z[4] / sub, z[5]);
+        }
+      }
       else if (nbuf == 2)
         k_scatter<4, 2, 8><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
@@ -1526,8 +1570,7 @@ void store_build_index(csg_store* s) {
                      st, c->lc);
       {
         ProfScope ps_(c->lc, "k_gather", st);
-        ScatterOut o{s->tso.as<ulonglong2>(), s->cc.as<int2>(), s->ko.as<uint8_t>(),
-                     s->perm.as<uint32_t>()};
+        ScatterOut o{s->tso.as<ulonglong2>(), s->meta.as<uint4>()};
         k_gather<<<grid_for(n), 256, 0, st>>>(recs, s->perm.as<uint32_t>(), n, o);
       }
     }

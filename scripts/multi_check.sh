@@ -1,7 +1,7 @@
 #!/bin/bash
-# Multi-GPU check on one box: sharded parity test and weak-scaling bench
-# lines at N = 2 and N = <gpus>.
-#   gpurun --gpus 4 --timeout 1800 -- bash scripts/multi_check.sh <tag>
+# Multi-GPU check on one box: sharded parity test, weak-scaling bench lines
+# (C2) at N = 2 and N = <gpus>, and the C4 job (strong scaling) at N = <gpus>.
+#   gpurun --gpus 4 --timeout 2400 -- bash scripts/multi_check.sh <tag>
 set -u
 O=gpurun_out/${1:-multi}
 mkdir -p "$O"
@@ -12,6 +12,10 @@ for N in 2 $G; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
       --master-addr 127.0.0.1 --master-port $((29500 + N)) bench.py --gpus $N --steps 10 \
       --warmup 3 > "$O/bench_n$N.json" 2> "$O/bench_n$N.err"
-  echo "bench n$N $?" >> "$O/status"
+  echo "bench n$N $? $(python scripts/roofline_line.py "$O/bench_n$N.json" 2>&1 | tail -1)" >> "$O/status"
 done
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G \
+    --master-addr 127.0.0.1 --master-port 29600 bench.py --gpus $G --workload c4 --steps 5 \
+    --warmup 3 > "$O/bench_c4_n$G.json" 2> "$O/bench_c4_n$G.err"
+echo "bench c4 n$G $? $(python scripts/roofline_line.py "$O/bench_c4_n$G.json" 2>&1 | tail -1)" >> "$O/status"
 cat "$O/status"
