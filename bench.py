@@ -216,12 +216,34 @@ def hbm_peak():
         return 6650.0, "fallback"
 
 
+def bind_to_gpu_numa(local):
+    """Pins this rank's threads to the CPUs next to its GPU (NVML's ideal
+    affinity), so its pinned staging buffers are first-touched on that NUMA
+    node and the e2e H2D copies do not cross the socket interconnect.
+    Returns the NUMA node (or None where NVML cannot tell)."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(local)  # CUDA index -> physical GPU
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(
+            "%04x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id))
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+        try:
+            return int(pynvml.nvmlDeviceGetNumaNodeId(h))
+        except Exception:
+            return None
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2509_03018_b200 import engine as E
 
     ws, rank, local = dist_env()
+    numa = bind_to_gpu_numa(local)
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -378,6 +400,7 @@ def run_ours(args):
                    "ranks": topo.world_size,
                    "channels_per_pair": json.load(open(CONFIG))["layout"]["channels_per_pair"],
                    "ticks_tripped": trips, "sampled_ranks": len(sampled),
+                   "numa_node": numa,
                    "parallelism": f"rank-range shards x{ws}, NCCL all-reduce of "
                                   "per-rank summaries" if ws > 1 else "single",
                    "l2": f"inputs ({n * 48 / 1e6:.0f} MB store) larger than the 126 MB L2"},
