@@ -108,6 +108,23 @@ def scaled_config(ngpus: int) -> str:
     return json.dumps(cfg)
 
 
+def synthesize(E, scen, target, ranks):
+    """Benchmark trace of the scenario: generated on this rank's GPU (host
+    schedule, device expansion and ordering, synth_gpu.cu; byte-identical to
+    the host generator, tests/test_gpu_synth.py) and brought to host memory
+    for the e2e and CPU legs; CSG_SYNTH_HOST=1 or no GPU: the host generator."""
+    import torch
+    if os.environ.get("CSG_SYNTH_HOST") or not torch.cuda.is_available():
+        return E.synthesize(scen, target, ranks)
+    ctx = E.Context(torch.cuda.current_device())
+    st = E.TraceStore(ctx)
+    E.synthesize_into(st, scen, target, ranks)
+    recs = st.records()
+    st.close()
+    ctx.close()
+    return recs
+
+
 def load_workload(ngpus: int = 1, shard: int = 0):
     from paper_2509_03018_b200 import engine as E
     from paper_2509_03018_b200._abi import RECORD_DTYPE
@@ -131,7 +148,7 @@ def load_workload(ngpus: int = 1, shard: int = 0):
             raise SystemExit(f"workload {WORKLOAD}: needs ~{need / 1e9:.0f} GB host "
                              f"memory, {avail / 1e9:.0f} GB available")
         t = time.time()
-        recs = E.synthesize(scen, 0, (lo, hi) if ngpus > 1 else None)
+        recs = synthesize(E, scen, 0, (lo, hi) if ngpus > 1 else None)
         log(f"synthesized {len(recs)} records (shard {shard}/{ngpus}) in "
             f"{time.time() - t:.1f}s")
         return scen, recs
@@ -142,7 +159,7 @@ def load_workload(ngpus: int = 1, shard: int = 0):
         # C2: the simulated time span bounds the trace (scaled_config); the
         # record target only bounds workloads without one
         target = 0 if CONFIG.endswith("c2_hang_1024.json") else TARGET_RECORDS
-        recs = E.synthesize(scen, target, (lo, hi) if ngpus > 1 else None)
+        recs = synthesize(E, scen, target, (lo, hi) if ngpus > 1 else None)
         recs.view(np.uint8).tofile(cache + ".tmp")
         os.replace(cache + ".tmp", cache)
         log(f"synthesized {len(recs)} records (shard {shard}/{ngpus}) in "

@@ -93,6 +93,15 @@ collsight_status collsight_b200_synthesize_ranks(const collsight_scenario* scena
                                                  int32_t rank_lo, int32_t rank_hi,
                                                  csg_packed_record** out, size_t* n);
 
+/* The same records generated on the store's GPU and appended to the store
+ * (*n records): the host schedules the op instances, the device expands
+ * every (instance, rank, channel) flow into its records and orders them by
+ * emission (synth_gpu.cu). Byte-identical to collsight_b200_synthesize_ranks. */
+collsight_status collsight_b200_synthesize_store(const collsight_scenario* scenario,
+                                                 uint64_t target_records,
+                                                 int32_t rank_lo, int32_t rank_hi,
+                                                 csg_store* store, uint64_t* n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

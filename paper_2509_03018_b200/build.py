@@ -89,7 +89,7 @@ def build(verbose: bool = False) -> str:
         objs.append(obj)
         if _stale(src, obj, hdr):
             jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-I", INCLUDE,
-                         "-I", os.path.join(CSRC, "host"), "-I", jdir,
+                         "-I", os.path.join(CSRC, "host"), "-I", CSRC, "-I", jdir,
                          "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include"),
                          "-c", src, "-o", obj])
     if jobs:

@@ -185,12 +185,20 @@ namespace {
 // memory, then publishes the sequence number: one launch instead of one
 // DMA copy per region plus a wait (each copy-engine transfer costs several
 // microseconds of latency on the path between two analysis phases).
-__global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long long v) {
+// Copies the fetch segments into mapped pinned host memory, then raises the
+// completion word the host polls. Several blocks share the copies (PCIe
+// writes from one SM were ~10 us for the affected-group rows); the last
+// block to finish (device-side counter) fences and raises the flag.
+constexpr unsigned kFetchBlocks = 8;
+__global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long long v,
+                        unsigned* __restrict__ done) {
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nt = gridDim.x * blockDim.x;
   for (int sgi = 0; sgi < a.n; ++sgi) {
     const FetchSeg& g = a.seg[sgi];
     if (g.row_len) {  // rows with device-side lengths, one warp per row
       const int lane = threadIdx.x & 31;
-      for (uint32_t rw = threadIdx.x >> 5; rw < g.nrows; rw += blockDim.x >> 5) {
+      for (uint32_t rw = gt >> 5; rw < g.nrows; rw += nt >> 5) {
         const uint32_t* s4 = reinterpret_cast<const uint32_t*>(g.src + rw * g.bytes);
         uint32_t* d4 = reinterpret_cast<uint32_t*>(g.dst + rw * g.bytes);
         const int32_t len = g.row_len[rw];
@@ -203,16 +211,21 @@ __global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long lon
     if (vec) {
       const uint4* s4 = reinterpret_cast<const uint4*>(g.src);
       uint4* d4 = reinterpret_cast<uint4*>(g.dst);
-      for (uint32_t i = threadIdx.x; i < g.bytes / 16; i += blockDim.x) d4[i] = s4[i];
+      for (uint32_t i = gt; i < g.bytes / 16; i += nt) d4[i] = s4[i];
     } else {
-      for (uint32_t i = threadIdx.x; i < g.bytes; i += blockDim.x) g.dst[i] = g.src[i];
+      for (uint32_t i = gt; i < g.bytes; i += nt) g.dst[i] = g.src[i];
     }
   }
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
-    *reinterpret_cast<volatile unsigned long long*>(flag) = v;
-    __threadfence_system();
+    const unsigned prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {
+      *done = 0;  // ready for the next fetch
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(flag) = v;
+      __threadfence_system();
+    }
   }
 }
 }  // namespace
@@ -235,8 +248,14 @@ void ctx_sync(csg_ctx* c, const FetchArgs* fetch) {
   volatile unsigned long long* f = c->sig.as<volatile unsigned long long>();
   const unsigned long long v = ++c->sig_seq;
   FetchArgs none{};
-  k_fetch<<<1, 256, 0, c->stream>>>(fetch ? *fetch : none, c->sig.as<unsigned long long>(),
-                                     v);
+  DevBuf& dn = c->buf("fetch.done");
+  if (dn.bytes < 16) {
+    dn.ensure(16);
+    CSG_CUDA(cudaMemsetAsync(dn.p, 0, 16, c->stream));
+  }
+  k_fetch<<<kFetchBlocks, 256, 0, c->stream>>>(fetch ? *fetch : none,
+                                               c->sig.as<unsigned long long>(), v,
+                                               dn.as<unsigned>());
   CSG_CUDA(cudaGetLastError());
   ++c->lc.launches;
   // spin briefly (the short waits of the analysis path), then let the
@@ -255,7 +274,13 @@ void ctx_sync(csg_ctx* c, const FetchArgs* fetch) {
 FetchTicket ctx_fetch_issue(csg_ctx* c, const FetchArgs& fetch) {
   c->sig.ensure(64);
   const unsigned long long v = ++c->sig_seq;
-  k_fetch<<<1, 256, 0, c->stream>>>(fetch, c->sig.as<unsigned long long>(), v);
+  DevBuf& dn = c->buf("fetch.done");
+  if (dn.bytes < 16) {
+    dn.ensure(16);
+    CSG_CUDA(cudaMemsetAsync(dn.p, 0, 16, c->stream));
+  }
+  k_fetch<<<kFetchBlocks, 256, 0, c->stream>>>(fetch, c->sig.as<unsigned long long>(), v,
+                                               dn.as<unsigned>());
   CSG_CUDA(cudaGetLastError());
   ++c->lc.launches;
   if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));

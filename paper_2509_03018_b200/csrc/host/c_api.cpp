@@ -402,4 +402,17 @@ collsight_status collsight_b200_synthesize_ranks(const collsight_scenario* s,
   });
 }
 
+collsight_status collsight_b200_synthesize_store(const collsight_scenario* s,
+                                                 uint64_t target, int32_t rank_lo,
+                                                 int32_t rank_hi, csg_store* store,
+                                                 uint64_t* n) {
+  if (!s || !store || !n) return fail(COLLSIGHT_ERR_ARG, "null argument");
+  return guarded([&] {
+    const csh::SynthPlan plan = csh::synth_plan(s->cfg, target, rank_lo, rank_hi);
+    *n = csg::synth_append_device(store, plan.flows.data(), plan.flows.size(), plan.params,
+                                  target);
+    return COLLSIGHT_OK;
+  });
+}
+
 }  // extern "C"

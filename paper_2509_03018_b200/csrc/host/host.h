@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "csg_engine.h"
+#include "synth_flow.h"
 
 namespace csh {
 
@@ -91,6 +92,15 @@ Scenario load_scenario_file(const std::string& path);
 std::vector<csg_packed_record> synthesize(const Scenario& s, uint64_t target,
                                           int32_t rank_lo = 0,
                                           int32_t rank_hi = 0x7fffffff);
+// The schedule half of it: one Flow per (op instance, executing rank) of
+// the shard, in emission order, plus the expansion parameters (the device
+// generator expands them, synth_gpu.cu).
+struct SynthPlan {
+  std::vector<csg_synth::Flow> flows;
+  csg_synth::Params params;
+  uint64_t target = 0;
+};
+SynthPlan synth_plan(const Scenario& s, uint64_t target, int32_t rank_lo, int32_t rank_hi);
 
 // Trace codec.
 // Multithreaded parse of a valid trace; false when the exact parser must

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "host.h"
+#include "synth_flow.h"
 
 namespace csh {
 
@@ -51,8 +52,7 @@ struct Rec {
 
 }  // namespace
 
-std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
-                                          int32_t rank_lo, int32_t rank_hi) {
+SynthPlan synth_plan(const Scenario& sc, uint64_t target, int32_t rank_lo, int32_t rank_hi) {
   const Layout l = sc.layout();
   const Program p = sc.program(l);
   const int opn = static_cast<int>(p.ops.size());
@@ -125,32 +125,29 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
   std::vector<char> blocked(W, 0);        // rank waits forever
   std::vector<double> op_end(opn, 0.0);   // this iteration's end per op
   std::vector<char> op_stalled(opn, 0);
-  std::vector<Rec> out;
-  out.reserve(target ? target + target / 8 : 1 << 20);
-  uint64_t seq = 0;
-  auto emit = [&](double key, const csg_packed_record& r) {
-    if (r.rank < rank_lo || r.rank >= rank_hi) return;  // another shard's rank
-    if (std::isfinite(stop_logs_at) && key > stop_logs_at &&
-        r.rank / l.ranks_per_node == hang_node)
-      return;
-    if (key > t_end) return;
-    out.push_back(Rec{key, seq++, r});
-  };
-  auto state_rec = [&](int32_t r, int s, int64_t gop, int ch, double ts,
-                       uint64_t total, uint64_t rd, uint64_t tx, uint64_t dn) {
-    csg_packed_record x;
-    std::memset(&x, 0, sizeof(x));
-    x.ts = ts;
-    x.op_seq = gop;
-    x.rank = r;
-    x.comm_id = p.ops[s].group;
-    x.channel = ch;
-    x.kind = CSG_KIND_STATE;
-    (void)total;
-    x.u.s.gpu_ready = static_cast<uint32_t>(rd);
-    x.u.s.rdma_transmitted = static_cast<uint32_t>(tx);
-    x.u.s.rdma_done = static_cast<uint32_t>(dn);
-    return x;
+  SynthPlan plan;
+  csg_synth::Params& P = plan.params;
+  P.window = window;
+  P.t_end = t_end;
+  P.ack = sc.ack_latency_ms;
+  P.hang_at = hang_at;
+  P.stop_logs_at = stop_logs_at;
+  P.msg_bytes = sc.msg_bytes;
+  P.cpp = cpp;
+  P.rank_lo = rank_lo;
+  P.rank_hi = rank_hi;
+  P.ranks_per_node = l.ranks_per_node;
+  P.hang_node = hang_node;
+  P.hang_nic = hang_nic;
+  P.nics_per_node = l.nics_per_node;
+  P.pad = 0;
+  plan.target = target;
+  uint64_t emitted = 0;  // records that pass the emit filter (the target cut)
+  auto count = [&](const csg_synth::Flow& f) {
+    for (int ch = 0; ch < cpp; ++ch)
+      csg_synth::expand(P, f, ch, [&](double key, const csg_packed_record& r) {
+        if (csg_synth::keep(P, key, r.rank)) ++emitted;
+      });
   };
   const int iters = sc.iterations > 0 ? sc.iterations : 1;
   for (int it = 0; it < iters; ++it) {
@@ -199,47 +196,22 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
         inst_end = std::max(inst_end, rend[i]);
       }
       const bool stalls = touches_dead && inst_end > hang_at;
-      const uint64_t total = chunks[s];
       for (size_t i = 0; i < ex[s].size(); ++i) {
         const int32_t r = ex[s][i];
-        const double rs = start + 0.01 * unit(sc.seed ^ 7, gop, r);
-        const double re = stalls ? INFINITY : rend[i];
-        for (int ch = 0; ch < cpp; ++ch) {
-          const double cs = rs + 0.002 * ch;
-          const double ce = stalls ? INFINITY : re - 0.003 * (cpp - 1 - ch);
-          const double span = std::max(1e-6, rend[i] - cs);
-          auto counters = [&](double t, uint64_t& rd, uint64_t& tx, uint64_t& dn) {
-            double f = (std::min(t, stalls ? hang_at : t) - cs) / span;
-            f = std::clamp(f, 0.0, 1.0);
-            rd = std::min<uint64_t>(total, static_cast<uint64_t>(total * std::min(1.0, f + 0.25)));
-            tx = std::min<uint64_t>(rd, static_cast<uint64_t>(total * f));
-            dn = std::min<uint64_t>(tx, static_cast<uint64_t>(total * std::max(0.0, f - 0.1)));
-            if (stalls && on_dead_nic(r, ch) && tx > 0 && dn == tx) dn = tx - 1;
-          };
-          // periodic snapshots at window boundaries inside the flow
-          const double stop = std::min(ce, t_end);
-          for (double w = std::floor(cs / window + 1) * window; w < stop; w += window) {
-            uint64_t rd, tx, dn;
-            counters(w, rd, tx, dn);
-            emit(w, state_rec(r, s, gop, ch, w, total, rd, tx, dn));
-          }
-          if (!stalls) {
-            // flush snapshot at flow end, then the completion (end <= flush)
-            const double flush = ce + sc.ack_latency_ms;
-            emit(flush, state_rec(r, s, gop, ch, flush, total, total, total, total));
-            csg_packed_record c;
-            std::memset(&c, 0, sizeof(c));
-            c.ts = ce;
-            c.op_seq = gop;
-            c.rank = r;
-            c.comm_id = op.group;
-            c.channel = ch;
-            c.kind = CSG_KIND_COMPLETION;
-            c.op_name = op.name;
-            c.u.c.start_ms = cs;
-            c.u.c.msg_bytes = std::max<uint64_t>(1, sc.msg_bytes / cpp);
-            emit(flush, c);
-          }
+        csg_synth::Flow f;
+        std::memset(&f, 0, sizeof(f));
+        f.rs = start + 0.01 * unit(sc.seed ^ 7, gop, r);
+        f.rend = rend[i];
+        f.gop = gop;
+        f.total = chunks[s];
+        f.r = r;
+        f.comm = op.group;
+        f.name = op.name;
+        f.stalls = stalls ? 1 : 0;
+        // flows of other shards' ranks emit nothing: not kept
+        if (r >= rank_lo && r < rank_hi) {
+          plan.flows.push_back(f);
+          if (target) count(f);
         }
         ready[r] = stalls ? INFINITY : rend[i];
         if (stalls) blocked[r] = 1;
@@ -248,8 +220,23 @@ std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
       op_end[s] = stalls ? INFINITY : inst_end;
     }
     if (!any_started) break;
-    if (target && out.size() >= target + target / 16) break;
+    if (target && emitted >= target + target / 16) break;
   }
+  return plan;
+}
+
+std::vector<csg_packed_record> synthesize(const Scenario& sc, uint64_t target,
+                                          int32_t rank_lo, int32_t rank_hi) {
+  const SynthPlan plan = synth_plan(sc, target, rank_lo, rank_hi);
+  const csg_synth::Params& P = plan.params;
+  std::vector<Rec> out;
+  out.reserve(target ? target + target / 8 : 1 << 20);
+  uint64_t seq = 0;
+  for (const csg_synth::Flow& f : plan.flows)
+    for (int ch = 0; ch < P.cpp; ++ch)
+      csg_synth::expand(P, f, ch, [&](double key, const csg_packed_record& r) {
+        if (csg_synth::keep(P, key, r.rank)) out.push_back(Rec{key, seq++, r});
+      });
   std::sort(out.begin(), out.end(), [](const Rec& a, const Rec& b) {
     return a.key != b.key ? a.key < b.key : a.seq < b.seq;
   });

@@ -3418,9 +3418,11 @@ __global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
                        const csg_evidence* __restrict__ ev,
                        csg_suspect* __restrict__ osus,
                        csg_evidence* __restrict__ oev) {
-  // block (j, kind): its packed offset is the sum of the earlier regions'
-  // counts in (trip, suspects / exonerated / evidence) order; the host
-  // derives the same offsets from the fetched trip table
+  // block (j, kind, slice): its packed offset is the sum of the earlier
+  // regions' counts in (trip, suspects / exonerated / evidence) order; the
+  // host derives the same offsets from the fetched trip table. grid.y slices
+  // each region (the PCIe writes into mapped memory of one block were the
+  // kernel's time).
   const int32_t j = blockIdx.x / 3, kind = blockIdx.x % 3;
   __shared__ uint32_t s_dst;
   if (threadIdx.x == 0) {
@@ -3434,7 +3436,7 @@ __global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
   const uint32_t n = kind == 0 ? t.n_sus : kind == 1 ? t.n_exo : t.n_ev;
   const uint32_t s0 = kind == 0 ? t.sus_off : kind == 1 ? t.exo_off : t.ev_off;
   const uint32_t d0 = s_dst;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (uint32_t i = blockIdx.y * blockDim.x + threadIdx.x; i < n; i += gridDim.y * blockDim.x) {
     if (kind < 2) osus[d0 + i] = sus[s0 + i];
     else oev[d0 + i] = ev[s0 + i];
   }
@@ -5509,7 +5511,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     h_ev.ensure(ev_cap * sizeof(csg_evidence) + 64);
     if (J > 0) {
       ProfScope ps_(c->lc, "k_pack", st);
-      k_pack<<<static_cast<unsigned>(3 * J), 128, 0, st>>>(
+      k_pack<<<dim3(static_cast<unsigned>(3 * J), 8), 128, 0, st>>>(
           d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
           h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>());
     }

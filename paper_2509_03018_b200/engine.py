@@ -644,6 +644,18 @@ def synthesize(scenario: Scenario, target_records: int = 0,
         lib().collsight_b200_free(out)
 
 
+def synthesize_into(store: "TraceStore", scenario: Scenario, target_records: int = 0,
+                    rank_range: Optional[Tuple[int, int]] = None) -> int:
+    """The same synthetic records as synthesize(), generated on the store's
+    GPU (synth_gpu.cu) and appended to the store; returns how many."""
+    n = C.c_uint64()
+    lo, hi = rank_range if rank_range else (0, 0x7FFFFFFF)
+    _ccheck(lib().collsight_b200_synthesize_store(scenario.h, C.c_uint64(target_records),
+                                                  C.c_int32(lo), C.c_int32(hi), store.h,
+                                                  C.byref(n)))
+    return n.value
+
+
 def comm_unique_id() -> bytes:
     """NCCL unique id for csg_ctx_comm_init (call on one rank, broadcast)."""
     buf = (C.c_ubyte * 128)()
