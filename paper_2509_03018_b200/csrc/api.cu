@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -229,6 +230,11 @@ __global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long lon
   }
 }
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("CSG_NO_PDL") == nullptr;
+  return on;
+}
 
 void smem_optin_raw(const void* func, size_t bytes) {
   static std::mutex mu;

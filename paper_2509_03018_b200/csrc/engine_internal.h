@@ -27,6 +27,37 @@ struct Error : std::runtime_error {
                              " at " __FILE__ ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// Programmatic dependent launch (PDL) for the latency-bound kernel chains
+// (index scans -> scatter -> chunk maxima, the failure RCA): a kernel
+// launched with launch_pdl may be scheduled while its predecessor's last
+// blocks still run; it calls pdl_wait() before touching any memory (which
+// returns once the predecessor has completed and its writes are visible),
+// and every chain kernel calls pdl_trigger() at its start so the next one
+// is launched as soon as all of its blocks are resident. Stream order is
+// otherwise unchanged; CSG_NO_PDL=1 launches plainly.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CSG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // Dynamic shared-memory opt-in for a kernel on the CURRENT device.
 // cudaFuncSetAttribute is per device, so the "already set" cache is keyed by
 // (device, kernel) and holds the largest size granted; thread-safe.

@@ -249,6 +249,8 @@ __global__ void k_rank_summary_fi(StoreView s, FlowView f, int32_t J,
                                   double delta_a, RankSum* __restrict__ out,
                                   unsigned long long* __restrict__ chan_key,
                                   int32_t nch, int32_t r0, int32_t nr) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint32_t sm_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -380,6 +382,8 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
                             unsigned long long* __restrict__ sp_key,
                             int32_t nch, const uint32_t* __restrict__ slots,
                             uint32_t nslots, const int32_t* __restrict__ trip_kind) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint32_t sp_tbl[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -652,6 +656,8 @@ __global__ void k_affected(StoreView s, ModelView m, int32_t J,
                            uint8_t* __restrict__ aff_flag,
                            int32_t* __restrict__ n_aff,
                            unsigned* __restrict__ slices_done) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t comps[64];
   __shared__ int32_t ncomp;
   __shared__ int32_t wsum[32];
@@ -2376,6 +2382,8 @@ __global__ void k_fail_count(StoreView s, ModelView m,
                              GroupPick* __restrict__ pick,
                              uint32_t* __restrict__ cnt,
                              const unsigned* __restrict__ n_dev) {
+  pdl_wait();
+  pdl_trigger();
   // n_items: grid bound (and scan length - 1); n_dev: the planned count when
   // the items were planned on the device (the tail up to n_items scans as 0)
   const int lane = threadIdx.x & 31;
@@ -2495,6 +2503,8 @@ __global__ void k_fail_cands(StoreView s, ModelView m,
                              csg_evidence* __restrict__ cev,
                              uint32_t* __restrict__ err,
                              const unsigned* __restrict__ n_dev) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kWarps = 4;
   constexpr int kStage = 256;  // members staged in shared memory
   __shared__ int32_t srank[kWarps][kStage];     // suspect ranks, else INT_MAX
@@ -2704,7 +2714,36 @@ struct ExoArgs {
   TripOut* out;
   uint64_t N;
   uint32_t* err;
+  int warp_sweep;  // CSG_EXO_WARP_SWEEP=1: the single-warp sweep only
 };
+
+// Block-wide inclusive scan (blockDim a multiple of 32, <= 1024) with an
+// associative op; wtot: 32 words of shared scratch. Block-collective.
+template <typename T, typename Op>
+__device__ T block_incl_scan(T v, T* wtot, Op op) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v = op(y, v);
+  }
+  __syncthreads();
+  if (lane == 31) wtot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    T x = wtot[lane < nw ? lane : 0];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x = op(y, x);
+    }
+    if (lane < nw) wtot[lane] = x;
+  }
+  __syncthreads();
+  if (warp > 0) v = op(wtot[warp - 1], v);
+  return v;
+}
 
 __device__ inline bool cand_before(const Cand* c, uint32_t x, uint32_t y) {
   // stable (stuck_op, rank) order; ties keep append order
@@ -2763,6 +2802,8 @@ struct ExoKey {
 constexpr size_t kExoStageBytes = kExoStage * (sizeof(ExoKey) + 4);
 
 __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned long long exo_dyn[];
   __shared__ int32_t sh_i[8];
   __shared__ unsigned long long sh_u[2];
@@ -3095,7 +3136,180 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
     }
     __syncthreads();
   }
-  if (tid < 32) {
+  // The whole block sweeps when the progress triples pack into one ordered
+  // u64 (done, tx, ready each < 2^21: done << 42 | tx << 21 | ready orders
+  // like prog_less): per op group, every candidate's dependency test runs on
+  // its own thread, and the same-op rule's exclusive run minimum is two
+  // block scans (a prefix minimum of the surviving known progress and a
+  // prefix maximum of the run starts) — a few barriers per group instead of
+  // a warp's chain of 64-bit shuffles per 32 candidates.
+  __shared__ int s_pack;
+  if (tid == 0) s_pack = a.warp_sweep ? 0 : 1;
+  __syncthreads();
+  for (uint32_t x2 = tid; x2 < C; x2 += blockDim.x) {
+    const ExoKey k2 = key(x2);
+    if (k2.known && (k2.done >= (1ull << 21) || k2.tx >= (1ull << 21) || k2.ready >= (1ull << 21)))
+      s_pack = 0;
+  }
+  __syncthreads();
+  if (s_pack) {
+    const bool masks = words <= kMaskWords;
+    __shared__ unsigned long long s_w64[32];
+    __shared__ uint32_t s_w32[32];
+    __shared__ unsigned long long s_pm[kExoThreads];
+    __shared__ uint32_t s_rs[kExoThreads];
+    __shared__ int32_t s_red[2][32];
+    __shared__ uint32_t s_kg;
+    uint32_t* gpos = reinterpret_cast<uint32_t*>(stmp);  // [K + 1] group starts
+    // group starts in sorted order
+    if (tid == 0) s_kg = 0;
+    for (int l = tid; l < K; l += blockDim.x) rsum[l] = -1;
+    for (int w = tid; w < kMaskWords; w += blockDim.x) NE[w] = MU[w] = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < C; b0 += blockDim.x) {
+      const uint32_t i = b0 + tid;
+      const uint32_t f = i < C && (i == 0 || key(ord[i]).op != key(ord[i - 1]).op) ? 1u : 0u;
+      const uint32_t inc = block_incl_scan(f, s_w32, [](uint32_t u, uint32_t v2) { return u + v2; });
+      const uint32_t base_g = s_kg;
+      if (f) gpos[base_g + inc - 1] = i;
+      __syncthreads();
+      if (tid == blockDim.x - 1) s_kg = base_g + inc;
+      __syncthreads();
+    }
+    const uint32_t KG = s_kg;
+    if (tid == 0) gpos[KG] = C;
+    __syncthreads();
+    const unsigned long long INF = ~0ull;
+    auto pk = [](const ExoKey& k2) {
+      return (k2.done << 42) | (k2.tx << 21) | k2.ready;
+    };
+    for (uint32_t gi = 0; gi < KG; ++gi) {
+      const uint32_t x = gpos[gi], y = gpos[gi + 1];
+      const int64_t op = key(ord[x]).op;
+      const bool dag = op >= 0 && K >= 2;
+      const int g = dag ? cidx[op - lo] : -1;
+      const unsigned long long* row = dag ? bits + (op - lo) * words : nullptr;
+      unsigned long long carry_all = INF;     // min over [x, base)
+      unsigned long long carry_closed = INF;  // min over [x, start of the open run)
+      int32_t open_rank = INT_MIN;
+      int32_t kmin = INT_MAX, kmax = INT_MIN;
+      for (uint32_t base = x; base < y; base += blockDim.x) {
+        const uint32_t i = base + tid;
+        const bool in = i < y;
+        ExoKey mk{};
+        if (in) mk = key(ord[i]);
+        bool dd = false;
+        if (in && dag) {
+          const int32_t r = mk.rank;
+          const unsigned long long* rb =
+              RB && r >= 0 && static_cast<uint32_t>(r) < Rs ? RB + static_cast<uint64_t>(minpos[r]) * words
+                                                          : nullptr;
+          if (rb) {
+            for (int w0 = 0; w0 < words && !dd; w0 += 8) {
+              unsigned long long av[8], rv[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                av[q] = w0 + q < words ? row[w0 + q] : 0ull;
+                rv[q] = w0 + q < words ? rb[w0 + q] : 0ull;
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (w0 + q < words)
+                  dd = dd || (av[q] & MU[w0 + q]) || (av[q] & NE[w0 + q] & ~MU[w0 + q] & ~rv[q]);
+            }
+          } else {
+            for (int w = 0; w < words && !dd; ++w) {
+              unsigned long long av2 = row[w];
+              if (masks) {
+                if (av2 & MU[w]) {
+                  dd = true;
+                  break;
+                }
+                av2 &= NE[w];
+              }
+              while (av2 && !dd) {
+                const int l = w * 64 + __ffsll(av2) - 1;
+                const int32_t q = rsum[l];
+                dd = q != -1 && q != r;
+                av2 &= av2 - 1;
+              }
+            }
+          }
+        }
+        const int32_t rk = in ? mk.rank : INT_MAX;
+        const unsigned long long v = in && !dd && mk.known ? pk(mk) : INF;
+        int32_t prev_rk = INT_MIN;
+        if (in && i > x) prev_rk = tid == 0 ? open_rank : key(ord[i - 1]).rank;
+        const bool start = in && (i == x || rk != prev_rk);
+        const unsigned long long pm = block_incl_scan(
+            v, s_w64, [](unsigned long long u, unsigned long long w2) { return u < w2 ? u : w2; });
+        const uint32_t rs = block_incl_scan(start ? i + 1 : 0u, s_w32,
+                                            [](uint32_t u, uint32_t w2) { return u > w2 ? u : w2; });
+        s_pm[tid] = pm;
+        s_rs[tid] = rs;
+        __syncthreads();
+        // least surviving known progress before my run
+        unsigned long long km;
+        if (rs) {  // my run starts in this chunk, at rs - 1
+          const uint32_t st0 = rs - 1;
+          km = carry_all;
+          if (st0 > base) {
+            const unsigned long long b2 = s_pm[st0 - 1 - base];
+            if (b2 < km) km = b2;
+          }
+        } else {
+          km = carry_closed;
+        }
+        bool kept = in && !dd;
+        if (kept && mk.known) kept = !(km < pk(mk));
+        if (in) keep[i] = kept ? 1 : 0;
+        if (kept) {
+          kmin = min(kmin, rk);
+          kmax = max(kmax, rk);
+        }
+        // carries: the chunk's last position
+        const uint32_t L = min(y, base + blockDim.x) - 1 - base;
+        const uint32_t rsL = s_rs[L];
+        if (rsL) {
+          const uint32_t st0 = rsL - 1;
+          unsigned long long c2 = carry_all;
+          if (st0 > base && s_pm[st0 - 1 - base] < c2) c2 = s_pm[st0 - 1 - base];
+          carry_closed = c2;
+        }
+        if (s_pm[L] < carry_all) carry_all = s_pm[L];
+        open_rank = key(ord[base + L]).rank;
+        __syncthreads();
+      }
+      // retained-rank summary: -1 none, the single rank, -2 several
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+      }
+      if ((tid & 31) == 0) {
+        s_red[0][tid >> 5] = kmin;
+        s_red[1][tid >> 5] = kmax;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+          kmin = min(kmin, s_red[0][w]);
+          kmax = max(kmax, s_red[1][w]);
+        }
+        const int32_t gs = kmin == INT_MAX ? -1 : (kmin == kmax ? kmin : -2);
+        if (g >= 0) {
+          rsum[g] = gs;
+          if (masks && gs != -1) {
+            NE[g >> 6] |= 1ull << (g & 63);
+            if (gs == -2) MU[g >> 6] |= 1ull << (g & 63);
+          }
+          if (RB && gs >= 0 && static_cast<uint32_t>(gs) < Rs)
+            RB[static_cast<uint64_t>(minpos[gs]) * words + (g >> 6)] |= 1ull << (g & 63);
+        }
+      }
+      __syncthreads();
+    }
+  } else if (tid < 32) {
     const int lane = tid;
     const bool masks = words <= kMaskWords;
     for (int l = lane; l < K; l += 32) rsum[l] = -1;
@@ -3418,6 +3632,8 @@ __global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
                        const csg_evidence* __restrict__ ev,
                        csg_suspect* __restrict__ osus,
                        csg_evidence* __restrict__ oev) {
+  pdl_wait();
+  pdl_trigger();
   // block (j, kind, slice): its packed offset is the sum of the earlier
   // regions' counts in (trip, suspects / exonerated / evidence) order; the
   // host derives the same offsets from the fetched trip table. grid.y slices
@@ -4798,8 +5014,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     static const bool no_fi = std::getenv("CSG_DISABLE_FLOW_INDEX") != nullptr;
     if (!no_fi && store_build_flow_index(s)) {
       ProfScope ps_(c->lc, "k_rank_summary_fi", st);
-      k_rank_summary_fi<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
-                          wpb * nch * 4, st>>>(sv, s->flow_view(), J, dt, cfg.delta_ms,
+      launch_pdl(k_rank_summary_fi, dim3(static_cast<unsigned>((warps + wpb - 1) / wpb)), dim3(wpb * 32), wpb * nch * 4, st, sv, s->flow_view(), J, dt, cfg.delta_ms,
                                                rs.as<RankSum>(),
                                                chan_key.as<unsigned long long>(), nch, r0, nr);
     } else {
@@ -4851,8 +5066,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     const uint64_t warps = static_cast<uint64_t>(E) * J;
     if (warps) {
       ProfScope ps_(c->lc, "k_succ_prog", st);
-      k_succ_prog<<<static_cast<unsigned>((warps + wpb - 1) / wpb), wpb * 32,
-                    wpb * nch * 4, st>>>(sv, s->flow_view(), mv, J, M,
+      launch_pdl(k_succ_prog, dim3(static_cast<unsigned>((warps + wpb - 1) / wpb)), dim3(wpb * 32), wpb * nch * 4, st, sv, s->flow_view(), mv, J, M,
                                          slot_group.as<uint32_t>(), rs.as<RankSum>(),
                                          succ.as<SuccProg>(),
                                          succ_key.as<unsigned long long>(), nch, slots, E,
@@ -4949,7 +5163,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       CSG_CUDA(cudaMemsetAsync(sdone.p, 0, sdone.bytes, st));
     }
     ProfScope ps_(c->lc, "k_affected", st);
-    k_affected<<<dim3(J, kAffSlices), 1024, 0, st>>>(
+    launch_pdl(k_affected, dim3(dim3(J, kAffSlices)), dim3(1024), 0, st, 
         sv, mv, J, dkind, drank, djs, rs.as<RankSum>(), gi.as<GroupIter>(), aff.as<int32_t>(),
         aff_flag.as<uint8_t>(), n_aff.as<int32_t>(), sdone.as<unsigned>());
   }
@@ -5115,14 +5329,14 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     const unsigned* n_dev = &d_plan.as<FailPlan>()->n_items;
     {
       ProfScope ps_(c->lc, "k_fail_count", st);
-      k_fail_count<<<static_cast<unsigned>((ub_items * 32 + 255) / 256), 256, 0, st>>>(
+      launch_pdl(k_fail_count, dim3(static_cast<unsigned>((ub_items * 32 + 255) / 256)), dim3(256), 0, st, 
           sv, mv, d_items.as<FailItem>(), static_cast<int32_t>(ub_items), rs.as<RankSum>(),
           d_pick.as<GroupPick>(), d_off.as<uint32_t>(), n_dev);
     }
     exclusive_scan_u32(d_off.as<uint32_t>(), ub_items + 1, c->buf("rca.scan_tmp"), st, c->lc);
     {
       ProfScope ps_(c->lc, "k_fail_cands", st);
-      k_fail_cands<<<static_cast<unsigned>((ub_items * 32 + 127) / 128), 128, 0, st>>>(
+      launch_pdl(k_fail_cands, dim3(static_cast<unsigned>((ub_items * 32 + 127) / 128)), dim3(128), 0, st, 
           sv, mv, d_items.as<FailItem>(), static_cast<int32_t>(ub_items), rs.as<RankSum>(),
           chan_key.as<unsigned long long>(), succ.as<SuccProg>(),
           succ_key.as<unsigned long long>(), M, nch, d_pick.as<GroupPick>(),
@@ -5154,8 +5368,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     d_exs.ensure(scratch_bytes + 256);
     {
       ProfScope ps_(c->lc, "k_fail_count", st);
-      k_fail_count<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 255) / 256),
-                     256, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
+      launch_pdl(k_fail_count, dim3(static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 255) / 256)), dim3(256), 0, st, sv, mv, d_items.as<FailItem>(), n_items,
                                    rs.as<RankSum>(), d_pick.as<GroupPick>(),
                                    d_off.as<uint32_t>(), nullptr);
     }
@@ -5163,8 +5376,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
                        c->buf("rca.scan_tmp"), st, c->lc);
     {
       ProfScope ps_(c->lc, "k_fail_cands", st);
-      k_fail_cands<<<static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 127) / 128),
-                     128, 0, st>>>(sv, mv, d_items.as<FailItem>(), n_items,
+      launch_pdl(k_fail_cands, dim3(static_cast<unsigned>((static_cast<uint64_t>(n_items) * 32 + 127) / 128)), dim3(128), 0, st, sv, mv, d_items.as<FailItem>(), n_items,
                                    rs.as<RankSum>(), chan_key.as<unsigned long long>(),
                                    succ.as<SuccProg>(), succ_key.as<unsigned long long>(),
                                    M, nch,
@@ -5370,6 +5582,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (n_exo_grid > 0) {
       ExoArgs ea;
       ea.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
+      ea.warp_sweep = std::getenv("CSG_EXO_BLOCK_SWEEP") == nullptr;  // block sweep: opt-in until verified
       ea.s = sv;
       ea.m = mv;
       ea.cand = d_cand.as<Cand>();
@@ -5389,7 +5602,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       ea.err = err.as<uint32_t>();
       smem_optin(k_exonerate, kExoSmemMax);
       ProfScope ps_(c->lc, "k_exonerate", st);
-      k_exonerate<<<static_cast<unsigned>(n_exo_grid), kExoThreads, kExoSmemMax, st>>>(ea);
+      launch_pdl(k_exonerate, dim3(static_cast<unsigned>(n_exo_grid)), dim3(kExoThreads), kExoSmemMax, st, ea);
     }
     if (a.sl_par) {  // straggler candidates, every (trip, group) in parallel
       const uint64_t wg = static_cast<uint64_t>(Js) * G;
@@ -5511,7 +5724,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     h_ev.ensure(ev_cap * sizeof(csg_evidence) + 64);
     if (J > 0) {
       ProfScope ps_(c->lc, "k_pack", st);
-      k_pack<<<dim3(static_cast<unsigned>(3 * J), 8), 128, 0, st>>>(
+      launch_pdl(k_pack, dim3(dim3(static_cast<unsigned>(3 * J), 8)), dim3(128), 0, st, 
           d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
           h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>());
     }

@@ -228,6 +228,8 @@ __device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint3
 __global__ void __launch_bounds__(1024)
     k_hist_colsum(const uint32_t* __restrict__ counts, uint32_t ntiles, uint32_t tpc,
                   uint32_t d0, int D, uint32_t* __restrict__ csum, const int* go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && !*go) return;  // speculative launch on a layout that did not hold
   const uint32_t c = blockIdx.x;
   const uint32_t t0 = c * tpc, t1 = min(t0 + tpc, ntiles);
@@ -246,6 +248,8 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(256)
     k_hist_chunkscan(uint32_t* __restrict__ csum, uint32_t nchunks, int D,
                      uint32_t* __restrict__ tot, const int* go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && !*go) return;
   __shared__ uint32_t part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -278,6 +282,8 @@ __global__ void __launch_bounds__(1024)
     k_hist_apply(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ cpre,
                  const uint32_t* __restrict__ tot, uint32_t ntiles, uint32_t tpc, uint32_t d0,
                  int D, uint32_t* __restrict__ goff, const int* go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && !*go) return;
   __shared__ uint32_t base[kHistDigits];
   __shared__ uint32_t wsum[32];
@@ -422,6 +428,8 @@ __global__ void __launch_bounds__(kTileThreads, NBUF == 1 ? 3 : 1)
               const uint32_t* __restrict__ goff, uint32_t T, int32_t min_rank,
               int32_t D, ScatterOut o, int32_t max_rank, int32_t R,
               uint32_t* __restrict__ rank_off, const int* go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && !*go) return;
   // CSG_DEBUG_SCATTER: per-phase cycle totals (thread 0 of every block)
   const bool prof = g_scatter_prof_on && threadIdx.x == 0;
@@ -915,6 +923,8 @@ __global__ void __launch_bounds__(1024)
                    uint32_t* __restrict__ unsorted, uint32_t* __restrict__ list,
                    unsigned* __restrict__ cnt, unsigned long long* __restrict__ max_seg,
                    int32_t r0, const int* go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && !*go) return;
   __shared__ double pmax[32];
   __shared__ int desc;
@@ -1478,15 +1488,15 @@ void store_build_index(csg_store* s) {
     uint32_t* tot = cs + static_cast<size_t>(D) * nchunks;
     {
       ProfScope ps_(c->lc, "k_hist_colsum", st);
-      k_hist_colsum<<<nchunks, 1024, 0, st>>>(hcnt.as<uint32_t>(), ntiles, tpc, d0, D, cs, go);
+      launch_pdl(k_hist_colsum, dim3(nchunks), dim3(1024), 0, st, hcnt.as<uint32_t>(), ntiles, tpc, d0, D, cs, go);
     }
     {
       ProfScope ps_(c->lc, "k_hist_chunkscan", st);
-      k_hist_chunkscan<<<(D + 31) / 32, 256, 0, st>>>(cs, nchunks, D, tot, go);
+      launch_pdl(k_hist_chunkscan, dim3((D + 31) / 32), dim3(256), 0, st, cs, nchunks, D, tot, go);
     }
     {
       ProfScope ps_(c->lc, "k_hist_apply", st);
-      k_hist_apply<<<nchunks, 1024, 0, st>>>(hcnt.as<uint32_t>(), cs, tot, ntiles, tpc, d0, D,
+      launch_pdl(k_hist_apply, dim3(nchunks), dim3(1024), 0, st, hcnt.as<uint32_t>(), cs, tot, ntiles, tpc, d0, D,
                                              goff.as<uint32_t>(), go);
     }
     ScatterOut o{s->tso.as<ulonglong2>(), s->meta.as<uint4>()};
@@ -1535,7 +1545,7 @@ void store_build_index(csg_store* s) {
           CSG_CUDA(cudaMemcpyToSymbolAsync(g_scatter_cyc, z, sizeof(z), 0,
                                            cudaMemcpyHostToDevice, st));
         }
-        k_scatter<8, 2, 4><<<grid, kTileThreads, smem, st>>>(recs, n, g, ntiles, lmin, D, o,
+        launch_pdl(k_scatter<8, 2, 4>, dim3(grid), dim3(kTileThreads), smem, st, recs, n, g, ntiles, lmin, D, o,
                                                              lmax_, R, ro, go);
         if (dbg) {
           unsigned long long z[6];
@@ -1592,13 +1602,14 @@ void store_build_index(csg_store* s) {
     // ranks outside [lmin, lmax] (a shard's foreign ranks) have no records:
     // their chunk maxima are never read and their flags stay 0
     const int32_t r0 = std::max(lmin_, 0), r1 = std::min(lmax_, R - 1);
-    // 512 threads: two blocks per SM overlap one block's scan tail with the
-    // other's loads (41 vs 52 us at 1024 threads on the C2 store)
+    // 128 threads: many blocks per SM overlap one block's scan tail with the
+    // others' loads and the ~1000 rank segments fit one wave (43 vs 45 / 51
+    // us at 256 / 512 threads on the C2 store, gpurun_out cm1)
     static const int cm_threads =
-        std::getenv("CSG_CM_THREADS") ? std::atoi(std::getenv("CSG_CM_THREADS")) : 512;
+        std::getenv("CSG_CM_THREADS") ? std::atoi(std::getenv("CSG_CM_THREADS")) : 128;
     ProfScope ps_(c->lc, "k_chunkmax", st);
     if (r1 >= r0)
-      k_chunkmax_blk<<<r1 - r0 + 1, cm_threads, 0, st>>>(
+      launch_pdl(k_chunkmax_blk, dim3(r1 - r0 + 1), dim3(cm_threads), 0, st, 
           s->tso.as<ulonglong2>(), s->rank_off.as<uint32_t>(), s->runmax.as<double>(),
           s->fl_unsorted.as<uint32_t>(), flist.as<uint32_t>(), fcnt.as<unsigned>(),
           &s->stats_dev.as<StoreStats>()->max_seg, r0, go);

@@ -39,7 +39,8 @@ print(json.dumps(got))
 """
 
 
-KNOBS = ("CSG_SF_SLOW", "CSG_ITER_PER_TRIP", "CSG_SL_SERIAL", "CSG_FLOW_SCAN")
+KNOBS = ("CSG_SF_SLOW", "CSG_ITER_PER_TRIP", "CSG_SL_SERIAL", "CSG_FLOW_SCAN",
+         "CSG_EXO_WARP_SWEEP")
 
 
 def run(cfg, slow=False, shuffle=False, per_trip=False):
@@ -51,6 +52,7 @@ def run(cfg, slow=False, shuffle=False, per_trip=False):
         env["CSG_SF_SLOW"] = "1"
         env["CSG_SL_SERIAL"] = "1"
         env["CSG_FLOW_SCAN"] = "1"
+        env["CSG_EXO_WARP_SWEEP"] = "1"
     if per_trip:
         env["CSG_ITER_PER_TRIP"] = "1"
     code = RUN % {"root": ROOT, "cfg": cfg, "shuffle": shuffle}
@@ -61,10 +63,12 @@ def run(cfg, slow=False, shuffle=False, per_trip=False):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["synth_strag_128", "scenario5", "scenario7"])
+@pytest.mark.parametrize("name", ["synth_strag_128", "scenario5", "scenario7", "scenario1",
+                                  "synth_hang_128"])
 def test_block_path_matches_reference(name):
-    """The per-candidate block filter and the per-trip iteration tables
-    (the paths the defaults defer to) against the reference."""
+    """The per-candidate block filter, the per-trip iteration tables, the
+    serial candidate loop and the single-warp exoneration sweep (the paths
+    the defaults replace or defer to) against the reference."""
     want = [json.loads(l) for l in open(os.path.join(GOLDEN, f"catalog_{name}.full.jsonl"))]
     assert run(name, slow=True, per_trip=True) == want
 
