@@ -5582,7 +5582,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     if (n_exo_grid > 0) {
       ExoArgs ea;
       ea.debug = std::getenv("CSG_DEBUG_EXO") != nullptr;
-      ea.warp_sweep = std::getenv("CSG_EXO_BLOCK_SWEEP") == nullptr;  // block sweep: opt-in until verified
+      ea.warp_sweep = std::getenv("CSG_EXO_WARP_SWEEP") != nullptr;
       ea.s = sv;
       ea.m = mv;
       ea.cand = d_cand.as<Cand>();
