@@ -1296,53 +1296,6 @@ __device__ int block_sum_i(int v, BlockShared& sh) {
   return t;
 }
 
-__device__ long long block_min_l(long long v, BlockShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
-  __syncthreads();
-  if (lane == 0) sh.red_l[warp] = v;
-  __syncthreads();
-  long long t = LLONG_MAX;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = min(t, sh.red_l[i]);
-  __syncthreads();
-  return t;
-}
-
-// Lexicographic minimum of (done, tx, ready) over the block.
-__device__ void block_min_prog(uint64_t& d, uint64_t& t, uint64_t& r,
-                               BlockShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t d2 = __shfl_xor_sync(FULL, d, o);
-    const uint64_t t2 = __shfl_xor_sync(FULL, t, o);
-    const uint64_t r2 = __shfl_xor_sync(FULL, r, o);
-    if (prog_less(d2, t2, r2, d, t, r)) {
-      d = d2;
-      t = t2;
-      r = r2;
-    }
-  }
-  __syncthreads();
-  if (lane == 0) {
-    sh.red_u[0][warp] = d;
-    sh.red_u[1][warp] = t;
-    sh.red_u[2][warp] = r;
-  }
-  __syncthreads();
-  d = sh.red_u[0][0];
-  t = sh.red_u[1][0];
-  r = sh.red_u[2][0];
-  for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
-    if (prog_less(sh.red_u[0][i], sh.red_u[1][i], sh.red_u[2][i], d, t, r)) {
-      d = sh.red_u[0][i];
-      t = sh.red_u[1][i];
-      r = sh.red_u[2][i];
-    }
-  __syncthreads();
-}
-
 // Stable order-preserving compaction of pred over [0, n) into dst (block).
 template <typename P>
 __device__ int block_compact(int n, P pred, uint32_t* dst, BlockShared& sh) {
@@ -1429,20 +1382,6 @@ __device__ double block_select(uint64_t n, uint64_t kth, G get,
   return dkey_inv(prefix);
 }
 
-// progress_of(rank, op, t) by a block scan of the rank's prefix
-// (rca.cpp:167-196); fills sh.chtbl with latest position + 1 per channel.
-__device__ void block_progress_scan(const DecideArgs& a, int32_t r,
-                                    uint32_t cutoff, int64_t op,
-                                    BlockShared& sh) {
-  for (int c = threadIdx.x; c < a.nch; c += blockDim.x) sh.chtbl[c] = 0;
-  __syncthreads();
-  const uint32_t b = a.s.rank_off[r];
-  for (uint32_t p = b + threadIdx.x; p < b + cutoff; p += blockDim.x)
-    if (a.s.op[p] == op && ko_kind(a.s.ko[p]) == CSG_KIND_STATE)
-      atomicMax(&sh.chtbl[a.s.chan[p]], p + 1);
-  __syncthreads();
-}
-
 __device__ void write_trip(const DecideArgs& a, int32_t j, int verdict,
                            int32_t naff, uint64_t scanned, BlockShared& sh) {
   if (threadIdx.x == 0) {
@@ -1499,16 +1438,6 @@ __device__ void push_cand(const DecideArgs& a, BlockShared& sh, const Cand& c) {
   }
   a.pools.cand[sh.cand_base + sh.ncand] = c;
   ++sh.ncand;
-}
-
-// Evidence refs of a per-channel table (ascending channel), thread 0.
-__device__ void add_table_evidence(const DecideArgs& a, BlockShared& sh,
-                                   Cand& c, int32_t rank,
-                                   const uint32_t* tbl) {
-  for (int ch = 0; ch < a.nch; ++ch) {
-    const uint32_t q = tbl[ch];
-    if (q) add_cev(a, sh, c, rank, ch, a.s.ts[q - 1], a.s.op[q - 1]);
-  }
 }
 
 // Final assembly shared by both analyzers: given candidates (in append
@@ -2743,13 +2672,6 @@ __device__ T block_incl_scan(T v, T* wtot, Op op) {
   __syncthreads();
   if (warp > 0) v = op(wtot[warp - 1], v);
   return v;
-}
-
-__device__ inline bool cand_before(const Cand* c, uint32_t x, uint32_t y) {
-  // stable (stuck_op, rank) order; ties keep append order
-  if (c[x].op != c[y].op) return c[x].op < c[y].op;
-  if (c[x].rank != c[y].rank) return c[x].rank < c[y].rank;
-  return x < y;
 }
 
 // In-place block bitonic sort of idx[0, P) (P power of two) by `less`;
