@@ -2859,6 +2859,69 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
       __syncthreads();
     }
   }
+  if (!packed) {
+    // large trips: the same packed (op - min op, rank, index) keys, sorted
+    // in the trip's global scratch (the report's staging area, free here)
+    __shared__ long long g_opmin, g_opmax;
+    __shared__ int g_rmax;
+    if (tid == 0) {
+      g_opmin = LLONG_MAX;
+      g_opmax = LLONG_MIN;
+      g_rmax = 0;
+    }
+    __syncthreads();
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    int rm = 0;
+    for (uint32_t i = tid; i < C; i += blockDim.x) {
+      const ExoKey k2 = key(i);
+      mn = min(mn, static_cast<long long>(k2.op));
+      mx = max(mx, static_cast<long long>(k2.op));
+      rm = max(rm, k2.rank);
+    }
+    atomicMin(&g_opmin, mn);
+    atomicMax(&g_opmax, mx);
+    atomicMax(&g_rmax, rm);
+    __syncthreads();
+    const unsigned long long span =
+        static_cast<unsigned long long>(g_opmax) - static_cast<unsigned long long>(g_opmin);
+    const int ib = 32 - __clz(static_cast<int>(P - 1) | 1);
+    const int rb = 32 - __clz(g_rmax | 1);
+    const int ob = 64 - __clzll(static_cast<long long>(span | 1));
+    if (g_rmax >= 0 && ob + rb + ib <= 64 && (span >> 62) == 0) {
+      packed = true;
+      unsigned long long* pk = reinterpret_cast<unsigned long long*>(stmp);
+      const long long omin = g_opmin;
+      for (uint32_t i = tid; i < P; i += blockDim.x) {
+        if (i < C) {
+          const ExoKey k2 = key(i);
+          pk[i] = (static_cast<unsigned long long>(k2.op - omin) << (rb + ib)) |
+                  (static_cast<unsigned long long>(k2.rank) << ib) | i;
+        } else {
+          pk[i] = ~0ull;
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t i = tid; i < P; i += blockDim.x) {
+            const uint32_t l = i ^ jj;
+            if (l > i) {
+              const unsigned long long x = pk[i], y = pk[l];
+              if (((i & k) == 0) == (x > y)) {
+                pk[i] = y;
+                pk[l] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      const unsigned long long im = (1ull << ib) - 1;
+      for (uint32_t i = tid; i < P; i += blockDim.x)
+        ord[i] = i < C ? static_cast<uint32_t>(pk[i] & im) : 0xFFFFFFFFu;
+      __syncthreads();
+    }
+  }
   if (!packed)
     block_bitonic(ord, C, P, [&](uint32_t x, uint32_t y) {
       const ExoKey kx = key(x), ky = key(y);
@@ -2992,23 +3055,64 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
       for (int32_t lv = 0; lv < a.m.n_levels; ++lv) {
         const uint32_t l0 = a.m.lvl_off[lv];
         const uint32_t nl = a.m.lvl_off[lv + 1] - l0;
-        for (uint32_t q = tid; q < nl * words; q += blockDim.x) {
-          const int32_t sop = a.m.lvl_ops[l0 + q / words];
-          const int wd = q % words;
+        // a thread per (op, run of 8 words) for wide rows: the parent list
+        // is read once per 8 words and the 8 parent words load
+        // independently; narrow rows keep a thread per (op, word)
+        constexpr int kWC = 8;
+        if (words < 24) {
+          for (uint32_t q = tid; q < nl * words; q += blockDim.x) {
+            const int32_t sop = a.m.lvl_ops[l0 + q / words];
+            const int wd = q % words;
+            const int64_t v = it * opn + sop;
+            if (v < lo || v > hi) continue;
+            unsigned long long acc = 0;
+            const uint32_t pe0 = __ldg(a.m.par_off + sop), pe1 = __ldg(a.m.par_off + sop + 1);
+#pragma unroll 8
+            for (uint32_t pe = pe0; pe < pe1; ++pe) {
+              const int64_t pit = it + __ldg(a.m.par_it + pe);
+              const int64_t pv = pit * opn + __ldg(a.m.par_op + pe);
+              if (pit < 0 || pv < lo) continue;
+              acc |= bits[(pv - lo) * words + wd];
+              const int l = cidx[pv - lo];
+              if (l >= 0 && (l >> 6) == wd) acc |= 1ull << (l & 63);
+            }
+            bits[(v - lo) * words + wd] = acc;
+          }
+          __syncthreads();
+          continue;
+        }
+        const int wc = kWC;
+        const uint32_t nwc = static_cast<uint32_t>(words + wc - 1) / wc;
+        for (uint32_t q = tid; q < nl * nwc; q += blockDim.x) {
+          const int32_t sop = a.m.lvl_ops[l0 + q / nwc];
+          const int w0 = static_cast<int>(q % nwc) * wc;
+          const int w1 = min(words, w0 + wc);
           const int64_t v = it * opn + sop;
           if (v < lo || v > hi) continue;
-          unsigned long long acc = 0;
+          unsigned long long acc[kWC];
+#pragma unroll
+          for (int k = 0; k < kWC; ++k) acc[k] = 0;
           const uint32_t pe0 = __ldg(a.m.par_off + sop), pe1 = __ldg(a.m.par_off + sop + 1);
-#pragma unroll 8
           for (uint32_t pe = pe0; pe < pe1; ++pe) {
             const int64_t pit = it + __ldg(a.m.par_it + pe);
             const int64_t pv = pit * opn + __ldg(a.m.par_op + pe);
             if (pit < 0 || pv < lo) continue;
-            acc |= bits[(pv - lo) * words + wd];
+            const unsigned long long* prow = bits + (pv - lo) * words;
+#pragma unroll
+            for (int k = 0; k < kWC; ++k)
+              if (w0 + k < w1) acc[k] |= prow[w0 + k];
             const int l = cidx[pv - lo];
-            if (l >= 0 && (l >> 6) == wd) acc |= 1ull << (l & 63);
+            const int lw = l >> 6;
+            if (l >= 0 && lw >= w0 && lw < w1) {
+#pragma unroll
+              for (int k = 0; k < kWC; ++k)
+                if (lw == w0 + k) acc[k] |= 1ull << (l & 63);
+            }
           }
-          bits[(v - lo) * words + wd] = acc;
+          unsigned long long* vrow = bits + (v - lo) * words;
+#pragma unroll
+          for (int k = 0; k < kWC; ++k)
+            if (w0 + k < w1) vrow[w0 + k] = acc[k];
         }
         __syncthreads();
       }
@@ -3031,7 +3135,7 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
   //      rank != rk1 (m2); c is dropped iff the least retained progress among
   //      OTHER ranks is below its own.
   //    Exactly the reference's O(C x retained) greedy, in O(C + K) steps.
-  constexpr int kMaskWords = 64;
+  constexpr int kMaskWords = 128;  // op groups up to 8192 keep the group masks
   __shared__ unsigned long long NE[kMaskWords], MU[kMaskWords];
   // [K] retained-rank summary (K <= C)
   int32_t* rsum = staged ? s_rsum : reinterpret_cast<int32_t*>(ret_g);
@@ -3105,12 +3209,34 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
     auto pk = [](const ExoKey& k2) {
       return (k2.done << 42) | (k2.tx << 21) | k2.ready;
     };
+    __shared__ unsigned long long s_T[kMaskWords];  // row & single-rank groups
+    __shared__ uint16_t s_nz[kMaskWords];           // words of s_T that are non-zero
+    __shared__ int s_nnz, s_mu;
     for (uint32_t gi = 0; gi < KG; ++gi) {
       const uint32_t x = gpos[gi], y = gpos[gi + 1];
       const int64_t op = key(ord[x]).op;
       const bool dag = op >= 0 && K >= 2;
       const int g = dag ? cidx[op - lo] : -1;
       const unsigned long long* row = dag ? bits + (op - lo) * words : nullptr;
+      // every candidate of the group shares its op's ancestor row: stage
+      // row & single-rank groups once (and whether the row meets a
+      // multi-rank group, which drops the whole group)
+      const bool staged_row = dag && masks && RB;
+      if (staged_row) {
+        if (tid == 0) {
+          s_nnz = 0;
+          s_mu = 0;
+        }
+        __syncthreads();
+        for (int w = tid; w < words; w += blockDim.x) {
+          const unsigned long long rw = row[w];
+          if (rw & MU[w]) s_mu = 1;
+          const unsigned long long t = rw & NE[w] & ~MU[w];
+          s_T[w] = t;
+          if (t) s_nz[atomicAdd(&s_nnz, 1)] = static_cast<uint16_t>(w);
+        }
+        __syncthreads();
+      }
       unsigned long long carry_all = INF;     // min over [x, base)
       unsigned long long carry_closed = INF;  // min over [x, start of the open run)
       int32_t open_rank = INT_MIN;
@@ -3121,7 +3247,19 @@ __global__ void __launch_bounds__(kExoThreads, 1) k_exonerate(ExoArgs a) {
         ExoKey mk{};
         if (in) mk = key(ord[i]);
         bool dd = false;
-        if (in && dag) {
+        if (in && dag && staged_row && mk.rank >= 0 && static_cast<uint32_t>(mk.rank) < Rs) {
+          dd = s_mu != 0;
+          const unsigned long long* rb = RB + static_cast<uint64_t>(minpos[mk.rank]) * words;
+          const int nnz = s_nnz;
+          for (int z0 = 0; z0 < nnz && !dd; z0 += 8) {
+            unsigned long long rv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) rv[q] = z0 + q < nnz ? rb[s_nz[z0 + q]] : ~0ull;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (z0 + q < nnz) dd = dd || (s_T[s_nz[z0 + q]] & ~rv[q]);
+          }
+        } else if (in && dag) {
           const int32_t r = mk.rank;
           const unsigned long long* rb =
               RB && r >= 0 && static_cast<uint32_t>(r) < Rs ? RB + static_cast<uint64_t>(minpos[r]) * words
