@@ -8,6 +8,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2509_03018_b200 import engine as E  # noqa: E402
 
+if len(sys.argv) > 1:  # python scripts/timeline.py c3
+    bench.select_workload(sys.argv[1])
+
 scen, recs = bench.load_workload(1, 0)
 topo, prog = scen.layout()
 tcfg, acfg, seed = scen.configs()
