@@ -1,6 +1,7 @@
 // engine_internal.h — shared internals of the B200 trace-analysis engine.
 #pragma once
 
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -84,7 +85,12 @@ struct HostBuf {
     p = nullptr;
     bytes = 0;
     const size_t want = b < 4096 ? 4096 : b + b / 2;
-    CSG_CUDA(cudaHostAlloc(&p, want, cudaHostAllocMapped));
+    CSG_CUDA(cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable));
+    // recycled pinned pages keep their old contents: a completion word
+    // (csg_ctx::sig) left at another context's sequence number would read
+    // as an already-finished fetch (large staging buffers are always
+    // written before they are read)
+    std::memset(p, 0, want < (64u << 10) ? want : (64u << 10));
     bytes = want;
   }
   template <typename T>

@@ -107,7 +107,11 @@ SynthPlan synth_plan(const Scenario& sc, uint64_t target, int32_t rank_lo, int32
         if (f.stop_logs_after_ms > 0) stop_logs_at = f.onset_ms + f.stop_logs_after_ms;
       }
     } else if (f.kind >= 1 && f.kind <= 5) {  // slowdowns
-      const double fac = f.kind == 4 ? f.copy_factor : f.bandwidth_factor;
+      // The reference simulator (sim.cpp:770-792) slows copies for
+      // pcie_downgrade / gpu_power_limit / background_compute (copy_factor)
+      // and flows for the NIC kinds (bandwidth_factor); this schedule has
+      // one per-rank slowdown, so it takes whichever factor was set.
+      const double fac = std::min(f.copy_factor, f.bandwidth_factor);
       for (int r = 0; r < W; ++r) {
         const bool hit = f.target == 2 ? r == f.rank : r / l.ranks_per_node == f.node;
         if (hit) {

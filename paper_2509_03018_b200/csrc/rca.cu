@@ -510,7 +510,10 @@ __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
 // so each record is folded into the table of the first trip whose prefix
 // holds it (one pass over the store instead of one per trip), and
 // k_iter_prefix then combines the tables over the trips (running min/max
-// per (slot, iteration) cell).
+// per (slot, iteration) cell). kIterParts warps per rank, each over one
+// contiguous part of the rank's segment (the walk is load-latency bound:
+// one warp per rank left 8 warps per SM on the C2 store).
+constexpr int kIterParts = 8;
 __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
                                   const int32_t* __restrict__ strag_trip,
                                   const RankSum* __restrict__ rs, int64_t it_min,
@@ -519,11 +522,16 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
                                   unsigned long long* __restrict__ tbl_e) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= s.R || w >= m.rank_space) return;
-  const int32_t r = static_cast<int32_t>(w);
+  const int64_t wr = w / kIterParts;
+  const int part = static_cast<int>(w % kIterParts);
+  if (wr >= s.R || wr >= m.rank_space) return;
+  const int32_t r = static_cast<int32_t>(wr);
   const uint32_t g0 = m.rg_off[r], g1 = m.rg_off[r + 1];
   if (g0 == g1) return;
   const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  const uint32_t plen = (e - b + kIterParts - 1) / kIterParts;
+  const uint32_t p0 = min(e, b + part * plen), p1 = min(e, p0 + plen);
+  if (p0 >= p1) return;
   // the rank's (group, slot) pairs in registers (a rank sits in <= 3 groups)
   int32_t gq[4];
   uint32_t sq[4];
@@ -535,10 +543,11 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
   }
   const bool many = g1 - g0 > 4;
   uint32_t done = b;
-  for (int32_t js = 0; js < Js && done < e; ++js) {
+  for (int32_t js = 0; js < Js && done < p1; ++js) {
     const int32_t j = strag_trip[js];
     const uint32_t cend = min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, e);
-    for (uint32_t p = done + lane; p < cend; p += 32) {
+    const uint32_t lo = max(done, p0), hi = min(cend, p1);
+    for (uint32_t p = lo + lane; p < hi; p += 32) {
       if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
       const int32_t cm = s.comm[p];
       uint32_t slot = kNoPos;
@@ -561,18 +570,99 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
   }
 }
 
-__global__ void k_iter_prefix(int32_t Js, uint64_t cells,
+// Running min/max over the trips' incremental tables, and the presence
+// counts: pc[(js, group, it)] += 1 for the trip at which a membership slot's
+// (slot, it) cell first holds a completion (k_pc_prefix turns them into the
+// number of the group's members present at iteration it for trip js).
+__global__ void k_iter_prefix(int32_t Js, uint64_t cells, int32_t n_it, int32_t G,
+                              const uint32_t* __restrict__ slot_group,
+                              const int32_t* __restrict__ members, int32_t own_lo,
+                              int32_t own_hi,
                               unsigned long long* __restrict__ tbl_s,
-                              unsigned long long* __restrict__ tbl_e) {
+                              unsigned long long* __restrict__ tbl_e,
+                              uint32_t* __restrict__ pc) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cells;
        c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t slot = static_cast<uint32_t>(c / n_it);
+    // sharded: other shards' members have empty cells here
+    const int32_t mr = members[slot];
+    if (mr < own_lo || mr > own_hi) continue;
     unsigned long long a = tbl_s[c], z = tbl_e[c];
+    const uint64_t gi0 = static_cast<uint64_t>(slot_group[slot]) * n_it + c % n_it;
+    const uint64_t gstride = static_cast<uint64_t>(G) * n_it;
+    if (a != ~0ull) atomicAdd(&pc[gi0], 1u);
     for (int32_t js = 1; js < Js; ++js) {
       const uint64_t i = static_cast<uint64_t>(js) * cells + c;
-      a = min(a, tbl_s[i]);
+      const unsigned long long a1 = min(a, tbl_s[i]);
+      if (a == ~0ull && a1 != ~0ull) atomicAdd(&pc[js * gstride + gi0], 1u);
+      a = a1;
       z = max(z, tbl_e[i]);
       tbl_s[i] = a;
       tbl_e[i] = z;
+    }
+  }
+}
+
+// Presence counts of per-trip (non-cumulative) tables: every present cell.
+__global__ void k_iter_count(int32_t Js, uint64_t cells, int32_t n_it, int32_t G,
+                             const uint32_t* __restrict__ slot_group,
+                             const unsigned long long* __restrict__ tbl_s,
+                             uint32_t* __restrict__ pc) {
+  const uint64_t total = static_cast<uint64_t>(Js) * cells;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (tbl_s[i] == ~0ull) continue;
+    const uint64_t js = i / cells, c = i % cells;
+    const uint32_t slot = static_cast<uint32_t>(c / n_it);
+    atomicAdd(&pc[(js * G + slot_group[slot]) * n_it + c % n_it], 1u);
+  }
+}
+
+__global__ void k_pc_prefix(int32_t Js, uint64_t cells, uint32_t* __restrict__ pc) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cells;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t a = pc[c];
+    for (int32_t js = 1; js < Js; ++js) {
+      a += pc[static_cast<uint64_t>(js) * cells + c];
+      pc[static_cast<uint64_t>(js) * cells + c] = a;
+    }
+  }
+}
+
+// Sharded stores: the only table cells read after k_group_iters are the
+// members' cells at each group's last k common iterations (gi_last); they
+// are packed (dir 0), min/max all-reduced, and written back (dir 1) instead
+// of all-reducing the whole (trip, slot, iteration) tables.
+__global__ void k_win_xfer(ModelView m, int32_t Js, int64_t it_min, int32_t n_it,
+                           uint32_t M, int32_t k, const GroupIter* __restrict__ gi,
+                           const int64_t* __restrict__ gi_last,
+                           unsigned long long* __restrict__ tbl_s,
+                           unsigned long long* __restrict__ tbl_e,
+                           unsigned long long* __restrict__ pk_s,
+                           unsigned long long* __restrict__ pk_e, int dir) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(m.n_groups) * Js) return;
+  const int32_t js = static_cast<int32_t>(w / m.n_groups);
+  const int32_t g = static_cast<int32_t>(w % m.n_groups);
+  const uint64_t gidx = static_cast<uint64_t>(js) * m.n_groups + g;
+  const int32_t cnt = gi[gidx].n_common;
+  const uint32_t mo = m.member_off[g];
+  const int32_t mm = static_cast<int32_t>(m.member_off[g + 1] - mo);
+  if (mm < 2 || cnt <= 0) return;
+  const int32_t q0 = k - min(cnt, k);
+  const int32_t nq = k - q0;
+  for (int32_t t = lane; t < mm * nq; t += 32) {
+    const int32_t x = t / nq, q = q0 + t % nq;
+    const uint64_t row = static_cast<uint64_t>(js) * M + m.member_slot[mo + x];
+    const uint64_t cell = row * n_it + static_cast<uint64_t>(gi_last[gidx * k + q] - it_min);
+    const uint64_t pi = row * k + q;
+    if (dir == 0) {
+      pk_s[pi] = tbl_s[cell];
+      pk_e[pi] = tbl_e[cell];
+    } else {
+      tbl_s[cell] = pk_s[pi];
+      tbl_e[cell] = pk_e[pi];
     }
   }
 }
@@ -581,11 +671,16 @@ __global__ void k_iter_prefix(int32_t Js, uint64_t cells,
 // K3: complete_iterations (rca.cpp:352-372) + group_has_late_member
 // (rca.cpp:374-396), one warp per (straggler trip, group).
 // ---------------------------------------------------------------------------
+// Presence of a group at an iteration comes from the member counts pc
+// (k_iter_prefix / k_iter_count); mode 1 finds the common iterations only,
+// mode 2 the medians / late flag at the latest one (after the sharded window
+// exchange), mode 3 both.
 __global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
                               int32_t n_it, uint32_t M, int32_t k,
                               double thr,
                               const unsigned long long* __restrict__ tbl_s,
                               const unsigned long long* __restrict__ tbl_e,
+                              const uint32_t* __restrict__ pc, int mode,
                               GroupIter* __restrict__ gi,
                               int64_t* __restrict__ gi_last) {
   const int lane = threadIdx.x & 31;
@@ -595,31 +690,35 @@ __global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
   const int32_t g = static_cast<int32_t>(w % m.n_groups);
   const uint32_t mo = m.member_off[g];
   const int32_t mm = static_cast<int32_t>(m.member_off[g + 1] - mo);
+  const uint64_t gidx = static_cast<uint64_t>(js) * m.n_groups + g;
   GroupIter out{0, 0};
-  int64_t* last = gi_last + (static_cast<uint64_t>(js) * m.n_groups + g) * k;
+  int64_t* last = gi_last + gidx * k;
   if (mm >= 2 && m.opn > 0) {
     const uint64_t rowbase = static_cast<uint64_t>(js) * M;
-    int32_t count = 0, got = 0;
+    int32_t count = 0;
     int64_t latest = 0;
-    for (int64_t top = n_it - 1; top >= 0; top -= 32) {
-      const int64_t it = top - lane;
-      bool present = it >= 0;
-      for (int32_t i = 0; present && i < mm; ++i) {
-        const uint32_t slot = m.member_slot[mo + i];
-        present = tbl_s[(rowbase + slot) * n_it + it] != ~0ull;
+    if (mode & 1) {
+      const uint32_t* pcg = pc + gidx * n_it;
+      int32_t got = 0;
+      for (int64_t top = n_it - 1; top >= 0; top -= 32) {
+        const int64_t it = top - lane;
+        const bool present = it >= 0 && pcg[it] == static_cast<uint32_t>(mm);
+        unsigned bm = __ballot_sync(FULL, present);
+        if (count == 0 && bm) latest = top - (__ffs(bm) - 1);
+        count += __popc(bm);
+        while (bm && got < k) {
+          const int f = __ffs(bm) - 1;
+          if (lane == 0) last[k - 1 - got] = top - f + it_min;
+          ++got;
+          bm &= bm - 1;
+        }
       }
-      unsigned bm = __ballot_sync(FULL, present);
-      if (count == 0 && bm) latest = top - (__ffs(bm) - 1);
-      count += __popc(bm);
-      while (bm && got < k) {
-        const int f = __ffs(bm) - 1;
-        if (lane == 0) last[k - 1 - got] = top - f + it_min;
-        ++got;
-        bm &= bm - 1;
-      }
+    } else {
+      count = gi[gidx].n_common;
+      if (count > 0) latest = last[k - 1] - it_min;
     }
     out.n_common = count;
-    if (count > 0) {
+    if ((mode & 2) && count > 0) {
       // lower medians of starts / ends at the latest common iteration
       auto sv = [&](int i) {
         return dkey_inv(tbl_s[(rowbase + m.member_slot[mo + i]) * n_it + latest]);
@@ -635,7 +734,7 @@ __global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
       out.late = __any_sync(FULL, late) ? 1 : 0;
     }
   }
-  if (lane == 0) gi[static_cast<uint64_t>(js) * m.n_groups + g] = out;
+  if (lane == 0) gi[gidx] = out;
 }
 
 // ---------------------------------------------------------------------------
@@ -5173,39 +5272,95 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       for (int32_t x = 1; x < Js; ++x)
         ordered = ordered && h_t[h_strag[x]] >= h_t[h_strag[x - 1]];
       static const bool inc_off = std::getenv("CSG_ITER_PER_TRIP") != nullptr;
-      if (R > 0 && ordered && !inc_off) {
+      DevBuf& pc = c->buf("rca.iter_pc");
+      const uint64_t per = static_cast<uint64_t>(M) * n_it;
+      const uint64_t pcells = static_cast<uint64_t>(G) * n_it;
+      pc.ensure(static_cast<size_t>(Js) * std::max<uint64_t>(pcells, 1) * 4);
+      CSG_CUDA(cudaMemsetAsync(pc.p, 0, static_cast<size_t>(Js) * pcells * 4, st));
+      auto grid_for = [](uint64_t n) {
+        return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)));
+      };
+      const bool inc = R > 0 && ordered && !inc_off;
+      if (inc) {
         {
-          const uint64_t warps = static_cast<uint64_t>(R);
+          const uint64_t warps = static_cast<uint64_t>(R) * kIterParts;
           ProfScope ps_(c->lc, "k_iter_tables", st);
           k_iter_tables_inc<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
               sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it, M,
               tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>());
         }
-        if (Js > 1) {
-          const uint64_t per = static_cast<uint64_t>(M) * n_it;
-          ProfScope ps_(c->lc, "k_iter_prefix", st);
-          k_iter_prefix<<<static_cast<unsigned>(std::min<uint64_t>((per + 255) / 256, 148 * 16)),
-                          256, 0, st>>>(Js, per, tbl_s.as<unsigned long long>(),
-                                        tbl_e.as<unsigned long long>());
+        ProfScope ps_(c->lc, "k_iter_prefix", st);
+        k_iter_prefix<<<grid_for(per), 256, 0, st>>>(
+            Js, per, n_it, G, slot_group.as<uint32_t>(), mv.members,
+            sharded ? r0 : INT_MIN, sharded ? r0 + nr - 1 : INT_MAX, tbl_s.as<unsigned long long>(),
+            tbl_e.as<unsigned long long>(), pc.as<uint32_t>());
+      } else {
+        if (R > 0) {
+          const uint64_t warps = static_cast<uint64_t>(R) * Js;
+          ProfScope ps_(c->lc, "k_iter_tables", st);
+          k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
+                          st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
+                                M, tbl_s.as<unsigned long long>(),
+                                tbl_e.as<unsigned long long>());
         }
-      } else if (R > 0) {
-        const uint64_t warps = static_cast<uint64_t>(R) * Js;
-        ProfScope ps_(c->lc, "k_iter_tables", st);
-        k_iter_tables<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0,
-                        st>>>(sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it,
-                              M, tbl_s.as<unsigned long long>(),
-                              tbl_e.as<unsigned long long>());
+        ProfScope ps_(c->lc, "k_iter_count", st);
+        k_iter_count<<<grid_for(static_cast<uint64_t>(Js) * per), 256, 0, st>>>(
+            Js, per, n_it, G, slot_group.as<uint32_t>(), tbl_s.as<unsigned long long>(),
+            pc.as<uint32_t>());
       }
-      comm_group_start(c);
-      comm_allreduce(c, tbl_s.p, cells, ncclUint64, ncclMin);
-      comm_allreduce(c, tbl_e.p, cells, ncclUint64, ncclMax);
-      comm_group_end(c);
+      // sharded: a slot's cells live on the shard owning its rank, so the
+      // member counts sum across shards; the tables themselves are only
+      // exchanged at the cells read from here on (k_win_xfer)
+      comm_allreduce(c, pc.p, static_cast<size_t>(Js) * pcells, ncclUint32, ncclSum);
+      if (inc && Js > 1) {
+        ProfScope ps_(c->lc, "k_pc_prefix", st);
+        k_pc_prefix<<<grid_for(pcells), 256, 0, st>>>(Js, pcells, pc.as<uint32_t>());
+      }
       const uint64_t gw = static_cast<uint64_t>(G) * Js;
+      const unsigned gblocks = static_cast<unsigned>((gw * 32 + 255) / 256);
+      if (sharded) {
+        {
+          ProfScope ps_(c->lc, "k_group_iters", st);
+          k_group_iters<<<gblocks, 256, 0, st>>>(
+              mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
+              tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
+              pc.as<uint32_t>(), 1, gi.as<GroupIter>(), gi_last.as<int64_t>());
+        }
+        DevBuf& pk_s = c->buf("rca.win_s");
+        DevBuf& pk_e = c->buf("rca.win_e");
+        const size_t pn = static_cast<size_t>(Js) * M * k;
+        pk_s.ensure(pn * 8);
+        pk_e.ensure(pn * 8);
+        CSG_CUDA(cudaMemsetAsync(pk_s.p, 0xff, pn * 8, st));
+        CSG_CUDA(cudaMemsetAsync(pk_e.p, 0, pn * 8, st));
+        {
+          ProfScope ps_(c->lc, "k_win_xfer", st);
+          k_win_xfer<<<gblocks, 256, 0, st>>>(mv, Js, it_min, n_it, M, k, gi.as<GroupIter>(),
+                                              gi_last.as<int64_t>(),
+                                              tbl_s.as<unsigned long long>(),
+                                              tbl_e.as<unsigned long long>(),
+                                              pk_s.as<unsigned long long>(),
+                                              pk_e.as<unsigned long long>(), 0);
+        }
+        comm_group_start(c);
+        comm_allreduce(c, pk_s.p, pn, ncclUint64, ncclMin);
+        comm_allreduce(c, pk_e.p, pn, ncclUint64, ncclMax);
+        comm_group_end(c);
+        {
+          ProfScope ps_(c->lc, "k_win_xfer", st);
+          k_win_xfer<<<gblocks, 256, 0, st>>>(mv, Js, it_min, n_it, M, k, gi.as<GroupIter>(),
+                                              gi_last.as<int64_t>(),
+                                              tbl_s.as<unsigned long long>(),
+                                              tbl_e.as<unsigned long long>(),
+                                              pk_s.as<unsigned long long>(),
+                                              pk_e.as<unsigned long long>(), 1);
+        }
+      }
       ProfScope ps_(c->lc, "k_group_iters", st);
-      k_group_iters<<<static_cast<unsigned>((gw * 32 + 255) / 256), 256, 0, st>>>(
+      k_group_iters<<<gblocks, 256, 0, st>>>(
           mv, Js, it_min, n_it, M, k, cfg.straggler_threshold_ms,
           tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>(),
-          gi.as<GroupIter>(), gi_last.as<int64_t>());
+          pc.as<uint32_t>(), sharded ? 2 : 3, gi.as<GroupIter>(), gi_last.as<int64_t>());
     }
   }
   // K4: affected groups

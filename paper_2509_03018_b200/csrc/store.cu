@@ -1794,7 +1794,13 @@ void store_build_op_index(csg_store* s, int32_t opn) {
       ProfScope ps_(c->lc, "k_iota", st);
       k_iota<<<grid_for(ng), 256, 0, st>>>(gi.as<uint32_t>(), ng);
     }
-    radix_sort_u64(gk.as<uint64_t>(), gi.as<uint32_t>(), ng, 64, s->sort, st, c->lc);
+    // keys are op - min_op over the global op range; the padding keys'
+    // low bits (all ones) still sort after every real key at that width.
+    // Stable: equal ops keep shard order, i.e. the global rank-major order.
+    const uint64_t grange =
+        s->max_op >= s->min_op ? static_cast<uint64_t>(s->max_op - s->min_op) : 0;
+    radix_sort_u64(gk.as<uint64_t>(), gi.as<uint32_t>(), ng, bits_for(grange + 1), s->sort, st,
+                   c->lc);
     s->opidx_keys.ensure(ng * 8 + 8);
     s->opidx_rank.ensure(ng * 4 + 4);
     s->opidx_ts.ensure(ng * 8 + 8);

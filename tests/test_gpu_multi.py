@@ -14,7 +14,7 @@ from tests.conftest import GOLDEN, ROOT
 pytestmark = pytest.mark.gpu
 
 CASES = ["scenario1", "scenario3", "scenario7", "synth_hang_128", "synth_strag_128",
-         "sweep_gpu_down", "sweep_slow_pcie", "sweep_opseq_lag"]
+         "sweep_gpu_down", "sweep_nic_flap", "sweep_slow_pcie", "sweep_opseq_lag"]
 
 
 def _free_port():
