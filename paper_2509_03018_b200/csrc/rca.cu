@@ -122,6 +122,35 @@ __device__ double warp_lower_median(int n, V val) {
   return 0;  // unreachable for n >= 1
 }
 
+// The same lower median over n <= 32 * S values held in registers, value
+// s * 32 + lane in v[s] (shuffles instead of n reloads per lane).
+template <int S>
+__device__ double warp_lower_median_reg(int n, const double (&v)[S]) {
+  const int lane = threadIdx.x & 31;
+  const int k = (n - 1) / 2;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    if (s * 32 >= n) break;
+    const int i = s * 32 + lane;
+    const double vi = v[s];
+    int less = 0, leq = 0;
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      if (t * 32 >= n) break;
+      const int lim = min(32, n - t * 32);
+      for (int l = 0; l < lim; ++l) {
+        const double vq = __shfl_sync(FULL, v[t], l);
+        less += vq < vi;
+        leq += vq <= vi;
+      }
+    }
+    const bool mine = i < n && less <= k && k < leq;
+    const unsigned mm = __ballot_sync(FULL, mine);
+    if (mm) return __shfl_sync(FULL, vi, __ffs(mm) - 1);
+  }
+  return 0;  // unreachable for n >= 1
+}
+
 // ---------------------------------------------------------------------------
 // K1: per (trip, rank) prefix summary.
 // ---------------------------------------------------------------------------
@@ -468,6 +497,34 @@ __global__ void k_succ_prog(StoreView s, FlowView f, ModelView m, int32_t J,
 // (trip, member slot, iteration) min start / max end of the member's prefix
 // completions with comm_id == group.
 // ---------------------------------------------------------------------------
+// Min / max of (start, end) keys into table cells, one atomic pair per
+// distinct cell of the warp: consecutive records of a rank segment mostly
+// fall into the same (slot, iteration) cell, and 32 same-address atomics
+// serialise at L2. Warp-uniform call; part = this lane has a record.
+__device__ __forceinline__ void warp_cell_minmax(bool part, uint64_t idx, unsigned long long ks,
+                                                 unsigned long long ke,
+                                                 unsigned long long* __restrict__ tbl_s,
+                                                 unsigned long long* __restrict__ tbl_e) {
+  const int lane = threadIdx.x & 31;
+  unsigned todo = __ballot_sync(FULL, part);
+  while (todo) {
+    const int l = __ffs(todo) - 1;
+    const uint64_t cidx = __shfl_sync(FULL, idx, l);
+    const bool mine = part && idx == cidx;
+    unsigned long long vmn = mine ? ks : ~0ull, vmx = mine ? ke : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      vmn = min(vmn, __shfl_xor_sync(FULL, vmn, o));
+      vmx = max(vmx, __shfl_xor_sync(FULL, vmx, o));
+    }
+    if (lane == l) {
+      atomicMin(&tbl_s[cidx], vmn);
+      atomicMax(&tbl_e[cidx], vmx);
+    }
+    todo &= ~__ballot_sync(FULL, mine);
+  }
+}
+
 __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
                               const int32_t* __restrict__ strag_trip,
                               const RankSum* __restrict__ rs, int64_t it_min,
@@ -488,20 +545,27 @@ __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
   // segment is walked (empty for ranks owned elsewhere)
   const uint32_t cend =
       min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, s.rank_off[r + 1]);
-  for (uint32_t p = b + lane; p < cend; p += 32) {
-    if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
-    const int32_t cm = s.comm[p];
+  for (uint32_t pw = b; pw < cend; pw += 32) {
+    const uint32_t p = pw + lane;
     uint32_t slot = kNoPos;
-    for (uint32_t q = g0; q < g1; ++q)
-      if (m.rg_group[q] == cm) {
-        slot = m.rg_slot[q];
-        break;
-      }
-    if (slot == kNoPos) continue;
-    const int64_t it = iter_of(s.op[p], m.opn) - it_min;
-    const uint64_t idx = (static_cast<uint64_t>(js) * M + slot) * n_it + it;
-    atomicMin(&tbl_s[idx], static_cast<unsigned long long>(dkey(as_double(s.pa[p]))));
-    atomicMax(&tbl_e[idx], static_cast<unsigned long long>(dkey(s.ts[p])));
+    if (p < cend && ko_kind(s.ko[p]) == CSG_KIND_COMPLETION) {
+      const int32_t cm = s.comm[p];
+      for (uint32_t q = g0; q < g1; ++q)
+        if (m.rg_group[q] == cm) {
+          slot = m.rg_slot[q];
+          break;
+        }
+    }
+    const bool part = slot != kNoPos;
+    uint64_t idx = 0;
+    unsigned long long ks = 0, ke = 0;
+    if (part) {
+      const int64_t it = iter_of(s.op[p], m.opn) - it_min;
+      idx = (static_cast<uint64_t>(js) * M + slot) * n_it + it;
+      ks = static_cast<unsigned long long>(dkey(as_double(s.pa[p])));
+      ke = static_cast<unsigned long long>(dkey(s.ts[p]));
+    }
+    warp_cell_minmax(part, idx, ks, ke, tbl_s, tbl_e);
   }
 }
 
@@ -514,10 +578,11 @@ __global__ void k_iter_tables(StoreView s, ModelView m, int32_t Js,
 // contiguous part of the rank's segment (the walk is load-latency bound:
 // one warp per rank left 8 warps per SM on the C2 store).
 constexpr int kIterParts = 8;
+constexpr int kIterUnroll = 4;
 __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
                                   const int32_t* __restrict__ strag_trip,
                                   const RankSum* __restrict__ rs, int64_t it_min,
-                                  int32_t n_it, uint32_t M,
+                                  int32_t n_it, uint32_t M, int32_t cached_js,
                                   unsigned long long* __restrict__ tbl_s,
                                   unsigned long long* __restrict__ tbl_e) {
   const int lane = threadIdx.x & 31;
@@ -529,6 +594,16 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
   const uint32_t g0 = m.rg_off[r], g1 = m.rg_off[r + 1];
   if (g0 == g1) return;
   const uint32_t b = s.rank_off[r], e = s.rank_off[r + 1];
+  // one block per rank (kIterParts warps): the trips' prefix ends once, in
+  // shared memory (cached_js of them; the rest are read from global)
+  extern __shared__ uint32_t s_cend[];
+  auto cend_g = [&](int32_t js) {
+    return min(b + rs[static_cast<uint64_t>(strag_trip[js]) * s.R + r].cutoff, e);
+  };
+  const int32_t cached = min(Js, cached_js);
+  for (int32_t js = threadIdx.x; js < cached; js += blockDim.x) s_cend[js] = cend_g(js);
+  __syncthreads();
+  auto cend_of = [&](int32_t js) { return js < cached ? s_cend[js] : cend_g(js); };
   const uint32_t plen = (e - b + kIterParts - 1) / kIterParts;
   const uint32_t p0 = min(e, b + part * plen), p1 = min(e, p0 + plen);
   if (p0 >= p1) return;
@@ -542,14 +617,42 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
     sq[q] = q < ng ? m.rg_slot[g0 + q] : kNoPos;
   }
   const bool many = g1 - g0 > 4;
-  uint32_t done = b;
-  for (int32_t js = 0; js < Js && done < p1; ++js) {
-    const int32_t j = strag_trip[js];
-    const uint32_t cend = min(b + rs[static_cast<uint64_t>(j) * s.R + r].cutoff, e);
-    const uint32_t lo = max(done, p0), hi = min(cend, p1);
-    for (uint32_t p = lo + lane; p < hi; p += 32) {
-      if (ko_kind(s.ko[p]) != CSG_KIND_COMPLETION) continue;
-      const int32_t cm = s.comm[p];
+  // record p belongs to the first trip js (in order) with cend(js) > p; p
+  // only grows along a lane, so each lane advances its own trip cursor
+  int32_t jl = 0;
+  uint32_t cl = Js > 0 ? cend_of(0) : 0;
+  const uint4* meta = reinterpret_cast<const uint4*>(s.comm.p);
+  const ulonglong2* tso = reinterpret_cast<const ulonglong2*>(s.ts.p);
+  for (uint32_t pw = p0; pw < p1; pw += 32 * kIterUnroll) {
+    // every load of the batch issued before any is used: the walk is bound
+    // by the dependent meta -> payload round trips, not by bandwidth
+    uint4 mt[kIterUnroll];
+#pragma unroll
+    for (int u = 0; u < kIterUnroll; ++u) {
+      const uint32_t p = pw + u * 32 + lane;
+      mt[u] = p < p1 ? meta[p] : make_uint4(0, 0, 0, 0);
+    }
+    ulonglong2 to[kIterUnroll];
+    unsigned long long pv[kIterUnroll];
+#pragma unroll
+    for (int u = 0; u < kIterUnroll; ++u) {
+      const uint32_t p = pw + u * 32 + lane;
+      const bool cmp = p < p1 && ko_kind(static_cast<uint8_t>(mt[u].w)) == CSG_KIND_COMPLETION;
+      to[u] = cmp ? tso[p] : make_ulonglong2(0, 0);
+      pv[u] = cmp ? *reinterpret_cast<const unsigned long long*>(
+                        s.pa.recs + static_cast<uint64_t>(mt[u].z) * 48 + 32)
+                  : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kIterUnroll; ++u) {
+      const uint32_t p = pw + u * 32 + lane;
+      if (p >= p1 || ko_kind(static_cast<uint8_t>(mt[u].w)) != CSG_KIND_COMPLETION) continue;
+      while (jl < Js && cl <= p) {
+        ++jl;
+        cl = jl < Js ? cend_of(jl) : 0;
+      }
+      if (jl >= Js) continue;
+      const int32_t cm = static_cast<int32_t>(mt[u].x);
       uint32_t slot = kNoPos;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -561,12 +664,13 @@ __global__ void k_iter_tables_inc(StoreView s, ModelView m, int32_t Js,
             break;
           }
       if (slot == kNoPos) continue;
-      const int64_t it = iter_of(s.op[p], m.opn) - it_min;
-      const uint64_t idx = (static_cast<uint64_t>(js) * M + slot) * n_it + it;
-      atomicMin(&tbl_s[idx], static_cast<unsigned long long>(dkey(as_double(s.pa[p]))));
-      atomicMax(&tbl_e[idx], static_cast<unsigned long long>(dkey(s.ts[p])));
+      const int64_t it = iter_of(static_cast<int64_t>(to[u].y), m.opn) - it_min;
+      const uint64_t idx = (static_cast<uint64_t>(jl) * M + slot) * n_it + it;
+      atomicMin(&tbl_s[idx], static_cast<unsigned long long>(dkey(__longlong_as_double(
+                                 static_cast<long long>(pv[u])))));
+      atomicMax(&tbl_e[idx], static_cast<unsigned long long>(dkey(__longlong_as_double(
+                                 static_cast<long long>(to[u].x)))));
     }
-    done = max(done, cend);
   }
 }
 
@@ -726,11 +830,27 @@ __global__ void k_group_iters(ModelView m, int32_t Js, int64_t it_min,
       auto ev = [&](int i) {
         return dkey_inv(tbl_e[(rowbase + m.member_slot[mo + i]) * n_it + latest]);
       };
-      const double ms = warp_lower_median(mm, sv);
-      const double me = warp_lower_median(mm, ev);
       bool late = false;
-      for (int32_t i = lane; i < mm; i += 32)
-        late |= (sv(i) - ms >= thr) || (ev(i) - me >= thr);
+      constexpr int S = 8;
+      if (mm <= 32 * S) {  // the members' cells once, in registers
+        double vs[S], ve[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          const int i = q * 32 + lane;
+          vs[q] = i < mm ? sv(i) : 0.0;
+          ve[q] = i < mm ? ev(i) : 0.0;
+        }
+        const double ms = warp_lower_median_reg(mm, vs);
+        const double me = warp_lower_median_reg(mm, ve);
+#pragma unroll
+        for (int q = 0; q < S; ++q)
+          if (q * 32 + lane < mm) late |= (vs[q] - ms >= thr) || (ve[q] - me >= thr);
+      } else {
+        const double ms = warp_lower_median(mm, sv);
+        const double me = warp_lower_median(mm, ev);
+        for (int32_t i = lane; i < mm; i += 32)
+          late |= (sv(i) - ms >= thr) || (ev(i) - me >= thr);
+      }
       out.late = __any_sync(FULL, late) ? 1 : 0;
     }
   }
@@ -5283,10 +5403,12 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
       const bool inc = R > 0 && ordered && !inc_off;
       if (inc) {
         {
-          const uint64_t warps = static_cast<uint64_t>(R) * kIterParts;
+          const int32_t cached = std::min(Js, 8192);
           ProfScope ps_(c->lc, "k_iter_tables", st);
-          k_iter_tables_inc<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
-              sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it, M,
+          // one block of kIterParts warps per rank
+          k_iter_tables_inc<<<static_cast<unsigned>(R), 32 * kIterParts,
+                              static_cast<size_t>(cached) * 4, st>>>(
+              sv, mv, Js, dstrag, rs.as<RankSum>(), it_min, n_it, M, cached,
               tbl_s.as<unsigned long long>(), tbl_e.as<unsigned long long>());
         }
         ProfScope ps_(c->lc, "k_iter_prefix", st);
