@@ -4121,8 +4121,9 @@ __global__ void __launch_bounds__(kDecideThreads) k_cohorts_lazy(DecideArgs a) {
 
 // The claimed cohorts as one multi-block radix select: every (trip, op name,
 // iteration) slot k_sf_fast claimed becomes an item over its iteration's
-// op-index range; a count pass and eight 8-bit digit passes run over all
-// items' entries at once (4096-entry units spread over the whole GPU, block
+// op-index range; eight 8-bit digit passes run over all
+// items' entries at once (the top digit's pass also counts the entries;
+// 4096-entry units spread over the whole GPU, block
 // histograms merged into per-item global ones), a tiny pick kernel narrows
 // each item's prefix between passes. The lower median of an item is element
 // (m - 1) / 2 of its entries with op name nm and ts <= t; fewer than two
@@ -4200,7 +4201,7 @@ __global__ void __launch_bounds__(1024) k_coh_collect(DecideArgs a, CohItem* __r
   }
 }
 
-// shift < 0: count pass; else the digit at `shift` of the keys matching the
+// shift < 0: count pass only (unused); else the digit at `shift` of the keys matching the
 // item's prefix above it
 __global__ void __launch_bounds__(256) k_coh_pass(DecideArgs a, CohItem* __restrict__ items,
                                                   const CohPlan* __restrict__ plan,
@@ -4227,13 +4228,15 @@ __global__ void __launch_bounds__(256) k_coh_pass(DecideArgs a, CohItem* __restr
     }
     __syncthreads();
     uint32_t cnt = 0;
+    const bool counting = shift < 0 || shift == 56;  // the top digit's pass counts too
+    if (shift == 56 && threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
     for (uint64_t b0 = y0; b0 < y1; b0 += blockDim.x) {
       const uint64_t y = b0 + threadIdx.x;
       uint32_t d = 256;
       if (y < y1 && a.op_nm[y] == it.nm && a.op_ts[y] <= it.t) {
-        if (shift < 0) {
-          ++cnt;
-        } else {
+        if (counting) ++cnt;
+        if (shift >= 0) {
           const uint64_t key = dkey(a.op_dur[y]);
           if ((key & mask) == (it.prefix & mask)) d = static_cast<uint32_t>((key >> shift) & 255);
         }
@@ -4243,15 +4246,14 @@ __global__ void __launch_bounds__(256) k_coh_pass(DecideArgs a, CohItem* __restr
         if (d < 256 && lane == __ffs(peers) - 1) atomicAdd(&sh[d], static_cast<uint32_t>(__popc(peers)));
       }
     }
-    if (shift < 0) {
+    if (counting) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
       if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     }
     __syncthreads();
-    if (shift < 0) {
-      if (threadIdx.x == 0 && s_cnt) atomicAdd(&items[lo].m, s_cnt);
-    } else {
+    if (counting && threadIdx.x == 0 && s_cnt) atomicAdd(&items[lo].m, s_cnt);
+    if (shift >= 0) {
       for (int i = threadIdx.x; i < 256; i += blockDim.x)
         if (sh[i]) atomicAdd(&hist[static_cast<uint64_t>(lo) * 256 + i], sh[i]);
     }
@@ -4267,9 +4269,9 @@ __global__ void k_coh_pick(DecideArgs a, CohItem* __restrict__ items,
   const unsigned n = plan->n_items;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     CohItem& it = items[i];
-    if (shift < 0) {
+    if (shift < 0 || shift == 56) {
       it.kth = it.m >= 1 ? (it.m - 1) / 2 : 0;
-      continue;
+      if (shift < 0) continue;
     }
     uint32_t* hh = hist + static_cast<uint64_t>(i) * 256;
     uint64_t acc = 0;
@@ -6018,8 +6020,7 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
             CohItem* citems = reinterpret_cast<CohItem*>(d_ci.as<unsigned char>() + 64);
             uint32_t* chist = reinterpret_cast<uint32_t*>(citems + kCohItemsCap);
             k_coh_collect<<<1, 1024, 0, st>>>(a, citems, cplan, chist);
-            k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, -1);
-            k_coh_pick<<<8, 256, 0, st>>>(a, citems, cplan, chist, -1);
+            // the top digit's pass also counts each item's entries
             for (int sh2 = 56; sh2 >= 0; sh2 -= 8) {
               k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
               k_coh_pick<<<8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
