@@ -4138,14 +4138,46 @@ struct CohItem {
   double t;
   int32_t nm;
   int32_t pad;
+  uint64_t off;    // compacted keys of the item: ckeys[off, off + m2)
+  uint64_t unit2;  // first work unit over the compacted keys
+  uint32_t m2;     // entries left after the digits down to kCohCompactShift
+  uint32_t fill;
 };
 struct CohPlan {
   unsigned n_items;
-  unsigned pad;
+  unsigned compact;  // the compacted keys fit: the low digits' passes read them
   unsigned long long units;
+  unsigned long long units2;
+  unsigned long long total2;
 };
+static_assert(sizeof(CohPlan) <= 64, "CohPlan sits in the first 64 bytes of the items buffer");
 constexpr int kCohUnit = 4096;
 constexpr uint32_t kCohItemsCap = 8192;
+// After the digits 63..40 the surviving entries of each item (a handful of
+// durations sharing sign, exponent and 12 mantissa bits) are compacted, so
+// the five low digits' passes stop rescanning the iterations' op ranges.
+constexpr int kCohCompactShift = 40;
+
+// Exclusive block scan of n values val(i) -> put(i, prefix); returns the total.
+template <typename V, typename P>
+__device__ unsigned long long block_excl_scan_n(uint32_t n, V val, P put,
+                                                unsigned long long* s_w,
+                                                unsigned long long* s_carry) {
+  if (threadIdx.x == 0) *s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const unsigned long long v = i < n ? val(i) : 0ull;
+    const unsigned long long inc = block_incl_scan(
+        v, s_w, [](unsigned long long x, unsigned long long y) { return x + y; });
+    const unsigned long long c0 = *s_carry;
+    if (i < n) put(i, c0 + inc - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) *s_carry = c0 + inc;
+    __syncthreads();
+  }
+  return *s_carry;
+}
 
 __global__ void __launch_bounds__(1024) k_coh_collect(DecideArgs a, CohItem* __restrict__ items,
                                                       CohPlan* __restrict__ plan,
@@ -4190,14 +4222,14 @@ __global__ void __launch_bounds__(1024) k_coh_collect(DecideArgs a, CohItem* __r
   __syncthreads();
   const unsigned n = min(s_n, kCohItemsCap);
   for (uint64_t i = threadIdx.x; i < static_cast<uint64_t>(n) * 256; i += blockDim.x) hist[i] = 0;
+  __shared__ unsigned long long s_w[32], s_carry;
+  const unsigned long long u = block_excl_scan_n(
+      n, [&](uint32_t i) { return (items[i].ce - items[i].cb + kCohUnit - 1) / kCohUnit; },
+      [&](uint32_t i, unsigned long long x) { items[i].unit0 = x; }, s_w, &s_carry);
   if (threadIdx.x == 0) {
-    unsigned long long u = 0;
-    for (unsigned i = 0; i < n; ++i) {
-      items[i].unit0 = u;
-      u += (items[i].ce - items[i].cb + kCohUnit - 1) / kCohUnit;
-    }
     plan->n_items = n;
     plan->units = u;
+    plan->compact = 0;
   }
 }
 
@@ -4205,12 +4237,46 @@ __global__ void __launch_bounds__(1024) k_coh_collect(DecideArgs a, CohItem* __r
 // item's prefix above it
 __global__ void __launch_bounds__(256) k_coh_pass(DecideArgs a, CohItem* __restrict__ items,
                                                   const CohPlan* __restrict__ plan,
-                                                  uint32_t* __restrict__ hist, int shift) {
+                                                  uint32_t* __restrict__ hist, int shift,
+                                                  const unsigned long long* __restrict__ ckeys) {
   __shared__ uint32_t sh[256];
   __shared__ uint32_t s_cnt;
   const unsigned n = plan->n_items;
-  const unsigned long long U = plan->units;
   const int lane = threadIdx.x & 31;
+  if (shift < kCohCompactShift && plan->compact) {
+    // the low digits over the compacted keys (all pass the op-name / time
+    // filters and match the prefix down to kCohCompactShift)
+    const unsigned long long U2 = plan->units2;
+    const uint64_t mask = ~0ull << (shift + 8);
+    for (unsigned long long u = blockIdx.x; u < U2; u += gridDim.x) {
+      unsigned lo = 0, hi = n;
+      while (hi - lo > 1) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (items[mid].unit2 <= u) lo = mid; else hi = mid;
+      }
+      const CohItem it = items[lo];
+      const uint64_t y0 = it.off + (u - it.unit2) * kCohUnit;
+      const uint64_t y1 = min(it.off + it.m2, y0 + kCohUnit);
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+      __syncthreads();
+      for (uint64_t b0 = y0; b0 < y1; b0 += blockDim.x) {
+        const uint64_t y = b0 + threadIdx.x;
+        uint32_t d = 256;
+        if (y < y1) {
+          const uint64_t key = ckeys[y];
+          if ((key & mask) == (it.prefix & mask)) d = static_cast<uint32_t>((key >> shift) & 255);
+        }
+        const unsigned peers = __match_any_sync(FULL, d);
+        if (d < 256 && lane == __ffs(peers) - 1) atomicAdd(&sh[d], static_cast<uint32_t>(__popc(peers)));
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[static_cast<uint64_t>(lo) * 256 + i], sh[i]);
+      __syncthreads();
+    }
+    return;
+  }
+  const unsigned long long U = plan->units;
   for (unsigned long long u = blockIdx.x; u < U; u += gridDim.x) {
     unsigned lo = 0, hi = n;  // items[lo].unit0 <= u < items[hi].unit0
     while (hi - lo > 1) {
@@ -4283,6 +4349,7 @@ __global__ void k_coh_pick(DecideArgs a, CohItem* __restrict__ items,
       }
       acc += hh[b];
     }
+    if (shift == kCohCompactShift) it.m2 = hh[bsel];
     for (int b = 0; b < 256; ++b) hh[b] = 0;
     it.prefix |= static_cast<uint64_t>(bsel) << shift;
     it.kth -= acc;
@@ -4290,6 +4357,66 @@ __global__ void k_coh_pick(DecideArgs a, CohItem* __restrict__ items,
       a.coh_val[it.slot] = it.m < 2 ? 0.0 : dkey_inv(it.prefix);
       __threadfence();
       atomicExch(a.coh_state + it.slot, 2u);
+    }
+  }
+}
+
+// Offsets of the items' compacted keys; compaction only when they fit.
+__global__ void __launch_bounds__(1024) k_coh_offsets(CohItem* __restrict__ items,
+                                                      CohPlan* __restrict__ plan,
+                                                      unsigned long long cap) {
+  __shared__ unsigned long long s_w[32], s_carry;
+  const unsigned n = plan->n_items;
+  const unsigned long long tot = block_excl_scan_n(
+      n, [&](uint32_t i) { return static_cast<unsigned long long>(items[i].m2); },
+      [&](uint32_t i, unsigned long long x) {
+        items[i].off = x;
+        items[i].fill = 0;
+      },
+      s_w, &s_carry);
+  const unsigned long long u2 = block_excl_scan_n(
+      n, [&](uint32_t i) { return (static_cast<unsigned long long>(items[i].m2) + kCohUnit - 1) / kCohUnit; },
+      [&](uint32_t i, unsigned long long x) { items[i].unit2 = x; }, s_w, &s_carry);
+  if (threadIdx.x == 0) {
+    plan->total2 = tot;
+    plan->units2 = u2;
+    plan->compact = tot <= cap ? 1u : 0u;
+  }
+}
+
+// The entries of each item matching its prefix down to kCohCompactShift,
+// copied (keys only, any order: a selection) into ckeys.
+__global__ void __launch_bounds__(256) k_coh_compact(DecideArgs a, CohItem* __restrict__ items,
+                                                     const CohPlan* __restrict__ plan,
+                                                     unsigned long long* __restrict__ ckeys) {
+  if (!plan->compact) return;
+  const unsigned n = plan->n_items;
+  const unsigned long long U = plan->units;
+  const int lane = threadIdx.x & 31;
+  const uint64_t mask = ~0ull << kCohCompactShift;
+  for (unsigned long long u = blockIdx.x; u < U; u += gridDim.x) {
+    unsigned lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (items[mid].unit0 <= u) lo = mid; else hi = mid;
+    }
+    const CohItem it = items[lo];
+    const uint64_t y0 = it.cb + (u - it.unit0) * kCohUnit;
+    const uint64_t y1 = min(it.ce, y0 + kCohUnit);
+    for (uint64_t b0 = y0; b0 < y1; b0 += blockDim.x) {
+      const uint64_t y = b0 + threadIdx.x;
+      bool keep = false;
+      uint64_t key = 0;
+      if (y < y1 && a.op_nm[y] == it.nm && a.op_ts[y] <= it.t) {
+        key = dkey(a.op_dur[y]);
+        keep = (key & mask) == (it.prefix & mask);
+      }
+      const unsigned mm = __ballot_sync(FULL, keep);
+      if (!mm) continue;
+      unsigned base = 0;
+      if (lane == __ffs(mm) - 1) base = atomicAdd(&items[lo].fill, static_cast<unsigned>(__popc(mm)));
+      base = __shfl_sync(FULL, base, __ffs(mm) - 1);
+      if (keep) ckeys[it.off + base + __popc(mm & ((1u << lane) - 1u))] = key;
     }
   }
 }
@@ -6019,11 +6146,19 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
             CohPlan* cplan = d_ci.as<CohPlan>();
             CohItem* citems = reinterpret_cast<CohItem*>(d_ci.as<unsigned char>() + 64);
             uint32_t* chist = reinterpret_cast<uint32_t*>(citems + kCohItemsCap);
+            DevBuf& d_ck = c->buf("rca.coh_ckeys");
+            const uint64_t ccap = std::max<uint64_t>(1u << 16, std::min<uint64_t>(a.n_opidx, 1u << 24));
+            d_ck.ensure(ccap * 8);
+            unsigned long long* ck = d_ck.as<unsigned long long>();
             k_coh_collect<<<1, 1024, 0, st>>>(a, citems, cplan, chist);
             // the top digit's pass also counts each item's entries
             for (int sh2 = 56; sh2 >= 0; sh2 -= 8) {
-              k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
+              k_coh_pass<<<148 * 8, 256, 0, st>>>(a, citems, cplan, chist, sh2, ck);
               k_coh_pick<<<8, 256, 0, st>>>(a, citems, cplan, chist, sh2);
+              if (sh2 == kCohCompactShift && !std::getenv("CSG_COH_NO_COMPACT")) {
+                k_coh_offsets<<<1, 1024, 0, st>>>(citems, cplan, ccap);
+                k_coh_compact<<<148 * 8, 256, 0, st>>>(a, citems, cplan, ck);
+              }
             }
           }
         }

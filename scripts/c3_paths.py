@@ -26,7 +26,8 @@ t0 = time.time(); got2, _ = E.run_detection(store, m, tc, ac, seed); dt = time.t
 assert got == got2
 print(json.dumps({"reports": got, "wall_s": dt}))
 """
-KNOBS = ["CSG_SF_SLOW", "CSG_SL_SERIAL", "CSG_ITER_PER_TRIP", "CSG_FLOW_SCAN", "CSG_EXO_WARP_SWEEP"]
+KNOBS = ["CSG_SF_SLOW", "CSG_SL_SERIAL", "CSG_ITER_PER_TRIP", "CSG_FLOW_SCAN", "CSG_EXO_WARP_SWEEP",
+         "CSG_COH_NO_COMPACT"]
 
 
 def run(slow):
