@@ -43,3 +43,24 @@ def test_shards_partition_the_trace(eng):
     assert sum(len(p) for p in parts) == len(full)
     for lo, p in zip(range(0, 128, 32), parts):
         assert ((p["rank"] >= lo) & (p["rank"] < lo + 32)).all()
+
+
+def test_copy_side_faults_take_copy_factor(eng):
+    """pcie_downgrade / gpu_power_limit / background_compute slow copies in
+    the reference (sim.cpp copy_factor); the generator's per-rank slowdown
+    takes whichever factor the fault sets, so a copy_factor fault slows the
+    rank exactly as the same bandwidth_factor one did, and differs from a
+    fault-free trace."""
+    cfg = json.load(open(os.path.join(GOLDEN, "configs", "synth_strag_128.json")))
+    f = [x for x in cfg["faults"] if x["kind"] == "pcie_downgrade"][0]
+    assert "bandwidth_factor" in f and "copy_factor" not in f
+
+    def synth(faults):
+        c = dict(cfg, faults=faults)
+        return eng.synthesize(eng.Scenario.parse(json.dumps(c)), 0).tobytes()
+
+    by_bw = synth([f])
+    g = {k: v for k, v in f.items() if k != "bandwidth_factor"}
+    g["copy_factor"] = f["bandwidth_factor"]
+    assert synth([g]) == by_bw
+    assert synth([]) != by_bw
