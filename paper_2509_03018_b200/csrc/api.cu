@@ -420,6 +420,7 @@ csg_status csg_store_invalidate(csg_store* s) {
   s->indexed = false;
   s->op_indexed = false;
   s->flow_indexed = false;
+  s->flow_early = false;
   return CSG_OK;
 }
 
@@ -476,6 +477,7 @@ static csg_status append_impl(csg_store* s, const csg_packed_record* src,
     s->indexed = false;
     s->op_indexed = false;
     s->flow_indexed = false;
+    s->flow_early = false;
     return CSG_OK;
   });
 }
@@ -530,6 +532,7 @@ csg_status csg_store_clear(csg_store* s) {
   s->indexed = false;
   s->op_indexed = false;
   s->flow_indexed = false;
+  s->flow_early = false;
   return CSG_OK;
 }
 

@@ -467,6 +467,7 @@ void store_append_jsonl(csg_store* s, const JsonlSource& src, uint64_t len, int*
   s->indexed = false;
   s->op_indexed = false;
   s->flow_indexed = false;
+  s->flow_early = false;
   *accepted = 1;
 }
 

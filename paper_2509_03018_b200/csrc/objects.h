@@ -114,6 +114,7 @@ struct csg_store {
   // flow index: per rank segment, positions ordered by (op_seq, store
   // order); identity for segments already ordered (see FlowView)
   bool flow_indexed = false;
+  bool flow_early = false;  // k_flow_fix launched ahead of the trip round trip
   csg::DevBuf fl_unsorted;  // u32 flag per rank
   csg::DevBuf fl_list;      // ranks with a descending op_seq (work list)
   csg::DevBuf fl_cnt;       // [0] list length, [1] overflow count
@@ -233,6 +234,7 @@ void store_build_index(csg_store* s);
 void store_build_op_index(csg_store* s, int32_t opn);
 // Returns false (and builds nothing) when the packed key exceeds 64 bits.
 bool store_build_flow_index(csg_store* s);
+void store_flow_index_early(csg_store* s);
 // Waits until everything enqueued on the context stream has completed
 // (spins on a mapped flag, falls back to cudaStreamSynchronize; errors are
 // reported like cudaStreamSynchronize's).

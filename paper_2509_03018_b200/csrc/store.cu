@@ -1689,6 +1689,7 @@ void store_build_index(csg_store* s) {
   s->indexed = true;
   s->op_indexed = false;
   s->flow_indexed = false;
+  s->flow_early = false;
 }
 
 void store_build_op_index(csg_store* s, int32_t opn) {
@@ -1844,6 +1845,32 @@ void store_resolve_max_seg(csg_store* s) {
   s->max_seg_pending = false;
 }
 
+// The flow index's segment fix-up launched ahead of the trip round trip of a
+// detection replay: k_flow_fix at the shared-memory cap (the longest segment
+// is only known once that round trip returns), so it runs while the host
+// reads the trips. store_build_flow_index then only does the overflow check.
+void store_flow_index_early(csg_store* s) {
+  static const bool off = std::getenv("CSG_FLOW_GLOBAL_SORT") != nullptr ||
+                          std::getenv("CSG_DISABLE_FLOW_INDEX") != nullptr ||
+                          std::getenv("CSG_FLOW_SMEM_CAP") != nullptr ||
+                          std::getenv("CSG_NO_EARLY_FLOW") != nullptr;
+  if (off || !s->indexed || s->flow_indexed || s->flow_early || !s->n || !s->R) return;
+  csg_ctx* c = s->ctx;
+  cudaStream_t st = c->stream;
+  s->fl_pos.ensure(s->n * 4 + 4);
+  unsigned* d_uns = s->fl_cnt.as<unsigned>();
+  smem_optin(k_flow_fix, kFlowSmemMax * 8);
+  {
+    ProfScope ps_(c->lc, "k_flow_fix", st);
+    k_flow_fix<<<static_cast<unsigned>(std::min<int32_t>(s->R, 148)), 1024,
+                 static_cast<size_t>(kFlowSmemMax) * 8, st>>>(
+        s->view(), s->fl_list.as<uint32_t>(), d_uns, kFlowSmemMax, s->fl_pos.as<uint32_t>(),
+        d_uns + 1);
+  }
+  CSG_CUDA(cudaGetLastError());
+  s->flow_early = true;
+}
+
 bool store_build_flow_index(csg_store* s) {
   store_build_index(s);
   if (s->flow_indexed) return true;
@@ -1876,9 +1903,11 @@ bool store_build_flow_index(csg_store* s) {
     }();
     int32_t P = 64;
     while (static_cast<uint64_t>(P) < s->max_seg && P < cap) P <<= 1;
-    const size_t smem = static_cast<size_t>(P) * 8;
-    smem_optin(k_flow_fix, kFlowSmemMax * 8);
-    {
+    if (s->flow_early) {
+      P = kFlowSmemMax;  // already launched at the cap (store_flow_index_early)
+    } else {
+      const size_t smem = static_cast<size_t>(P) * 8;
+      smem_optin(k_flow_fix, kFlowSmemMax * 8);
       ProfScope ps_(c->lc, "k_flow_fix", st);
       k_flow_fix<<<static_cast<unsigned>(std::min<int32_t>(R, 148)), 1024, smem, st>>>(
           s->view(), list.as<uint32_t>(), d_uns, P, s->fl_pos.as<uint32_t>(), d_ovf);

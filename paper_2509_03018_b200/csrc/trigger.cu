@@ -569,7 +569,11 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   fa.add(events.p, h + 16, static_cast<size_t>(T) * sizeof(csg_trigger_event));
   const bool ms = s->max_seg_pending;  // rides on the same round trip
   if (ms) fa.add(&s->stats_dev.as<StoreStats>()->max_seg, h + 8, 8);
-  ctx_sync(c, &fa);
+  // the flow index's fix-up queues behind the fetch: the GPU runs it while
+  // the host reads the trips (RCA needs it for any trip)
+  const FetchTicket tk = ctx_fetch_issue(c, fa);
+  store_flow_index_early(s);
+  ctx_fetch_wait(c, tk);
   tl_mark("trigger sync returned");
   if (ms) {
     std::memcpy(&s->max_seg, h + 8, 8);
