@@ -237,6 +237,17 @@ struct WinMax {
   unsigned long long mn_inv, mx;
 };
 
+// Mapped-memory publication of the trip list by the block that compacts it
+// (the fused single-GPU trigger): [0] trip count, [8] longest store segment
+// (when pending), [16..) the events, then the completion word — what the
+// k_fetch of ctx_fetch_issue would copy, without its launch.
+struct TrigPublish {
+  unsigned char* h = nullptr;
+  const unsigned long long* max_seg = nullptr;
+  unsigned long long* flag = nullptr;
+  unsigned long long seq = 0;
+};
+
 // EMA of sampled rank si over all ticks (evaluate, trigger.cpp:57-136) from
 // the accumulated windows staged in shared memory, then — in the last block
 // to finish (done[S] ticket) — the lowest tripped rank of every tick,
@@ -247,7 +258,8 @@ __device__ void trigger_ema_pick(int32_t si, int32_t T, const double* st, int32_
                                  const WinMax* __restrict__ amax, unsigned* __restrict__ done,
                                  uint8_t* __restrict__ trip,
                                  csg_trigger_event* __restrict__ events,
-                                 int32_t* __restrict__ n_events, WinStat* ws) {
+                                 int32_t* __restrict__ n_events, WinStat* ws,
+                                 TrigPublish pub = TrigPublish{}) {
   __shared__ int last;
   __threadfence();
   for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
@@ -325,6 +337,26 @@ __device__ void trigger_ema_pick(int32_t si, int32_t T, const double* st, int32_
     __syncthreads();
   }
   if (threadIdx.x == 0) *n_events = base;
+  if (pub.h) {
+    __threadfence();
+    __syncthreads();
+    const int32_t ne = base;
+    const uint32_t* e4 = reinterpret_cast<const uint32_t*>(events);
+    uint32_t* d4 = reinterpret_cast<uint32_t*>(pub.h + 16);
+    const uint32_t words = static_cast<uint32_t>(ne) * (sizeof(csg_trigger_event) / 4);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) d4[i] = __ldcg(e4 + i);
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<int32_t*>(pub.h) = ne;
+      if (pub.max_seg)
+        *reinterpret_cast<unsigned long long*>(pub.h + 8) = __ldcg(pub.max_seg);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<volatile unsigned long long*>(pub.flag) = pub.seq;
+      __threadfence_system();
+    }
+  }
 }
 
 // Whole trigger stage of run_detection in one launch:
@@ -339,7 +371,7 @@ __global__ void __launch_bounds__(512)
               const int32_t* __restrict__ sampled, int32_t S, TrigParams p, int32_t B,
               WinSum* __restrict__ asum, WinMax* __restrict__ amax, unsigned* __restrict__ done,
               uint8_t* __restrict__ trip, csg_trigger_event* __restrict__ events,
-              int32_t* __restrict__ n_events, int chain) {
+              int32_t* __restrict__ n_events, int chain, TrigPublish pub) {
   extern __shared__ __align__(16) unsigned char tg_dyn[];
   double* st = reinterpret_cast<double*>(tg_dyn);                       // [T]
   unsigned long long* bytes = reinterpret_cast<unsigned long long*>(st + T);
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(512)
   // the bins are merged: the 40 T bytes behind the tick times (launched with
   // T * (8 + sizeof(WinStat)) bytes) stage the T window statistics
   trigger_ema_pick(si, T, st, S, sampled, p, asum, amax, done, trip, events, n_events,
-                   reinterpret_cast<WinStat*>(bytes));
+                   reinterpret_cast<WinStat*>(bytes), pub);
 }
 
 // Sharded finish: one block per sampled rank over the all-reduced windows.
@@ -501,6 +533,8 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   ws.ensure(static_cast<size_t>(T) * S * sizeof(WinStat));
   trip.ensure(static_cast<size_t>(T) * S);
   dn.ensure(4);
+  static const bool no_publish = std::getenv("CSG_TRIG_FETCH") != nullptr;
+  FetchTicket published;  // seq 0: the trips come back through k_fetch
   // bins need 44 B per tick; after the merge the last block of a sampled
   // rank stages its window statistics behind the tick times (8 + 40 B)
   static_assert(sizeof(WinStat) == 40, "WinStat layout");
@@ -521,11 +555,27 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     smem_optin(k_trigger, 200 * 1024);
     smem_optin(k_trigger_ema, 200 * 1024);
     const bool sharded = comm_active(c);
+    TrigPublish pub;
+    if (!sharded && !no_publish) {  // the compacting block publishes the trips
+      HostBuf& hb = c->hbuf("trig.out");
+      hb.ensure(16 + static_cast<size_t>(T) * sizeof(csg_trigger_event));
+      c->sig.ensure(64);
+      pub.h = hb.as<unsigned char>();
+      pub.max_seg = s->max_seg_pending ? &s->stats_dev.as<StoreStats>()->max_seg : nullptr;
+      pub.flag = c->sig.as<unsigned long long>();
+      pub.seq = ++c->sig_seq;
+    }
     {
       ProfScope ps_(c->lc, "k_trigger", c->stream);
       k_trigger<<<dim3(B, S), 512, tsmem, c->stream>>>(
           s->view(), d_ticks, T, d_sampled, S, p, B, asum, amax, done, trip.as<uint8_t>(),
-          events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1);
+          events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1, pub);
+    }
+    if (pub.h) {
+      CSG_CUDA(cudaGetLastError());
+      if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
+      CSG_CUDA(cudaEventRecord(c->ev_fetch, c->stream));
+      published = FetchTicket{pub.seq};
     }
     if (sharded) {
       // shards own disjoint rank ranges: windows combine by sum / max
@@ -571,7 +621,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
   if (ms) fa.add(&s->stats_dev.as<StoreStats>()->max_seg, h + 8, 8);
   // the flow index's fix-up queues behind the fetch: the GPU runs it while
   // the host reads the trips (RCA needs it for any trip)
-  const FetchTicket tk = ctx_fetch_issue(c, fa);
+  const FetchTicket tk = published.seq ? published : ctx_fetch_issue(c, fa);
   store_flow_index_early(s);
   ctx_fetch_wait(c, tk);
   tl_mark("trigger sync returned");
