@@ -449,14 +449,15 @@ __global__ void __launch_bounds__(512)
                   const int32_t* __restrict__ sampled, int32_t S, TrigParams p,
                   const WinSum* __restrict__ asum, const WinMax* __restrict__ amax,
                   unsigned* __restrict__ done, uint8_t* __restrict__ trip,
-                  csg_trigger_event* __restrict__ events, int32_t* __restrict__ n_events) {
+                  csg_trigger_event* __restrict__ events, int32_t* __restrict__ n_events,
+                  TrigPublish pub) {
   extern __shared__ __align__(16) unsigned char te_dyn[];
   double* st = reinterpret_cast<double*>(te_dyn);       // [T]
   WinStat* ws = reinterpret_cast<WinStat*>(st + T);      // [T]
   for (int32_t k = threadIdx.x; k < T; k += blockDim.x) st[k] = ticks[k];
   __syncthreads();
   trigger_ema_pick(blockIdx.x, T, st, S, sampled, p, asum, amax, done, trip, events,
-                   n_events, ws);
+                   n_events, ws, pub);
 }
 
 // csg_evaluate: one tick, the caller's sampled list in order (duplicates
@@ -556,7 +557,7 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
     smem_optin(k_trigger_ema, 200 * 1024);
     const bool sharded = comm_active(c);
     TrigPublish pub;
-    if (!sharded && !no_publish) {  // the compacting block publishes the trips
+    if (!no_publish) {  // the compacting block publishes the trips
       HostBuf& hb = c->hbuf("trig.out");
       hb.ensure(16 + static_cast<size_t>(T) * sizeof(csg_trigger_event));
       c->sig.ensure(64);
@@ -569,9 +570,10 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
       ProfScope ps_(c->lc, "k_trigger", c->stream);
       k_trigger<<<dim3(B, S), 512, tsmem, c->stream>>>(
           s->view(), d_ticks, T, d_sampled, S, p, B, asum, amax, done, trip.as<uint8_t>(),
-          events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1, pub);
+          events.as<csg_trigger_event>(), dn.as<int32_t>(), sharded ? 0 : 1,
+          sharded ? TrigPublish{} : pub);
     }
-    if (pub.h) {
+    if (pub.h && !sharded) {
       CSG_CUDA(cudaGetLastError());
       if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
       CSG_CUDA(cudaEventRecord(c->ev_fetch, c->stream));
@@ -587,7 +589,14 @@ int32_t trigger_run(csg_store* s, const double* d_ticks, int32_t T,
       ProfScope ps_(c->lc, "k_trigger_ema", c->stream);
       k_trigger_ema<<<S, 512, tsmem, c->stream>>>(
           d_ticks, T, d_sampled, S, p, asum, amax, done, trip.as<uint8_t>(),
-          events.as<csg_trigger_event>(), dn.as<int32_t>());
+          events.as<csg_trigger_event>(), dn.as<int32_t>(), pub);
+      if (pub.h) {
+        CSG_CUDA(cudaGetLastError());
+        if (!c->ev_fetch)
+          CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
+        CSG_CUDA(cudaEventRecord(c->ev_fetch, c->stream));
+        published = FetchTicket{pub.seq};
+      }
     }
   } else {
   trigger_window_stats(s, d_ticks, T, d_sampled, S, p.delta, ws.as<WinStat>());
