@@ -18,6 +18,7 @@
 
 #include "comm.cuh"
 #include "objects.h"
+#include "fetch.cuh"
 #include "rca.cuh"
 #include "rca_table.h"
 #include "trigger.cuh"
@@ -195,28 +196,7 @@ __global__ void k_fetch(FetchArgs a, unsigned long long* flag, unsigned long lon
                         unsigned* __restrict__ done) {
   const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nt = gridDim.x * blockDim.x;
-  for (int sgi = 0; sgi < a.n; ++sgi) {
-    const FetchSeg& g = a.seg[sgi];
-    if (g.row_len) {  // rows with device-side lengths, one warp per row
-      const int lane = threadIdx.x & 31;
-      for (uint32_t rw = gt >> 5; rw < g.nrows; rw += nt >> 5) {
-        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(g.src + rw * g.bytes);
-        uint32_t* d4 = reinterpret_cast<uint32_t*>(g.dst + rw * g.bytes);
-        const int32_t len = g.row_len[rw];
-        for (int32_t i = lane; i < len; i += 32) d4[i] = s4[i];
-      }
-      continue;
-    }
-    const bool vec = ((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) |
-                       g.bytes) & 15) == 0;
-    if (vec) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(g.src);
-      uint4* d4 = reinterpret_cast<uint4*>(g.dst);
-      for (uint32_t i = gt; i < g.bytes / 16; i += nt) d4[i] = s4[i];
-    } else {
-      for (uint32_t i = gt; i < g.bytes; i += nt) g.dst[i] = g.src[i];
-    }
-  }
+  fetch_copy(a, gt, nt);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {

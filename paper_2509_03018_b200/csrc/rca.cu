@@ -23,6 +23,7 @@
 #include <cstring>
 
 #include "comm.cuh"
+#include "fetch.cuh"
 #include "rca.cuh"
 #include "rca_table.h"
 
@@ -3910,7 +3911,9 @@ __global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
                        const csg_suspect* __restrict__ sus,
                        const csg_evidence* __restrict__ ev,
                        csg_suspect* __restrict__ osus,
-                       csg_evidence* __restrict__ oev) {
+                       csg_evidence* __restrict__ oev, FetchArgs fa,
+                       unsigned long long* flag, unsigned long long v,
+                       unsigned* __restrict__ fdone) {
   pdl_wait();
   pdl_trigger();
   // block (j, kind, slice): its packed offset is the sum of the earlier
@@ -3935,6 +3938,9 @@ __global__ void k_pack(const TripOut* __restrict__ out, int32_t J,
     if (kind < 2) osus[d0 + i] = sus[s0 + i];
     else oev[d0 + i] = ev[s0 + i];
   }
+  // the batch's tail (error word, pool usage, trip table) rides on the
+  // last block: no k_fetch launch behind the pack
+  fetch_tail(fa, flag, v, fdone);
 }
 
 __global__ void __launch_bounds__(kDecideThreads)
@@ -6195,12 +6201,6 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
     // the pool usage and the error word all come back in ONE round trip
     h_sus.ensure(sus_cap * sizeof(csg_suspect) + 64);
     h_ev.ensure(ev_cap * sizeof(csg_evidence) + 64);
-    if (J > 0) {
-      ProfScope ps_(c->lc, "k_pack", st);
-      launch_pdl(k_pack, dim3(dim3(static_cast<unsigned>(3 * J), 8)), dim3(128), 0, st, 
-          d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
-          h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>());
-    }
     // pinned: [0] error word, [16] pool usage, [80] packed totals, [96..) trips
     HostBuf& hr = c->hbuf("rca.tail");
     hr.ensure(96 + static_cast<size_t>(J) * sizeof(TripOut));
@@ -6216,7 +6216,50 @@ void rca_batch(csg_store* s, const csg_model* m, const csg_analysis_config& cfg,
         fa.add(d_plan.p, d_plan.stage.p ? d_plan.stage.p : (d_plan.stage.ensure(64), d_plan.stage.p),
                sizeof(FailPlan));
       }
-      ctx_sync(c, &fa);
+      static const bool pack_fetch = std::getenv("CSG_PACK_FETCH") != nullptr;
+      if (J > 0 && !pack_fetch) {
+        // k_pack's last block copies the tail and raises the completion word
+        c->sig.ensure(64);
+        DevBuf& fdn = c->buf("fetch.done");
+        if (fdn.bytes < 16) {
+          fdn.ensure(16);
+          CSG_CUDA(cudaMemsetAsync(fdn.p, 0, 16, st));
+        }
+        const unsigned long long v = ++c->sig_seq;
+        {
+          ProfScope ps_(c->lc, "k_pack", st);
+          launch_pdl(k_pack, dim3(dim3(static_cast<unsigned>(3 * J), 8)), dim3(128), 0, st,
+                     d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
+                     h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>(), fa,
+                     c->sig.as<unsigned long long>(), v, fdn.as<unsigned>());
+        }
+        CSG_CUDA(cudaGetLastError());
+        if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
+        CSG_CUDA(cudaEventRecord(c->ev_fetch, st));
+        ctx_fetch_wait(c, FetchTicket{v});
+        // as ctx_sync: the stream is idle on return
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) CSG_CUDA(e);
+        if (e == cudaErrorNotReady) CSG_CUDA(cudaStreamSynchronize(st));
+      } else {
+        if (J > 0) {
+          // unfused: the pack's own tail is a no-op (a null flag never fires
+          // because fa is empty and the counter is private)
+          DevBuf& pdn = c->buf("rca.pack_done");
+          if (pdn.bytes < 16) {
+            pdn.ensure(16);
+            CSG_CUDA(cudaMemsetAsync(pdn.p, 0, 16, st));
+          }
+          DevBuf& pfl = c->buf("rca.pack_flag");
+          pfl.ensure(16);
+          ProfScope ps_(c->lc, "k_pack", st);
+          launch_pdl(k_pack, dim3(dim3(static_cast<unsigned>(3 * J), 8)), dim3(128), 0, st,
+                     d_out.as<TripOut>(), J, p_sus.as<csg_suspect>(), p_ev.as<csg_evidence>(),
+                     h_sus.as<csg_suspect>(), h_ev.as<csg_evidence>(), FetchArgs{},
+                     pfl.as<unsigned long long>(), 0ull, pdn.as<unsigned>());
+        }
+        ctx_sync(c, &fa);
+      }
     }
     if (dev_plan) {
       const FailPlan* fp = d_plan.stage.as<FailPlan>();
