@@ -38,9 +38,13 @@ __device__ inline void fetch_copy(const FetchArgs& a, uint32_t gt, uint32_t nt) 
 // raises the completion word — a kernel's own tail instead of a k_fetch
 // launch behind it.
 __device__ inline void fetch_tail(const FetchArgs& a, unsigned long long* flag,
-                                  unsigned long long v, unsigned* done) {
+                                  unsigned long long v, unsigned* done,
+                                  bool wrote_host = true) {
   __shared__ unsigned s_last;
-  __threadfence_system();  // this block's own mapped-memory writes first
+  // this block's own writes first (system scope if it wrote mapped memory:
+  // the host reads them once the completion word is up)
+  if (wrote_host) __threadfence_system();
+  else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0)
     s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1 ? 1u : 0u;

@@ -20,6 +20,7 @@
 
 #include "comm.cuh"
 #include "objects.h"
+#include "fetch.cuh"
 
 namespace csg {
 namespace {
@@ -149,7 +150,9 @@ constexpr uint32_t kHistChunks = 148;   // tile chunks of the histogram scan (<=
 
 __global__ void __launch_bounds__(kTileThreads, 2)
     k_stats_hist(const csg_packed_record* __restrict__ r, uint64_t n,
-                 StoreStats* __restrict__ st, uint32_t* __restrict__ counts) {
+                 StoreStats* __restrict__ st, uint32_t* __restrict__ counts,
+                 FetchArgs fa, unsigned long long* flag, unsigned long long v,
+                 unsigned* __restrict__ fdone) {
   __shared__ __align__(16) uint32_t hist[kHistDigits];
   for (int d = threadIdx.x; d < kHistDigits; d += kTileThreads) hist[d] = 0;
   StatAcc acc;
@@ -187,6 +190,9 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   const uint4* h4 = reinterpret_cast<const uint4*>(hist);
   for (int d = threadIdx.x; d < kHistDigits / 4; d += kTileThreads) row[d] = h4[d];
   acc.commit(st);
+  // flag set: the statistics travel to the host from the last block (no
+  // k_fetch launch between this pass and the speculative scatter)
+  if (flag) fetch_tail(fa, flag, v, fdone, false);
 }
 
 __device__ inline uint32_t block_excl_scan_u32(uint32_t v, uint32_t* wsum, uint32_t* total) {
@@ -1423,14 +1429,38 @@ void store_build_index(csg_store* s) {
     k_stats_keys<<<g, 256, 0, st>>>(recs, n, sdst, s->keys.as<uint32_t>(),
                                     s->perm.as<uint32_t>());
   };
-  auto stats_hist = [&](StoreStats* sdst) {
+  HostBuf& hs = c->hbuf("store.stats");
+  hs.ensure(sizeof(h));
+  FetchArgs fa{};
+  fa.add(s->stats_dev.p, hs.p, sizeof(h));
+  auto stats_hist = [&](StoreStats* sdst, unsigned long long* flag = nullptr,
+                        unsigned long long v = 0, unsigned* fdone = nullptr) {
     ProfScope ps_(c->lc, "k_stats_hist", st);
-    k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, sdst, hcnt.as<uint32_t>());
+    k_stats_hist<<<ntiles, kTileThreads, 0, st>>>(recs, n, sdst, hcnt.as<uint32_t>(), fa, flag,
+                                                  v, fdone);
   };
   DevBuf& st2 = c->buf("index.stats2");  // statistics of a second pass (discarded)
   st2.ensure(sizeof(StoreStats));
-  if (keys_first) stats_keys(s->stats_dev.as<StoreStats>());
-  else if (n) stats_hist(s->stats_dev.as<StoreStats>());
+  static const bool stats_fetch = std::getenv("CSG_STATS_FETCH") != nullptr;
+  FetchTicket tk;
+  if (keys_first) {
+    stats_keys(s->stats_dev.as<StoreStats>());
+  } else if (n && !comm_active(c) && !stats_fetch) {
+    c->sig.ensure(64);
+    DevBuf& fdn = c->buf("fetch.done");
+    if (fdn.bytes < 16) {
+      fdn.ensure(16);
+      CSG_CUDA(cudaMemsetAsync(fdn.p, 0, 16, st));
+    }
+    tk.seq = ++c->sig_seq;
+    stats_hist(s->stats_dev.as<StoreStats>(), c->sig.as<unsigned long long>(), tk.seq,
+               fdn.as<unsigned>());
+    CSG_CUDA(cudaGetLastError());
+    if (!c->ev_fetch) CSG_CUDA(cudaEventCreateWithFlags(&c->ev_fetch, cudaEventDisableTiming));
+    CSG_CUDA(cudaEventRecord(c->ev_fetch, st));
+  } else if (n) {
+    stats_hist(s->stats_dev.as<StoreStats>());
+  }
   if (comm_active(c)) {
     // global stats over the shards (identical rank space, ticks, op range)
     // one MAX all-reduce over order-preserving u64 images (minima as
@@ -1453,11 +1483,7 @@ void store_build_index(csg_store* s) {
                                      pk.as<unsigned long long>(), 1, P, c->rank);
     }
   }
-  HostBuf& hs = c->hbuf("store.stats");
-  hs.ensure(sizeof(h));
-  FetchArgs fa{};
-  fa.add(s->stats_dev.p, hs.p, sizeof(h));
-  const FetchTicket tk = ctx_fetch_issue(c, fa);
+  if (!tk.seq) tk = ctx_fetch_issue(c, fa);
   static const bool force_general = std::getenv("CSG_INDEX_RADIX") != nullptr;
   // Index layout for own rank span [lmin_, lmax_] and rank space R. With
   // go != nullptr the launches are speculative: every kernel first reads
